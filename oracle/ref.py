@@ -1,0 +1,97 @@
+"""ctypes front end of oracle/_ref (TEST INFRASTRUCTURE ONLY).
+
+oracle/_ref/libref_{canon,fast}.so are the reference's own gpss.cpp / prox.cpp /
+linear_operator.cpp / objective.cpp compiled by oracle/build_ref.sh against the Eigen
+stand-in in oracle/eigen_shim (Eigen is absent from this image).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import oracle as O
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_libs = {}
+
+
+def path(kind="canon"):
+    return os.path.join(HERE, "_ref", f"libref_{kind}.so")
+
+
+def available(kind="canon"):
+    return os.path.exists(path(kind))
+
+
+def lib(kind="canon"):
+    if kind not in _libs:
+        L = C.CDLL(path(kind))
+        L.ref_op_create.restype = C.c_void_p
+        L.ref_op_create.argtypes = [_dp, C.c_long, C.c_long]
+        L.ref_op_free.argtypes = [C.c_void_p]
+        L.ref_project_l1.restype = C.c_int
+        L.ref_project_l1.argtypes = [_dp, C.c_long, C.c_double, _dp, C.POINTER(C.c_double)]
+        L.ref_apply.restype = C.c_int
+        L.ref_apply.argtypes = [C.c_void_p, _dp, _dp, C.c_int]
+        L.ref_spectral_norm.restype = C.c_int
+        L.ref_spectral_norm.argtypes = [C.c_void_p, C.c_int, C.c_double, C.POINTER(C.c_double)]
+        L.ref_gpss_solve.restype = C.c_int
+        L.ref_gpss_solve.argtypes = [C.c_void_p, _dp, C.c_double, C.POINTER(O.GpConfig),
+                                     C.POINTER(O.StopRule), C.c_void_p, _dp,
+                                     C.POINTER(O.Result), C.c_void_p, C.c_long]
+        _libs[kind] = L
+    return _libs[kind]
+
+
+class RefOperator:
+    def __init__(self, K, kind="canon"):
+        self.L = lib(kind)
+        K = np.ascontiguousarray(K, dtype=np.float64)
+        self.n, self.p = K.shape
+        self.h = self.L.ref_op_create(K, self.n, self.p)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.ref_op_free(self.h)
+            self.h = None
+
+    def apply(self, x, adjoint=False):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty(self.p if adjoint else self.n)
+        O._check(self.L.ref_apply(self.h, x, out, int(adjoint)), "apply")
+        return out
+
+    def spectral_norm(self, max_iters=1000, tol=1e-8):
+        s = C.c_double()
+        O._check(self.L.ref_spectral_norm(self.h, max_iters, tol, C.byref(s)), "spectral")
+        return s.value
+
+    def gpss_solve(self, y, rho, cfg=None, stop=None, x0=None, trace=True):
+        cfg = cfg or O.GpConfig()
+        stop = stop or O.StopRule()
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        x = np.zeros(self.p)
+        res = O.Result()
+        cap = int(stop.max_iterations) if (trace and stop.max_iterations > 0) else 0
+        recs = (O.IterRecord * max(cap, 1))()
+        x0a = np.ascontiguousarray(x0, dtype=np.float64) if x0 is not None else None
+        rc = self.L.ref_gpss_solve(self.h, y, rho, C.byref(cfg), C.byref(stop),
+                                   x0a.ctypes.data if x0a is not None else None, x,
+                                   C.byref(res), C.addressof(recs) if cap else None, cap)
+        O._check(rc, "gpss_solve")
+        out = {f: getattr(res, f) for f, _ in O.Result._fields_ if f != "f_history"}
+        out["f_history"] = [res.f_history[i] for i in range(res.f_history_len)]
+        out["reason_name"] = O.REASONS[res.reason]
+        rec = O.records_to_dicts(recs, min(cap, res.iterations)) if cap else []
+        return x, out, rec
+
+
+def project_l1(x, rho, kind="canon"):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    th = C.c_double()
+    O._check(lib(kind).ref_project_l1(x, x.size, rho, out, C.byref(th)), "project_l1_ball")
+    return out, th.value

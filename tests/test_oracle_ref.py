@@ -1,0 +1,76 @@
+"""The oracle restatement against the reference's own sources (oracle/_ref, CPU only).
+
+oracle/_ref/libref_canon.so is /root/reference/proj/core/src/{gpss,prox,linear_operator,
+objective}.cpp compiled unmodified against the Eigen stand-in (oracle/build_ref.sh).  With
+the same reduction order the two must agree bit for bit, which pins every control-flow
+decision and scalar formula of the restatement to the reference code itself.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from oracle import ref as R
+from tests import problems as PB
+
+pytestmark = pytest.mark.skipif(not R.available("canon"), reason="oracle/_ref not built")
+
+FIELDS = ["k", "f", "stationarity", "alpha", "step", "matvecs", "bb_active", "bb1_raw",
+          "bb2_raw", "tau_before", "tau_after", "f_max", "dir_derivative"]
+
+
+def same(a, b):
+    return a == b or (np.isnan(a) and np.isnan(b))
+
+
+@pytest.mark.parametrize("spec,iters,memory", [
+    (PB.C1, 500, 1), (PB.C2_MINI, 300, 1), (PB.C3_MINI, 400, 1), (PB.RAGGED, 200, 5),
+    (PB.TINY, 50, 1), (PB.C4_MINI, 200, 3)], ids=lambda v: getattr(v, "name", str(v)))
+def test_trajectory_bit_identical(spec, iters, memory):
+    P = O.build_problem(spec)
+    cfg, stop = O.GpConfig(memory=memory), O.StopRule(iters, 0, 0, 0.0)
+    xo, ro, reco, _ = O.gpss_solve(P["K"], P["y"], P["rho"], cfg, stop)
+    xr, rr, recr = R.RefOperator(P["K"]).gpss_solve(P["y"], P["rho"], cfg, stop)
+    assert ro["iterations"] == rr["iterations"] and ro["reason"] == rr["reason"]
+    assert ro["matvecs"] == rr["matvecs"]
+    assert np.array_equal(xo, xr)
+    assert ro["objective"] == rr["objective"] and ro["f_history"] == rr["f_history"]
+    assert len(reco) == len(recr)
+    for a, b in zip(reco, recr):
+        for f in FIELDS:
+            assert same(a[f], b[f]), (a["k"], f, a[f], b[f])
+
+
+def test_projection_bit_identical():
+    rng = np.random.default_rng(5)
+    for rep in range(300):
+        p = int(rng.integers(1, 400))
+        x = rng.normal(size=p) * (10.0 ** rng.uniform(-3, 3))
+        if rep % 7 == 0:
+            x[rng.integers(0, p, size=max(1, p // 3))] = 0.0
+        rho = float(rng.uniform(0.0, 1.2)) * float(np.abs(x).sum())
+        u, th, _ = O.project_l1(x, rho)
+        ur, thr = R.project_l1(x, rho)
+        assert np.array_equal(u, ur) and th == thr
+
+
+def test_operator_and_power_iteration():
+    K = O.gaussian_matrix(9, 70, 230)
+    op = R.RefOperator(K)
+    rng = np.random.default_rng(2)
+    for _ in range(5):
+        x, r = rng.normal(size=230), rng.normal(size=70)
+        assert np.array_equal(op.apply(x), O.apply(K, x))
+        assert np.array_equal(op.apply(r, adjoint=True), O.apply_adjoint(K, r))
+    assert op.spectral_norm() == O.spectral_norm(K)[0]
+
+
+def test_literal_mode_within_tolerance():
+    """Plain sequential reductions stay within the north-star tolerance of canonical ones
+    on a trajectory that does not reach the arithmetic floor."""
+    P = O.build_problem(PB.C2_MINI)
+    cfg, stop = O.GpConfig(), O.StopRule(40, 0, 0, 0.0)
+    xc, rc, recc, _ = O.gpss_solve(P["K"], P["y"], P["rho"], cfg, stop)
+    with O.mode(O.LITERAL):
+        xl, rl, recl, _ = O.gpss_solve(P["K"], P["y"], P["rho"], cfg, stop)
+    assert np.linalg.norm(xc - xl) <= 1e-9 * np.linalg.norm(xc)
+    assert abs(rc["objective"] - rl["objective"]) <= 1e-9 * abs(rc["objective"])
