@@ -1,0 +1,181 @@
+/*
+ * l1g.h -- C-ABI of the B200-native GPSS engine (libl1g.so).
+ *
+ * This is the drop-in boundary for the reference solver path of l1solve
+ * (/root/reference/proj/core).  Plain pointers and sizes only; every host pointer is a
+ * caller-owned array of doubles, every device pointer a CUDA global-memory address on
+ * the context's device.  Status codes mirror the reference's exception classes:
+ *   L1G_OK (0), L1G_EINVAL (1) = std::invalid_argument, L1G_ERUNTIME (2) =
+ *   std::runtime_error (CUDA failures, backtracking cap).  l1g_last_error() returns the
+ *   thread's last message.
+ *
+ * Entry point -> reference interface it replaces (paths under proj/core):
+ *   l1g_op_create_dense / l1g_op_destroy  -> DenseOperator(Matrix)      linear_operator.hpp:36-52
+ *   l1g_op_apply / l1g_op_apply_adjoint   -> LinearOperator::apply /
+ *                                             apply_adjoint (+1 matvec)  linear_operator.cpp:19-29
+ *   l1g_op_spectral_norm                  -> spectral_norm_estimate     linear_operator.cpp:43-60
+ *   l1g_project_l1                        -> project_l1_ball_with_threshold prox.cpp:38-73
+ *   l1g_soft_threshold                    -> soft_threshold             prox.cpp:23-36
+ *   l1g_steplength_select                 -> steplength_select          gpss.cpp:59-91
+ *   l1g_backtrack                         -> backtracking_search core   gpss.cpp:25-37
+ *   l1g_alpha0_from_gradient              -> alpha0_from_gradient       gpss.cpp:93-98
+ *   l1g_solver_create / l1g_solver_init   -> gp_init                    gpss.cpp:117-134
+ *   l1g_solver_iterate                    -> gp_iterate                 gpss.cpp:136-219
+ *   l1g_gpss_solve / l1g_solver_run       -> gpss_solve                 gpss.cpp:221-292
+ *   l1g_config_validate / l1g_stop_validate -> GpConfig::validate / StopRule::validate
+ *                                                                        gpss.cpp:41-50,
+ *                                                                        objective.cpp:42-48
+ * Harness (BASELINE configs, not part of the reference API):
+ *   l1g_op_generate_gaussian / l1g_op_generate_blur / l1g_op_scale / l1g_op_download.
+ */
+#ifndef L1G_H
+#define L1G_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { L1G_OK = 0, L1G_EINVAL = 1, L1G_ERUNTIME = 2 };
+
+/* StopReason, solver.hpp:38-44 */
+enum { L1G_STATIONARY = 0, L1G_MAX_ITERATIONS = 1, L1G_MAX_MATVECS = 2, L1G_MAX_SECONDS = 3,
+       L1G_OBJECTIVE_TOL = 4 };
+
+typedef struct l1g_ctx l1g_ctx;
+typedef struct l1g_op l1g_op;
+typedef struct l1g_solver l1g_solver;
+
+/* GpConfig, gpss.hpp:14-24 (memory and alpha2_memory are capped at 64 here) */
+typedef struct {
+  double beta, theta;
+  int32_t memory, alpha2_memory;
+  double alpha_min, alpha_max, tau1;
+} l1g_gp_config;
+
+/* StopRule, solver.hpp:52-60 */
+typedef struct {
+  int64_t max_iterations, max_matvecs;
+  double max_seconds, stationarity_tol, objective_tol;
+} l1g_stop_rule;
+
+/* IterationRecord, solver.hpp:68-84, plus halvings, projection threshold and support */
+typedef struct {
+  int64_t k;
+  double f, stationarity, alpha, step;
+  int64_t matvecs;
+  double elapsed_seconds;
+  int32_t bb_active, halvings;
+  double bb1_raw, bb2_raw, tau_before, tau_after, f_max, dir_derivative;
+  double theta;
+  int64_t support;
+} l1g_iter_record;
+
+/* SolverState scalars, solver.hpp:91-100 */
+typedef struct {
+  int64_t iterations, matvecs;
+  double objective, stationarity, elapsed_seconds;
+  int32_t reason, status;
+  double f_history[64];
+  int32_t f_history_len;
+} l1g_result;
+
+/* SteplengthState (gpss.hpp:31-36) without the cached vectors, and SteplengthChoice */
+typedef struct {
+  double tau;
+  double hist[66];
+  int32_t hist_len;
+} l1g_sl_state;
+
+typedef struct {
+  double alpha;
+  int32_t bb_active;
+  double bb1_raw, bb2_raw, tau_before, tau_after;
+} l1g_sl_choice;
+
+const char* l1g_last_error(void);
+const char* l1g_version(void);
+
+/* ---- context ---- */
+int l1g_ctx_create(int device, l1g_ctx** out);
+void l1g_ctx_destroy(l1g_ctx* ctx);
+int l1g_ctx_info(l1g_ctx* ctx, int* sm_count, int64_t* free_bytes);
+
+/* ---- operator (device-resident tiled K) ---- */
+int l1g_op_create_dense(l1g_ctx* ctx, const double* K, int64_t n, int64_t p, int row_major,
+                        l1g_op** out);
+int l1g_op_generate_gaussian(l1g_ctx* ctx, int64_t n, int64_t p, uint64_t seed,
+                             int64_t col_offset, int64_t p_total, l1g_op** out);
+int l1g_op_generate_blur(l1g_ctx* ctx, int64_t n, const double* taps, int radius,
+                         l1g_op** out);
+int l1g_op_scale(l1g_op* op, double c);
+int l1g_op_dims(const l1g_op* op, int64_t* n, int64_t* p);
+int l1g_op_download(l1g_op* op, double* K_row_major);
+void l1g_op_destroy(l1g_op* op);
+
+int l1g_op_apply(l1g_op* op, const double* x, double* out);
+int l1g_op_apply_adjoint(l1g_op* op, const double* r, double* out);
+/* device-pointer forms; stream may be NULL (legacy default stream of the context) */
+int l1g_op_apply_dev(l1g_op* op, const double* x_dev, double* out_dev, void* stream);
+int l1g_op_apply_adjoint_dev(l1g_op* op, const double* r_dev, double* out_dev, void* stream);
+int l1g_op_spectral_norm(l1g_op* op, int max_iters, double tol, double* sigma,
+                         int64_t* matvecs);
+
+/* ---- prox ---- */
+int l1g_project_l1(l1g_ctx* ctx, const double* x, int64_t m, double rho, double* out,
+                   double* theta, int64_t* support);
+int l1g_soft_threshold(l1g_ctx* ctx, const double* x, int64_t m, double t, double* out);
+/* canonical reductions of host vectors: op 0 = a'b, 1 = ||a||^2, 2 = ||a||_1, 3 = ||a||_inf
+ * (the Eigen dot / squaredNorm / lpNorm<1> / lpNorm<Infinity> the reference calls) */
+int l1g_reduce(l1g_ctx* ctx, const double* a, const double* b, int64_t m, int op, double* out);
+
+/* ---- GPSS pieces ---- */
+int l1g_config_validate(const l1g_gp_config* cfg);
+int l1g_stop_validate(const l1g_stop_rule* stop);
+void l1g_steplength_init(l1g_sl_state* st, const l1g_gp_config* cfg);
+int l1g_steplength_select(l1g_ctx* ctx, l1g_sl_state* st, const double* s, const double* z,
+                          int64_t m, const l1g_gp_config* cfg, int64_t k, l1g_sl_choice* out);
+int l1g_backtrack(l1g_ctx* ctx, double f0, double a, double b, double f_max, double gd,
+                  const l1g_gp_config* cfg, double* step, double* f_new, int32_t* halvings);
+int l1g_alpha0_from_gradient(l1g_ctx* ctx, double rho, const double* x0, const double* grad,
+                             int64_t m, const l1g_gp_config* cfg, double* alpha0);
+
+/* ---- solver (device-resident state) ---- */
+int l1g_solver_create(l1g_op* op, const double* y, double rho, const l1g_gp_config* cfg,
+                      l1g_solver** out);
+int l1g_solver_set_y(l1g_solver* s, const double* y);
+int l1g_solver_set_y_dev(l1g_solver* s, const double* y_dev);
+int l1g_solver_init(l1g_solver* s, const double* x0 /* NULL = zero */);
+int l1g_solver_iterate(l1g_solver* s, double stationarity_tol, l1g_iter_record* info,
+                       int32_t* stationary);
+int l1g_solver_run(l1g_solver* s, const l1g_stop_rule* stop, l1g_result* res,
+                   l1g_iter_record* trace, int64_t trace_cap);
+/* gpss_solve with an IterationCallback (solver.hpp:86-88): cb(record, x, p, user) after
+ * every completed iteration; x is valid only during the call */
+typedef void (*l1g_iter_cb)(const l1g_iter_record* rec, const double* x, int64_t p, void* user);
+int l1g_solver_run_cb(l1g_solver* s, const l1g_stop_rule* stop, l1g_result* res,
+                      l1g_iter_cb cb, void* user);
+int l1g_solver_get(l1g_solver* s, double* x, double* kx_minus_y, double* grad, double* f,
+                   int64_t* k, double* alpha0, int64_t* matvecs);
+int l1g_solver_x_dev(l1g_solver* s, const double** x_dev);
+int l1g_solver_stream(l1g_solver* s, void** stream);
+/* per-kernel CUDA-event timing of the device loop (projection / forward / adjoint), summed
+ * over completed iterations, and the number of kernels this solver launched */
+int l1g_solver_set_timing(l1g_solver* s, int on);
+int l1g_solver_timing(l1g_solver* s, double* proj_ms, double* fwd_ms, double* adj_ms,
+                      int64_t* iterations, int64_t* launches, int reset);
+void l1g_solver_destroy(l1g_solver* s);
+
+/* gpss_solve(Objective(op, y), L1Ball(rho), cfg, stop, {}, x0) */
+int l1g_gpss_solve(l1g_op* op, const double* y, double rho, const l1g_gp_config* cfg,
+                   const l1g_stop_rule* stop, const double* x0, double* x_out, l1g_result* res,
+                   l1g_iter_record* trace, int64_t trace_cap);
+
+/* pinned host buffers for the end-to-end path */
+int l1g_host_alloc(int64_t bytes, void** ptr);
+void l1g_host_free(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,13 @@
+"""B200-native GPSS engine: the gradient-projection iteration loop of arXiv 0902.4424
+(l1solve's gpss_solve) on sm_100a.  See DESIGN.md."""
+from ._lib import load as _load_lib  # noqa: F401
+from .api import (  # noqa: F401
+    BacktrackResult, Context, DenseOperator, GpConfig, GpIterationState, GpStepInfo,
+    IterationRecord, L1Ball, L1Projection, LinearOperator, MatvecCounter, Objective,
+    PenaltyWeight, SolverState, SteplengthChoice, SteplengthState, StopReason, StopRule,
+    alpha0_from_gradient, alpha0_init, backtracking_search, default_context, dot, gp_init,
+    gp_iterate, gpss_solve, l1_norm, lambda_from_rho, lambda_max, linf_norm,
+    project_l1_ball, project_l1_ball_with_threshold, rho_from_lambda, soft_threshold,
+    spectral_norm_estimate, squared_norm, steplength_init, steplength_select, to_string)
+
+__version__ = "0.1.0"

@@ -1,0 +1,40 @@
+"""Build recipe for libl1g.so (sm_100a only)."""
+from __future__ import annotations
+
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+SOURCES = ["gemv.cu", "project.cu", "vec.cu", "abi.cu"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+         "-fmad=false", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
+
+
+def lib_path():
+    return os.path.join(HERE, "libl1g.so")
+
+
+def needs_build():
+    out = lib_path()
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    deps.append(os.path.join(HERE, "..", "include", "l1g.h"))
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def build(force: bool = False, verbose: bool = False):
+    if not force and not needs_build():
+        return lib_path()
+    cmd = [NVCC, *FLAGS, "-o", lib_path(), *[os.path.join(CSRC, s) for s in SOURCES]]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return lib_path()
+
+
+if __name__ == "__main__":
+    build(force=True, verbose=True)

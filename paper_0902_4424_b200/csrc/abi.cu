@@ -1,0 +1,1053 @@
+// abi.cu -- the extern "C" boundary (include/l1g.h) and the host runtime behind it.
+//
+// Every entry point catches C++ exceptions and maps them onto status codes the way the
+// reference maps them onto exception classes (solver.hpp / gpss.cpp: invalid_argument for
+// validation, runtime_error for computation failures).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/l1g.h"
+#include "common.cuh"
+#include "engine.h"
+#include "vec.h"
+
+using namespace l1g;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return L1G_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return L1G_EINVAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return L1G_ERUNTIME;
+  } catch (...) {
+    g_err = "unknown error";
+    return L1G_ERUNTIME;
+  }
+}
+
+template <class T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  L1G_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+  L1G_CUDA(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+int64_t pad_to(int64_t v, int64_t m) { return ((std::max<int64_t>(v, 1) + m - 1) / m) * m; }
+
+void check_cfg(const l1g_gp_config& c) {  // gpss.cpp:41-50 (+ the history cap of this port)
+  if (!(c.beta > 0.0 && c.beta < 1.0)) throw InvalidArgument("GpConfig: beta must be in (0,1)");
+  if (!(c.theta > 0.0 && c.theta < 1.0)) throw InvalidArgument("GpConfig: theta must be in (0,1)");
+  if (c.memory < 1) throw InvalidArgument("GpConfig: memory (M) must be >= 1");
+  if (c.memory > kMaxHist) throw InvalidArgument("GpConfig: memory (M) must be <= 64 here");
+  if (!(c.alpha_min > 0.0 && c.alpha_min < c.alpha_max))
+    throw InvalidArgument("GpConfig: need 0 < alpha_min < alpha_max");
+  if (!(c.tau1 > 0.0 && c.tau1 < 1.0)) throw InvalidArgument("GpConfig: tau1 must be in (0,1)");
+  if (c.alpha2_memory < 0) throw InvalidArgument("GpConfig: alpha2_memory must be >= 0");
+  if (c.alpha2_memory > kMaxHist) throw InvalidArgument("GpConfig: alpha2_memory must be <= 64 here");
+}
+void check_stop(const l1g_stop_rule& s) {  // objective.cpp:42-48
+  if (s.max_iterations <= 0 && s.max_matvecs <= 0 && s.max_seconds <= 0.0)
+    throw InvalidArgument(
+        "StopRule: at least one of max_iterations, max_matvecs, max_seconds must be finite");
+  if (s.stationarity_tol < 0.0 || s.objective_tol < 0.0)
+    throw InvalidArgument("StopRule: tolerances must be >= 0");
+}
+void check_rho(double rho) {  // prox.cpp:11-13
+  if (!(rho >= 0.0)) throw InvalidArgument("L1Ball: radius must be >= 0");
+}
+
+void alloc_ws(Workspace& ws, const GemvPlan& pl) {
+  ws.fwd_part = dalloc<double>((size_t)pl.ncr * pl.n_pad);
+  ws.adj_part = dalloc<double>((size_t)pl.nrr * pl.p_pad);
+  ws.grpsum = dalloc<double>((size_t)std::max(2 * pl.nrg, 3 * pl.ncg) + 8);
+  ws.counters = dalloc<unsigned>((size_t)(pl.nrg + pl.ncg + 2));
+}
+void free_ws(Workspace& ws) {
+  dfree(ws.fwd_part);
+  dfree(ws.adj_part);
+  dfree(ws.grpsum);
+  dfree(ws.counters);
+  ws = Workspace{};
+}
+
+__global__ void configure_kernel(DevState* st, l1g_stop_rule stop, int single_step,
+                                 l1g_iter_record* trace, int64_t cap) {
+  st->max_iterations = stop.max_iterations;
+  st->max_matvecs = stop.max_matvecs;
+  st->max_seconds = stop.max_seconds;
+  st->stationarity_tol = stop.stationarity_tol;
+  st->objective_tol = stop.objective_tol;
+  st->single_step = single_step;
+  st->trace = trace;
+  st->trace_cap = cap;
+  if (st->status == STOPPED) st->status = RUNNING;
+}
+}  // namespace
+
+struct l1g_ctx : Ctx {
+  std::mutex mu;
+  // growable scratch for host-vector entry points
+  int64_t cap = 0;
+  double *a = nullptr, *b = nullptr, *o = nullptr, *pscr = nullptr;
+  l1g_sl_state* sl = nullptr;
+  l1g_sl_choice* ch = nullptr;
+  double* host_pinned = nullptr;
+  void ensure(int64_t m) {
+    const int64_t need = pad_to(m, 256);
+    if (need <= cap) return;
+    dfree(a);
+    dfree(b);
+    dfree(o);
+    dfree(pscr);
+    a = dalloc<double>(need);
+    b = dalloc<double>(need);
+    o = dalloc<double>(need);
+    pscr = dalloc<double>(proj_scratch_doubles(need));
+    cap = need;
+  }
+  void upload(double* dst, const double* src, int64_t m, int64_t padded) {
+    L1G_CUDA(cudaMemsetAsync(dst, 0, padded * sizeof(double), stream));
+    if (m) L1G_CUDA(cudaMemcpyAsync(dst, src, m * sizeof(double), cudaMemcpyHostToDevice, stream));
+  }
+};
+
+struct l1g_solver;
+
+struct l1g_op : Op {
+  l1g_ctx* c = nullptr;
+  std::mutex mu;  // guards ws + scratch vectors for the generic applies
+  Workspace ws;
+  double *vin = nullptr, *vout = nullptr, *vtmp = nullptr, *scal = nullptr;
+  std::mutex solver_mu;
+  l1g_solver* cached = nullptr;
+};
+
+struct l1g_solver {
+  l1g_op* op = nullptr;
+  cudaStream_t stream = nullptr;
+  Workspace ws;
+  VecBufs vb{};
+  double* y = nullptr;
+  DevState* st = nullptr;
+  double* pscr = nullptr;
+  double* scal = nullptr;
+  ProjPlan pp{};
+  l1g_gp_config cfg{};
+  double rho = 0.0;
+  l1g_iter_record* trace = nullptr;
+  int64_t trace_cap = 0;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  int gsize = 0;
+  // optional per-kernel timing: events [graph][iteration][4] around proj / fwd / adj
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;
+  double t_proj = 0.0, t_fwd = 0.0, t_adj = 0.0;
+  int64_t t_iters = 0, launches = 0;
+  int* status_host = nullptr;
+  bool inited = false;
+  std::chrono::steady_clock::time_point t0;
+};
+
+namespace {
+
+void set_device(const Ctx* c) { L1G_CUDA(cudaSetDevice(c->device)); }
+
+void download(double* dst, const double* src, int64_t m, cudaStream_t s) {
+  if (dst && m) L1G_CUDA(cudaMemcpyAsync(dst, src, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+}
+
+DevState host_state(const l1g_gp_config& cfg, double rho) {
+  DevState h;
+  std::memset(&h, 0, sizeof(h));
+  h.cfg = cfg;
+  h.rho = rho;
+  h.max_iterations = 0;
+  h.status = RUNNING;
+  h.cur = 0;
+  h.k = 0;
+  h.matvecs = 0;
+  h.tau = cfg.tau1;
+  h.out_stationarity = INFINITY;
+  h.alpha0 = cfg.alpha_max;
+  return h;
+}
+
+void solver_free(l1g_solver* s) {
+  if (!s) return;
+  cudaSetDevice(s->op->c->device);
+  for (auto& g : s->gexec)
+    if (g) cudaGraphExecDestroy(g);
+  for (auto e : s->tev) cudaEventDestroy(e);
+  free_ws(s->ws);
+  for (int i = 0; i < 2; ++i) {
+    dfree(s->vb.x[i]);
+    dfree(s->vb.g[i]);
+    dfree(s->vb.r[i]);
+  }
+  dfree(s->vb.d);
+  dfree(s->vb.kd);
+  dfree(s->y);
+  dfree(s->st);
+  dfree(s->pscr);
+  dfree(s->scal);
+  dfree(s->trace);
+  if (s->status_host) cudaFreeHost(s->status_host);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+}
+
+l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho) {
+  check_cfg(cfg);
+  check_rho(rho);
+  set_device(op->c);
+  auto* s = new l1g_solver();
+  s->op = op;
+  try {
+    const GemvPlan& pl = op->plan;
+    L1G_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    alloc_ws(s->ws, pl);
+    for (int i = 0; i < 2; ++i) {
+      s->vb.x[i] = dalloc<double>(pl.p_pad);
+      s->vb.g[i] = dalloc<double>(pl.p_pad);
+      s->vb.r[i] = dalloc<double>(pl.n_pad);
+    }
+    s->vb.d = dalloc<double>(pl.p_pad);
+    s->vb.kd = dalloc<double>(pl.n_pad);
+    s->y = dalloc<double>(pl.n_pad);
+    s->vb.y = s->y;
+    s->st = dalloc<DevState>(1);
+    s->pp = make_proj_plan(pl.p_pad);
+    s->pscr = dalloc<double>(proj_scratch_doubles(pl.p_pad));
+    s->scal = dalloc<double>(16);
+    L1G_CUDA(cudaHostAlloc(&s->status_host, 256, cudaHostAllocDefault));
+    s->cfg = cfg;
+    s->rho = rho;
+  } catch (...) {
+    solver_free(s);
+    throw;
+  }
+  return s;
+}
+
+void solver_set_y(l1g_solver* s, const double* y_host) {
+  const GemvPlan& pl = s->op->plan;
+  L1G_CUDA(cudaMemcpyAsync(s->y, y_host, pl.n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+}
+
+// gpss.cpp:117-134
+void solver_init(l1g_solver* s, const double* x0_host) {
+  set_device(s->op->c);
+  const GemvPlan& pl = s->op->plan;
+  s->t0 = std::chrono::steady_clock::now();
+  L1G_CUDA(cudaMemsetAsync(s->vb.x[0], 0, pl.p_pad * sizeof(double), s->stream));
+  if (x0_host) {
+    L1G_CUDA(cudaMemcpyAsync(s->vb.x[0], x0_host, pl.p * sizeof(double), cudaMemcpyHostToDevice,
+                             s->stream));
+    // L1Ball::contains(x0, 1e-12), prox.cpp:15-17 (zero start is always feasible)
+    reduce(s->vb.x[0], nullptr, pl.p_pad, RED_ABS, s->scal, 0, s->stream);
+    double l1 = 0.0;
+    L1G_CUDA(cudaMemcpyAsync(&l1, s->scal, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+    L1G_CUDA(cudaStreamSynchronize(s->stream));
+    if (!(l1 <= s->rho + 1e-12)) throw InvalidArgument("gp_init: starting point is infeasible");
+  }
+  DevState h = host_state(s->cfg, s->rho);
+  h.matvecs = 2;
+  L1G_CUDA(cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, s->stream));
+  state_start(s->st, s->stream);
+  launch_fwd(*s->op, s->ws, FWD_INIT, s->vb.x[0], nullptr, &s->vb, s->st, s->stream);
+  launch_adj(*s->op, s->ws, ADJ_INIT, nullptr, nullptr, &s->vb, s->st, s->stream);
+  launch_proj(s->pp, PROJ_ALPHA0, pl.p, pl.p_pad, s->vb.x[0], s->vb.g[0], nullptr, s->pscr, s->st,
+              &s->vb, s->stream);
+  s->launches += x0_host ? 5 : 4;
+  s->inited = true;
+}
+
+void enqueue_iteration(l1g_solver* s) {
+  const GemvPlan& pl = s->op->plan;
+  launch_proj(s->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, s->pscr, s->st, &s->vb,
+              s->stream);
+  launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
+  launch_adj(*s->op, s->ws, ADJ_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
+}
+
+void drop_graphs(l1g_solver* s) {
+  for (auto& g : s->gexec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  for (auto e : s->tev) cudaEventDestroy(e);
+  s->tev.clear();
+}
+
+cudaEvent_t& tev(l1g_solver* s, int g, int i, int j) {
+  return s->tev[((size_t)g * s->gsize + i) * 4 + j];
+}
+
+// Two instances of a graph holding gsize iterations (proj -> fwd -> adj), alternated so the
+// host can read one chunk's timing events while the next chunk runs.
+void build_graphs(l1g_solver* s) {
+  if (s->gexec[0]) return;
+  const GemvPlan& pl = s->op->plan;
+  // iterations per graph: ~2 ms of streaming work, between 1 and 64
+  const double bytes = 2.0 * (double)pl.n_pad * (double)pl.p_pad * 8.0;
+  const double est_us = bytes / 6.0e6 + 15.0;
+  s->gsize = (int)std::max(1.0, std::min(64.0, 2000.0 / est_us));
+  if (s->timing) {
+    s->tev.resize((size_t)2 * s->gsize * 4);
+    for (auto& e : s->tev) L1G_CUDA(cudaEventCreate(&e));
+  }
+  for (int gi = 0; gi < 2; ++gi) {
+    cudaGraph_t g;
+    L1G_CUDA(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < s->gsize; ++i) {
+      if (s->timing) {
+        L1G_CUDA(cudaEventRecord(tev(s, gi, i, 0), s->stream));
+        launch_proj(s->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, s->pscr, s->st,
+                    &s->vb, s->stream);
+        L1G_CUDA(cudaEventRecord(tev(s, gi, i, 1), s->stream));
+        launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
+        L1G_CUDA(cudaEventRecord(tev(s, gi, i, 2), s->stream));
+        launch_adj(*s->op, s->ws, ADJ_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
+        L1G_CUDA(cudaEventRecord(tev(s, gi, i, 3), s->stream));
+      } else {
+        enqueue_iteration(s);
+      }
+    }
+    L1G_CUDA(cudaStreamEndCapture(s->stream, &g));
+    L1G_CUDA(cudaGraphInstantiate(&s->gexec[gi], g, 0));
+    cudaGraphDestroy(g);
+  }
+}
+
+void accumulate_timing(l1g_solver* s, int gi, int64_t real_iters) {
+  for (int64_t i = 0; i < std::min<int64_t>(real_iters, s->gsize); ++i) {
+    float a = 0.f, b = 0.f, c = 0.f;
+    L1G_CUDA(cudaEventElapsedTime(&a, tev(s, gi, (int)i, 0), tev(s, gi, (int)i, 1)));
+    L1G_CUDA(cudaEventElapsedTime(&b, tev(s, gi, (int)i, 1), tev(s, gi, (int)i, 2)));
+    L1G_CUDA(cudaEventElapsedTime(&c, tev(s, gi, (int)i, 2), tev(s, gi, (int)i, 3)));
+    s->t_proj += a;
+    s->t_fwd += b;
+    s->t_adj += c;
+    ++s->t_iters;
+  }
+}
+
+void read_state(l1g_solver* s, DevState* h) {
+  L1G_CUDA(cudaMemcpyAsync(h, s->st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+  L1G_CUDA(cudaStreamSynchronize(s->stream));
+  if (h->status == FAILED)
+    throw RuntimeFailure(
+        "backtracking_search: no acceptable step after 60 shrink steps; "
+        "the gradient or the search direction is inconsistent");
+}
+
+void configure(l1g_solver* s, const l1g_stop_rule& stop, int single, l1g_iter_record* trace,
+               int64_t cap) {
+  configure_kernel<<<1, 1, 0, s->stream>>>(s->st, stop, single, trace, cap);
+  L1G_CUDA(cudaGetLastError());
+}
+
+void finalize(l1g_solver* s, l1g_result* res, l1g_iter_record* trace_host, int64_t cap);
+
+// gpss.cpp:221-292 loop, device resident; the host only polls the status word
+void solver_run(l1g_solver* s, const l1g_stop_rule& stop, l1g_result* res,
+                l1g_iter_record* trace_host, int64_t cap) {
+  check_stop(stop);
+  if (!s->inited) throw InvalidArgument("solver: gp_init has not been run");
+  set_device(s->op->c);
+  if (trace_host && cap > 0 && cap > s->trace_cap) {
+    dfree(s->trace);
+    s->trace = dalloc<l1g_iter_record>(cap);
+    s->trace_cap = cap;
+  }
+  configure(s, stop, 0, trace_host && cap > 0 ? s->trace : nullptr, trace_host ? cap : 0);
+  build_graphs(s);
+  s->launches += 1;
+  cudaEvent_t ev[2];
+  L1G_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  L1G_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  // pinned words per slot: [0] status, [2..3] k (int64)
+  volatile int* flag = s->status_host;
+  int64_t k_seen = 0;
+  {
+    DevState h0;
+    L1G_CUDA(cudaMemcpyAsync(&h0.k, &s->st->k, sizeof(int64_t), cudaMemcpyDeviceToHost, s->stream));
+    L1G_CUDA(cudaStreamSynchronize(s->stream));
+    k_seen = h0.k;
+  }
+  int64_t launched = 0;
+  const int64_t hard_cap =
+      stop.max_iterations > 0 ? (stop.max_iterations - k_seen + 1) / s->gsize + 3 : INT64_MAX;
+  bool done = false;
+  auto inspect = [&](int64_t chunk) {
+    const int sl = (int)(chunk & 1);
+    L1G_CUDA(cudaEventSynchronize(ev[sl]));
+    const int64_t k = *reinterpret_cast<volatile int64_t*>(flag + 16 * sl + 2);
+    if (s->timing) accumulate_timing(s, sl, k - k_seen);
+    k_seen = k;
+    if (flag[16 * sl] != RUNNING) done = true;
+  };
+  while (!done) {
+    const int slot = (int)(launched & 1);
+    L1G_CUDA(cudaGraphLaunch(s->gexec[slot], s->stream));
+    s->launches += 3LL * s->gsize;
+    L1G_CUDA(cudaMemcpyAsync((void*)(flag + 16 * slot), &s->st->status, sizeof(int),
+                             cudaMemcpyDeviceToHost, s->stream));
+    L1G_CUDA(cudaMemcpyAsync((void*)(flag + 16 * slot + 2), &s->st->k, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, s->stream));
+    L1G_CUDA(cudaEventRecord(ev[slot], s->stream));
+    ++launched;
+    if (launched >= 2) inspect(launched - 2);  // one chunk stays in flight
+    if (launched >= hard_cap) done = true;
+  }
+  if (launched >= 1) inspect(launched - 1);
+  L1G_CUDA(cudaStreamSynchronize(s->stream));
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  finalize(s, res, trace_host, cap);
+}
+
+void finalize(l1g_solver* s, l1g_result* res, l1g_iter_record* trace_host, int64_t cap) {
+  DevState h;
+  read_state(s, &h);
+  if (h.status == RUNNING) throw RuntimeFailure("gpss_solve: run did not reach a stop rule");
+  std::memset(res, 0, sizeof(*res));
+  res->iterations = h.k;
+  res->matvecs = h.matvecs;
+  res->objective = h.f;
+  res->stationarity = h.out_stationarity;
+  res->elapsed_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - s->t0).count();
+  res->reason = h.reason;
+  res->status = 0;
+  res->f_history_len = h.fh_len;
+  std::memcpy(res->f_history, h.fh, sizeof(double) * h.fh_len);
+  if (trace_host && cap > 0) {
+    const int64_t nrec = std::min<int64_t>(cap, h.k);
+    if (nrec > 0)
+      L1G_CUDA(cudaMemcpy(trace_host, s->trace, nrec * sizeof(l1g_iter_record),
+                          cudaMemcpyDeviceToHost));
+  }
+}
+
+// gpss_solve with an IterationCallback (solver.hpp:86-88): the same device iteration, one
+// synchronisation per step so the callback sees every record and iterate in order.
+void solver_run_cb(l1g_solver* s, const l1g_stop_rule& stop, l1g_result* res, l1g_iter_cb cb,
+                   void* user) {
+  check_stop(stop);
+  if (!s->inited) throw InvalidArgument("solver: gp_init has not been run");
+  set_device(s->op->c);
+  configure(s, stop, 0, nullptr, 0);
+  const GemvPlan& pl = s->op->plan;
+  std::vector<double> x((size_t)pl.p);
+  int64_t k_prev = 0;
+  for (;;) {
+    enqueue_iteration(s);
+    s->launches += 3;
+    DevState h;
+    read_state(s, &h);
+    if (h.k > k_prev) {
+      k_prev = h.k;
+      download(x.data(), s->vb.x[h.cur], pl.p, s->stream);
+      L1G_CUDA(cudaStreamSynchronize(s->stream));
+      if (cb) cb(&h.last, x.data(), pl.p, user);
+    }
+    if (h.status != RUNNING) break;
+  }
+  finalize(s, res, nullptr, 0);
+}
+
+void solver_iterate(l1g_solver* s, double tol, l1g_iter_record* info, int32_t* stationary) {
+  if (!s->inited) throw InvalidArgument("solver: gp_init has not been run");
+  set_device(s->op->c);
+  l1g_stop_rule st{};
+  st.max_iterations = 1;
+  st.stationarity_tol = tol;
+  configure(s, st, 1, nullptr, 0);
+  enqueue_iteration(s);
+  s->launches += 4;
+  DevState h;
+  read_state(s, &h);
+  *stationary = h.stationary;
+  if (info) {
+    *info = h.last;
+    if (h.stationary) {
+      info->bb_active = h.choice.bb_active;
+      info->bb1_raw = h.choice.bb1_raw;
+      info->bb2_raw = h.choice.bb2_raw;
+      info->tau_before = h.choice.tau_before;
+      info->tau_after = h.choice.tau_after;
+      info->f_max = std::nan("");
+      info->halvings = 0;
+    }
+  }
+}
+
+l1g_op* op_alloc(l1g_ctx* ctx, int64_t n, int64_t p) {
+  if (n < 1 || p < 1) throw InvalidArgument("DenseOperator: dimensions must be positive");
+  set_device(ctx);
+  auto* op = new l1g_op();
+  op->c = ctx;
+  op->ctx = ctx;
+  op->plan = make_plan(n, p, ctx->sm_count);
+  const GemvPlan& pl = op->plan;
+  try {
+    op->K = dalloc<double>((size_t)pl.n_pad * pl.p_pad);
+    alloc_ws(op->ws, pl);
+    op->vin = dalloc<double>(pl.p_pad);
+    op->vout = dalloc<double>(std::max(pl.n_pad, pl.p_pad));
+    op->vtmp = dalloc<double>(std::max(pl.n_pad, pl.p_pad));
+    op->scal = dalloc<double>(16);
+  } catch (...) {
+    dfree(op->K);
+    free_ws(op->ws);
+    delete op;
+    throw;
+  }
+  return op;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+const char* l1g_last_error(void) { return g_err.c_str(); }
+const char* l1g_version(void) { return "l1g 0.1 (sm_100a)"; }
+
+int l1g_ctx_create(int device, l1g_ctx** out) {
+  return guarded([&] {
+    *out = nullptr;
+    int ndev = 0;
+    L1G_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw InvalidArgument("l1g_ctx_create: no such device");
+    L1G_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    L1G_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw RuntimeFailure("l1g: this build targets sm_100a (B200) only");
+    auto* c = new l1g_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    L1G_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->scratch_state = dalloc<DevState>(1);
+    c->scratch_d = dalloc<double>(64);
+    c->sl = dalloc<l1g_sl_state>(1);
+    c->ch = dalloc<l1g_sl_choice>(1);
+    *out = c;
+  });
+}
+
+void l1g_ctx_destroy(l1g_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  dfree(c->a);
+  dfree(c->b);
+  dfree(c->o);
+  dfree(c->pscr);
+  dfree(c->scratch_state);
+  dfree(c->scratch_d);
+  dfree(c->sl);
+  dfree(c->ch);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int l1g_ctx_info(l1g_ctx* c, int* sm_count, int64_t* free_bytes) {
+  return guarded([&] {
+    set_device(c);
+    size_t fr = 0, tot = 0;
+    L1G_CUDA(cudaMemGetInfo(&fr, &tot));
+    if (sm_count) *sm_count = c->sm_count;
+    if (free_bytes) *free_bytes = (int64_t)fr;
+  });
+}
+
+int l1g_op_create_dense(l1g_ctx* c, const double* K, int64_t n, int64_t p, int row_major,
+                        l1g_op** out) {
+  return guarded([&] {
+    *out = nullptr;
+    l1g_op* op = op_alloc(c, n, p);
+    try {
+      const GemvPlan& pl = op->plan;
+      // stream row blocks through a bounded device buffer (<= 256 MB)
+      int64_t chunk = std::max<int64_t>(TR, ((int64_t)(256 << 20) / (p * 8)) / TR * TR);
+      chunk = std::min<int64_t>(chunk, pad_to(n, TR));
+      double* tmp = dalloc<double>((size_t)chunk * p);
+      std::vector<double> rowbuf;
+      for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+        const int64_t rows = std::min<int64_t>(chunk, n - r0);
+        const double* src = K + r0 * p;
+        if (!row_major) {  // column-major host matrix (Eigen's default): gather rows
+          rowbuf.resize((size_t)rows * p);
+          for (int64_t i = 0; i < rows; ++i)
+            for (int64_t j = 0; j < p; ++j) rowbuf[(size_t)(i * p + j)] = K[j * n + r0 + i];
+          src = rowbuf.data();
+        }
+        L1G_CUDA(cudaMemcpyAsync(tmp, src, (size_t)rows * p * 8, cudaMemcpyHostToDevice, c->stream));
+        tile_rows_from_rowmajor(op->K, pl, tmp, r0, pad_to(rows, TR), c->stream);
+        L1G_CUDA(cudaStreamSynchronize(c->stream));
+      }
+      dfree(tmp);
+    } catch (...) {
+      l1g_op_destroy(op);
+      throw;
+    }
+    *out = op;
+  });
+}
+
+int l1g_op_generate_gaussian(l1g_ctx* c, int64_t n, int64_t p, uint64_t seed, int64_t col_offset,
+                             int64_t p_total, l1g_op** out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (p_total <= 0) p_total = p;
+    if (col_offset < 0 || col_offset + p > p_total)
+      throw InvalidArgument("generate_gaussian: column range outside the matrix");
+    l1g_op* op = op_alloc(c, n, p);
+    generate_gaussian(op->K, op->plan, seed, col_offset, p_total, c->stream);
+    L1G_CUDA(cudaStreamSynchronize(c->stream));
+    *out = op;
+  });
+}
+
+int l1g_op_generate_blur(l1g_ctx* c, int64_t n, const double* taps, int radius, l1g_op** out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (radius < 0) throw InvalidArgument("generate_blur: radius must be >= 0");
+    l1g_op* op = op_alloc(c, n, n);
+    double* t = dalloc<double>(2 * radius + 1);
+    L1G_CUDA(cudaMemcpy(t, taps, (2 * radius + 1) * sizeof(double), cudaMemcpyHostToDevice));
+    generate_blur(op->K, op->plan, t, radius, c->stream);
+    L1G_CUDA(cudaStreamSynchronize(c->stream));
+    dfree(t);
+    *out = op;
+  });
+}
+
+int l1g_op_scale(l1g_op* op, double cfac) {
+  return guarded([&] {
+    set_device(op->c);
+    scale(op->K, op->plan.n_pad * op->plan.p_pad, cfac, op->c->stream);
+    L1G_CUDA(cudaStreamSynchronize(op->c->stream));
+  });
+}
+
+int l1g_op_dims(const l1g_op* op, int64_t* n, int64_t* p) {
+  if (!op) return L1G_EINVAL;
+  *n = op->plan.n;
+  *p = op->plan.p;
+  return L1G_OK;
+}
+
+int l1g_op_download(l1g_op* op, double* K) {
+  return guarded([&] {
+    set_device(op->c);
+    const GemvPlan& pl = op->plan;
+    int64_t chunk = std::max<int64_t>(1, (int64_t)(128 << 20) / (pl.p * 8));
+    chunk = std::min<int64_t>(chunk, pl.n);
+    double* tmp = dalloc<double>((size_t)chunk * pl.p);
+    for (int64_t r0 = 0; r0 < pl.n; r0 += chunk) {
+      const int64_t rows = std::min<int64_t>(chunk, pl.n - r0);
+      untile_rows(op->K, pl, tmp, r0, rows, op->c->stream);
+      L1G_CUDA(cudaMemcpyAsync(K + r0 * pl.p, tmp, rows * pl.p * 8, cudaMemcpyDeviceToHost,
+                               op->c->stream));
+      L1G_CUDA(cudaStreamSynchronize(op->c->stream));
+    }
+    dfree(tmp);
+  });
+}
+
+void l1g_op_destroy(l1g_op* op) {
+  if (!op) return;
+  cudaSetDevice(op->c->device);
+  if (op->cached) solver_free(op->cached);
+  dfree(op->K);
+  free_ws(op->ws);
+  dfree(op->vin);
+  dfree(op->vout);
+  dfree(op->vtmp);
+  dfree(op->scal);
+  delete op;
+}
+
+int l1g_op_apply_dev(l1g_op* op, const double* x, double* out, void* stream) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(op->mu);
+    set_device(op->c);
+    const cudaStream_t s = stream ? (cudaStream_t)stream : op->c->stream;
+    const GemvPlan& pl = op->plan;
+    L1G_CUDA(cudaMemsetAsync(op->vin, 0, pl.p_pad * 8, s));
+    L1G_CUDA(cudaMemcpyAsync(op->vin, x, pl.p * 8, cudaMemcpyDeviceToDevice, s));
+    launch_fwd(*op, op->ws, FWD_APPLY, op->vin, op->vout, nullptr, nullptr, s);
+    L1G_CUDA(cudaMemcpyAsync(out, op->vout, pl.n * 8, cudaMemcpyDeviceToDevice, s));
+  });
+}
+
+int l1g_op_apply_adjoint_dev(l1g_op* op, const double* r, double* out, void* stream) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(op->mu);
+    set_device(op->c);
+    const cudaStream_t s = stream ? (cudaStream_t)stream : op->c->stream;
+    const GemvPlan& pl = op->plan;
+    L1G_CUDA(cudaMemsetAsync(op->vin, 0, pl.n_pad * 8, s));
+    L1G_CUDA(cudaMemcpyAsync(op->vin, r, pl.n * 8, cudaMemcpyDeviceToDevice, s));
+    launch_adj(*op, op->ws, ADJ_APPLY, op->vin, op->vout, nullptr, nullptr, s);
+    L1G_CUDA(cudaMemcpyAsync(out, op->vout, pl.p * 8, cudaMemcpyDeviceToDevice, s));
+  });
+}
+
+int l1g_op_apply(l1g_op* op, const double* x, double* out) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(op->mu);
+    set_device(op->c);
+    const cudaStream_t s = op->c->stream;
+    const GemvPlan& pl = op->plan;
+    L1G_CUDA(cudaMemsetAsync(op->vin, 0, pl.p_pad * 8, s));
+    L1G_CUDA(cudaMemcpyAsync(op->vin, x, pl.p * 8, cudaMemcpyHostToDevice, s));
+    launch_fwd(*op, op->ws, FWD_APPLY, op->vin, op->vout, nullptr, nullptr, s);
+    L1G_CUDA(cudaMemcpyAsync(out, op->vout, pl.n * 8, cudaMemcpyDeviceToHost, s));
+    L1G_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int l1g_op_apply_adjoint(l1g_op* op, const double* r, double* out) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(op->mu);
+    set_device(op->c);
+    const cudaStream_t s = op->c->stream;
+    const GemvPlan& pl = op->plan;
+    L1G_CUDA(cudaMemsetAsync(op->vin, 0, pl.n_pad * 8, s));
+    L1G_CUDA(cudaMemcpyAsync(op->vin, r, pl.n * 8, cudaMemcpyHostToDevice, s));
+    launch_adj(*op, op->ws, ADJ_APPLY, op->vin, op->vout, nullptr, nullptr, s);
+    L1G_CUDA(cudaMemcpyAsync(out, op->vout, pl.p * 8, cudaMemcpyDeviceToHost, s));
+    L1G_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// linear_operator.cpp:43-60
+int l1g_op_spectral_norm(l1g_op* op, int max_iters, double tol, double* sigma, int64_t* matvecs) {
+  return guarded([&] {
+    if (max_iters < 1) throw InvalidArgument("spectral_norm_estimate: max_iters must be >= 1");
+    std::lock_guard<std::mutex> lk(op->mu);
+    set_device(op->c);
+    const cudaStream_t s = op->c->stream;
+    const GemvPlan& pl = op->plan;
+    double* v = op->vin;
+    double* kv = op->vout;
+    double* w = op->vtmp;
+    fill(v, pl.p_pad, pl.p, 1.0 / std::sqrt((double)pl.p), s);
+    double sig = 0.0;
+    int64_t mv = 0;
+    for (int it = 0; it < max_iters; ++it) {
+      launch_fwd(*op, op->ws, FWD_APPLY, v, kv, nullptr, nullptr, s);
+      ++mv;
+      reduce(kv, nullptr, pl.n_pad, RED_SQ, op->scal, 1, s);
+      double sn = 0.0;
+      L1G_CUDA(cudaMemcpyAsync(&sn, op->scal, 8, cudaMemcpyDeviceToHost, s));
+      L1G_CUDA(cudaStreamSynchronize(s));
+      if (sn == 0.0) {
+        sig = 0.0;
+        break;
+      }
+      launch_adj(*op, op->ws, ADJ_APPLY, kv, w, nullptr, nullptr, s);
+      ++mv;
+      reduce(w, nullptr, pl.p_pad, RED_SQ, op->scal + 1, 1, s);
+      div_by(w, v, pl.p_pad, op->scal + 1, s);
+      if (it > 0 && std::fabs(sn - sig) <= tol * sn) {
+        sig = sn;
+        break;
+      }
+      sig = sn;
+    }
+    L1G_CUDA(cudaStreamSynchronize(s));
+    *sigma = sig;
+    if (matvecs) *matvecs = mv;
+  });
+}
+
+int l1g_project_l1(l1g_ctx* c, const double* x, int64_t m, double rho, double* out,
+                   double* theta, int64_t* support) {
+  return guarded([&] {
+    check_rho(rho);
+    if (m < 0) throw InvalidArgument("project_l1_ball: negative length");
+    std::lock_guard<std::mutex> lk(c->mu);
+    set_device(c);
+    c->ensure(m);
+    const int64_t pp_pad = pad_to(m, COL_GROUP);
+    c->upload(c->a, x, m, pp_pad);
+    DevState h = host_state(l1g_gp_config{1e-4, 0.5, 1, 2, 1e-10, 1e10, 0.5}, rho);
+    L1G_CUDA(cudaMemcpyAsync(c->scratch_state, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+    launch_proj(make_proj_plan(pp_pad), PROJ_PLAIN, m, pp_pad, c->a, nullptr, c->o, c->pscr,
+                c->scratch_state, nullptr, c->stream);
+    download(out, c->o, m, c->stream);
+    L1G_CUDA(cudaMemcpyAsync(&h, c->scratch_state, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    L1G_CUDA(cudaStreamSynchronize(c->stream));
+    if (theta) *theta = h.theta;
+    if (support) *support = h.support;
+  });
+}
+
+int l1g_soft_threshold(l1g_ctx* c, const double* x, int64_t m, double t, double* out) {
+  return guarded([&] {
+    if (!(t >= 0.0)) throw InvalidArgument("soft_threshold: threshold must be >= 0");
+    std::lock_guard<std::mutex> lk(c->mu);
+    set_device(c);
+    c->ensure(m);
+    c->upload(c->a, x, m, m);
+    soft_threshold(c->a, c->o, m, t, c->stream);
+    download(out, c->o, m, c->stream);
+    L1G_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int l1g_reduce(l1g_ctx* c, const double* a, const double* b, int64_t m, int op, double* out) {
+  return guarded([&] {
+    if (op < 0 || op > 3) throw InvalidArgument("l1g_reduce: unknown op");
+    std::lock_guard<std::mutex> lk(c->mu);
+    set_device(c);
+    c->ensure(m);
+    c->upload(c->a, a, m, m);
+    if (op == RED_DOT) c->upload(c->b, b, m, m);
+    reduce(c->a, c->b, m, op, c->scratch_d, 0, c->stream);
+    L1G_CUDA(cudaMemcpyAsync(out, c->scratch_d, 8, cudaMemcpyDeviceToHost, c->stream));
+    L1G_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int l1g_config_validate(const l1g_gp_config* cfg) { return guarded([&] { check_cfg(*cfg); }); }
+int l1g_stop_validate(const l1g_stop_rule* s) { return guarded([&] { check_stop(*s); }); }
+
+void l1g_steplength_init(l1g_sl_state* st, const l1g_gp_config* cfg) {
+  std::memset(st, 0, sizeof(*st));
+  st->tau = cfg->tau1;
+  st->hist_len = 0;
+}
+
+// gpss.cpp:59-91: secant dots on the device, then the scalar rule on the device
+int l1g_steplength_select(l1g_ctx* c, l1g_sl_state* sl, const double* s, const double* z,
+                          int64_t m, const l1g_gp_config* cfg, int64_t k, l1g_sl_choice* out) {
+  return guarded([&] {
+    if (k < 1) throw InvalidArgument("steplength_select: defined for k >= 1");
+    std::lock_guard<std::mutex> lk(c->mu);
+    set_device(c);
+    c->ensure(m);
+    c->upload(c->a, s, m, m);
+    c->upload(c->b, z, m, m);
+    reduce(c->a, c->b, m, RED_DOT, c->scratch_d + 0, 0, c->stream);
+    reduce(c->a, c->a, m, RED_DOT, c->scratch_d + 1, 0, c->stream);
+    reduce(c->b, c->b, m, RED_DOT, c->scratch_d + 2, 0, c->stream);
+    L1G_CUDA(cudaMemcpyAsync(c->sl, sl, sizeof(*sl), cudaMemcpyHostToDevice, c->stream));
+    steplength_device(c->sl, c->scratch_d, *cfg, c->ch, c->stream);
+    L1G_CUDA(cudaMemcpyAsync(sl, c->sl, sizeof(*sl), cudaMemcpyDeviceToHost, c->stream));
+    L1G_CUDA(cudaMemcpyAsync(out, c->ch, sizeof(*out), cudaMemcpyDeviceToHost, c->stream));
+    L1G_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int l1g_backtrack(l1g_ctx* c, double f0, double a, double b, double f_max, double gd,
+                  const l1g_gp_config* cfg, double* step, double* f_new, int32_t* halvings) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(c->mu);
+    set_device(c);
+    const double in[5] = {f0, a, b, f_max, gd};
+    L1G_CUDA(cudaMemcpyAsync(c->scratch_d, in, sizeof(in), cudaMemcpyHostToDevice, c->stream));
+    backtrack_device(c->scratch_d, *cfg, c->scratch_d + 8, c->stream);
+    double o[4];
+    L1G_CUDA(cudaMemcpyAsync(o, c->scratch_d + 8, sizeof(o), cudaMemcpyDeviceToHost, c->stream));
+    L1G_CUDA(cudaStreamSynchronize(c->stream));
+    if (o[3] == 0.0)
+      throw RuntimeFailure(
+          "backtracking_search: no acceptable step after 60 shrink steps; "
+          "the gradient or the search direction is inconsistent");
+    *step = o[0];
+    *f_new = o[1];
+    *halvings = (int32_t)o[2];
+  });
+}
+
+int l1g_alpha0_from_gradient(l1g_ctx* c, double rho, const double* x0, const double* grad,
+                             int64_t m, const l1g_gp_config* cfg, double* alpha0) {
+  return guarded([&] {
+    check_rho(rho);
+    std::lock_guard<std::mutex> lk(c->mu);
+    set_device(c);
+    c->ensure(m);
+    const int64_t pp_pad = pad_to(m, COL_GROUP);
+    c->upload(c->a, x0, m, pp_pad);
+    c->upload(c->b, grad, m, pp_pad);
+    DevState h = host_state(*cfg, rho);
+    L1G_CUDA(cudaMemcpyAsync(c->scratch_state, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+    launch_proj(make_proj_plan(pp_pad), PROJ_ALPHA0, m, pp_pad, c->a, c->b, nullptr, c->pscr,
+                c->scratch_state, nullptr, c->stream);
+    L1G_CUDA(cudaMemcpyAsync(&h, c->scratch_state, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    L1G_CUDA(cudaStreamSynchronize(c->stream));
+    *alpha0 = h.alpha0;
+  });
+}
+
+int l1g_solver_create(l1g_op* op, const double* y, double rho, const l1g_gp_config* cfg,
+                      l1g_solver** out) {
+  return guarded([&] {
+    *out = nullptr;
+    l1g_solver* s = solver_new(op, *cfg, rho);
+    try {
+      if (y) solver_set_y(s, y);
+    } catch (...) {
+      solver_free(s);
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int l1g_solver_set_y(l1g_solver* s, const double* y) {
+  return guarded([&] {
+    set_device(s->op->c);
+    solver_set_y(s, y);
+  });
+}
+
+int l1g_solver_set_y_dev(l1g_solver* s, const double* y_dev) {
+  return guarded([&] {
+    set_device(s->op->c);
+    L1G_CUDA(cudaMemcpyAsync(s->y, y_dev, s->op->plan.n * 8, cudaMemcpyDeviceToDevice, s->stream));
+  });
+}
+
+int l1g_solver_init(l1g_solver* s, const double* x0) {
+  return guarded([&] { solver_init(s, x0); });
+}
+
+int l1g_solver_iterate(l1g_solver* s, double tol, l1g_iter_record* info, int32_t* stationary) {
+  return guarded([&] { solver_iterate(s, tol, info, stationary); });
+}
+
+int l1g_solver_run(l1g_solver* s, const l1g_stop_rule* stop, l1g_result* res,
+                   l1g_iter_record* trace, int64_t cap) {
+  return guarded([&] { solver_run(s, *stop, res, trace, cap); });
+}
+
+int l1g_solver_run_cb(l1g_solver* s, const l1g_stop_rule* stop, l1g_result* res,
+                      l1g_iter_cb cb, void* user) {
+  return guarded([&] { solver_run_cb(s, *stop, res, cb, user); });
+}
+
+int l1g_solver_get(l1g_solver* s, double* x, double* r, double* g, double* f, int64_t* k,
+                   double* alpha0, int64_t* matvecs) {
+  return guarded([&] {
+    set_device(s->op->c);
+    DevState h;
+    read_state(s, &h);
+    const GemvPlan& pl = s->op->plan;
+    download(x, s->vb.x[h.cur], pl.p, s->stream);
+    download(r, s->vb.r[h.cur], pl.n, s->stream);
+    download(g, s->vb.g[h.cur], pl.p, s->stream);
+    L1G_CUDA(cudaStreamSynchronize(s->stream));
+    if (f) *f = h.f;
+    if (k) *k = h.k;
+    if (alpha0) *alpha0 = h.alpha0;
+    if (matvecs) *matvecs = h.matvecs;
+  });
+}
+
+int l1g_solver_x_dev(l1g_solver* s, const double** x_dev) {
+  return guarded([&] {
+    DevState h;
+    read_state(s, &h);
+    *x_dev = s->vb.x[h.cur];
+  });
+}
+
+int l1g_solver_set_timing(l1g_solver* s, int on) {
+  return guarded([&] {
+    set_device(s->op->c);
+    L1G_CUDA(cudaStreamSynchronize(s->stream));
+    if (s->timing != (on != 0)) drop_graphs(s);
+    s->timing = on != 0;
+  });
+}
+
+int l1g_solver_timing(l1g_solver* s, double* proj_ms, double* fwd_ms, double* adj_ms,
+                      int64_t* iterations, int64_t* launches, int reset) {
+  if (proj_ms) *proj_ms = s->t_proj;
+  if (fwd_ms) *fwd_ms = s->t_fwd;
+  if (adj_ms) *adj_ms = s->t_adj;
+  if (iterations) *iterations = s->t_iters;
+  if (launches) *launches = s->launches;
+  if (reset) {
+    s->t_proj = s->t_fwd = s->t_adj = 0.0;
+    s->t_iters = 0;
+    s->launches = 0;
+  }
+  return L1G_OK;
+}
+
+int l1g_solver_stream(l1g_solver* s, void** stream) {
+  *stream = s->stream;
+  return L1G_OK;
+}
+
+void l1g_solver_destroy(l1g_solver* s) { solver_free(s); }
+
+int l1g_gpss_solve(l1g_op* op, const double* y, double rho, const l1g_gp_config* cfg,
+                   const l1g_stop_rule* stop, const double* x0, double* x_out, l1g_result* res,
+                   l1g_iter_record* trace, int64_t cap) {
+  return guarded([&] {
+    check_stop(*stop);  // StopRule::validate precedes gp_init (gpss.cpp:223)
+    check_cfg(*cfg);
+    check_rho(rho);
+    // reuse the operator's cached workspace unless another thread holds it
+    std::unique_lock<std::mutex> lk(op->solver_mu, std::try_to_lock);
+    l1g_solver* s = nullptr;
+    bool temp = false;
+    if (lk.owns_lock()) {
+      if (!op->cached) op->cached = solver_new(op, *cfg, rho);
+      s = op->cached;
+      s->cfg = *cfg;
+      s->rho = rho;
+    } else {
+      s = solver_new(op, *cfg, rho);
+      temp = true;
+    }
+    try {
+      set_device(op->c);
+      solver_set_y(s, y);
+      solver_init(s, x0);
+      solver_run(s, *stop, res, trace, cap);
+      DevState h;
+      read_state(s, &h);
+      download(x_out, s->vb.x[h.cur], op->plan.p, s->stream);
+      L1G_CUDA(cudaStreamSynchronize(s->stream));
+    } catch (...) {
+      if (temp) solver_free(s);
+      throw;
+    }
+    if (temp) solver_free(s);
+  });
+}
+
+int l1g_host_alloc(int64_t bytes, void** ptr) {
+  return guarded([&] { L1G_CUDA(cudaHostAlloc(ptr, (size_t)std::max<int64_t>(bytes, 1), 0)); });
+}
+void l1g_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// engine.h -- internal structures shared by the host runtime and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "../../include/l1g.h"
+
+namespace l1g {
+
+struct CudaError : std::runtime_error {
+  CudaError(cudaError_t e, const char* call, const char* file, int line)
+      : std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " in " + call +
+                           " at " + file + ":" + std::to_string(line)) {}
+};
+struct InvalidArgument : std::invalid_argument {
+  explicit InvalidArgument(const std::string& m) : std::invalid_argument(m) {}
+};
+struct RuntimeFailure : std::runtime_error {
+  explicit RuntimeFailure(const std::string& m) : std::runtime_error(m) {}
+};
+
+constexpr int kMaxHist = 64;
+
+enum Status : int { RUNNING = 0, STOPPED = 1, FAILED = 2 };
+enum Failure : int { FAIL_NONE = 0, FAIL_BACKTRACK = 1 };
+
+// Device-resident scalar state of one GPSS run (GpIterationState + SteplengthState +
+// the gpss_solve loop variables, gpss.hpp:31-36, :89-98; gpss.cpp:226-231).
+struct DevState {
+  // configuration
+  l1g_gp_config cfg;
+  double rho;
+  double stationarity_tol, objective_tol, max_seconds;
+  int64_t max_iterations, max_matvecs;
+  int single_step;  // 1: gp_iterate semantics (no budget checks, no objective_tol)
+  // run control
+  int status, reason, failure, cur;
+  uint64_t t_start;
+  // GP state
+  int64_t k, matvecs;
+  double f, f_prev;
+  double fh[kMaxHist];
+  int fh_len;
+  double tau;
+  double a2h[kMaxHist + 2];
+  int a2_len;
+  double alpha0;
+  int stationary;
+  double out_stationarity;
+  // secant dots of the last step (s = x_k - x_{k-1}, z = g_k - g_{k-1})
+  double sz, ss, zz;
+  // per-iteration values
+  l1g_sl_choice choice;
+  double alpha_used, stat, gd, theta, f_max, step, f_new, a, b;
+  int32_t halvings;
+  int64_t support;
+  l1g_iter_record last;  // record of the last completed (or stationary) iteration
+  // telemetry
+  l1g_iter_record* trace;
+  int64_t trace_cap;
+  // init checks
+  double x0_l1;
+  double h_inf;  // alpha0 projection inf-norm
+};
+
+// GEMV launch plan for one operator
+struct GemvPlan {
+  int64_t n, p, n_pad, p_pad, nrb, ncb;
+  // forward: tasks = row group (128 rows) x column range (fwd_stages * 64 columns)
+  int fwd_stages, nrg, ncr;
+  // adjoint: tasks = column group (256 columns) x row range (adj_blocks * 32 rows)
+  int adj_blocks, ncg, nrr;
+  int grid;
+};
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  // scratch for host-vector entry points
+  double* scratch = nullptr;
+  size_t scratch_len = 0;
+  DevState* scratch_state = nullptr;
+  double* scratch_d = nullptr;  // small device scalars
+};
+
+struct Op {
+  Ctx* ctx = nullptr;
+  GemvPlan plan{};
+  double* K = nullptr;  // tiled
+};
+
+// per-run scratch of the two GEMV kernels (one per solver / per op for generic applies)
+struct Workspace {
+  double* fwd_part = nullptr;    // ncr * n_pad
+  double* adj_part = nullptr;    // nrr * p_pad
+  double* grpsum = nullptr;      // max(nrg*2, ncg*3)
+  unsigned* counters = nullptr;  // [nrg + ncg + 2], zero between launches
+};
+
+// projection plan (cluster of cs CTAs, each holding an aligned slice of ls elements)
+struct ProjPlan {
+  int cs;
+  int64_t ls;
+  int64_t cand_cap;  // candidates sortable in CTA 0 shared memory
+  size_t smem;
+};
+
+enum FwdMode : int { FWD_APPLY = 0, FWD_INIT = 1, FWD_ITER = 2 };
+enum AdjMode : int { ADJ_APPLY = 0, ADJ_INIT = 1, ADJ_ITER = 2 };
+enum ProjMode : int { PROJ_PLAIN = 0, PROJ_ALPHA0 = 1, PROJ_ITER = 2 };
+
+struct VecBufs {
+  double* x[2];
+  double* g[2];
+  double* r[2];
+  double* d;
+  double* kd;
+  const double* y;
+};
+
+// host launchers (gemv.cu, project.cu)
+GemvPlan make_plan(int64_t n, int64_t p, int sm_count);
+void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
+                DevState* st, cudaStream_t s);
+void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
+                DevState* st, cudaStream_t s);
+ProjPlan make_proj_plan(int64_t p_pad);
+void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const double* xin,
+                 const double* gin, double* out, double* scratch, DevState* st,
+                 const VecBufs* vb, cudaStream_t s);
+size_t proj_scratch_doubles(int64_t p_pad);
+
+}  // namespace l1g

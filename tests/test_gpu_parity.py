@@ -1,0 +1,153 @@
+"""Bit-level parity of the B200 path with the CPU oracle on seeded problems.
+
+The oracle (oracle/l1oracle.c) is itself checked bit-for-bit against the reference's own
+sources (tests/test_oracle_ref.py).  With the canonical reduction order the GPU
+must reproduce every iterate, every telemetry field and the stop iteration exactly; values
+are compared with ==, so +0.0 and -0.0 count as equal.
+"""
+import numpy as np
+import pytest
+
+import paper_0902_4424_b200 as l1
+from oracle import oracle as O
+from tests import problems as PB
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ["k", "f", "stationarity", "alpha", "step", "matvecs", "bb_active", "halvings",
+          "bb1_raw", "bb2_raw", "tau_before", "tau_after", "f_max", "dir_derivative", "theta",
+          "support"]
+
+
+def same(a, b):
+    return a == b or (isinstance(a, float) and np.isnan(a) and np.isnan(b))
+
+
+def run_both(spec, iters, memory=1, tol=0.0):
+    P = O.build_problem(spec)
+    xo, ro, reco, _ = O.gpss_solve(P["K"], P["y"], P["rho"], O.GpConfig(memory=memory),
+                                   O.StopRule(iters, 0, 0, tol))
+    op = l1.DenseOperator(P["K"])
+    trace = []
+    sol = l1.gpss_solve(l1.Objective(op, P["y"]), l1.L1Ball(P["rho"]), l1.GpConfig(memory=memory),
+                        l1.StopRule(max_iterations=iters, stationarity_tol=tol), trace=trace)
+    return P, (xo, ro, reco), (sol, trace)
+
+
+@pytest.mark.parametrize("spec,iters,memory", [
+    (PB.TINY, 50, 1), (PB.RAGGED, 200, 5), (PB.C1, 500, 1), (PB.C2_MINI, 300, 1),
+    (PB.C3_MINI, 400, 1), (PB.C4_MINI, 200, 3)], ids=lambda v: getattr(v, "name", str(v)))
+def test_trajectory_bit_identical(spec, iters, memory):
+    P, (xo, ro, reco), (sol, trace) = run_both(spec, iters, memory)
+    assert sol.iterations == ro["iterations"]
+    assert int(sol.reason) == ro["reason"]
+    assert sol.matvecs.count == ro["matvecs"]
+    assert np.array_equal(sol.x, xo), np.abs(sol.x - xo).max()
+    assert sol.objective == ro["objective"]
+    assert list(sol.f_history) == ro["f_history"]
+    assert len(trace) == len(reco)
+    for a, b in zip(trace, reco):
+        for f in FIELDS:
+            assert same(getattr(a, f), b[f]), (b["k"], f, getattr(a, f), b[f])
+
+
+def test_operator_bit_identical():
+    rng = np.random.default_rng(3)
+    for (n, p) in [(1, 1), (5, 8), (77, 301), (256, 1024), (129, 257), (700, 2100)]:
+        K = rng.normal(size=(n, p))
+        op = l1.DenseOperator(K)
+        x, r = rng.normal(size=p), rng.normal(size=n)
+        assert np.array_equal(op.apply(x), O.apply(K, x))
+        assert np.array_equal(op.apply_adjoint(r), O.apply_adjoint(K, r))
+        assert np.array_equal(op.matrix(), K)
+
+
+def test_projection_bit_identical():
+    rng = np.random.default_rng(5)
+    for rep in range(200):
+        p = int(rng.integers(1, 3000))
+        x = rng.normal(size=p) * (10.0 ** rng.uniform(-3, 3))
+        if rep % 7 == 0:
+            x[rng.integers(0, p, size=max(1, p // 3))] = 0.0
+        rho = float(rng.uniform(0.0, 1.2)) * float(np.abs(x).sum())
+        u, th, sup = O.project_l1(x, rho)
+        pr = l1.project_l1_ball_with_threshold(x, l1.L1Ball(rho))
+        assert np.array_equal(pr.point, u) and pr.threshold == th and pr.support == sup
+
+
+@pytest.mark.parametrize("p", [40000, 131072, 262144])
+def test_projection_large(p):
+    """Cluster path (cs > 1) and the global-memory sort for large candidate sets."""
+    rng = np.random.default_rng(p)
+    x = rng.normal(size=p)
+    for frac in (0.9, 0.3, 0.01):
+        rho = frac * float(np.abs(x).sum())
+        u, th, sup = O.project_l1(x, rho)
+        pr = l1.project_l1_ball_with_threshold(x, l1.L1Ball(rho))
+        assert pr.threshold == th and pr.support == sup
+        assert np.array_equal(pr.point, u)
+
+
+def test_generators_bit_identical():
+    K = O.gaussian_matrix(11, 130, 333)
+    op = l1.DenseOperator.generate_gaussian(130, 333, 11)
+    assert np.array_equal(op.matrix(), K)
+    taps = O.blur_taps()
+    opb = l1.DenseOperator.generate_blur(200, taps, O.BLUR_RADIUS)
+    assert np.array_equal(opb.matrix(), O.blur_matrix(200, taps))
+    # column shard of a larger matrix (multi-GPU layout)
+    sh = l1.DenseOperator.generate_gaussian(130, 100, 11, col_offset=200, p_total=333)
+    assert np.array_equal(sh.matrix(), K[:, 200:300])
+
+
+def test_spectral_norm_bit_identical():
+    K = O.gaussian_matrix(21, 150, 420)
+    op = l1.DenseOperator.generate_gaussian(150, 420, 21)
+    mv = l1.MatvecCounter()
+    s = l1.spectral_norm_estimate(op, 1000, 1e-8, mv)
+    so, mvo = O.spectral_norm(K, 1000, 1e-8)
+    assert s == so and mv.count == mvo
+
+
+def test_gp_iterate_steps_match_solve():
+    P = O.build_problem(PB.C2_MINI)
+    st = O.GpState(P["K"], P["y"], P["rho"])
+    obj = l1.Objective(l1.DenseOperator(P["K"]), P["y"])
+    ball, cfg, mv = l1.L1Ball(P["rho"]), l1.GpConfig(), l1.MatvecCounter()
+    gs = l1.gp_init(obj, ball, None, cfg, mv)
+    assert gs.alpha0 == st.get()["alpha0"] and gs.f == st.get()["f"]
+    for _ in range(25):
+        info_o, so = st.iterate(0.0)
+        info_g = l1.gp_iterate(obj, ball, cfg, gs, None, mv, 0.0)
+        assert info_g.stationary == so
+        assert info_g.alpha == info_o["alpha"] and info_g.step == info_o["step"]
+        assert np.array_equal(gs.x, st.get()["x"])
+    assert mv.count == st.get()["matvecs"]
+
+
+def test_callback_path_matches_graph_path():
+    P = O.build_problem(PB.C2_MINI)
+    obj = l1.Objective(l1.DenseOperator(P["K"]), P["y"])
+    ball, cfg = l1.L1Ball(P["rho"]), l1.GpConfig()
+    stop = l1.StopRule(max_iterations=80, stationarity_tol=0.0)
+    recs, xs = [], []
+    a = l1.gpss_solve(obj, ball, cfg, stop, cb=lambda r, x: (recs.append(r), xs.append(x)))
+    t = []
+    b = l1.gpss_solve(obj, ball, cfg, stop, trace=t)
+    assert np.array_equal(a.x, b.x) and a.iterations == b.iterations == len(recs)
+    assert [r.f for r in recs] == [r.f for r in t]
+    assert np.array_equal(xs[-1], a.x)
+
+
+def test_budgets_and_objective_tol():
+    P = O.build_problem(PB.C2_MINI)
+    op = l1.DenseOperator(P["K"])
+    obj, ball, cfg = l1.Objective(op, P["y"]), l1.L1Ball(P["rho"]), l1.GpConfig()
+    for stop in [O.StopRule(0, 41, 0, 0.0), O.StopRule(300, 0, 0, 0.0, 1e-6),
+                 O.StopRule(7, 0, 0, 0.0), O.StopRule(300, 0, 0, 1e-9)]:
+        xo, ro, _, _ = O.gpss_solve(P["K"], P["y"], P["rho"], O.GpConfig(), stop)
+        sol = l1.gpss_solve(obj, ball, cfg, l1.StopRule(stop.max_iterations, stop.max_matvecs,
+                                                        stop.max_seconds, stop.stationarity_tol,
+                                                        stop.objective_tol))
+        assert sol.iterations == ro["iterations"] and int(sol.reason) == ro["reason"]
+        assert sol.matvecs.count == ro["matvecs"] and np.array_equal(sol.x, xo)
