@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the GPSS iteration loop (BASELINE.json metric: projected-gradient
+iterations/s and achieved HBM GB/s of K streamed vs peak).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl b200|reference]
+
+A step is one gpss_solve of the config (C2: 8192x32768, 300 iterations, x0 = 0) with K
+resident in HBM.  K (2 GiB) is larger than L2, so no flush is needed between steps.
+`value` = iterations / device time (CUDA events on the solver stream, max over ranks);
+`e2e` = the same metric through the C-ABI call l1g_gpss_solve with host y and x buffers
+(copies inside the timed region).  Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "projected-gradient iterations/s"
+UNIT = "iterations/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def sigma_fixture(name):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "sigma_hat.json")) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        mx = float(rows[0][2])
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        pg = dist
+    return world, rank, local, pg
+
+
+def max_over_ranks(pg, v):
+    if pg is None:
+        return v
+    import torch
+    dev = "cuda" if pg.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle)
+def ref_time(K, y, rho, iters, threads=None):
+    """Time the reference's own gpss_solve (oracle/_ref fast build: reference sources +
+    Eigen stand-in with OpenMP GEMVs) for `iters` iterations from x0 = 0."""
+    from oracle import oracle as O
+    from oracle import ref as R
+    kind = "fast" if R.available("fast") else None
+    if threads:
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+    if kind is None:
+        t0 = time.perf_counter()
+        _, res, _, _ = O.gpss_solve(K, y, rho, O.GpConfig(), O.StopRule(iters, 0, 0, 0.0),
+                                    trace=False)
+        return time.perf_counter() - t0, res["iterations"], "port", 1
+    op = R.RefOperator(K, kind)
+    t0 = time.perf_counter()
+    _, res, _ = op.gpss_solve(y, rho, O.GpConfig(), O.StopRule(iters, 0, 0, 0.0), trace=False)
+    dt = time.perf_counter() - t0
+    return dt, res["iterations"], "reference", int(os.environ.get("OMP_NUM_THREADS",
+                                                                   os.cpu_count() or 1))
+
+
+def host_problem(spec_name):
+    """C2-shaped problem built on the host with the oracle generators (no GPU code)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    from tests import problems as PB
+    spec = getattr(PB, spec_name)
+    n, p = spec.n, spec.p
+    K = np.empty((n, p))
+    rows = max(1, (1 << 24) // p)
+
+    def fill(r0):
+        r1 = min(n, r0 + rows)
+        seg = K[r0:r1].reshape(-1)
+        seg[:] = O.fill_normal(spec.seed, 0, r0 * p, (r1 - r0) * p)
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        list(ex.map(fill, range(0, n, rows)))
+    sigma = sigma_fixture(spec_name)
+    if sigma is None:  # short power iteration as a stand-in scale (timing only)
+        sigma, _ = O.spectral_norm(K, 8, 1e-8)
+    K *= 0.9 / sigma
+    x_true = np.zeros(p)
+    sup = O.sample_support(spec.seed, 1, p, spec.nnz)
+    x_true[sup] = O.x_true_values(spec, spec.nnz)
+    clean = K @ x_true
+    e = O.fill_normal(spec.seed, 2, 0, n)
+    sig = spec.noise * math.sqrt(float(clean @ clean)) / math.sqrt(n)
+    y = clean + sig * e
+    return K, y, float(np.abs(x_true).sum())
+
+
+def run_reference(args, world, rank, pg):
+    """--impl reference: the reference CPU path on this box's host cores."""
+    if rank != 0:
+        return
+    cfgname = args.config
+    K, y, rho = host_problem(cfgname)
+    from oracle import ref as R
+    n, p = K.shape
+    # bounded sample per step: enough iterations for ~5 s of CPU work
+    dt1, it1, kind, cores = ref_time(K, y, rho, 2)
+    per_step = max(1, min(args.ref_iters or 1000, int(5.0 * max(it1, 1) / max(dt1, 1e-3))))
+    for _ in range(args.warmup):
+        ref_time(K, y, rho, per_step)
+    times, total_it = [], 0
+    for _ in range(args.steps):
+        dt, itn, kind, cores = ref_time(K, y, rho, per_step)
+        times.append(dt)
+        total_it += itn
+    total_t = sum(times)
+    v = total_it / total_t
+    sample = (f"{per_step} GPSS iterations per step of {cfgname} ({n}x{p}) from x0=0, "
+              f"reference gpss.cpp/prox.cpp/linear_operator.cpp via oracle/_ref "
+              f"({'OpenMP Eigen stand-in' if kind == 'reference' else 'C port'})")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Philox Gaussian, oracle generator on the host)",
+            "config": {"workload": cfgname, "n": n, "p": p, "iterations_per_step": per_step},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gbs_K": v * 2 * n * p * 8 / 1e9}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(args, world, rank, local, pg):
+    import ctypes as C
+
+    import paper_0902_4424_b200 as l1
+    from paper_0902_4424_b200 import _lib as L
+    from paper_0902_4424_b200 import harness as H
+
+    import torch
+    torch.cuda.set_device(local)
+    ctx = l1.Context(local)
+    spec = H.CONFIGS[args.config]
+    iters = args.iters or H.ITERATIONS[args.config]
+    fix = sigma_fixture(args.config)
+    t_setup = time.perf_counter()
+    if fix is not None and not args.recompute_sigma:
+        spec.sigma_hat = fix
+    P = H.build_problem(spec, ctx)
+    op, y, rho = P["op"], P["y"], P["rho"]
+    n, p = spec.n, spec.p
+    setup_s = time.perf_counter() - t_setup
+    lib = L.load()
+    cfg = l1.GpConfig()._c()
+    stop = l1.StopRule(max_iterations=iters, stationarity_tol=0.0)._c()
+
+    # ---- device-resident solver (inputs already in HBM)
+    h = C.c_void_p()
+    L.check(lib.l1g_solver_create(op.h, L.ptr(np.ascontiguousarray(y)), rho, C.byref(cfg),
+                                  C.byref(h)), "solver_create")
+    L.check(lib.l1g_solver_set_timing(h, 1))
+    sp = C.c_void_p()
+    lib.l1g_solver_stream(h, C.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value)
+    res = L.ResultC()
+
+    def solve_once():
+        L.check(lib.l1g_solver_init(h, None), "init")
+        L.check(lib.l1g_solver_run(h, C.byref(stop), C.byref(res), None, 0), "run")
+        return res.iterations
+
+    for _ in range(args.warmup):
+        solve_once()
+    lib.l1g_solver_timing(h, None, None, None, None, None, 1)
+    barrier(pg)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    done_iters = 0
+    with clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            done_iters += solve_once()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+    barrier(pg)
+    dev_ms = e0.elapsed_time(e1)
+    dev_ms = max_over_ranks(pg, dev_ms)
+    tp, tf, ta = C.c_double(), C.c_double(), C.c_double()
+    ti, tl = C.c_int64(), C.c_int64()
+    lib.l1g_solver_timing(h, C.byref(tp), C.byref(tf), C.byref(ta), C.byref(ti), C.byref(tl), 1)
+    value = world * done_iters / (dev_ms / 1e3)  # whole-job iterations/s (replicas)
+    reason = L.REASONS[res.reason]
+
+    # ---- end to end through the C-ABI with host buffers (pinned)
+    yp, xp = C.c_void_p(), C.c_void_p()
+    L.check(lib.l1g_host_alloc(n * 8, C.byref(yp)))
+    L.check(lib.l1g_host_alloc(p * 8, C.byref(xp)))
+    np.ctypeslib.as_array((C.c_double * n).from_address(yp.value))[:] = y
+    res2 = L.ResultC()
+
+    def e2e_once():
+        L.check(lib.l1g_gpss_solve(op.h, yp, rho, C.byref(cfg), C.byref(stop), None, xp,
+                                   C.byref(res2), None, 0), "gpss_solve")
+        return res2.iterations
+
+    for _ in range(max(1, args.warmup)):
+        e2e_once()
+    barrier(pg)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_iters = 0
+    for _ in range(args.steps):
+        e2e_iters += e2e_once()
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(pg, time.perf_counter() - t0)
+    e2e_value = world * e2e_iters / e2e_s
+    x_e2e = np.ctypeslib.as_array((C.c_double * p).from_address(xp.value)).copy()
+    x_dev = np.empty(p)
+    L.check(lib.l1g_solver_get(h, L.ptr(x_dev), None, None, None, None, None, None))
+    lib.l1g_host_free(yp)
+    lib.l1g_host_free(xp)
+
+    # ---- roofline of the dominant kernel (per-launch CUDA events inside the timed loop)
+    hbm, peak_src = peaks()
+    k_bytes = n * p * 8.0
+    it = max(ti.value, 1)
+    avg = {"proj": tp.value / it, "fwd": tf.value / it, "adj": ta.value / it}
+    dom = "adj" if avg["adj"] >= avg["fwd"] else "fwd"
+    achieved = k_bytes / (avg[dom] / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(f"{args.config}_{dom}")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": {"adj": "adj_kernel (2 K^T r)",
+                                           "fwd": "fwd_kernel (K d)"}[dom],
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "peak_source": peak_src, "traffic": traffic,
+                "algorithmic_bytes_per_launch": k_bytes,
+                "avg_launch_ms": {k: round(v, 5) for k, v in avg.items()},
+                "share_of_iteration": {k: round(v / sum(avg.values()), 4)
+                                       for k, v in avg.items()},
+                "iteration_GBps_2npx8": 2 * k_bytes * done_iters / (dev_ms / 1e3) / 1e9 / world}
+
+    # ---- CPU baseline on rank 0 at N=1 (bounded sample of the same workload)
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline and args.config in ("C1", "C2",
+                                                                                   "C3"):
+        try:
+            K = op.matrix()  # the same bits the oracle generator produces (tests pin this)
+            it_cpu = 2 if n * p > 1e8 else 20
+            dt, itn, kind, cores = ref_time(K, y, rho, it_cpu)
+            per = max(1, min(400, int(12.0 * max(itn, 1) / max(dt, 1e-4))))
+            dt, itn, kind, cores = ref_time(K, y, rho, per)
+            cpu = {"value": itn / dt, "unit": UNIT, "cores": cores, "kind": kind,
+                   "sample": f"{itn} GPSS iterations (incl. gp_init) of {args.config} from x0=0 "
+                             f"({'reference sources, OpenMP Eigen stand-in' if kind == 'reference' else 'C port, 1 thread'})"}
+            del K
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded Philox Gaussian K scaled to ||K||_2=0.9, generated "
+                        "on device; BASELINE.json configs[1])",
+                "config": {"workload": f"{args.config}: {spec.kind} {n}x{p}, nnz {spec.nnz}, "
+                                       f"{iters} iterations, x0=0, stationarity_tol=0",
+                           "n": n, "p": p, "iterations_per_step": done_iters / args.steps,
+                           "stop_reason": reason, "rho": rho, "sigma_hat": P["sigma_hat"],
+                           "l2": "inputs larger than L2 (K = %.2f GiB)" % (k_bytes / 2**30),
+                           "parallelism": "replicas" if world > 1 else "single",
+                           "setup_s": round(setup_s, 3)},
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 8,
+                        "d2h_bytes_per_step": p * 8 + C.sizeof(L.ResultC),
+                        "x_matches_device_run": bool(np.array_equal(x_e2e, x_dev))},
+                "gpu_launches": int(tl.value),
+                "roofline": roofline,
+                "cpu_baseline": cpu,
+                "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    lib.l1g_solver_destroy(h)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--iters", type=int, default=0)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--recompute-sigma", action="store_true")
+    ap.add_argument("--ref-iters", type=int, default=0)
+    args = ap.parse_args()
+    world, rank, local, pg = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank, pg)
+    else:
+        run_b200(args, world, rank, local, pg)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -162,6 +162,9 @@ int l1g_solver_stream(l1g_solver* s, void** stream);
 /* per-kernel CUDA-event timing of the device loop (projection / forward / adjoint), summed
  * over completed iterations, and the number of kernels this solver launched */
 int l1g_solver_set_timing(l1g_solver* s, int on);
+/* projection phase profile accumulated since gp_init: [0..7] SM cycles per phase,
+ * [8] calls, [9] attempts, [10] pivot rounds, [11] candidates, [12] bumps, [13] retries */
+int l1g_solver_proj_profile(l1g_solver* s, double* out16);
 int l1g_solver_timing(l1g_solver* s, double* proj_ms, double* fwd_ms, double* adj_ms,
                       int64_t* iterations, int64_t* launches, int reset);
 void l1g_solver_destroy(l1g_solver* s);
@@ -170,6 +173,11 @@ void l1g_solver_destroy(l1g_solver* s);
 int l1g_gpss_solve(l1g_op* op, const double* y, double rho, const l1g_gp_config* cfg,
                    const l1g_stop_rule* stop, const double* x0, double* x_out, l1g_result* res,
                    l1g_iter_record* trace, int64_t trace_cap);
+
+/* harness random streams: kind 0 = standard normal #index, 1 = uniform [0,1) #index of the
+ * Philox stream (seed, stream) -- bit-identical to oracle orc_normal / orc_uniform */
+int l1g_rng_fill(l1g_ctx* ctx, int kind, uint64_t seed, uint32_t stream, uint64_t first,
+                 int64_t count, double* out);
 
 /* pinned host buffers for the end-to-end path */
 int l1g_host_alloc(int64_t bytes, void** ptr);

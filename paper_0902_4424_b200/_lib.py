@@ -108,10 +108,12 @@ _SIGS = {
     "l1g_solver_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "l1g_solver_destroy": (None, [_vp]),
     "l1g_solver_set_timing": (C.c_int, [_vp, C.c_int]),
+    "l1g_solver_proj_profile": (C.c_int, [_vp, _dp]),
     "l1g_solver_timing": (C.c_int, [_vp, _dp, _dp, _dp, C.POINTER(_i64), C.POINTER(_i64),
                                     C.c_int]),
     "l1g_gpss_solve": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(GpConfigC),
                                  C.POINTER(StopRuleC), _vp, _vp, C.POINTER(ResultC), _vp, _i64]),
+    "l1g_rng_fill": (C.c_int, [_vp, C.c_int, C.c_uint64, C.c_uint32, C.c_uint64, _i64, _vp]),
     "l1g_host_alloc": (C.c_int, [_i64, C.POINTER(_vp)]),
     "l1g_host_free": (None, [_vp]),
 }

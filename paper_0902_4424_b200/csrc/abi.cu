@@ -274,7 +274,7 @@ void solver_init(l1g_solver* s, const double* x0_host) {
   launch_adj(*s->op, s->ws, ADJ_INIT, nullptr, nullptr, &s->vb, s->st, s->stream);
   launch_proj(s->pp, PROJ_ALPHA0, pl.p, pl.p_pad, s->vb.x[0], s->vb.g[0], nullptr, s->pscr, s->st,
               &s->vb, s->stream);
-  s->launches += x0_host ? 5 : 4;
+  s->launches += x0_host ? 7 : 6;
   s->inited = true;
 }
 
@@ -318,14 +318,14 @@ void build_graphs(l1g_solver* s) {
     L1G_CUDA(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < s->gsize; ++i) {
       if (s->timing) {
-        L1G_CUDA(cudaEventRecord(tev(s, gi, i, 0), s->stream));
+        L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 0), s->stream, cudaEventRecordExternal));
         launch_proj(s->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, s->pscr, s->st,
                     &s->vb, s->stream);
-        L1G_CUDA(cudaEventRecord(tev(s, gi, i, 1), s->stream));
+        L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 1), s->stream, cudaEventRecordExternal));
         launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
-        L1G_CUDA(cudaEventRecord(tev(s, gi, i, 2), s->stream));
+        L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 2), s->stream, cudaEventRecordExternal));
         launch_adj(*s->op, s->ws, ADJ_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
-        L1G_CUDA(cudaEventRecord(tev(s, gi, i, 3), s->stream));
+        L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 3), s->stream, cudaEventRecordExternal));
       } else {
         enqueue_iteration(s);
       }
@@ -407,7 +407,7 @@ void solver_run(l1g_solver* s, const l1g_stop_rule& stop, l1g_result* res,
   while (!done) {
     const int slot = (int)(launched & 1);
     L1G_CUDA(cudaGraphLaunch(s->gexec[slot], s->stream));
-    s->launches += 3LL * s->gsize;
+    s->launches += 5LL * s->gsize;
     L1G_CUDA(cudaMemcpyAsync((void*)(flag + 16 * slot), &s->st->status, sizeof(int),
                              cudaMemcpyDeviceToHost, s->stream));
     L1G_CUDA(cudaMemcpyAsync((void*)(flag + 16 * slot + 2), &s->st->k, sizeof(int64_t),
@@ -460,7 +460,7 @@ void solver_run_cb(l1g_solver* s, const l1g_stop_rule& stop, l1g_result* res, l1
   int64_t k_prev = 0;
   for (;;) {
     enqueue_iteration(s);
-    s->launches += 3;
+    s->launches += 5;
     DevState h;
     read_state(s, &h);
     if (h.k > k_prev) {
@@ -482,7 +482,7 @@ void solver_iterate(l1g_solver* s, double tol, l1g_iter_record* info, int32_t* s
   st.stationarity_tol = tol;
   configure(s, st, 1, nullptr, 0);
   enqueue_iteration(s);
-  s->launches += 4;
+  s->launches += 6;
   DevState h;
   read_state(s, &h);
   *stationary = h.stationary;
@@ -999,6 +999,14 @@ int l1g_solver_timing(l1g_solver* s, double* proj_ms, double* fwd_ms, double* ad
   return L1G_OK;
 }
 
+int l1g_solver_proj_profile(l1g_solver* s, double* out16) {
+  return guarded([&] {
+    DevState h;
+    read_state(s, &h);
+    std::memcpy(out16, h.prof, sizeof(h.prof));
+  });
+}
+
 int l1g_solver_stream(l1g_solver* s, void** stream) {
   *stream = s->stream;
   return L1G_OK;
@@ -1040,6 +1048,19 @@ int l1g_gpss_solve(l1g_op* op, const double* y, double rho, const l1g_gp_config*
       throw;
     }
     if (temp) solver_free(s);
+  });
+}
+
+int l1g_rng_fill(l1g_ctx* c, int kind, uint64_t seed, uint32_t stream, uint64_t first,
+                 int64_t count, double* out) {
+  return guarded([&] {
+    if (kind < 0 || kind > 1 || count < 0) throw InvalidArgument("l1g_rng_fill: bad arguments");
+    std::lock_guard<std::mutex> lk(c->mu);
+    set_device(c);
+    c->ensure(count);
+    rng_fill(kind, seed, stream, first, count, c->o, c->stream);
+    download(out, c->o, count, c->stream);
+    L1G_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

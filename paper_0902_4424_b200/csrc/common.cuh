@@ -60,15 +60,21 @@ __device__ __forceinline__ double tree(const F& leaf, int base = 0) {
 template <int L>
 struct Counter {
   double lvl[L];
+  __device__ __forceinline__ Counter() {
+#pragma unroll
+    for (int l = 0; l < L; ++l) lvl[l] = 0.0;
+  }
+  // branch-free carry chain so lvl[] stays in registers
   __device__ __forceinline__ void push(double v, uint32_t idx) {
+    bool open = true;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      if ((idx >> l) & 1u) {
-        v = add(lvl[l], v);
-      } else {
-        lvl[l] = v;
-        return;
-      }
+      const bool bit = (idx >> l) & 1u;
+      const double merged = add(lvl[l], v);
+      const bool store = open && !bit;
+      lvl[l] = store ? v : lvl[l];
+      v = (open && bit) ? merged : v;
+      open = open && bit;
     }
   }
   __device__ __forceinline__ double final_value(uint32_t count) const {

@@ -64,6 +64,8 @@ struct DevState {
   // init checks
   double x0_l1;
   double h_inf;  // alpha0 projection inf-norm
+  // projection phase profile (SM cycles of CTA 0 / event counts), see project.cu
+  double prof[16];
 };
 
 // GEMV launch plan for one operator

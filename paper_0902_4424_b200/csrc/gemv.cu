@@ -3,29 +3,33 @@
 // Replaces DenseOperator::do_apply / do_apply_adjoint (linear_operator.hpp:45-48) on the
 // GPSS hot path (gpss.cpp:194-196 and :206-211).  Both kernels are persistent (one CTA per
 // SM) and warp specialised: warp 0 streams 32x64 K tiles into a 3-stage shared-memory ring
-// with cp.async.bulk (TMA engine) + mbarriers; warps 1-4 reduce them.  Every output is the
-// canonical pairwise sum of rounded products (common.cuh), evaluated as
-//   per-lane 32/64-leaf trees inside a tile -> a binary counter over the tiles of a task ->
-//   a tree over task partials, done by the CTA that completes a group last.
+// with cp.async.bulk (TMA engine) + mbarriers; 4*SPLIT consumer warps reduce them, SPLIT
+// warps per tile (lane groups own a slice of the tile, a shuffle joins the slices).  Every
+// output is the canonical pairwise sum of rounded products (common.cuh), evaluated as
+//   per-lane trees inside a tile -> shuffle join -> a binary counter over the tiles of a
+//   task -> a tree over task partials, done by the CTA that completes a group last.
 // The same completing CTA runs the fused epilogue:
 //   forward/ITER : a = (Kx - y)'Kd, b = ||Kd||^2, then the backtracking line search;
 //   forward/INIT : r = Kx0 - y, f = ||r||^2;
 //   adjoint/ITER : r += lambda Kd (prologue), g' = 2 K^T r, x' = x + lambda d,
 //                  s'z, s's, z'z for the next BB step, telemetry, stop tests.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "engine.h"
 #include "scalar.cuh"
 
 namespace l1g {
 
-constexpr int NCONS = 4;                 // consumer warps
-constexpr int NTHREADS = 32 * (NCONS + 1);
 constexpr int STAGES = 3;
-constexpr int FWD_STAGE_DBL = 4 * TILE + 64;   // 4 tiles + the matching 64-entry slice of d
-constexpr int ADJ_STAGE_DBL = 4 * TILE;
-constexpr int FWD_MAX_STAGES = 128;      // column blocks per forward task (counter depth 8)
-constexpr int ADJ_MAX_BLOCKS = 32;       // row blocks per adjoint task (counter depth 6)
+constexpr int TILES_PER_STAGE = 4;
+constexpr int DPAD = 16;  // padding of the d slice (doubles), covers d_pos<4>(31)
+constexpr int FWD_STAGE_DBL = TILES_PER_STAGE * TILE + 64 + DPAD;
+constexpr int ADJ_STAGE_DBL = TILES_PER_STAGE * TILE;
+constexpr int FWD_MAX_STAGES = 128;  // column blocks per forward task (counter depth 8)
+constexpr int ADJ_MAX_BLOCKS = 16;   // row blocks per adjoint task (counter depth 6)
 constexpr int MAX_TR = ADJ_MAX_BLOCKS * TR;
+constexpr int RS_PAD = MAX_TR / 8;   // padding of the shared r slice (see rs_pos)
 
 struct FwdArgs {
   const double* K;
@@ -81,16 +85,50 @@ __device__ __forceinline__ double warp_tree_array(const double* v, int count, in
   return acc.final_value(chunks);
 }
 
-// ============================================================================ forward
-__device__ __noinline__ void fwd_finish(const FwdArgs& a, int rg, int ct, int cw, int lane,
-                                        double (*wsum)[3], int* s_flag) {
-  const int64_t row = (int64_t)rg * ROW_GROUP + ct;
+// position of d unit u (16-byte pair) in the padded per-stage slice: the SPLIT lane groups
+// read units u, u + 32/SPLIT, ... at once, which must fall in distinct bank groups
+template <int SPLIT>
+__device__ __forceinline__ int d_pos(int u) {
+  if constexpr (SPLIT == 1) return u;
+  else if constexpr (SPLIT == 2) return u + 4 * (u >> 4);
+  else return u + 2 * (u >> 3);
+}
+// position of r[i] in the padded shared r slice (same idea for 8-byte words)
+__device__ __forceinline__ int rs_pos(int i) { return i + (i >> 3); }
+
+// ============================================================================ finish kernels
+// One CTA of 128 threads per group: thread t <-> row (forward) or column pair (adjoint).
+// Tree over the task partials -> fused epilogue -> block tree (4 warp subtrees, joined as
+// ((w0 + w1) + (w2 + w3))) -> the group's subtree; the CTA that counts last joins the
+// groups and runs the scalar part of gp_iterate.
+constexpr int FIN_T = 128;
+
+template <int N>
+__device__ __forceinline__ double block4(double v, double (*ws)[3], int c) {
+  v = warp_tree(v);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5][c] = v;
+  return v;
+}
+
+__global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
+  if (a.mode != FWD_APPLY && a.st->status != RUNNING) return;
+  __shared__ double ws[4][3];
+  __shared__ unsigned s_last;
+  const int rg = blockIdx.x;
+  const int64_t row = (int64_t)rg * ROW_GROUP + threadIdx.x;
   Counter<20> acc;
-  for (int cr = 0; cr < a.ncr; ++cr) acc.push(__ldcg(a.part + (int64_t)cr * a.n_pad + row), cr);
+  int cr = 0;
+  for (; cr + 8 <= a.ncr; cr += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcg(a.part + (int64_t)(cr + u) * a.n_pad + row);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc.push(v[u], cr + u);
+  }
+  for (; cr < a.ncr; ++cr) acc.push(__ldcg(a.part + (int64_t)cr * a.n_pad + row), cr);
   const double kd = acc.final_value(a.ncr);
   if (a.mode == FWD_APPLY) {
     a.vout[row] = kd;
-    if (ct == 0) a.cnt_grp[rg] = 0;
     return;
   }
   const int cur = a.st->cur;
@@ -104,25 +142,19 @@ __device__ __noinline__ void fwd_finish(const FwdArgs& a, int rg, int ct, int cw
     l0 = mul(a.vb.r[cur][row], kd);         // (Kx-y)'Kd (gpss.cpp:195)
     l1 = mul(kd, kd);                       // ||Kd||^2  (gpss.cpp:196)
   }
-  l0 = warp_tree(l0);
-  l1 = warp_tree(l1);
-  if (lane == 0) {
-    wsum[cw][0] = l0;
-    wsum[cw][1] = l1;
-  }
-  named_bar_sync(1, 32 * NCONS);
-  if (ct == 0) {
-    a.grpsum[2 * rg + 0] = add(add(wsum[0][0], wsum[1][0]), add(wsum[2][0], wsum[3][0]));
-    a.grpsum[2 * rg + 1] = add(add(wsum[0][1], wsum[1][1]), add(wsum[2][1], wsum[3][1]));
-    a.cnt_grp[rg] = 0;
+  block4<0>(l0, ws, 0);
+  block4<0>(l1, ws, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a.grpsum[2 * rg + 0] = add(add(ws[0][0], ws[1][0]), add(ws[2][0], ws[3][0]));
+    a.grpsum[2 * rg + 1] = add(add(ws[0][1], ws[1][1]), add(ws[2][1], ws[3][1]));
     __threadfence();
-    const unsigned old = atomicAdd(a.cnt_all, 1u);
-    *s_flag = (old == (unsigned)a.nrg - 1u);
+    s_last = atomicAdd(a.cnt_all, 1u) == (unsigned)a.nrg - 1u;
   }
-  named_bar_sync(1, 32 * NCONS);
-  if (!*s_flag) return;
+  __syncthreads();
+  if (!s_last || threadIdx.x >= 32) return;
   __threadfence();
-  if (cw != 0) return;
+  const int lane = threadIdx.x;
   const double A = warp_tree_array(a.grpsum + 0, a.nrg, 2, lane);
   const double B = warp_tree_array(a.grpsum + 1, a.nrg, 2, lane);
   if (lane != 0) return;
@@ -153,101 +185,27 @@ __device__ __noinline__ void fwd_finish(const FwdArgs& a, int rg, int ct, int cw
   }
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) fwd_kernel(const FwdArgs a) {
-  if (a.mode != FWD_APPLY && a.st->status != RUNNING) return;
-  extern __shared__ __align__(128) unsigned char smem[];
-  double* sbase = reinterpret_cast<double*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * FWD_STAGE_DBL * 8);
-  uint64_t* empty = full + STAGES;
-  __shared__ double wsum[NCONS][3];
-  __shared__ int s_last, s_flag;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCONS);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  const int ntasks = a.nrg * a.ncr;
-  if (warp == 0) {  // ---- producer: one elected lane issues every bulk copy
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
-        const int rg = t / a.ncr, cr = t - rg * a.ncr;
-        const int64_t cb0 = (int64_t)cr * a.stages;
-        const int nst = (int)(a.ncb - cb0 < (int64_t)a.stages ? a.ncb - cb0 : (int64_t)a.stages);
-        for (int s = 0; s < nst; ++s) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          double* dst = sbase + (size_t)stage * FWD_STAGE_DBL;
-          mbar_arrive_expect_tx(&full[stage], 4 * TILE_BYTES + 512);
-#pragma unroll
-          for (int w = 0; w < 4; ++w)
-            bulk_g2s(dst + w * TILE, a.K + tile_offset(4 * rg + w, cb0 + s, a.ncb), TILE_BYTES,
-                     &full[stage]);
-          bulk_g2s(dst + 4 * TILE, a.vin + (cb0 + s) * TC, 512, &full[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1u;
-          }
-        }
-      }
-    }
-    return;
-  }
-  // ---- consumers: warp cw owns row block 4*rg + cw, lane = row inside the block
-  const int cw = warp - 1, ct = threadIdx.x - 32;
-  const int sw = lane & 7;
-  int stage = 0;
-  uint32_t phase = 0;
-  for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
-    const int rg = t / a.ncr, cr = t - rg * a.ncr;
-    const int64_t cb0 = (int64_t)cr * a.stages;
-    const int nst = (int)(a.ncb - cb0 < (int64_t)a.stages ? a.ncb - cb0 : (int64_t)a.stages);
-    Counter<8> acc;
-    for (int s = 0; s < nst; ++s) {
-      mbar_wait(&full[stage], phase);
-      const double* sb = sbase + (size_t)stage * FWD_STAGE_DBL;
-      const double2* ku = reinterpret_cast<const double2*>(sb + cw * TILE) + lane * 32;
-      const double2* du = reinterpret_cast<const double2*>(sb + 4 * TILE);
-      const double v = tree<32>([&](int q) {
-        const double2 k = ku[q ^ sw];
-        const double2 d = du[q];
-        return add(mul(k.x, d.x), mul(k.y, d.y));
-      });
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      acc.push(v, (uint32_t)s);
-      if (++stage == STAGES) {
-        stage = 0;
-        phase ^= 1u;
-      }
-    }
-    const int64_t row = (int64_t)rg * ROW_GROUP + ct;
-    a.part[(int64_t)cr * a.n_pad + row] = acc.final_value((uint32_t)nst);
-    __threadfence();
-    named_bar_sync(1, 32 * NCONS);
-    if (ct == 0) {
-      const unsigned old = atomicAdd(&a.cnt_grp[rg], 1u);
-      s_last = (old == (unsigned)a.ncr - 1u);
-    }
-    named_bar_sync(1, 32 * NCONS);
-    if (s_last) {
-      __threadfence();
-      fwd_finish(a, rg, ct, cw, lane, wsum, &s_flag);
-    }
-    named_bar_sync(1, 32 * NCONS);
-  }
-}
-
-// ============================================================================ adjoint
-__device__ __noinline__ void adj_finish(const AdjArgs& a, int cg, int ct, int cw, int lane,
-                                        double (*wsum)[3], int* s_flag) {
-  const int64_t col = (int64_t)cg * COL_GROUP + 2 * ct;
+__global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a) {
+  if (a.mode != ADJ_APPLY && a.st->status != RUNNING) return;
+  __shared__ double ws[4][3];
+  __shared__ unsigned s_last;
+  DevState* st = a.st;
+  const int cg = blockIdx.x;
+  const int64_t col = (int64_t)cg * COL_GROUP + 2 * threadIdx.x;
   Counter<20> acc0, acc1;
-  for (int rr = 0; rr < a.nrr; ++rr) {
+  int rr = 0;
+  for (; rr + 8 <= a.nrr; rr += 8) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)(rr + u) * a.p_pad + col));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc0.push(v[u].x, rr + u);
+      acc1.push(v[u].y, rr + u);
+    }
+  }
+  for (; rr < a.nrr; ++rr) {
     const double2 v = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)rr * a.p_pad + col));
     acc0.push(v.x, rr);
     acc1.push(v.y, rr);
@@ -255,18 +213,15 @@ __device__ __noinline__ void adj_finish(const AdjArgs& a, int cg, int ct, int cw
   const double s0 = acc0.final_value(a.nrr), s1 = acc1.final_value(a.nrr);
   if (a.mode == ADJ_APPLY) {
     *reinterpret_cast<double2*>(a.vout + col) = make_double2(s0, s1);
-    if (ct == 0) a.cnt_grp[cg] = 0;
     return;
   }
-  DevState* st = a.st;
   const int cur = st->cur;
   const double g0 = mul(2.0, s0), g1 = mul(2.0, s1);  // 2 K^T r (gpss.cpp:130, :211)
   if (a.mode == ADJ_INIT) {
     *reinterpret_cast<double2*>(a.vb.g[cur] + col) = make_double2(g0, g1);
-    if (ct == 0) a.cnt_grp[cg] = 0;
     return;
   }
-  // ADJ_ITER epilogue: x' = x + lambda d (gpss.cpp:208), s = x' - x, z = g' - g (:150-151)
+  // x' = x + lambda d (gpss.cpp:208), s = x' - x, z = g' - g (gpss.cpp:150-151)
   const double lam = st->step;
   const double2 xo = *reinterpret_cast<const double2*>(a.vb.x[cur] + col);
   const double2 go = *reinterpret_cast<const double2*>(a.vb.g[cur] + col);
@@ -276,31 +231,21 @@ __device__ __noinline__ void adj_finish(const AdjArgs& a, int cg, int ct, int cw
   *reinterpret_cast<double2*>(a.vb.g[cur ^ 1] + col) = make_double2(g0, g1);
   const double sa = sub(x0n, xo.x), sb = sub(x1n, xo.y);
   const double za = sub(g0, go.x), zb = sub(g1, go.y);
-  double lsz = add(mul(sa, za), mul(sb, zb));
-  double lss = add(mul(sa, sa), mul(sb, sb));
-  double lzz = add(mul(za, za), mul(zb, zb));
-  lsz = warp_tree(lsz);
-  lss = warp_tree(lss);
-  lzz = warp_tree(lzz);
-  if (lane == 0) {
-    wsum[cw][0] = lsz;
-    wsum[cw][1] = lss;
-    wsum[cw][2] = lzz;
-  }
-  named_bar_sync(1, 32 * NCONS);
-  if (ct == 0) {
+  block4<0>(add(mul(sa, za), mul(sb, zb)), ws, 0);
+  block4<0>(add(mul(sa, sa), mul(sb, sb)), ws, 1);
+  block4<0>(add(mul(za, za), mul(zb, zb)), ws, 2);
+  __syncthreads();
+  if (threadIdx.x == 0) {
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-      a.grpsum[3 * cg + c] = add(add(wsum[0][c], wsum[1][c]), add(wsum[2][c], wsum[3][c]));
-    a.cnt_grp[cg] = 0;
+      a.grpsum[3 * cg + c] = add(add(ws[0][c], ws[1][c]), add(ws[2][c], ws[3][c]));
     __threadfence();
-    const unsigned old = atomicAdd(a.cnt_all, 1u);
-    *s_flag = (old == (unsigned)a.ncg - 1u);
+    s_last = atomicAdd(a.cnt_all, 1u) == (unsigned)a.ncg - 1u;
   }
-  named_bar_sync(1, 32 * NCONS);
-  if (!*s_flag) return;
+  __syncthreads();
+  if (!s_last || threadIdx.x >= 32) return;
   __threadfence();
-  if (cw != 0) return;
+  const int lane = threadIdx.x;
   const double SZ = warp_tree_array(a.grpsum + 0, a.ncg, 3, lane);
   const double SS = warp_tree_array(a.grpsum + 1, a.ncg, 3, lane);
   const double ZZ = warp_tree_array(a.grpsum + 2, a.ncg, 3, lane);
@@ -355,15 +300,17 @@ __device__ __noinline__ void adj_finish(const AdjArgs& a, int cg, int ct, int cw
   st->cur = cur ^ 1;
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) adj_kernel(const AdjArgs a) {
-  if (a.mode != ADJ_APPLY && a.st->status != RUNNING) return;
+// ============================================================================ forward
+template <int SPLIT>
+__global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdArgs a) {
+  constexpr int NCONS = 4 * SPLIT;
+  constexpr int NQ = 32 / SPLIT;  // column pairs per lane group
+  constexpr int RPW = 32 / SPLIT; // rows per warp
+  if (a.mode != FWD_APPLY && a.st->status != RUNNING) return;
   extern __shared__ __align__(128) unsigned char smem[];
   double* sbase = reinterpret_cast<double*>(smem);
-  double* rs = sbase + (size_t)STAGES * ADJ_STAGE_DBL;
-  uint64_t* full = reinterpret_cast<uint64_t*>(rs + MAX_TR);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * FWD_STAGE_DBL * 8);
   uint64_t* empty = full + STAGES;
-  __shared__ double wsum[NCONS][3];
-  __shared__ int s_last, s_flag;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -373,22 +320,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) adj_kernel(const AdjArgs a) {
     fence_barrier_init();
   }
   __syncthreads();
-  const int ntasks = a.ncg * a.nrr;
-  const int64_t tr = (int64_t)a.blocks * TR;
-  if (warp == 0) {
+  const int ntasks = a.nrg * a.ncr;
+  if (warp == 0) {  // ---- producer: one elected lane issues every bulk copy
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
-        const int cg = t / a.nrr, rr = t - cg * a.nrr;
-        const int64_t rb0 = (int64_t)rr * a.blocks;
-        const int nb = (int)(a.nrb - rb0 < (int64_t)a.blocks ? a.nrb - rb0 : (int64_t)a.blocks);
-        for (int s = 0; s < nb; ++s) {
+        const int rg = t / a.ncr, cr = t - rg * a.ncr;
+        const int64_t cb0 = (int64_t)cr * a.stages;
+        const int nst = (int)(a.ncb - cb0 < (int64_t)a.stages ? a.ncb - cb0 : (int64_t)a.stages);
+        for (int s = 0; s < nst; ++s) {
           mbar_wait(&empty[stage], phase ^ 1u);
-          mbar_arrive_expect_tx(&full[stage], 4 * TILE_BYTES);
-          bulk_g2s(sbase + (size_t)stage * ADJ_STAGE_DBL,
-                   a.K + tile_offset(rb0 + s, 4 * (int64_t)cg, a.ncb), 4 * TILE_BYTES,
-                   &full[stage]);
+          double* dst = sbase + (size_t)stage * FWD_STAGE_DBL;
+          mbar_arrive_expect_tx(&full[stage], TILES_PER_STAGE * TILE_BYTES + 512);
+#pragma unroll
+          for (int w = 0; w < TILES_PER_STAGE; ++w)
+            bulk_g2s(dst + w * TILE, a.K + tile_offset(4 * rg + w, cb0 + s, a.ncb), TILE_BYTES,
+                     &full[stage]);
+          const double* dsrc = a.vin + (cb0 + s) * TC;
+          double* ddst = dst + TILES_PER_STAGE * TILE;
+#pragma unroll
+          for (int g = 0; g < SPLIT; ++g)
+            bulk_g2s(ddst + 2 * d_pos<SPLIT>(g * NQ), dsrc + 2 * g * NQ, 512 / SPLIT, &full[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -398,40 +351,162 @@ __global__ void __launch_bounds__(NTHREADS, 1) adj_kernel(const AdjArgs a) {
     }
     return;
   }
-  const int cw = warp - 1, ct = threadIdx.x - 32;
-  const int cur = (a.mode == ADJ_APPLY) ? 0 : a.st->cur;
-  const double lam = (a.mode == ADJ_ITER) ? a.st->step : 0.0;
-  const double* rin = (a.mode == ADJ_APPLY) ? a.vin : a.vb.r[cur];
+  // ---- consumers: warp cw -> tile cw / SPLIT (row block 4*rg + tile), row slice
+  //      (cw % SPLIT) * RPW + (lane % RPW), column-pair group lane / RPW
+  const int cw = warp - 1;
+  const int tile = cw / SPLIT;
+  const int row = (cw % SPLIT) * RPW + (lane % RPW);  // row inside the tile
+  const int qg = lane / RPW;                           // column-pair group
+  const int sw = row & 7;
   int stage = 0;
   uint32_t phase = 0;
   for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    const int rg = t / a.ncr, cr = t - rg * a.ncr;
+    const int64_t cb0 = (int64_t)cr * a.stages;
+    const int nst = (int)(a.ncb - cb0 < (int64_t)a.stages ? a.ncb - cb0 : (int64_t)a.stages);
+    Counter<8> acc;
+    for (int s = 0; s < nst; ++s) {
+      mbar_wait(&full[stage], phase);
+      const double* sb = sbase + (size_t)stage * FWD_STAGE_DBL;
+      const double2* ku = reinterpret_cast<const double2*>(sb + tile * TILE) + row * 32;
+      const double2* du = reinterpret_cast<const double2*>(sb + TILES_PER_STAGE * TILE);
+      double v = tree<NQ>([&](int k) {
+        const int q = qg * NQ + k;
+        const double2 kk = ku[q ^ sw];
+        const double2 d = du[d_pos<SPLIT>(q)];
+        return add(mul(kk.x, d.x), mul(kk.y, d.y));
+      });
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      // join the SPLIT column slices of the row: adjacent groups are adjacent subtrees
+#pragma unroll
+      for (int o = RPW; o < 32; o <<= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
+      acc.push(v, (uint32_t)s);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+    if (qg == 0) {
+      const int64_t grow = (int64_t)rg * ROW_GROUP + tile * TR + row;
+      a.part[(int64_t)cr * a.n_pad + grow] = acc.final_value((uint32_t)nst);
+    }
+  }
+}
+
+// ============================================================================ adjoint
+template <int SPLIT>
+__global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) adj_kernel(const AdjArgs a) {
+  constexpr int NCONS = 4 * SPLIT;
+  constexpr int NQ = 32 / SPLIT;  // column pairs per warp
+  constexpr int RPL = 32 / SPLIT; // rows per lane group
+  if (a.mode != ADJ_APPLY && a.st->status != RUNNING) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* sbase = reinterpret_cast<double*>(smem);
+  double* vslot = sbase + (size_t)STAGES * ADJ_STAGE_DBL;         // [2][2][MAX_TR] r, kd
+  double* rs = vslot + 4 * MAX_TR;                                 // padded r_new slice
+  uint64_t* full = reinterpret_cast<uint64_t*>(rs + MAX_TR + RS_PAD);
+  uint64_t* empty = full + STAGES;
+  uint64_t* vfull = empty + STAGES;  // [2]
+  uint64_t* vempty = vfull + 2;      // [2]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&vfull[i], 1);
+      mbar_init(&vempty[i], NCONS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int ntasks = a.ncg * a.nrr;
+  const int64_t tr = (int64_t)a.blocks * TR;
+  const int cur = (a.mode == ADJ_APPLY) ? 0 : a.st->cur;
+  const double* rin = (a.mode == ADJ_APPLY) ? a.vin : a.vb.r[cur];
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int j = 0;
+      for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++j) {
+        const int cg = t / a.nrr, rr = t - cg * a.nrr;
+        const int64_t rb0 = (int64_t)rr * a.blocks;
+        const int nb = (int)(a.nrb - rb0 < (int64_t)a.blocks ? a.nrb - rb0 : (int64_t)a.blocks);
+        const int64_t row0 = rr * tr;
+        // the task's slices of r (and Kd) into vector slot j&1
+        if (j >= 2) mbar_wait(&vempty[j & 1], (uint32_t)(((j - 2) >> 1) & 1));
+        double* vs = vslot + (j & 1) * 2 * MAX_TR;
+        const uint32_t vbytes = (uint32_t)(nb * TR * 8);
+        mbar_arrive_expect_tx(&vfull[j & 1], a.mode == ADJ_ITER ? 2 * vbytes : vbytes);
+        bulk_g2s(vs, rin + row0, vbytes, &vfull[j & 1]);
+        if (a.mode == ADJ_ITER) bulk_g2s(vs + MAX_TR, a.vb.kd + row0, vbytes, &vfull[j & 1]);
+        for (int s = 0; s < nb; ++s) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_arrive_expect_tx(&full[stage], TILES_PER_STAGE * TILE_BYTES);
+          bulk_g2s(sbase + (size_t)stage * ADJ_STAGE_DBL,
+                   a.K + tile_offset(rb0 + s, 4 * (int64_t)cg, a.ncb),
+                   TILES_PER_STAGE * TILE_BYTES, &full[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+  // consumers: warp cw -> tile cw / SPLIT (column block 4*cg + tile), column pair
+  // (cw % SPLIT) * NQ + (lane % NQ), row slice lane / NQ
+  const int cw = warp - 1, ct = threadIdx.x - 32;
+  const int tile = cw / SPLIT;
+  const int q = (cw % SPLIT) * NQ + (lane % NQ);
+  const int rgp = lane / NQ;
+  const double lam = (a.mode == ADJ_ITER) ? a.st->step : 0.0;
+  int stage = 0;
+  uint32_t phase = 0;
+  int j = 0;
+  for (int t = blockIdx.x; t < ntasks; t += gridDim.x, ++j) {
     const int cg = t / a.nrr, rr = t - cg * a.nrr;
     const int64_t rb0 = (int64_t)rr * a.blocks;
     const int nb = (int)(a.nrb - rb0 < (int64_t)a.blocks ? a.nrb - rb0 : (int64_t)a.blocks);
     const int64_t row0 = rr * tr;
-    // prologue: the task's slice of r (ITER: r + lambda Kd, gpss.cpp:209)
+    // the task's slice of r (ITER: r + lambda Kd, gpss.cpp:209) from the staged slot
+    mbar_wait(&vfull[j & 1], (uint32_t)((j >> 1) & 1));
+    const double* vs = vslot + (j & 1) * 2 * MAX_TR;
+    named_bar_sync(1, 32 * NCONS);  // previous task's readers of rs are done
     for (int i = ct; i < nb * TR; i += 32 * NCONS) {
-      double r = rin[row0 + i];
+      double r = vs[i];
       if (a.mode == ADJ_ITER) {
-        r = add(r, mul(lam, a.vb.kd[row0 + i]));
+        r = add(r, mul(lam, vs[MAX_TR + i]));
         if (cg == 0) a.vb.r[cur ^ 1][row0 + i] = r;
       }
-      rs[i] = r;
+      rs[rs_pos(i)] = r;
     }
     named_bar_sync(1, 32 * NCONS);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&vempty[j & 1]);
     Counter<6> acc0, acc1;
     for (int s = 0; s < nb; ++s) {
       mbar_wait(&full[stage], phase);
       const double2* ku =
-          reinterpret_cast<const double2*>(sbase + (size_t)stage * ADJ_STAGE_DBL + cw * TILE);
-      const double* rr_s = rs + s * TR;
-      const double2 v = tree2<32>([&](int i) {
-        const double2 k = ku[i * 32 + (lane ^ (i & 7))];
-        const double r = rr_s[i];
-        return make_double2(mul(k.x, r), mul(k.y, r));
+          reinterpret_cast<const double2*>(sbase + (size_t)stage * ADJ_STAGE_DBL + tile * TILE);
+      const int rbase = s * TR + rgp * RPL;
+      double2 v = tree2<RPL>([&](int k) {
+        const int i = rgp * RPL + k;
+        const double2 kk = ku[i * 32 + (q ^ (i & 7))];
+        const double r = rs[rs_pos(rbase + k)];
+        return make_double2(mul(kk.x, r), mul(kk.y, r));
       });
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
+#pragma unroll
+      for (int o = NQ; o < 32; o <<= 1) {
+        v.x = add(v.x, __shfl_xor_sync(0xffffffffu, v.x, o));
+        v.y = add(v.y, __shfl_xor_sync(0xffffffffu, v.y, o));
+      }
       acc0.push(v.x, (uint32_t)s);
       acc1.push(v.y, (uint32_t)s);
       if (++stage == STAGES) {
@@ -439,21 +514,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) adj_kernel(const AdjArgs a) {
         phase ^= 1u;
       }
     }
-    const int64_t col = (int64_t)cg * COL_GROUP + cw * TC + 2 * lane;
-    *reinterpret_cast<double2*>(a.part + (int64_t)rr * a.p_pad + col) =
-        make_double2(acc0.final_value((uint32_t)nb), acc1.final_value((uint32_t)nb));
-    __threadfence();
-    named_bar_sync(1, 32 * NCONS);
-    if (ct == 0) {
-      const unsigned old = atomicAdd(&a.cnt_grp[cg], 1u);
-      s_last = (old == (unsigned)a.nrr - 1u);
+    if (rgp == 0) {
+      const int64_t col = (int64_t)cg * COL_GROUP + tile * TC + 2 * q;
+      *reinterpret_cast<double2*>(a.part + (int64_t)rr * a.p_pad + col) =
+          make_double2(acc0.final_value((uint32_t)nb), acc1.final_value((uint32_t)nb));
     }
-    named_bar_sync(1, 32 * NCONS);
-    if (s_last) {
-      __threadfence();
-      adj_finish(a, cg, ct, cw, lane, wsum, &s_flag);
-    }
-    named_bar_sync(1, 32 * NCONS);
   }
 }
 
@@ -484,16 +549,50 @@ GemvPlan make_plan(int64_t n, int64_t p, int sm_count) {
 }
 
 static size_t fwd_smem() { return (size_t)STAGES * FWD_STAGE_DBL * 8 + 2 * STAGES * 8; }
-static size_t adj_smem() { return (size_t)STAGES * ADJ_STAGE_DBL * 8 + MAX_TR * 8 + 2 * STAGES * 8; }
+static size_t adj_smem() {
+  return (size_t)STAGES * ADJ_STAGE_DBL * 8 + (4 * MAX_TR + MAX_TR + RS_PAD) * 8 +
+         (2 * STAGES + 4) * 8;
+}
 
-void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
-                DevState* st, cudaStream_t s) {
+static int split_choice() {
+  static int s = [] {
+    const char* e = getenv("L1G_SPLIT");
+    const int v = e ? atoi(e) : 1;
+    return (v == 1 || v == 2 || v == 4) ? v : 1;
+  }();
+  return s;
+}
+
+template <int SPLIT>
+static void fwd_launch(const FwdArgs& a, int grid, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    L1G_CUDA(cudaFuncSetAttribute(fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    L1G_CUDA(cudaFuncSetAttribute(fwd_kernel<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)fwd_smem()));
     attr = true;
   }
+  fwd_kernel<SPLIT><<<grid, 32 * (4 * SPLIT + 1), fwd_smem(), s>>>(a);
+  L1G_CUDA(cudaGetLastError());
+  fwd_finish_kernel<<<a.nrg, FIN_T, 0, s>>>(a);
+  L1G_CUDA(cudaGetLastError());
+}
+
+template <int SPLIT>
+static void adj_launch(const AdjArgs& a, int grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    L1G_CUDA(cudaFuncSetAttribute(adj_kernel<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)adj_smem()));
+    attr = true;
+  }
+  adj_kernel<SPLIT><<<grid, 32 * (4 * SPLIT + 1), adj_smem(), s>>>(a);
+  L1G_CUDA(cudaGetLastError());
+  adj_finish_kernel<<<a.ncg, FIN_T, 0, s>>>(a);
+  L1G_CUDA(cudaGetLastError());
+}
+
+void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
+                const VecBufs* vb, DevState* st, cudaStream_t s) {
   const GemvPlan& pl = op.plan;
   FwdArgs a{};
   a.K = op.K;
@@ -512,18 +611,15 @@ void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, 
   a.st = st;
   if (vb) a.vb = *vb;
   const int grid = (int)std::min<int64_t>(pl.grid, (int64_t)pl.nrg * pl.ncr);
-  fwd_kernel<<<grid, NTHREADS, fwd_smem(), s>>>(a);
-  L1G_CUDA(cudaGetLastError());
+  switch (split_choice()) {
+    case 1: fwd_launch<1>(a, grid, s); break;
+    case 4: fwd_launch<4>(a, grid, s); break;
+    default: fwd_launch<2>(a, grid, s); break;
+  }
 }
 
-void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
-                DevState* st, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    L1G_CUDA(cudaFuncSetAttribute(adj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)adj_smem()));
-    attr = true;
-  }
+void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
+                const VecBufs* vb, DevState* st, cudaStream_t s) {
   const GemvPlan& pl = op.plan;
   AdjArgs a{};
   a.K = op.K;
@@ -543,8 +639,11 @@ void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, 
   a.st = st;
   if (vb) a.vb = *vb;
   const int grid = (int)std::min<int64_t>(pl.grid, (int64_t)pl.ncg * pl.nrr);
-  adj_kernel<<<grid, NTHREADS, adj_smem(), s>>>(a);
-  L1G_CUDA(cudaGetLastError());
+  switch (split_choice()) {
+    case 1: adj_launch<1>(a, grid, s); break;
+    case 4: adj_launch<4>(a, grid, s); break;
+    default: adj_launch<2>(a, grid, s); break;
+  }
 }
 
 }  // namespace l1g

@@ -199,6 +199,18 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   __shared__ int s_dec;
   DevState* st = a.st;
   if (threadIdx.x == 0) sh.red_par = 0;
+  const bool prof = (a.mode == PROJ_ITER) && cl.block_rank() == 0 && threadIdx.x == 0;
+  long long t_last = clock64();
+  auto mark = [&](int idx) {
+    if (prof) {
+      const long long t = clock64();
+      st->prof[idx] += (double)(t - t_last);
+      t_last = t;
+    }
+  };
+  auto count = [&](int idx, double v) {
+    if (prof) st->prof[idx] += v;
+  };
   if (a.mode == PROJ_ITER && st->status != RUNNING) return;  // uniform over the cluster
   const l1g_gp_config cfg = st->cfg;
   const double rho = a.mode == PROJ_PLAIN ? st->rho : st->rho;
@@ -257,7 +269,10 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   }
 
   double first_stat = 0.0;
+  count(8, 1.0);
+  mark(0);
   for (int attempt = 0;; ++attempt) {
+    count(9, 1.0);
     // ---- v = x - alpha g  (gpss.cpp:167; alpha0: x0 - grad, gpss.cpp:95)
     for (int64_t j = threadIdx.x; j < a.ls; j += PT) {
       double v = 0.0;
@@ -278,6 +293,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     red[1] = block_max(lm, sh);
     cluster_combine(red, k_l1max, 2, sh, cl, cs);
     const double l1v = red[0], vinf = red[1];
+    mark(1);
 
     // ---- threshold (prox.cpp:40-53)
     double theta = 0.0;
@@ -318,10 +334,12 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         __syncthreads();
         double v2[2] = {cc, ss};
         cluster_combine(v2, kinds_cs, 2, sh, cl, cs);
+        count(10, 1.0);
         if (v2[0] == cnt_prev || v2[0] == 0.0) break;
         cnt_prev = v2[0];
         th = dvd(sub(v2[1], rho), v2[0]);
       }
+      mark(2);
       // exact sort-and-scan on the elements above a bracket below theta
       double lo = th > 0.0 ? sub(th, mul(th, 0x1.0p-20)) : -1.0;
       for (int tries = 0;; ++tries) {
@@ -375,6 +393,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         }
         __threadfence();
         cl.sync();
+        mark(3);
+        count(11, (double)total);
         __shared__ int s_ff;
         if (rank == 0) {
           double* c = in_smem ? cand : a.gcand;
@@ -383,6 +403,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           bitonic_desc(c, n2);
           if (threadIdx.x == 0 && next >= 0.0) c[total] = next;
           __syncthreads();
+          mark(4);
           double* pre = a.gpre;
           if (threadIdx.x == 0) {  // the reference's sequential cumulative sum
             double S = 0.0;
@@ -430,10 +451,12 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           s_dec = *f0;
         }
         cl.sync();
+        mark(5);
         if (!s_dec) {
           theta = sh.bc[3];
           break;
         }
+        count(13, 1.0);
         lo = (lo > 0.0 && tries < 4) ? mul(lo, 0.5) : -1.0;
       }
       if (theta < 0.0) theta = 0.0;
@@ -450,9 +473,11 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         }, sh);
         cluster_combine(l1u, k_sum, 1, sh, cl, cs);
         if (!(l1u[0] > rho && guard++ < 64)) break;
+        count(12, 1.0);
         theta = add(theta, bump);
         bump = mul(bump, 2.0);
       }
+      mark(6);
     }
 
     // ---- h, d = h - x, ||h - x||_inf, g'd, support  (gpss.cpp:167-178)
@@ -489,6 +514,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     cluster_combine(red2, kinds2, 4, sh, cl, cs);
     const double gd = red2[0], stat = red2[1], hinf = red2[2];
     const long long support = (long long)red2[3];
+    mark(7);
 
     if (a.mode != PROJ_ITER) {
       if (rank == 0 && threadIdx.x == 0) {

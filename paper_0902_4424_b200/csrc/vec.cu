@@ -347,3 +347,26 @@ void state_start(DevState* st, cudaStream_t s) {
 }
 
 }  // namespace l1g
+
+namespace l1g {
+// harness random streams (bit-identical to orc_normal / orc_uniform)
+__global__ void rng_fill_kernel(int kind, uint64_t seed, uint32_t stream, uint64_t first,
+                                int64_t count, double* out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t idx = first + (uint64_t)e;
+    if (kind == 0) {
+      out[e] = det_normal(seed, stream, idx);
+    } else {
+      uint32_t c[4] = {(uint32_t)idx, (uint32_t)(idx >> 32), stream, 0x5555u};
+      philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+      out[e] = u53(c[0], c[1]);
+    }
+  }
+}
+void rng_fill(int kind, uint64_t seed, uint32_t stream, uint64_t first, int64_t count,
+              double* out, cudaStream_t s) {
+  rng_fill_kernel<<<fill_grid(count), 256, 0, s>>>(kind, seed, stream, first, count, out);
+  L1G_CUDA(cudaGetLastError());
+}
+}  // namespace l1g

@@ -29,5 +29,7 @@ void steplength_device(l1g_sl_state* sl, const double* dots, const l1g_gp_config
                        l1g_sl_choice* out, cudaStream_t s);
 void backtrack_device(const double* in, const l1g_gp_config& cfg, double* out, cudaStream_t s);
 void state_start(DevState* st, cudaStream_t s);
+void rng_fill(int kind, uint64_t seed, uint32_t stream, uint64_t first, int64_t count,
+              double* out, cudaStream_t s);
 
 }  // namespace l1g

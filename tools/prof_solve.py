@@ -1,0 +1,69 @@
+"""Short solve for profiling (ncu launch lists / --set full captures).
+
+  python tools/prof_solve.py --config C2 --iters 20 [--solves 1]
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import paper_0902_4424_b200 as l1  # noqa: E402
+from paper_0902_4424_b200 import _lib as L  # noqa: E402
+from paper_0902_4424_b200 import harness as H  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--solves", type=int, default=1)
+    ap.add_argument("--profile", action="store_true", help="print projection phase profile")
+    ap.add_argument("--timing", action="store_true", help="per-kernel CUDA-event timing")
+    a = ap.parse_args()
+    spec = H.CONFIGS[a.config]
+    fx = os.path.join(ROOT, "tests", "golden", "sigma_hat.json")
+    if os.path.exists(fx):
+        spec.sigma_hat = json.load(open(fx)).get(a.config)
+    P = H.build_problem(spec)
+    lib = L.load()
+    cfg = l1.GpConfig()._c()
+    stop = l1.StopRule(max_iterations=a.iters, stationarity_tol=0.0)._c()
+    h = C.c_void_p()
+    L.check(lib.l1g_solver_create(P["op"].h, L.ptr(np.ascontiguousarray(P["y"])), P["rho"],
+                                  C.byref(cfg), C.byref(h)))
+    res = L.ResultC()
+    if a.timing:
+        L.check(lib.l1g_solver_set_timing(h, 1))
+    for s in range(a.solves):
+        t = time.perf_counter()
+        L.check(lib.l1g_solver_init(h, None))
+        L.check(lib.l1g_solver_run(h, C.byref(stop), C.byref(res), None, 0))
+        dt = time.perf_counter() - t
+        print(f"solve {s}: {res.iterations} iterations ({L.REASONS[res.reason]}) in {dt*1e3:.2f} ms"
+              f" = {res.iterations / dt:.1f} it/s, f={res.objective:.6e}", flush=True)
+    if a.timing:
+        tp, tf, ta, ti, tl = (C.c_double(), C.c_double(), C.c_double(), C.c_int64(),
+                              C.c_int64())
+        lib.l1g_solver_timing(h, C.byref(tp), C.byref(tf), C.byref(ta), C.byref(ti),
+                              C.byref(tl), 0)
+        it = max(ti.value, 1)
+        kb = spec.n * spec.p * 8
+        print(f"per iteration ms: proj {tp.value/it:.4f} fwd {tf.value/it:.4f} "
+              f"adj {ta.value/it:.4f}  GB/s fwd {kb/(tf.value/it)/1e6:.0f} "
+              f"adj {kb/(ta.value/it)/1e6:.0f}  ({it} iterations, {tl.value} launches)")
+    if a.profile and hasattr(lib, "l1g_solver_proj_profile"):
+        out = (C.c_double * 16)()
+        lib.l1g_solver_proj_profile(h, out)
+        print("proj profile:", [round(v, 3) for v in out])
+    lib.l1g_solver_destroy(h)
+
+
+if __name__ == "__main__":
+    main()
