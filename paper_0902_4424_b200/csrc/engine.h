@@ -67,6 +67,7 @@ struct DevState {
   // projection phase profile (SM cycles of CTA 0 / event counts), see project.cu
   double prof[16];
 };
+static_assert(sizeof(DevState) % 8 == 0, "DevState is copied as 8-byte words");
 
 // GEMV launch plan for one operator
 struct GemvPlan {

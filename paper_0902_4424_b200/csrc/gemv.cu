@@ -103,6 +103,14 @@ __device__ __forceinline__ int rs_pos(int i) { return i + (i >> 3); }
 // groups and runs the scalar part of gp_iterate.
 constexpr int FIN_T = 128;
 
+// warp-cooperative copy of the device state into shared memory (one coalesced pass)
+__device__ __forceinline__ void snapshot(DevState* dst, const DevState* src, int lane) {
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(dst);
+  for (int i = lane; i < (int)(sizeof(DevState) / 8); i += 32) d[i] = __ldcg(s + i);
+  __syncwarp();
+}
+
 template <int N>
 __device__ __forceinline__ double block4(double v, double (*ws)[3], int c) {
   v = warp_tree(v);
@@ -157,6 +165,8 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
   const int lane = threadIdx.x;
   const double A = warp_tree_array(a.grpsum + 0, a.nrg, 2, lane);
   const double B = warp_tree_array(a.grpsum + 1, a.nrg, 2, lane);
+  __shared__ DevState s;
+  snapshot(&s, a.st, lane);
   if (lane != 0) return;
   DevState* st = a.st;
   *a.cnt_all = 0;
@@ -170,12 +180,12 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
   // gpss.cpp:199-203 -- nonmonotone reference value and quadratic backtracking
   st->a = A;
   st->b = B;
-  double f_max = st->fh[0];
-  for (int i = 1; i < st->fh_len; ++i) f_max = st->fh[i] > f_max ? st->fh[i] : f_max;
+  double f_max = s.fh[0];
+  for (int i = 1; i < s.fh_len; ++i) f_max = s.fh[i] > f_max ? s.fh[i] : f_max;
   st->f_max = f_max;
   double step, f_new;
   int h;
-  if (backtrack_quadratic(st->f, A, B, f_max, st->gd, st->cfg, &step, &f_new, &h)) {
+  if (backtrack_quadratic(s.f, A, B, f_max, s.gd, s.cfg, &step, &f_new, &h)) {
     st->step = step;
     st->f_new = f_new;
     st->halvings = h;
@@ -249,55 +259,63 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a) {
   const double SZ = warp_tree_array(a.grpsum + 0, a.ncg, 3, lane);
   const double SS = warp_tree_array(a.grpsum + 1, a.ncg, 3, lane);
   const double ZZ = warp_tree_array(a.grpsum + 2, a.ncg, 3, lane);
+  __shared__ DevState s;
+  snapshot(&s, st, lane);
   if (lane != 0) return;
   *a.cnt_all = 0;
-  // gpss.cpp:206-217 state advance, gpss.cpp:255-283 loop bookkeeping
+  // gpss.cpp:206-217 state advance, gpss.cpp:255-283 loop bookkeeping (on the snapshot,
+  // then written back field by field)
   st->sz = SZ;
   st->ss = SS;
   st->zz = ZZ;
-  st->f = st->f_new;
-  if (st->fh_len < kMaxHist) {
-    st->fh[st->fh_len++] = st->f;
+  const double f = s.f_new;
+  st->f = f;
+  int fl = s.fh_len;
+  if (fl < kMaxHist) {
+    s.fh[fl++] = f;
   } else {
-    for (int i = 0; i + 1 < st->fh_len; ++i) st->fh[i] = st->fh[i + 1];
-    st->fh[st->fh_len - 1] = st->f;
+    for (int i = 0; i + 1 < fl; ++i) s.fh[i] = s.fh[i + 1];
+    s.fh[fl - 1] = f;
   }
-  while (st->fh_len > st->cfg.memory) {
-    for (int i = 0; i + 1 < st->fh_len; ++i) st->fh[i] = st->fh[i + 1];
-    --st->fh_len;
+  while (fl > s.cfg.memory) {
+    for (int i = 0; i + 1 < fl; ++i) s.fh[i] = s.fh[i + 1];
+    --fl;
   }
-  const int64_t k = st->k;
+  for (int i = 0; i < fl; ++i) st->fh[i] = s.fh[i];
+  st->fh_len = fl;
+  const int64_t k = s.k;
   st->k = k + 1;
-  st->matvecs += 2;
+  const int64_t mv = s.matvecs + 2;
+  st->matvecs = mv;
   l1g_iter_record rec;
   rec.k = k;
-  rec.f = st->f;
-  rec.stationarity = st->stat;
-  rec.alpha = st->alpha_used;
-  rec.step = st->step;
-  rec.matvecs = st->matvecs;
-  rec.elapsed_seconds = elapsed_s(st);
-  rec.bb_active = st->choice.bb_active;
-  rec.halvings = st->halvings;
-  rec.bb1_raw = st->choice.bb1_raw;
-  rec.bb2_raw = st->choice.bb2_raw;
-  rec.tau_before = st->choice.tau_before;
-  rec.tau_after = st->choice.tau_after;
-  rec.f_max = st->f_max;
-  rec.dir_derivative = st->gd;
-  rec.theta = st->theta;
-  rec.support = st->support;
+  rec.f = f;
+  rec.stationarity = s.stat;
+  rec.alpha = s.alpha_used;
+  rec.step = s.step;
+  rec.matvecs = mv;
+  rec.elapsed_seconds = elapsed_s(&s);
+  rec.bb_active = s.choice.bb_active;
+  rec.halvings = s.halvings;
+  rec.bb1_raw = s.choice.bb1_raw;
+  rec.bb2_raw = s.choice.bb2_raw;
+  rec.tau_before = s.choice.tau_before;
+  rec.tau_after = s.choice.tau_after;
+  rec.f_max = s.f_max;
+  rec.dir_derivative = s.gd;
+  rec.theta = s.theta;
+  rec.support = s.support;
   st->last = rec;
-  if (st->trace && k < st->trace_cap) st->trace[k] = rec;
-  if (!st->single_step && st->objective_tol > 0.0) {
-    const double af = fabs(st->f);
-    if (fabs(sub(st->f_prev, st->f)) <= mul(st->objective_tol, af > 1.0 ? af : 1.0)) {
+  if (s.trace && k < s.trace_cap) s.trace[k] = rec;
+  if (!s.single_step && s.objective_tol > 0.0) {
+    const double af = fabs(f);
+    if (fabs(sub(s.f_prev, f)) <= mul(s.objective_tol, af > 1.0 ? af : 1.0)) {
       st->status = STOPPED;
       st->reason = L1G_OBJECTIVE_TOL;
     }
   }
-  st->f_prev = st->f;
-  st->cur = cur ^ 1;
+  st->f_prev = f;
+  st->cur = s.cur ^ 1;
 }
 
 // ============================================================================ forward

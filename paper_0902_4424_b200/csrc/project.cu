@@ -4,14 +4,16 @@
 // 1-3 of gp_iterate (gpss.cpp:146-192): steplength choice, v = x - alpha g, h = P(v),
 // d = h - x, ||h - x||_inf, g'd and the alpha escalation loop, all on device.
 //
-// A cluster of `cs` CTAs keeps v resident in distributed shared memory (CTA r owns the
-// aligned slice [r*ls, (r+1)*ls)).  The threshold is found without a host sort:
-//   1. Michelot's pivot iteration (cluster-wide counts and sums) brackets theta;
-//   2. the elements above the bracket (plus the largest one below it) are gathered into
+// A cluster of `cs` CTAs (512 threads each) owns the vector; thread t of CTA r keeps the
+// aligned run of M elements [r*ls + t*M, r*ls + (t+1)*M) in registers, so every canonical
+// pairwise reduction is a register tree -> warp butterfly -> 16 warp values -> cs CTAs.
+// The threshold is found without a host sort:
+//   1. Michelot's pivot iteration (cluster-wide counts and sums) brackets theta from below;
+//   2. the elements above the bracket plus the largest one below it are gathered into
 //      CTA 0 and bitonic-sorted (shared memory, or L2-resident global memory if large);
 //   3. one thread forms the *sequential* descending prefix sums exactly as prox.cpp:43-52
-//      does, then all threads test |v|_(k) > (S_k - rho)/k in parallel and the first
-//      failure fixes theta -- bit-identical to the reference's sort-and-scan;
+//      does, all threads test |v|_(k) > (S_k - rho)/k in parallel and the first failure
+//      fixes theta -- bit-identical to the reference's sort-and-scan;
 //   4. the feasibility bump loop of prox.cpp:58-65 on canonical cluster-wide l1 norms.
 #include <cooperative_groups.h>
 
@@ -27,8 +29,9 @@ namespace l1g {
 
 constexpr int PT = 512;
 constexpr int PW = PT / 32;
-constexpr int64_t MAX_LS = 16384;
+constexpr int MAX_M = 32;
 constexpr int MAX_CS = 16;
+constexpr int64_t SMEM_CAND = 16384;             // candidates sortable in shared memory
 
 struct ProjArgs {
   int mode;
@@ -46,106 +49,64 @@ struct ProjArgs {
 
 struct ProjShared {
   double slot[2][MAX_CS][4];  // cluster reduction slots (double-buffered)
+  long long slotl[2][MAX_CS];
   double wv[PW][4];
-  double bc[8];
   long long wl[PW][2];
-  long long slotl[2][MAX_CS][2];
+  double bc[8];
   int red_par;
+  int dec;
 };
 
-// ---------------------------------------------------------------- block helpers
-// canonical tree over the CTA slice: warp w owns contiguous 32-element chunks
-template <class F>
-__device__ __forceinline__ double slice_tree(int64_t ls, const F& leaf, ProjShared& sh) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nchunks = ls >> 5;
-  const int64_t per = nchunks >= PW ? nchunks / PW : 1;
-  const int active = nchunks >= PW ? PW : (int)nchunks;
-  double v = 0.0;
-  if (warp < active) {
-    Counter<16> acc;
-    for (int64_t c = 0; c < per; ++c) {
-      const int64_t j = ((int64_t)warp * per + c) * 32 + lane;
-      acc.push(warp_tree(leaf(j)), (uint32_t)c);
-    }
-    v = acc.final_value((uint32_t)per);
-  }
-  if (lane == 0) sh.wv[warp][0] = v;
+// ---------------------------------------------------------------- helpers
+template <int M>
+__device__ __forceinline__ int swz(int e) {  // bank-conflict-free thread-run layout
+  constexpr int C = M >= 16 ? 15 : M - 1;
+  const int t = e / M, k = e - t * M;
+  return t * M + (k ^ (t & C));
+}
+
+// canonical block tree of one value per thread (threads own consecutive aligned runs)
+__device__ __forceinline__ double block_tree(double v, ProjShared& sh, int c) {
+  v = warp_tree(v);
+  if ((threadIdx.x & 31) == 0) sh.wv[threadIdx.x >> 5][c] = v;
   __syncthreads();
   double r = 0.0;
-  if (warp == 0) {
-    double x = lane < PW ? sh.wv[lane][0] : 0.0;
+  if (threadIdx.x < 32) {
+    double x = threadIdx.x < PW ? sh.wv[threadIdx.x][c] : 0.0;
 #pragma unroll
     for (int o = 1; o < PW; o <<= 1) x = add(x, __shfl_xor_sync(0xffffffffu, x, o));
     r = x;
   }
   __syncthreads();
-  if (threadIdx.x == 0) sh.wv[0][1] = r;
+  if (threadIdx.x == 0) sh.wv[0][c] = r;
   __syncthreads();
-  r = sh.wv[0][1];
+  r = sh.wv[0][c];
   __syncthreads();
   return r;
-}
-
-// Cluster-wide combine of per-CTA values.  kinds[c]: 0 = canonical tree sum over ranks,
-// 1 = max, 2 = plain sum.  Every CTA of the cluster must call it in the same order.
-__device__ void cluster_combine(double* vals, const int* kinds, int nv, ProjShared& sh,
-                                cg::cluster_group& cl, int cs) {
-  const int par = sh.red_par;
-  const unsigned rank = cl.block_rank();
-  if (threadIdx.x == 0)
-    for (int c = 0; c < nv; ++c) sh.slot[par][rank][c] = vals[c];
-  cl.sync();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    for (int c = 0; c < nv; ++c) {
-      double x = 0.0;
-      if (lane < cs) {
-        const ProjShared* rem = cl.map_shared_rank(&sh, lane);
-        x = rem->slot[par][lane][c];
-      }
-      for (int o = 1; o < cs; o <<= 1) {
-        const double y = __shfl_xor_sync(0xffffffffu, x, o);
-        x = kinds[c] == 1 ? fmax(x, y) : add(x, y);
-      }
-      if (lane == 0) sh.bc[c] = x;
-    }
-  }
-  __syncthreads();
-  for (int c = 0; c < nv; ++c) vals[c] = sh.bc[c];
-  __syncthreads();
-  if (threadIdx.x == 0) sh.red_par = par ^ 1;
-  __syncthreads();
 }
 
 __device__ __forceinline__ double block_max(double v, ProjShared& sh) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   v = warp_max(v);
-  if (lane == 0) sh.wv[warp][2] = v;
+  if ((threadIdx.x & 31) == 0) sh.wv[threadIdx.x >> 5][3] = v;
   __syncthreads();
-  if (warp == 0) {
-    double x = lane < PW ? sh.wv[lane][2] : -1.0;
-    x = warp_max(x);
-    if (lane == 0) sh.wv[0][3] = x;
-  }
-  __syncthreads();
-  const double r = sh.wv[0][3];
+  double r = -1.0;
+#pragma unroll
+  for (int w = 0; w < PW; ++w) r = fmax(r, sh.wv[w][3]);
   __syncthreads();
   return r;
 }
 
-__device__ __forceinline__ long long block_sum_ll(long long v, ProjShared& sh) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  v = warp_sum_ll(v);
-  if (lane == 0) sh.wl[warp][0] = v;
+__device__ __forceinline__ double block_sum_any(double v, ProjShared& sh) {  // order-free
+  v = warp_tree(v);
+  if ((threadIdx.x & 31) == 0) sh.wv[threadIdx.x >> 5][2] = v;
   __syncthreads();
-  long long r = 0;
-  for (int w = 0; w < PW; ++w) r += sh.wl[w][0];
+  double r = 0.0;
+#pragma unroll
+  for (int w = 0; w < PW; ++w) r += sh.wv[w][2];
   __syncthreads();
   return r;
 }
 
-// exclusive prefix of per-thread counts inside the block
 __device__ __forceinline__ long long block_excl_scan(long long v, ProjShared& sh,
                                                      long long* total) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -158,93 +119,263 @@ __device__ __forceinline__ long long block_excl_scan(long long v, ProjShared& sh
   if (lane == 31) sh.wl[warp][1] = inc;
   __syncthreads();
   long long base = 0, tot = 0;
+#pragma unroll
   for (int w = 0; w < PW; ++w) {
-    if (w < warp) base += sh.wl[w][1];
-    tot += sh.wl[w][1];
+    const long long c = sh.wl[w][1];
+    base += w < warp ? c : 0;
+    tot += c;
   }
   __syncthreads();
   *total = tot;
   return base + inc - v;
 }
 
-template <class T>
-__device__ void bitonic_desc(T* c, int64_t n2) {
-  for (int64_t k = 2; k <= n2; k <<= 1) {
-    for (int64_t j = k >> 1; j > 0; j >>= 1) {
-      for (int64_t i = threadIdx.x; i < n2; i += PT) {
-        const int64_t ixj = i ^ j;
-        if (ixj > i) {
-          const double a = c[i], b = c[ixj];
-          const bool desc = (i & k) == 0;
-          if (desc ? (a < b) : (a > b)) {
-            c[i] = b;
-            c[ixj] = a;
-          }
+// Cluster-wide combine of per-CTA values.  kinds[c]: 0 = canonical tree over ranks,
+// 1 = max, 2 = plain sum.  Every CTA must call it in the same order.
+__device__ void cluster_combine(double* vals, const int* kinds, int nv, ProjShared& sh,
+                                cg::cluster_group& cl, int cs) {
+  if (cs == 1) return;
+  const int par = sh.red_par;
+  const unsigned rank = cl.block_rank();
+  if (threadIdx.x == 0)
+    for (int c = 0; c < nv; ++c) sh.slot[par][rank][c] = vals[c];
+  cl.sync();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double x[4] = {0.0, 0.0, 0.0, 0.0};
+    if (lane < cs) {
+      const ProjShared* rem = cl.map_shared_rank(&sh, lane);
+      for (int c = 0; c < nv; ++c) x[c] = rem->slot[par][lane][c];
+    }
+    for (int c = 0; c < nv; ++c) {
+      for (int o = 1; o < cs; o <<= 1) {
+        const double y = __shfl_xor_sync(0xffffffffu, x[c], o);
+        x[c] = kinds[c] == 1 ? fmax(x[c], y) : add(x[c], y);
+      }
+      if (lane == 0) sh.bc[c] = x[c];
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < nv; ++c) vals[c] = sh.bc[c];
+  __syncthreads();
+  if (threadIdx.x == 0) sh.red_par = par ^ 1;
+  __syncthreads();
+}
+
+// descending bitonic sort of n2 (power of two) values by the first min(PT, n2/2) threads
+// (whole warps) of one CTA; the other threads return immediately.
+template <class P>
+__device__ void bitonic_desc(P c, int n2) {
+  const int half = n2 >> 1;
+  const int nthr = half >= PT ? PT : (half < 32 ? 32 : half);
+  if ((int)threadIdx.x >= nthr) return;
+  for (int k = 2; k <= n2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int pidx = threadIdx.x; pidx < half; pidx += nthr) {
+        const int i = ((pidx & ~(j - 1)) << 1) | (pidx & (j - 1));
+        const int ixj = i + j;
+        const double a = c[i], b = c[ixj];
+        const bool desc = (i & k) == 0;
+        if (desc ? (a < b) : (a > b)) {
+          c[i] = b;
+          c[ixj] = a;
         }
       }
-      __syncthreads();
+      if (nthr == 32) __syncwarp();
+      else named_bar_sync(2, nthr);
     }
   }
 }
 
+// Exact emulation of the reference's sequential cumulative sum (prox.cpp:44-51) over the
+// sorted candidates c[0..L) (descending, >= 0), fused with its break test.  While the
+// running sum S stays inside one binade [2^e, 2^(e+1)), every fl(S + m) is S plus m rounded
+// to the fixed grid u = 2^(e-52) (round-to-nearest; ties depend on S and are left to a
+// scalar step), so a block of positions is an exact integer prefix scan of grid counts.
+// The first position whose sum leaves the binade (or ties) is done as one IEEE addition and
+// starts the next epoch.  Returns the first failing index ff (L if none) and S_{ff-1}.
+struct ScanShared {
+  long long wsum[PW];
+  long long fmin[PW];
+  double sv[PT];
+};
+
+__device__ long long prefix_break(const double* c, long long L, double rho, ScanShared& ss,
+                                  ProjShared& sh, double* s_before) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  long long i0 = 0;
+  double S_prev = 0.0;  // fl-sequential sum of c[0..i0)
+  long long ff = L;
+  while (i0 < L) {
+    // scalar step: first position, a binade crossing, a tie, or a (sub)tiny running sum
+    const bool scalar = (i0 == 0) || !(S_prev >= 0x1.0p-960);
+    long long f = 0;  // positions [i0, i0+f) are exact from the scan
+    long long fail = LLONG_MAX;
+    if (!scalar) {
+      const long long i = i0 + tid;
+      const bool valid = i < L;
+      const long long ebits = (__double_as_longlong(S_prev) >> 52) & 0x7ff;
+      const double u = __longlong_as_double((ebits - 52) << 52);           // 2^(e-52)
+      const double inv_u = __longlong_as_double((2046 - ebits + 52) << 52); // 2^(52-e)
+      const long long base_q = (long long)(S_prev * inv_u);                // exact, < 2^53
+      long long inc = 0;
+      bool tie = false;
+      double m = 0.0;
+      if (valid) {
+        m = c[i];
+        const double qd = floor(m * inv_u);
+        const double r = sub(m, qd * u);
+        const double hu = 0.5 * u;
+        tie = (r == hu);
+        inc = (long long)qd + (r > hu ? 1 : 0);
+      }
+      // inclusive block scan of inc
+      long long p = inc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, p, o);
+        if (lane >= o) p += y;
+      }
+      if (lane == 31) ss.wsum[warp] = p;
+      __syncthreads();
+      long long off = 0;
+#pragma unroll
+      for (int w = 0; w < PW; ++w) off += w < warp ? ss.wsum[w] : 0;
+      p += off;
+      const bool bad = valid && (tie || base_q + p >= (1LL << 53));
+      // first bad position
+      long long fb = bad ? (long long)tid : LLONG_MAX;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) fb = min(fb, __shfl_xor_sync(0xffffffffu, fb, o));
+      if (lane == 0) ss.fmin[warp] = fb;
+      __syncthreads();
+      long long fbad = LLONG_MAX;
+#pragma unroll
+      for (int w = 0; w < PW; ++w) fbad = min(fbad, ss.fmin[w]);
+      const long long nvalid = (L - i0) < PT ? (L - i0) : PT;
+      f = fbad < nvalid ? fbad : nvalid;
+      double S = 0.0;
+      bool my_fail = false;
+      if (tid < f) {
+        S = (double)(base_q + p) * u;  // exact: integer < 2^53 times a power of two
+        ss.sv[tid] = S;
+        const double cand = dvd(sub(S, rho), (double)(i + 1));
+        my_fail = !(m > cand);
+      }
+      long long fl = my_fail ? (long long)tid : LLONG_MAX;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) fl = min(fl, __shfl_xor_sync(0xffffffffu, fl, o));
+      __syncthreads();
+      if (lane == 0) ss.fmin[warp] = fl;
+      __syncthreads();
+#pragma unroll
+      for (int w = 0; w < PW; ++w) fail = min(fail, ss.fmin[w]);
+      if (fail != LLONG_MAX) {
+        ff = i0 + fail;
+        *s_before = fail == 0 ? S_prev : ss.sv[fail - 1];
+        __syncthreads();
+        return ff;
+      }
+      if (f > 0) S_prev = ss.sv[f - 1];
+      __syncthreads();
+      i0 += f;
+      if (f == nvalid) continue;
+    }
+    // one IEEE addition at position i0
+    if (tid == 0) {
+      const double S = add(S_prev, c[i0]);
+      const double cand = dvd(sub(S, rho), (double)(i0 + 1));
+      sh.bc[7] = S;
+      sh.dec = !(c[i0] > cand);
+    }
+    __syncthreads();
+    const double S = sh.bc[7];
+    const int failed = sh.dec;
+    __syncthreads();
+    if (failed) {
+      *s_before = S_prev;
+      return i0;
+    }
+    S_prev = S;
+    ++i0;
+  }
+  *s_before = S_prev;
+  return ff;
+}
+
+__device__ __forceinline__ double soft(double v, double th) {
+  return v > th ? sub(v, th) : (v < -th ? add(v, th) : 0.0);
+}
+
 // ---------------------------------------------------------------- the kernel
+template <int M>
 __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   cg::cluster_group cl = cg::this_cluster();
   const unsigned rank = cl.block_rank();
   const int cs = a.cs;
-  extern __shared__ __align__(16) double dyn[];
-  double* vs = dyn;               // v slice (ls)
-  double* cand = dyn + a.ls;      // CTA 0 candidate buffer (cand_cap + 1)
+  constexpr int64_t LS = (int64_t)PT * M;
+  extern __shared__ __align__(16) double dyn[];  // staging (LS) / CTA 0 candidates
   __shared__ ProjShared sh;
-  __shared__ int s_dec;
+  __shared__ ScanShared scan_sh;
+  __shared__ DevState sst;
   DevState* st = a.st;
-  if (threadIdx.x == 0) sh.red_par = 0;
-  const bool prof = (a.mode == PROJ_ITER) && cl.block_rank() == 0 && threadIdx.x == 0;
+  const int tid = threadIdx.x;
+  if (tid == 0) sh.red_par = 0;
+  const bool prof = (a.mode == PROJ_ITER) && rank == 0 && tid == 0;
   long long t_last = clock64();
   auto mark = [&](int idx) {
     if (prof) {
       const long long t = clock64();
-      st->prof[idx] += (double)(t - t_last);
+      sst.prof[idx] += (double)(t - t_last);
       t_last = t;
     }
   };
   auto count = [&](int idx, double v) {
-    if (prof) st->prof[idx] += v;
+    if (prof) sst.prof[idx] += v;
   };
-  if (a.mode == PROJ_ITER && st->status != RUNNING) return;  // uniform over the cluster
-  const l1g_gp_config cfg = st->cfg;
-  const double rho = a.mode == PROJ_PLAIN ? st->rho : st->rho;
-  const int cur = a.mode == PROJ_ITER ? st->cur : 0;
+  // one coalesced copy of the device state instead of many dependent scalar loads
+  {
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sst);
+    for (int i = tid; i < (int)(sizeof(DevState) / 8); i += PT) dst[i] = src[i];
+  }
+  __syncthreads();
+  if (a.mode == PROJ_ITER && sst.status != RUNNING) return;  // uniform over the cluster
+  const l1g_gp_config cfg = sst.cfg;
+  const double rho = sst.rho;
+  const int cur = a.mode == PROJ_ITER ? sst.cur : 0;
   const double* x = a.mode == PROJ_ITER ? a.vb.x[cur] : a.xin;
   const double* g = a.mode == PROJ_ITER ? a.vb.g[cur] : a.gin;
-  const int64_t base = (int64_t)rank * a.ls;
-  const int64_t lim = a.p_pad - base < a.ls ? (a.p_pad - base > 0 ? a.p_pad - base : 0) : a.ls;
+  const int64_t base = (int64_t)rank * LS;
+  const int64_t lim = a.p_pad - base < LS ? (a.p_pad - base > 0 ? a.p_pad - base : 0) : LS;
 
   // ---- steplength and loop-top checks (gpss.cpp:233-245, :147-153), CTA 0 decides
   double alpha = 1.0, first_alpha = 1.0;
   if (a.mode == PROJ_ITER) {
-    if (rank == 0 && threadIdx.x == 0) {
+    if (rank == 0 && tid == 0) {
       int dec = 0;
-      if (!st->single_step) {
-        if (st->max_iterations > 0 && st->k >= st->max_iterations) dec = 1 + L1G_MAX_ITERATIONS;
-        else if (st->max_matvecs > 0 && st->matvecs >= st->max_matvecs) dec = 1 + L1G_MAX_MATVECS;
-        else if (st->max_seconds > 0.0 && elapsed_s(st) >= st->max_seconds) dec = 1 + L1G_MAX_SECONDS;
-      } else if (st->stationary) {
+      if (!sst.single_step) {
+        if (sst.max_iterations > 0 && sst.k >= sst.max_iterations) dec = 1 + L1G_MAX_ITERATIONS;
+        else if (sst.max_matvecs > 0 && sst.matvecs >= sst.max_matvecs) dec = 1 + L1G_MAX_MATVECS;
+        else if (sst.max_seconds > 0.0 && elapsed_s(&sst) >= sst.max_seconds) dec = 1 + L1G_MAX_SECONDS;
+      } else if (sst.stationary) {
         dec = 1 + L1G_STATIONARY;
       }
-      double al = st->alpha0;
+      double al = sst.alpha0;
       if (dec == 0) {
-        if (st->k == 0) {
-          l1g_sl_choice c;
-          c.alpha = st->alpha0;
+        l1g_sl_choice c;
+        if (sst.k == 0) {
+          c.alpha = sst.alpha0;
           c.bb_active = 0;
           c.bb1_raw = c.bb2_raw = c.tau_before = c.tau_after = nan_d();
-          st->choice = c;
         } else {
-          steplength_from_dots(&st->tau, st->a2h, &st->a2_len, st->sz, st->ss, st->zz, cfg,
-                               &st->choice);
+          steplength_from_dots(&sst.tau, sst.a2h, &sst.a2_len, sst.sz, sst.ss, sst.zz, cfg, &c);
+          st->tau = sst.tau;
+          for (int i = 0; i < sst.a2_len; ++i) st->a2h[i] = sst.a2h[i];
+          st->a2_len = sst.a2_len;
         }
-        al = st->choice.alpha;
+        st->choice = c;
+        al = c.alpha;
       } else {
         st->status = STOPPED;
         st->reason = dec - 1;
@@ -254,44 +385,52 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         }
       }
       sh.bc[6] = al;
-      s_dec = dec;
+      sh.dec = dec;
     }
     cl.sync();
-    if (threadIdx.x == 0) {
+    if (tid == 0 && rank != 0) {
       const ProjShared* r0 = cl.map_shared_rank(&sh, 0);
-      const int* d0 = cl.map_shared_rank(&s_dec, 0);
-      sh.bc[7] = r0->bc[6];
-      s_dec = *d0;
+      sh.bc[6] = r0->bc[6];
+      sh.dec = r0->dec;
     }
     cl.sync();
-    if (s_dec != 0) return;
-    alpha = first_alpha = sh.bc[7];
+    if (sh.dec != 0) return;
+    alpha = first_alpha = sh.bc[6];
   }
 
   double first_stat = 0.0;
   count(8, 1.0);
   mark(0);
+  double v[M];
   for (int attempt = 0;; ++attempt) {
     count(9, 1.0);
-    // ---- v = x - alpha g  (gpss.cpp:167; alpha0: x0 - grad, gpss.cpp:95)
-    for (int64_t j = threadIdx.x; j < a.ls; j += PT) {
-      double v = 0.0;
+    // ---- v = x - alpha g  (gpss.cpp:167; alpha0: x0 - grad, gpss.cpp:95): coalesced
+    //      loads, staged through shared memory into per-thread registers
+    for (int64_t j = tid; j < LS; j += PT) {
+      double val = 0.0;
       if (j < lim) {
         const int64_t gj = base + j;
-        if (a.mode == PROJ_PLAIN) v = x[gj];
-        else if (a.mode == PROJ_ALPHA0) v = sub(x[gj], g[gj]);
-        else v = sub(x[gj], mul(alpha, g[gj]));
+        if (a.mode == PROJ_PLAIN) val = x[gj];
+        else if (a.mode == PROJ_ALPHA0) val = sub(x[gj], g[gj]);
+        else val = sub(x[gj], mul(alpha, g[gj]));
       }
-      vs[j] = v;
+      dyn[swz<M>((int)j)] = val;
     }
     __syncthreads();
-    double red[4];
-    const int k_l1max[2] = {0, 1};
-    red[0] = slice_tree(a.ls, [&](int64_t j) { return fabs(vs[j]); }, sh);
-    double lm = 0.0;
-    for (int64_t j = threadIdx.x; j < a.ls; j += PT) lm = fmax(lm, fabs(vs[j]));
-    red[1] = block_max(lm, sh);
-    cluster_combine(red, k_l1max, 2, sh, cl, cs);
+#pragma unroll
+    for (int k = 0; k < M; ++k) v[k] = dyn[swz<M>(tid * M + k)];
+    __syncthreads();
+    double red[2];
+    {
+      const double t = tree<M>([&](int k) { return fabs(v[k]); });
+      double m = 0.0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) m = fmax(m, fabs(v[k]));
+      red[0] = block_tree(t, sh, 0);
+      red[1] = block_max(m, sh);
+      const int kinds[2] = {0, 1};
+      cluster_combine(red, kinds, 2, sh, cl, cs);
+    }
     const double l1v = red[0], vinf = red[1];
     mark(1);
 
@@ -305,39 +444,28 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       branch = 1;
     } else {
       branch = 2;
-      // Michelot pivot iteration: theta_{t+1} = (sum_{|v|>theta_t} |v| - rho) / #{|v|>theta_t}
+      // Michelot pivot iteration from below: th_{t+1} = (sum_{|v|>th_t} |v| - rho) / count
       double th = dvd(sub(l1v, rho), (double)a.p_pad);
-      double cnt_prev = -1.0;
+      double cnt_prev = (double)a.p_pad + 1.0;
       const int kinds_cs[2] = {2, 2};
       for (int it = 0; it < 64; ++it) {
         double c = 0.0, s = 0.0;
-        for (int64_t j = threadIdx.x; j < lim; j += PT) {
-          const double m = fabs(vs[j]);
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          const double m = fabs(v[k]);
           if (m > th) {
             c += 1.0;
             s += m;
           }
         }
-        // block sums (order irrelevant: only brackets the exact search below)
-        c = warp_tree(c);
-        s = warp_tree(s);
-        if ((threadIdx.x & 31) == 0) {
-          sh.wv[threadIdx.x >> 5][0] = c;
-          sh.wv[threadIdx.x >> 5][1] = s;
-        }
-        __syncthreads();
-        double cc = 0.0, ss = 0.0;
-        for (int w = 0; w < PW; ++w) {
-          cc += sh.wv[w][0];
-          ss += sh.wv[w][1];
-        }
-        __syncthreads();
-        double v2[2] = {cc, ss};
+        double v2[2] = {block_sum_any(c, sh), block_sum_any(s, sh)};
         cluster_combine(v2, kinds_cs, 2, sh, cl, cs);
         count(10, 1.0);
-        if (v2[0] == cnt_prev || v2[0] == 0.0) break;
+        if (v2[0] == 0.0 || v2[0] >= cnt_prev) break;
+        const double shrink = cnt_prev - v2[0];
         cnt_prev = v2[0];
         th = dvd(sub(v2[1], rho), v2[0]);
+        if (shrink * 64.0 <= v2[0]) break;  // converged to within ~1.5% of the support
       }
       mark(2);
       // exact sort-and-scan on the elements above a bracket below theta
@@ -345,115 +473,90 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       for (int tries = 0;; ++tries) {
         long long myc = 0;
         double mynext = -1.0;
-        for (int64_t j = threadIdx.x; j < lim; j += PT) {
-          const double m = fabs(vs[j]);
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          const double m = fabs(v[k]);
           if (m > lo) ++myc;
           else mynext = fmax(mynext, m);
         }
         long long ctot;
         const long long off = block_excl_scan(myc, sh, &ctot);
         const double bnext = block_max(mynext, sh);
-        // cluster: per-rank counts -> offsets; global next
-        if (threadIdx.x == 0) {
-          sh.slotl[sh.red_par][rank][0] = ctot;
-          sh.slot[sh.red_par][rank][0] = bnext;
-        }
-        cl.sync();
-        if (threadIdx.x == 0) {
-          long long before = 0, total = 0;
-          double nx = -1.0;
-          const int par = sh.red_par;
-          for (int r = 0; r < cs; ++r) {
-            const ProjShared* rem = cl.map_shared_rank(&sh, r);
-            const long long cr = rem->slotl[par][r][0];
-            if (r < (int)rank) before += cr;
-            total += cr;
-            nx = fmax(nx, rem->slot[par][r][0]);
+        long long before = 0, total = ctot;
+        double next = bnext;
+        if (cs > 1) {
+          if (tid == 0) {
+            sh.slotl[sh.red_par][rank] = ctot;
+            sh.slot[sh.red_par][rank][0] = bnext;
           }
-          sh.wl[0][0] = before;
-          sh.wl[0][1] = total;
-          sh.bc[5] = nx;
+          cl.sync();
+          if (tid == 0) {
+            long long b = 0, tt = 0;
+            double nx = -1.0;
+            const int par = sh.red_par;
+            for (int r = 0; r < cs; ++r) {
+              const ProjShared* rem = cl.map_shared_rank(&sh, r);
+              const long long cr = rem->slotl[par][r];
+              b += r < (int)rank ? cr : 0;
+              tt += cr;
+              nx = fmax(nx, rem->slot[par][r][0]);
+            }
+            sh.wl[0][0] = b;
+            sh.wl[0][1] = tt;
+            sh.bc[5] = nx;
+          }
+          __syncthreads();
+          before = sh.wl[0][0];
+          total = sh.wl[0][1];
+          next = sh.bc[5];
+          __syncthreads();
+          if (tid == 0) sh.red_par ^= 1;
+          __syncthreads();
         }
-        __syncthreads();
-        const long long before = sh.wl[0][0], total = sh.wl[0][1];
-        const double next = sh.bc[5];
-        __syncthreads();
-        if (threadIdx.x == 0) sh.red_par ^= 1;
-        __syncthreads();
         const long long L = total + (next >= 0.0 ? 1 : 0);
         int64_t n2 = 1;
         while (n2 < total) n2 <<= 1;
         const bool in_smem = (n2 + 1 <= a.cand_cap);
-        double* cbuf = in_smem ? cl.map_shared_rank(cand, 0) : a.gcand;
-        // scatter candidates (order is irrelevant: they are sorted next)
+        double* cbuf = in_smem ? cl.map_shared_rank(dyn, 0) : a.gcand;
         long long pos = before + off;
-        for (int64_t j = threadIdx.x; j < lim; j += PT) {
-          const double m = fabs(vs[j]);
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          const double m = fabs(v[k]);
           if (m > lo) cbuf[pos++] = m;
         }
-        __threadfence();
+        if (!in_smem) __threadfence();
         cl.sync();
         mark(3);
         count(11, (double)total);
-        __shared__ int s_ff;
         if (rank == 0) {
-          double* c = in_smem ? cand : a.gcand;
-          for (int64_t i = total + threadIdx.x; i < n2; i += PT) c[i] = 0.0;
+          double* c = in_smem ? dyn : a.gcand;
+          for (int64_t i = total + tid; i < n2; i += PT) c[i] = 0.0;
           __syncthreads();
-          bitonic_desc(c, n2);
-          if (threadIdx.x == 0 && next >= 0.0) c[total] = next;
+          bitonic_desc(c, (int)n2);
+          __syncthreads();
+          if (tid == 0 && next >= 0.0) c[total] = next;
           __syncthreads();
           mark(4);
-          double* pre = a.gpre;
-          if (threadIdx.x == 0) {  // the reference's sequential cumulative sum
-            double S = 0.0;
-            for (long long i = 0; i < L; ++i) {
-              S = add(S, c[i]);
-              pre[i] = S;
-            }
-          }
-          __syncthreads();
-          long long ff = L;  // first failing index
-          for (long long i = threadIdx.x; i < L; i += PT) {
-            const double cand_i = dvd(sub(__ldcg(pre + i), rho), (double)(i + 1));
-            if (!(c[i] > cand_i)) {
-              ff = i;
-              break;
-            }
-          }
-          // block min
-          ff = -ff;
-          {
-            long long v = ff;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-            if ((threadIdx.x & 31) == 0) sh.wl[threadIdx.x >> 5][0] = v;
-            __syncthreads();
-            long long m = LLONG_MIN;
-            for (int w = 0; w < PW; ++w) m = max(m, sh.wl[w][0]);
-            __syncthreads();
-            ff = -m;
-          }
-          if (threadIdx.x == 0) {
-            double thv = 0.0;
-            if (ff > 0) thv = dvd(sub(__ldcg(pre + ff - 1), rho), (double)ff);
+          double s_before = 0.0;
+          const long long ff = prefix_break(c, L, rho, scan_sh, sh, &s_before);
+          if (tid == 0) {
+            // theta = candidate of the last passing index (prox.cpp:47-50); 0 if none passed
+            sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
             // all passed although smaller elements exist: the bracket was too high
-            const int retry = (ff == L && next >= 0.0) ? 1 : 0;
-            sh.bc[4] = thv;
-            s_ff = retry;
+            sh.dec = (ff == L && next >= 0.0) ? 1 : 0;
           }
+          mark(5);
         }
         cl.sync();
-        if (threadIdx.x == 0) {
+        if (tid == 0 && rank != 0) {
           const ProjShared* r0 = cl.map_shared_rank(&sh, 0);
-          const int* f0 = cl.map_shared_rank(&s_ff, 0);
-          sh.bc[3] = r0->bc[4];
-          s_dec = *f0;
+          sh.bc[4] = r0->bc[4];
+          sh.dec = r0->dec;
         }
-        cl.sync();
-        mark(5);
-        if (!s_dec) {
-          theta = sh.bc[3];
+        if (cs > 1) cl.sync();
+        else __syncthreads();
+        if (!sh.dec) {
+          theta = sh.bc[4];
           break;
         }
         count(13, 1.0);
@@ -465,12 +568,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       const int k_sum[1] = {0};
       int guard = 0;
       for (;;) {
-        double l1u[1];
         const double thc = theta;
-        l1u[0] = slice_tree(a.ls, [&](int64_t j) {
-          const double v = vs[j];
-          return fabs(v > thc ? sub(v, thc) : (v < -thc ? add(v, thc) : 0.0));
-        }, sh);
+        double l1u[1] = {block_tree(tree<M>([&](int k) { return fabs(soft(v[k], thc)); }), sh, 1)};
         cluster_combine(l1u, k_sum, 1, sh, cl, cs);
         if (!(l1u[0] > rho && guard++ < 64)) break;
         count(12, 1.0);
@@ -482,34 +581,44 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
 
     // ---- h, d = h - x, ||h - x||_inf, g'd, support  (gpss.cpp:167-178)
     const double th = theta;
-    auto hval = [&](double v) {
-      if (branch == 0) return 0.0;
-      if (branch == 1) return v;
-      return v > th ? sub(v, th) : (v < -th ? add(v, th) : 0.0);
-    };
-    double lmax = 0.0, hmax = 0.0;
+    double hmax = 0.0;
     long long sup = 0;
-    for (int64_t j = threadIdx.x; j < a.ls; j += PT) {
-      const double h = hval(vs[j]);
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double h = branch == 0 ? 0.0 : (branch == 1 ? v[k] : soft(v[k], th));
+      v[k] = h;  // v holds h from here on (an escalation recomputes v)
       sup += (h != 0.0);
       hmax = fmax(hmax, fabs(h));
-      if (j < lim && a.mode != PROJ_ALPHA0) {
-        const int64_t gj = base + j;
-        const double dj = a.mode == PROJ_PLAIN ? h : sub(h, x[gj]);
-        lmax = fmax(lmax, fabs(dj));
-        a.out[gj] = dj;
-      }
     }
-    double gdl = 0.0;
-    if (a.mode == PROJ_ITER) {
-      gdl = slice_tree(a.ls, [&](int64_t j) {
-        if (j >= lim) return 0.0;
-        const int64_t gj = base + j;
-        return mul(g[gj], sub(hval(vs[j]), x[gj]));
-      }, sh);
+    double gdl = 0.0, lmax = 0.0;
+    if (a.mode != PROJ_ALPHA0) {
+      // stage h, then coalesced d = h - x (written out) and leaf g_j d_j
+#pragma unroll
+      for (int k = 0; k < M; ++k) dyn[swz<M>(tid * M + k)] = v[k];
+      __syncthreads();
+      for (int64_t j = tid; j < LS; j += PT) {
+        const int p = swz<M>((int)j);
+        const double h = dyn[p];
+        double leaf = 0.0;
+        if (j < lim) {
+          const int64_t gj = base + j;
+          const double dj = a.mode == PROJ_PLAIN ? h : sub(h, x[gj]);
+          lmax = fmax(lmax, fabs(dj));
+          a.out[gj] = dj;
+          if (a.mode == PROJ_ITER) leaf = mul(g[gj], dj);
+        }
+        dyn[p] = leaf;
+      }
+      __syncthreads();
+      if (a.mode == PROJ_ITER) {
+#pragma unroll
+        for (int k = 0; k < M; ++k) v[k] = dyn[swz<M>(tid * M + k)];
+        gdl = block_tree(tree<M>([&](int k) { return v[k]; }), sh, 2);
+      }
+      __syncthreads();
     }
     double red2[4] = {gdl, block_max(lmax, sh), block_max(hmax, sh),
-                      (double)block_sum_ll(sup, sh)};
+                      block_sum_any((double)sup, sh)};
     const int kinds2[4] = {0, 1, 1, 2};
     cluster_combine(red2, kinds2, 4, sh, cl, cs);
     const double gd = red2[0], stat = red2[1], hinf = red2[2];
@@ -517,7 +626,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     mark(7);
 
     if (a.mode != PROJ_ITER) {
-      if (rank == 0 && threadIdx.x == 0) {
+      if (rank == 0 && tid == 0) {
         st->theta = theta;
         st->support = support;
         st->h_inf = hinf;
@@ -529,7 +638,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     // escalation (gpss.cpp:169-191); every CTA takes the same decision
     if (attempt == 0) first_stat = stat;
     int outcome;  // 0 stationary, 1 accepted, 2 floor stop, 3 escalate
-    if (stat <= st->stationarity_tol) outcome = 0;
+    if (stat <= sst.stationarity_tol) outcome = 0;
     else if (gd < 0.0) outcome = 1;
     else if (alpha >= cfg.alpha_max) outcome = 2;
     else outcome = 3;
@@ -538,7 +647,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       alpha = a10 < cfg.alpha_max ? a10 : cfg.alpha_max;
       continue;
     }
-    if (rank == 0 && threadIdx.x == 0) {
+    if (rank == 0 && tid == 0) {
       st->out_stationarity = outcome == 2 ? first_stat : stat;
       if (outcome == 1) {
         st->alpha_used = alpha;
@@ -551,8 +660,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         st->status = STOPPED;
         st->reason = L1G_STATIONARY;
         l1g_iter_record& r = st->last;
-        r.k = st->k;
-        r.f = st->f;
+        r.k = sst.k;
+        r.f = sst.f;
         r.alpha = outcome == 2 ? first_alpha : alpha;
         r.stationarity = outcome == 2 ? first_stat : stat;
         r.step = nan_d();
@@ -563,50 +672,71 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     }
     break;
   }
+  if (prof)
+    for (int i = 0; i < 16; ++i) st->prof[i] = sst.prof[i];
   cl.sync();
 }
 
 // ---------------------------------------------------------------- host side
-ProjPlan make_proj_plan(int64_t p_pad) {
-  ProjPlan pp{};
-  int cs = 1;
-  while (cs < MAX_CS && (p_pad + cs - 1) / cs > 8192) cs <<= 1;
-  int64_t per = (p_pad + cs - 1) / cs;
-  int64_t ls = 32;
-  while (ls < per) ls <<= 1;
-  if (ls > MAX_LS) throw InvalidArgument("projection: p too large for the cluster kernel");
-  pp.cs = cs;
-  pp.ls = ls;
-  const size_t budget = 227 * 1024 - sizeof(ProjShared) - 256;
-  const int64_t cap = (int64_t)(budget / 8) - ls;
-  int64_t c2 = 1;
-  while (c2 * 2 <= cap) c2 <<= 1;
-  pp.cand_cap = c2 < cap ? c2 + 1 : c2;
-  if (pp.cand_cap > cap) pp.cand_cap = cap;
-  pp.smem = (size_t)(ls + pp.cand_cap) * 8;
-  return pp;
-}
-
 static int64_t pow2_at_least(int64_t v) {
   int64_t n = 1;
   while (n < v) n <<= 1;
   return n;
 }
 
+ProjPlan make_proj_plan(int64_t p_pad) {
+  // small vectors: one CTA; otherwise >= 4 elements per thread spread over up to 16 CTAs
+  // so the O(p) passes use enough SMs
+  ProjPlan pp{};
+  int64_t m = 1;
+  int cs = 1;
+  if (p_pad <= 8 * PT) {
+    while (PT * m < p_pad) m <<= 1;
+  } else {
+    m = 4;
+    while (PT * m * MAX_CS < p_pad) m <<= 1;
+    if (m > MAX_M) throw InvalidArgument("projection: p too large for the cluster kernel");
+    const int64_t need = (p_pad + PT * m - 1) / (PT * m);
+    while (cs < need) cs <<= 1;
+  }
+  pp.cs = cs;
+  pp.ls = PT * m;
+  pp.cand_cap = (pp.ls > SMEM_CAND ? pp.ls : SMEM_CAND) + 1;
+  pp.smem = (size_t)pp.cand_cap * 8;
+  return pp;
+}
+
 size_t proj_scratch_doubles(int64_t p_pad) {
   return (size_t)(pow2_at_least(p_pad) + 1) + (size_t)(p_pad + 2) + 64;
+}
+
+template <int M>
+static void proj_launch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    L1G_CUDA(cudaFuncSetAttribute(proj_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)((SMEM_CAND + 1) * 8)));
+    L1G_CUDA(cudaFuncSetAttribute(proj_kernel<M>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pp.cs, 1, 1);
+  cfg.blockDim = dim3(PT, 1, 1);
+  cfg.dynamicSmemBytes = pp.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = pp.cs;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  L1G_CUDA(cudaLaunchKernelEx(&cfg, proj_kernel<M>, a));
 }
 
 void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const double* xin,
                  const double* gin, double* out, double* scratch, DevState* st,
                  const VecBufs* vb, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    L1G_CUDA(cudaFuncSetAttribute(proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(227 * 1024 - sizeof(ProjShared) - 64)));
-    L1G_CUDA(cudaFuncSetAttribute(proj_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
   ProjArgs a{};
   a.mode = mode;
   a.p = p;
@@ -621,19 +751,15 @@ void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const d
   a.gpre = scratch + pow2_at_least(p_pad) + 1;
   a.st = st;
   if (vb) a.vb = *vb;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pp.cs, 1, 1);
-  cfg.blockDim = dim3(PT, 1, 1);
-  cfg.dynamicSmemBytes = pp.smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = pp.cs;
-  attrs[0].val.clusterDim.y = 1;
-  attrs[0].val.clusterDim.z = 1;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 1;
-  L1G_CUDA(cudaLaunchKernelEx(&cfg, proj_kernel, a));
+  switch (pp.ls / PT) {
+    case 1: proj_launch<1>(pp, a, s); break;
+    case 2: proj_launch<2>(pp, a, s); break;
+    case 4: proj_launch<4>(pp, a, s); break;
+    case 8: proj_launch<8>(pp, a, s); break;
+    case 16: proj_launch<16>(pp, a, s); break;
+    case 32: proj_launch<32>(pp, a, s); break;
+    default: throw InvalidArgument("projection: unsupported slice length");
+  }
 }
 
 }  // namespace l1g

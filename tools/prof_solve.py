@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--solves", type=int, default=1)
     ap.add_argument("--profile", action="store_true", help="print projection phase profile")
     ap.add_argument("--timing", action="store_true", help="per-kernel CUDA-event timing")
+    ap.add_argument("--trace", action="store_true", help="print per-iteration support sizes")
     a = ap.parse_args()
     spec = H.CONFIGS[a.config]
     fx = os.path.join(ROOT, "tests", "golden", "sigma_hat.json")
@@ -44,10 +45,17 @@ def main():
     for s in range(a.solves):
         t = time.perf_counter()
         L.check(lib.l1g_solver_init(h, None))
-        L.check(lib.l1g_solver_run(h, C.byref(stop), C.byref(res), None, 0))
+        cap = a.iters if a.trace else 0
+        recs = (L.IterRecordC * max(cap, 1))()
+        L.check(lib.l1g_solver_run(h, C.byref(stop), C.byref(res),
+                                   C.addressof(recs) if cap else None, cap))
         dt = time.perf_counter() - t
         print(f"solve {s}: {res.iterations} iterations ({L.REASONS[res.reason]}) in {dt*1e3:.2f} ms"
               f" = {res.iterations / dt:.1f} it/s, f={res.objective:.6e}", flush=True)
+    if a.trace:
+        sup = [recs[i].support for i in range(min(res.iterations, a.iters))]
+        print("support per iteration:", sup)
+        print("alpha per iteration:", [f"{recs[i].alpha:.3g}" for i in range(min(res.iterations, a.iters))])
     if a.timing:
         tp, tf, ta, ti, tl = (C.c_double(), C.c_double(), C.c_double(), C.c_int64(),
                               C.c_int64())
