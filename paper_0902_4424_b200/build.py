@@ -16,6 +16,25 @@ def lib_path():
     return os.path.join(HERE, "libl1g.so")
 
 
+def dropin_path():
+    return os.path.join(HERE, "libl1solve_b200.so")
+
+
+INCLUDE = os.path.join(HERE, "..", "include")
+CXX = os.environ.get("L1G_CXX", "/usr/bin/g++")
+
+
+def build_dropin(verbose=False):
+    """The reference's C++ API (include/l1solve/*.hpp) over the C-ABI."""
+    cmd = [CXX, "-std=c++17", "-O2", "-fPIC", "-shared", "-ffp-contract=off",
+           f"-I{INCLUDE}", os.path.join(CSRC, "l1solve_dropin.cpp"), "-o", dropin_path(),
+           f"-L{HERE}", "-l:libl1g.so", "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return dropin_path()
+
+
 def needs_build():
     out = lib_path()
     if not os.path.exists(out):
@@ -33,6 +52,7 @@ def build(force: bool = False, verbose: bool = False):
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
+    build_dropin(verbose)
     return lib_path()
 
 

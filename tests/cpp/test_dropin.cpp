@@ -1,0 +1,136 @@
+// Drop-in check of the C++ API (include/l1solve/*.hpp over libl1g.so): the calls a
+// reference caller makes (DenseOperator, Objective, L1Ball, gpss_solve with and without a
+// callback, gp_init/gp_iterate, steplength/backtracking/projection pieces, error classes),
+// each checked against closed forms or against the other entry points.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "l1solve/gpss.hpp"
+
+using namespace l1solve;
+
+static int g_fail = 0, g_pass = 0;
+#define EXPECT(c)                                                              \
+  do {                                                                         \
+    if (c) ++g_pass;                                                           \
+    else {                                                                     \
+      ++g_fail;                                                                \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);                 \
+    }                                                                          \
+  } while (0)
+#define EXPECT_THROW(stmt, E)                                                  \
+  do {                                                                         \
+    bool t_ = false;                                                           \
+    try {                                                                      \
+      stmt;                                                                    \
+    } catch (const E&) {                                                       \
+      t_ = true;                                                               \
+    }                                                                          \
+    EXPECT(t_);                                                                \
+  } while (0)
+
+static bool near(double a, double b, double eps) { return std::abs(a - b) <= eps * (1 + std::abs(b)); }
+
+// small seeded Gaussian-ish matrix without any RNG library: a fixed LCG
+static Matrix lcg_matrix(Index n, Index p, unsigned seed) {
+  Matrix m(n, p);
+  unsigned long long s = seed * 2654435761ull + 1;
+  for (Index j = 0; j < p; ++j)
+    for (Index i = 0; i < n; ++i) {
+      s = s * 6364136223846793005ull + 1442695040888963407ull;
+      m(i, j) = ((double)(s >> 11) * 0x1.0p-53 - 0.5) / std::sqrt((double)n);
+    }
+  return m;
+}
+
+int main() {
+  // operator arithmetic (2x2) and dimension errors
+  Matrix k2(2, 2);
+  k2(0, 0) = 1; k2(0, 1) = 2; k2(1, 0) = 0; k2(1, 1) = 1;
+  DenseOperator op2(k2);
+  MatvecCounter mv;
+  Vector y2 = op2.apply(Vector{1.0, 1.0}, mv);
+  EXPECT(y2[0] == 3.0 && y2[1] == 1.0);
+  Vector a2 = op2.apply_adjoint(Vector{1.0, 0.0}, mv);
+  EXPECT(a2[0] == 1.0 && a2[1] == 2.0);
+  EXPECT(mv.count == 2);
+  EXPECT_THROW(op2.apply(Vector{1.0, 2.0, 3.0}, mv), std::invalid_argument);
+
+  // projection known answers (prox.cpp semantics)
+  auto pr = project_l1_ball_with_threshold(Vector{0.9, 0.5}, L1Ball(1.0));
+  EXPECT(near(pr.threshold, 0.2, 1e-12) && near(pr.point[0], 0.7, 1e-12) && near(pr.point[1], 0.3, 1e-12));
+  EXPECT_THROW(L1Ball(-1.0), std::invalid_argument);
+  EXPECT_THROW(soft_threshold(Vector{1.0}, -0.1), std::invalid_argument);
+
+  // steplength worked example and backtracking hand trace
+  GpConfig cfg;
+  SteplengthState sl = steplength_init(cfg);
+  auto ch = steplength_select(sl, Vector{1.0, 1.0}, Vector{1.0, 3.0}, cfg, 1);
+  EXPECT(ch.bb_active && near(ch.alpha, 0.5, 1e-15) && near(sl.tau, 0.55, 1e-15));
+  Matrix one(1, 1);
+  one(0, 0) = 1.0;
+  DenseOperator op1(one);
+  Objective o1(op1, Vector{0.0});
+  auto bt = backtracking_search(o1, Vector{1.0}, Vector{-2.0}, 1.0, -4.0, cfg, mv);
+  EXPECT(near(bt.step, 0.5, 1e-15) && bt.halvings == 1);
+  EXPECT_THROW(backtracking_search(o1, Vector{1.0}, Vector{-2.0}, -1e10, -4.0, cfg, mv),
+               std::runtime_error);
+
+  // identity operator: gpss reaches the projection of y
+  DenseOperator id(Matrix::Identity(2, 2));
+  StopRule stop;
+  stop.max_iterations = 50;
+  stop.stationarity_tol = 1e-10;
+  SolverState s = gpss_solve(Objective(id, Vector{3.0, 0.0}), L1Ball(1.0), cfg, stop);
+  EXPECT(std::abs(s.x[0] - 1.0) <= 1e-10 && s.x[1] == 0.0 && s.reason == StopReason::Stationary);
+  EXPECT_THROW(gpss_solve(Objective(id, Vector{1.0, 1.0}), L1Ball(0.5), cfg, stop, {},
+                          Vector{1.0, 1.0}),
+               std::invalid_argument);
+
+  // a 60 x 200 problem: graph path == callback path == gp_iterate steps; records consistent
+  const Matrix K = lcg_matrix(60, 200, 7);
+  DenseOperator op(K);
+  Vector xt(200);
+  xt[3] = 1.0; xt[50] = -1.0; xt[120] = 0.5;
+  MatvecCounter m0;
+  const Vector y = op.apply(xt, m0);
+  const Objective obj(op, y);
+  const L1Ball ball(2.5);
+  StopRule st2;
+  st2.max_iterations = 40;
+  st2.stationarity_tol = 0.0;
+  const SolverState sa = gpss_solve(obj, ball, cfg, st2);
+  std::vector<IterationRecord> recs;
+  Vector last;
+  const SolverState sb = gpss_solve(obj, ball, cfg, st2, [&](const IterationRecord& r, const Vector& x) {
+    recs.push_back(r);
+    last = x;
+  });
+  EXPECT(sa.iterations == sb.iterations && (long)recs.size() == sa.iterations);
+  bool same = sa.x.size() == sb.x.size();
+  for (Index i = 0; same && i < sa.x.size(); ++i) same = sa.x[i] == sb.x[i] && last[i] == sa.x[i];
+  EXPECT(same);
+  EXPECT(sa.matvecs.count == 2 + 2 * sa.iterations);
+  bool mono = true;
+  for (std::size_t i = 1; i < recs.size(); ++i) mono = mono && recs[i].f <= recs[i - 1].f;
+  EXPECT(mono);
+  MatvecCounter mv2;
+  GpIterationState gs = gp_init(obj, ball, Vector(), cfg, mv2);
+  SteplengthState sls = steplength_init(cfg);
+  for (long i = 0; i < sa.iterations; ++i) gp_iterate(obj, ball, cfg, gs, sls, mv2, 0.0);
+  const Vector gx = gs.x();
+  bool same2 = true;
+  for (Index i = 0; i < gx.size(); ++i) same2 = same2 && gx[i] == sa.x[i];
+  EXPECT(same2 && mv2.count == sa.matvecs.count);
+
+  // spectral norm of a diagonal operator
+  Matrix dg = Matrix::Zero(2, 2);
+  dg(0, 0) = 1.0;
+  dg(1, 1) = 5.0;
+  EXPECT(near(spectral_norm_estimate(DenseOperator(dg)), 5.0, 1e-10));
+
+  std::printf("%d passed, %d failed\n", g_pass, g_fail);
+  return g_fail ? 1 : 0;
+}
