@@ -162,9 +162,10 @@ int l1g_solver_stream(l1g_solver* s, void** stream);
 /* per-kernel CUDA-event timing of the device loop (projection / forward / adjoint), summed
  * over completed iterations, and the number of kernels this solver launched */
 int l1g_solver_set_timing(l1g_solver* s, int on);
-/* projection phase profile accumulated since gp_init: [0..7] SM cycles per phase,
- * [8] calls, [9] attempts, [10] pivot rounds, [11] candidates, [12] bumps, [13] retries */
-int l1g_solver_proj_profile(l1g_solver* s, double* out16);
+/* projection phase profile accumulated since gp_init (24 doubles): [0..7] SM cycles per
+ * phase, [8] calls, [9] attempts, [10] pivot rounds, [11] candidates, [12] bumps,
+ * [13] retries, [14..17] sub-phases of the cluster sort */
+int l1g_solver_proj_profile(l1g_solver* s, double* out24);
 int l1g_solver_timing(l1g_solver* s, double* proj_ms, double* fwd_ms, double* adj_ms,
                       int64_t* iterations, int64_t* launches, int reset);
 void l1g_solver_destroy(l1g_solver* s);

@@ -1003,7 +1003,7 @@ int l1g_solver_proj_profile(l1g_solver* s, double* out16) {
   return guarded([&] {
     DevState h;
     read_state(s, &h);
-    std::memcpy(out16, h.prof, sizeof(h.prof));
+    std::memcpy(out16, h.prof, sizeof(h.prof));  // 24 doubles
   });
 }
 

@@ -65,7 +65,7 @@ struct DevState {
   double x0_l1;
   double h_inf;  // alpha0 projection inf-norm
   // projection phase profile (SM cycles of CTA 0 / event counts), see project.cu
-  double prof[16];
+  double prof[24];
 };
 static_assert(sizeof(DevState) % 8 == 0, "DevState is copied as 8-byte words");
 

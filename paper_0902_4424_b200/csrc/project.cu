@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "engine.h"
 #include "scalar.cuh"
+#include "prefix.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -55,6 +56,20 @@ struct ProjShared {
   double bc[8];
   int red_par;
   int dec;
+};
+
+// ---------------------------------------------------------------- distributed sort state
+constexpr int NB = 256;  // key-bit bins of the cluster bucket sort
+struct SortShared {
+  int hist[NB];    // this CTA's candidates per bin
+  int gcnt[NB];    // cluster-wide candidates per bin
+  int myoff[NB];   // this CTA's offset inside each bin
+  int start[NB];   // global position of each bin (bins in descending value order)
+  int cursor[NB];
+  int dest[NB];
+  int base[MAX_CS + 1];
+  double next;
+  int total, shift, ok;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -187,122 +202,6 @@ __device__ void bitonic_desc(P c, int n2) {
   }
 }
 
-// Exact emulation of the reference's sequential cumulative sum (prox.cpp:44-51) over the
-// sorted candidates c[0..L) (descending, >= 0), fused with its break test.  While the
-// running sum S stays inside one binade [2^e, 2^(e+1)), every fl(S + m) is S plus m rounded
-// to the fixed grid u = 2^(e-52) (round-to-nearest; ties depend on S and are left to a
-// scalar step), so a block of positions is an exact integer prefix scan of grid counts.
-// The first position whose sum leaves the binade (or ties) is done as one IEEE addition and
-// starts the next epoch.  Returns the first failing index ff (L if none) and S_{ff-1}.
-struct ScanShared {
-  long long wsum[PW];
-  long long fmin[PW];
-  double sv[PT];
-};
-
-__device__ long long prefix_break(const double* c, long long L, double rho, ScanShared& ss,
-                                  ProjShared& sh, double* s_before) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  long long i0 = 0;
-  double S_prev = 0.0;  // fl-sequential sum of c[0..i0)
-  long long ff = L;
-  while (i0 < L) {
-    // scalar step: first position, a binade crossing, a tie, or a (sub)tiny running sum
-    const bool scalar = (i0 == 0) || !(S_prev >= 0x1.0p-960);
-    long long f = 0;  // positions [i0, i0+f) are exact from the scan
-    long long fail = LLONG_MAX;
-    if (!scalar) {
-      const long long i = i0 + tid;
-      const bool valid = i < L;
-      const long long ebits = (__double_as_longlong(S_prev) >> 52) & 0x7ff;
-      const double u = __longlong_as_double((ebits - 52) << 52);           // 2^(e-52)
-      const double inv_u = __longlong_as_double((2046 - ebits + 52) << 52); // 2^(52-e)
-      const long long base_q = (long long)(S_prev * inv_u);                // exact, < 2^53
-      long long inc = 0;
-      bool tie = false;
-      double m = 0.0;
-      if (valid) {
-        m = c[i];
-        const double qd = floor(m * inv_u);
-        const double r = sub(m, qd * u);
-        const double hu = 0.5 * u;
-        tie = (r == hu);
-        inc = (long long)qd + (r > hu ? 1 : 0);
-      }
-      // inclusive block scan of inc
-      long long p = inc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long y = __shfl_up_sync(0xffffffffu, p, o);
-        if (lane >= o) p += y;
-      }
-      if (lane == 31) ss.wsum[warp] = p;
-      __syncthreads();
-      long long off = 0;
-#pragma unroll
-      for (int w = 0; w < PW; ++w) off += w < warp ? ss.wsum[w] : 0;
-      p += off;
-      const bool bad = valid && (tie || base_q + p >= (1LL << 53));
-      // first bad position
-      long long fb = bad ? (long long)tid : LLONG_MAX;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) fb = min(fb, __shfl_xor_sync(0xffffffffu, fb, o));
-      if (lane == 0) ss.fmin[warp] = fb;
-      __syncthreads();
-      long long fbad = LLONG_MAX;
-#pragma unroll
-      for (int w = 0; w < PW; ++w) fbad = min(fbad, ss.fmin[w]);
-      const long long nvalid = (L - i0) < PT ? (L - i0) : PT;
-      f = fbad < nvalid ? fbad : nvalid;
-      double S = 0.0;
-      bool my_fail = false;
-      if (tid < f) {
-        S = (double)(base_q + p) * u;  // exact: integer < 2^53 times a power of two
-        ss.sv[tid] = S;
-        const double cand = dvd(sub(S, rho), (double)(i + 1));
-        my_fail = !(m > cand);
-      }
-      long long fl = my_fail ? (long long)tid : LLONG_MAX;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) fl = min(fl, __shfl_xor_sync(0xffffffffu, fl, o));
-      __syncthreads();
-      if (lane == 0) ss.fmin[warp] = fl;
-      __syncthreads();
-#pragma unroll
-      for (int w = 0; w < PW; ++w) fail = min(fail, ss.fmin[w]);
-      if (fail != LLONG_MAX) {
-        ff = i0 + fail;
-        *s_before = fail == 0 ? S_prev : ss.sv[fail - 1];
-        __syncthreads();
-        return ff;
-      }
-      if (f > 0) S_prev = ss.sv[f - 1];
-      __syncthreads();
-      i0 += f;
-      if (f == nvalid) continue;
-    }
-    // one IEEE addition at position i0
-    if (tid == 0) {
-      const double S = add(S_prev, c[i0]);
-      const double cand = dvd(sub(S, rho), (double)(i0 + 1));
-      sh.bc[7] = S;
-      sh.dec = !(c[i0] > cand);
-    }
-    __syncthreads();
-    const double S = sh.bc[7];
-    const int failed = sh.dec;
-    __syncthreads();
-    if (failed) {
-      *s_before = S_prev;
-      return i0;
-    }
-    S_prev = S;
-    ++i0;
-  }
-  *s_before = S_prev;
-  return ff;
-}
-
 __device__ __forceinline__ double soft(double v, double th) {
   return v > th ? sub(v, th) : (v < -th ? add(v, th) : 0.0);
 }
@@ -318,6 +217,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   __shared__ ProjShared sh;
   __shared__ ScanShared scan_sh;
   __shared__ DevState sst;
+  __shared__ SortShared srt;
   DevState* st = a.st;
   const int tid = threadIdx.x;
   if (tid == 0) sh.red_par = 0;
@@ -514,6 +414,149 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           __syncthreads();
         }
         const long long L = total + (next >= 0.0 ? 1 : 0);
+        mark(14);
+        if (cs > 1 && total + 1 <= a.cand_cap && lo >= 0.0) {
+          // ---- cluster bucket sort: bins on the key bits (~log scale), whole bins to CTAs,
+          //      DSMEM scatter, local bitonic sorts, gather of the sorted ranges into CTA 0
+          const long long kmin = __double_as_longlong(lo);
+          const long long kspan = __double_as_longlong(vinf) - kmin;  // candidates: key > kmin
+          if (tid == 0) {
+            int sh_ = 0;
+            while ((kspan >> sh_) >= NB) ++sh_;
+            srt.shift = sh_;
+          }
+          for (int t = tid; t < NB; t += PT) {
+            srt.hist[t] = 0;
+            srt.cursor[t] = 0;
+          }
+          __syncthreads();
+          const int shft = srt.shift;
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            const double m = fabs(v[k]);
+            if (m > lo) atomicAdd(&srt.hist[(int)((__double_as_longlong(m) - kmin) >> shft)], 1);
+          }
+          cl.sync();
+          for (int t = tid; t < NB; t += PT) {
+            int h[MAX_CS];
+#pragma unroll
+            for (int r = 0; r < MAX_CS; ++r)
+              h[r] = r < cs ? cl.map_shared_rank(&srt, r)->hist[t] : 0;
+            int gsum = 0, mine = 0;
+#pragma unroll
+            for (int r = 0; r < MAX_CS; ++r) {
+              gsum += h[r];
+              mine += r < (int)rank ? h[r] : 0;
+            }
+            srt.gcnt[t] = gsum;
+            srt.myoff[t] = mine;
+          }
+          __syncthreads();
+          if (tid < 32) {  // descending exclusive scan over bins, destination CTAs
+            const int lane = tid;
+            int carry = 0;
+            for (int c0 = NB - 32; c0 >= 0; c0 -= 32) {
+              const int b = c0 + 31 - lane;  // lane 0 takes the highest bin of the chunk
+              int x = srt.gcnt[b], inc = x;
+#pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+              }
+              srt.start[b] = carry + inc - x;
+              carry += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            const int share = (carry + cs - 1) / cs;
+            for (int b = lane; b < NB; b += 32) {
+              const int d = share > 0 ? srt.start[b] / share : 0;
+              srt.dest[b] = d < cs ? d : cs - 1;
+            }
+            if (lane == 0) srt.total = carry;
+          }
+          __syncthreads();
+          {  // base[d] = first position owned by CTA d: one warp per d, min over bins
+            const int w = tid >> 5, lane = tid & 31;
+            if (w < cs) {
+              int bmin = srt.total;
+              for (int b = lane; b < NB; b += 32)
+                if (srt.dest[b] >= w && srt.gcnt[b] > 0) bmin = min(bmin, srt.start[b]);
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+              if (lane == 0) srt.base[w] = w == 0 ? 0 : bmin;
+            }
+            if (tid == 0) srt.base[cs] = srt.total;
+          }
+          __syncthreads();
+          if (tid == 0) {
+            int ok = 1;
+            for (int d = 0; d < cs; ++d) {
+              if (srt.base[d + 1] < srt.base[d]) srt.base[d + 1] = srt.base[d];
+              if (srt.base[d + 1] - srt.base[d] + 1 > a.cand_cap) ok = 0;
+            }
+            srt.ok = ok;
+          }
+          __syncthreads();
+          mark(15);
+          if (srt.ok) {
+#pragma unroll
+            for (int k = 0; k < M; ++k) {
+              const double m = fabs(v[k]);
+              if (m > lo) {
+                const int b = (int)((__double_as_longlong(m) - kmin) >> shft);
+                const int d = srt.dest[b];
+                const int pos = srt.start[b] + srt.myoff[b] + atomicAdd(&srt.cursor[b], 1) - srt.base[d];
+                cl.map_shared_rank(dyn, d)[pos] = m;
+              }
+            }
+          }
+          cl.sync();
+          mark(16);
+          if (srt.ok) {
+            const int cnt = srt.base[rank + 1] - srt.base[rank];
+            int m2 = 1;
+            while (m2 < cnt) m2 <<= 1;
+            for (int i = cnt + tid; i < m2; i += PT) dyn[i] = 0.0;
+            __syncthreads();
+            if (cnt > 1) bitonic_desc(dyn, m2);
+            __syncthreads();
+            cl.sync();  // every range sorted before CTA 0's buffer receives the others
+            mark(17);
+            if (rank != 0) {
+              double* dst = cl.map_shared_rank(dyn, 0) + srt.base[rank];
+              for (int i = tid; i < cnt; i += PT) dst[i] = dyn[i];
+            }
+            cl.sync();
+            mark(3);
+            count(11, (double)total);
+            if (rank == 0) {
+              if (tid == 0 && next >= 0.0) dyn[total] = next;
+              __syncthreads();
+              mark(4);
+              double s_before = 0.0;
+              const long long ff = prefix_break(dyn, L, rho, scan_sh, &s_before);
+              if (tid == 0) {
+                sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
+                sh.dec = (ff == L && next >= 0.0) ? 1 : 0;
+              }
+              mark(5);
+            }
+            cl.sync();
+            if (tid == 0 && rank != 0) {
+              const ProjShared* r0 = cl.map_shared_rank(&sh, 0);
+              sh.bc[4] = r0->bc[4];
+              sh.dec = r0->dec;
+            }
+            cl.sync();
+            if (!sh.dec) {
+              theta = sh.bc[4];
+              break;
+            }
+            count(13, 1.0);
+            lo = (lo > 0.0 && tries < 4) ? mul(lo, 0.5) : -1.0;
+            continue;
+          }
+          // bins too unbalanced for the shared-memory ranges: single-CTA path below
+        }
         int64_t n2 = 1;
         while (n2 < total) n2 <<= 1;
         const bool in_smem = (n2 + 1 <= a.cand_cap);
@@ -538,7 +581,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           __syncthreads();
           mark(4);
           double s_before = 0.0;
-          const long long ff = prefix_break(c, L, rho, scan_sh, sh, &s_before);
+          const long long ff = prefix_break(c, L, rho, scan_sh, &s_before);
           if (tid == 0) {
             // theta = candidate of the last passing index (prox.cpp:47-50); 0 if none passed
             sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
@@ -673,7 +716,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     break;
   }
   if (prof)
-    for (int i = 0; i < 16; ++i) st->prof[i] = sst.prof[i];
+    for (int i = 0; i < 24; ++i) st->prof[i] = sst.prof[i];
   cl.sync();
 }
 

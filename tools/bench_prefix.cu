@@ -1,0 +1,101 @@
+// bench_prefix.cu -- cycles of the exact sorted-prefix threshold search (prefix.cuh) versus
+// a single-thread sequential chain, on sorted half-normal magnitudes of several lengths.
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -fmad=false \
+//        -Ipaper_0902_4424_b200/csrc -o tools/bench_prefix tools/bench_prefix.cu
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "prefix.cuh"
+
+using namespace l1g;
+
+__global__ void k_parallel(const double* c, long long L, double rho, long long* ff, double* sb,
+                           long long* cycles) {
+  __shared__ ScanShared ss;
+  extern __shared__ double sc[];
+  for (long long i = threadIdx.x; i < L; i += blockDim.x) sc[i] = c[i];
+  __syncthreads();
+  const long long t0 = clock64();
+  double s = 0;
+  const long long f = prefix_break(sc, L, rho, ss, &s);
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) {
+    *ff = f;
+    *sb = s;
+    *cycles = t1 - t0;
+  }
+}
+
+__global__ void k_sequential(const double* c, long long L, double rho, long long* ff, double* sb,
+                             long long* cycles) {
+  extern __shared__ double sc[];
+  for (long long i = threadIdx.x; i < L; i += blockDim.x) sc[i] = c[i];
+  __syncthreads();
+  const long long t0 = clock64();
+  if (threadIdx.x == 0) {
+    double S = 0.0, prev = 0.0;
+    long long f = L;
+    for (long long i = 0; i < L; ++i) {
+      prev = S;
+      S = __dadd_rn(S, sc[i]);
+      if (!(sc[i] > __ddiv_rn(__dsub_rn(S, rho), (double)(i + 1)))) {
+        f = i;
+        break;
+      }
+    }
+    if (f == L) prev = S;
+    *ff = f;
+    *sb = prev;
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) *cycles = t1 - t0;
+}
+
+int main() {
+  std::mt19937_64 g(7);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  for (long long L : {120LL, 600LL, 2800LL, 9000LL, 16000LL}) {
+    std::vector<double> c(L);
+    for (auto& x : c) x = std::fabs(nd(g));
+    std::sort(c.begin(), c.end(), std::greater<double>());
+    double tot = 0;
+    for (double x : c) tot += x;
+    for (double frac : {0.5, 0.95}) {
+      const double rho = frac * tot;  // break point inside the array
+      double *dc, *dsb;
+      long long *dff, *dcy;
+      cudaMalloc(&dc, L * 8);
+      cudaMalloc(&dsb, 8);
+      cudaMalloc(&dff, 8);
+      cudaMalloc(&dcy, 8);
+      cudaMemcpy(dc, c.data(), L * 8, cudaMemcpyHostToDevice);
+      const size_t sm = L * 8;
+      cudaFuncSetAttribute(k_parallel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+      cudaFuncSetAttribute(k_sequential, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+      long long ff1, ff2, cy1, cy2;
+      double s1, s2;
+      for (int rep = 0; rep < 3; ++rep) k_parallel<<<1, 512, sm>>>(dc, L, rho, dff, dsb, dcy);
+      cudaMemcpy(&ff1, dff, 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&s1, dsb, 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&cy1, dcy, 8, cudaMemcpyDeviceToHost);
+      for (int rep = 0; rep < 3; ++rep) k_sequential<<<1, 512, sm>>>(dc, L, rho, dff, dsb, dcy);
+      cudaMemcpy(&ff2, dff, 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&s2, dsb, 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&cy2, dcy, 8, cudaMemcpyDeviceToHost);
+      std::printf("L=%6lld rho=%.2f*sum  parallel: ff=%lld cycles=%lld | sequential: ff=%lld cycles=%lld | %s\n",
+                  L, frac, ff1, cy1, ff2, cy2, (ff1 == ff2 && s1 == s2) ? "equal" : "MISMATCH");
+      cudaFree(dc);
+      cudaFree(dsb);
+      cudaFree(dff);
+      cudaFree(dcy);
+    }
+  }
+  return 0;
+}

@@ -67,7 +67,7 @@ def main():
               f"adj {ta.value/it:.4f}  GB/s fwd {kb/(tf.value/it)/1e6:.0f} "
               f"adj {kb/(ta.value/it)/1e6:.0f}  ({it} iterations, {tl.value} launches)")
     if a.profile and hasattr(lib, "l1g_solver_proj_profile"):
-        out = (C.c_double * 16)()
+        out = (C.c_double * 24)()
         lib.l1g_solver_proj_profile(h, out)
         print("proj profile:", [round(v, 3) for v in out])
     lib.l1g_solver_destroy(h)
