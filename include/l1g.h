@@ -162,6 +162,10 @@ int l1g_solver_stream(l1g_solver* s, void** stream);
 /* per-kernel CUDA-event timing of the device loop (projection / forward / adjoint), summed
  * over completed iterations, and the number of kernels this solver launched */
 int l1g_solver_set_timing(l1g_solver* s, int on);
+/* forward product of the iteration (gpss.cpp:194, DenseOperator::do_apply,
+ * linear_operator.hpp:45-46): 1 = over the columns where d != 0 only (default; same bits),
+ * 0 = dense streaming pass over all of K.  Environment L1G_FWD=dense sets 0 at creation. */
+int l1g_solver_set_forward(l1g_solver* s, int sparse);
 /* projection phase profile accumulated since gp_init (24 doubles): [0..7] SM cycles per
  * phase, [8] calls, [9] attempts, [10] pivot rounds, [11] candidates, [12] bumps,
  * [13] retries, [14..17] sub-phases of the cluster sort */

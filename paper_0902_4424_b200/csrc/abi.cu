@@ -73,10 +73,10 @@ void check_rho(double rho) {  // prox.cpp:11-13
 }
 
 void alloc_ws(Workspace& ws, const GemvPlan& pl) {
-  ws.fwd_part = dalloc<double>((size_t)pl.ncr * pl.n_pad);
+  ws.fwd_part = dalloc<double>((size_t)std::max(pl.ncr, pl.sp_ncr) * pl.n_pad);
   ws.adj_part = dalloc<double>((size_t)pl.nrr * pl.p_pad);
   ws.grpsum = dalloc<double>((size_t)std::max(2 * pl.nrg, 3 * pl.ncg) + 8);
-  ws.counters = dalloc<unsigned>((size_t)(pl.nrg + pl.ncg + 2));
+  ws.counters = dalloc<unsigned>((size_t)(pl.nrg + pl.ncg + 3));
 }
 void free_ws(Workspace& ws) {
   dfree(ws.fwd_part);
@@ -156,6 +156,7 @@ struct l1g_solver {
   int gsize = 0;
   // optional per-kernel timing: events [graph][iteration][4] around proj / fwd / adj
   bool timing = false;
+  bool fwd_sparse = true;  // forward product over the support of d only (gemv.cu)
   std::vector<cudaEvent_t> tev;
   double t_proj = 0.0, t_fwd = 0.0, t_adj = 0.0;
   int64_t t_iters = 0, launches = 0;
@@ -202,6 +203,7 @@ void solver_free(l1g_solver* s) {
   }
   dfree(s->vb.d);
   dfree(s->vb.kd);
+  dfree(s->vb.dmask);
   dfree(s->y);
   dfree(s->st);
   dfree(s->pscr);
@@ -229,6 +231,11 @@ l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho) {
     }
     s->vb.d = dalloc<double>(pl.p_pad);
     s->vb.kd = dalloc<double>(pl.n_pad);
+    s->vb.dmask = dalloc<uint32_t>((size_t)pl.p_pad / 32 + 2);
+    {
+      const char* e = getenv("L1G_FWD");
+      s->fwd_sparse = !(e && std::strcmp(e, "dense") == 0);
+    }
     s->y = dalloc<double>(pl.n_pad);
     s->vb.y = s->y;
     s->st = dalloc<DevState>(1);
@@ -282,7 +289,7 @@ void enqueue_iteration(l1g_solver* s) {
   const GemvPlan& pl = s->op->plan;
   launch_proj(s->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, s->pscr, s->st, &s->vb,
               s->stream);
-  launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
+  launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream, s->fwd_sparse);
   launch_adj(*s->op, s->ws, ADJ_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
 }
 
@@ -322,7 +329,7 @@ void build_graphs(l1g_solver* s) {
         launch_proj(s->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, s->pscr, s->st,
                     &s->vb, s->stream);
         L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 1), s->stream, cudaEventRecordExternal));
-        launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
+        launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream, s->fwd_sparse);
         L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 2), s->stream, cudaEventRecordExternal));
         launch_adj(*s->op, s->ws, ADJ_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
         L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 3), s->stream, cudaEventRecordExternal));
@@ -981,6 +988,15 @@ int l1g_solver_set_timing(l1g_solver* s, int on) {
     L1G_CUDA(cudaStreamSynchronize(s->stream));
     if (s->timing != (on != 0)) drop_graphs(s);
     s->timing = on != 0;
+  });
+}
+
+int l1g_solver_set_forward(l1g_solver* s, int sparse) {
+  return guarded([&] {
+    set_device(s->op->c);
+    L1G_CUDA(cudaStreamSynchronize(s->stream));
+    if (s->fwd_sparse != (sparse != 0)) drop_graphs(s);
+    s->fwd_sparse = sparse != 0;
   });
 }
 

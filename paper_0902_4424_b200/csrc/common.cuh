@@ -18,10 +18,12 @@ namespace l1g {
 
 // ---- K tile layout ------------------------------------------------------------------
 // K (n x p, fp64) is stored as 32 x 64 tiles, tile (rb, cb) at ((rb * NCB) + cb) * 2048
-// doubles.  Inside a tile, row i is 32 16-byte units (column pairs); unit q of row i lives
-// at position i*32 + (q ^ (i & 7)).  This XOR swizzle makes both access patterns the
-// kernels use conflict-free in shared memory: lanes = rows at a fixed pair (forward) and
-// lanes = pairs at a fixed row (adjoint).
+// doubles.  Inside a tile each column is one contiguous 256-byte run of its 32 rows, with
+// the rows XOR-swizzled by the column pair: element (i, j) at j*32 + (i ^ ((j >> 1) & 15)).
+// Shared-memory reads are conflict-free for both dense patterns (lanes = rows at a fixed
+// column for the forward product, lanes = column pairs at a fixed row for the adjoint), and
+// one column of a tile is a single coalesced 256-byte global read, which is what the
+// support-sparse forward product gathers.
 constexpr int TR = 32;
 constexpr int TC = 64;
 constexpr int TILE = TR * TC;            // doubles per tile
@@ -32,10 +34,9 @@ constexpr int COL_GROUP = 4 * TC;        // 256 columns per adjoint task column 
 __host__ __device__ __forceinline__ int64_t tile_offset(int64_t rb, int64_t cb, int64_t ncb) {
   return (rb * ncb + cb) * TILE;
 }
+__host__ __device__ __forceinline__ int col_swz(int j) { return (j >> 1) & 15; }
 // position (in doubles) of element (i, j) inside its tile
-__host__ __device__ __forceinline__ int in_tile(int i, int j) {
-  return ((i * 32 + ((j >> 1) ^ (i & 7))) << 1) | (j & 1);
-}
+__host__ __device__ __forceinline__ int in_tile(int i, int j) { return j * 32 + (i ^ col_swz(j)); }
 
 // ---- exact-rounding arithmetic ----------------------------------------------------
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }

@@ -76,6 +76,8 @@ struct GemvPlan {
   int fwd_stages, nrg, ncr;
   // adjoint: tasks = column group (256 columns) x row range (adj_blocks * 32 rows)
   int adj_blocks, ncg, nrr;
+  // sparse forward (support columns only): column ranges of sp_tiles * 64 columns
+  int sp_tiles, sp_ncr;
   int grid;
 };
 
@@ -123,12 +125,13 @@ struct VecBufs {
   double* d;
   double* kd;
   const double* y;
+  uint32_t* dmask;  // support bitmap of d (bit j of word j/32), written by proj_kernel
 };
 
 // host launchers (gemv.cu, project.cu)
 GemvPlan make_plan(int64_t n, int64_t p, int sm_count);
 void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
-                DevState* st, cudaStream_t s);
+                DevState* st, cudaStream_t s, bool sparse = false);
 void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
                 DevState* st, cudaStream_t s);
 ProjPlan make_proj_plan(int64_t p_pad);

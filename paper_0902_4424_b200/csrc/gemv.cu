@@ -41,6 +41,7 @@ struct FwdArgs {
   double* grpsum;
   unsigned* cnt_grp;
   unsigned* cnt_all;
+  unsigned* task_ctr;  // sparse forward: dynamic task counter (reset by fwd_finish)
   DevState* st;
   VecBufs vb;
 };
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
   if (lane != 0) return;
   DevState* st = a.st;
   *a.cnt_all = 0;
+  if (a.task_ctr) *a.task_ctr = 0;
   if (a.mode == FWD_INIT) {
     st->f = A;
     st->f_prev = A;
@@ -375,7 +377,6 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdA
   const int tile = cw / SPLIT;
   const int row = (cw % SPLIT) * RPW + (lane % RPW);  // row inside the tile
   const int qg = lane / RPW;                           // column-pair group
-  const int sw = row & 7;
   int stage = 0;
   uint32_t phase = 0;
   for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
@@ -386,13 +387,13 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdA
     for (int s = 0; s < nst; ++s) {
       mbar_wait(&full[stage], phase);
       const double* sb = sbase + (size_t)stage * FWD_STAGE_DBL;
-      const double2* ku = reinterpret_cast<const double2*>(sb + tile * TILE) + row * 32;
+      const double* kt = sb + tile * TILE;
       const double2* du = reinterpret_cast<const double2*>(sb + TILES_PER_STAGE * TILE);
       double v = tree<NQ>([&](int k) {
         const int q = qg * NQ + k;
-        const double2 kk = ku[q ^ sw];
+        const int o = 64 * q + (row ^ (q & 15));  // in_tile(row, 2q); column 2q+1 is 32 later
         const double2 d = du[d_pos<SPLIT>(q)];
-        return add(mul(kk.x, d.x), mul(kk.y, d.y));
+        return add(mul(kt[o], d.x), mul(kt[o + 32], d.y));
       });
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
@@ -509,14 +510,13 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) adj_kernel(const AdjA
     Counter<6> acc0, acc1;
     for (int s = 0; s < nb; ++s) {
       mbar_wait(&full[stage], phase);
-      const double2* ku =
-          reinterpret_cast<const double2*>(sbase + (size_t)stage * ADJ_STAGE_DBL + tile * TILE);
+      const double* kt = sbase + (size_t)stage * ADJ_STAGE_DBL + tile * TILE;
       const int rbase = s * TR + rgp * RPL;
       double2 v = tree2<RPL>([&](int k) {
         const int i = rgp * RPL + k;
-        const double2 kk = ku[i * 32 + (q ^ (i & 7))];
+        const int o = 64 * q + (i ^ (q & 15));  // in_tile(i, 2q); column 2q+1 is 32 later
         const double r = rs[rs_pos(rbase + k)];
-        return make_double2(mul(kk.x, r), mul(kk.y, r));
+        return make_double2(mul(kt[o], r), mul(kt[o + 32], r));
       });
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
@@ -537,6 +537,204 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) adj_kernel(const AdjA
       *reinterpret_cast<double2*>(a.part + (int64_t)rr * a.p_pad + col) =
           make_double2(acc0.final_value((uint32_t)nb), acc1.final_value((uint32_t)nb));
     }
+  }
+}
+
+// ============================================================================ sparse forward
+// K d for a direction with few nonzeros (gpss.cpp:194: d = h - x, and both h and x live on
+// the l1 ball, so d is supported on a small fraction of the columns).  The canonical value
+// is unchanged: a column with d_j = 0 contributes an exact-zero leaf and fl(s + 0) = s, so
+// the pairwise tree over all columns equals the tree over the support with the same nesting
+// (bit for bit, up to the sign of an exactly-zero result; K is finite).
+//
+// Task = (16 row blocks = 512 rows, aligned column range of <= 1024 columns), handed out
+// dynamically.  Warp 0 turns the range's support bitmap (written by proj_kernel) into a
+// schedule in shared memory (double-buffered across tasks): per support column its offset
+// in the tiled K, d_j, and its fold step.  The fold is the same for every row: leaf k meets
+// its right neighbour at level l_k = bitlength(j_k ^ j_{k+1}) (j = column offset in the
+// range), so it first absorbs the pending groups below l_k (increasing level order), then
+// waits in slot l_k; the last leaf absorbs everything.  The open-slot sets come from a warp
+// scan over the maps v -> (v & ~low(l_k)) | bit(l_k), which compose associatively.
+// Consumer warp w owns row block w of the task (lane = row) and streams its 256-byte column
+// runs straight from HBM with a SP_PF-deep register prefetch; slots live in shared memory.
+// Range partials go to the dense kernel's buffer, so fwd_finish_kernel is shared.
+constexpr int SP_NCW = 16;     // consumer warps = row blocks per task
+constexpr int SP_NT = SP_NCW * 32;
+constexpr int SP_MAXT = 16;    // tiles per range (<= 1024 columns, levels 1..10)
+constexpr int SP_W = SP_MAXT * TC;
+constexpr int SP_LVLS = 11;
+constexpr int SP_PF = 8;       // loads in flight per consumer thread
+struct SpEnt {
+  int coff;  // (tile column block) * TILE + j * 32
+  int meta;  // [0,5) level (31 = last leaf), [5,9) column swizzle, [9,20) open slots absorbed
+  double d;
+};
+struct SpInfo {
+  int task, count;
+};
+static size_t sp_smem() {
+  return (size_t)2 * SP_W * sizeof(SpEnt) + (size_t)SP_LVLS * SP_NT * 8 + 2 * sizeof(SpInfo) +
+         4 * 8 + 16;
+}
+
+__global__ void __launch_bounds__(32 * (SP_NCW + 1), 1) fwd_sparse_kernel(const FwdArgs a) {
+  if (a.st->status != RUNNING) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  SpEnt* ent = reinterpret_cast<SpEnt*>(smem);  // [2][SP_W]
+  double* slots = reinterpret_cast<double*>(ent + 2 * SP_W);
+  SpInfo* info = reinterpret_cast<SpInfo*>(slots + (size_t)SP_LVLS * SP_NT);
+  uint64_t* sfull = reinterpret_cast<uint64_t*>(info + 2) + 1;  // 8-byte aligned
+  uint64_t* sempty = sfull + 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sfull[i], 1);
+      mbar_init(&sempty[i], SP_NCW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t nrb = a.n_pad / TR;
+  const int64_t nrq = (nrb + SP_NCW - 1) / SP_NCW;
+  const int ntasks = (int)(nrq * a.ncr);
+  if (warp == 0) {  // ---- schedule builder
+    const uint64_t* mask = reinterpret_cast<const uint64_t*>(a.vb.dmask);
+    for (int it = 0;; ++it) {
+      const int bb = it & 1;
+      mbar_wait(&sempty[bb], (uint32_t)(((it >> 1) & 1) ^ 1));
+      int t = 0;
+      if (lane == 0) t = (int)atomicAdd(a.task_ctr, 1u);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= ntasks) {
+        if (lane == 0) {
+          info[bb].task = -1;
+          mbar_arrive(&sfull[bb]);
+        }
+        break;
+      }
+      const int rq = t / a.ncr, cr = t - rq * a.ncr;
+      const int64_t cb0 = (int64_t)cr * a.stages;
+      const int nst = (int)(a.ncb - cb0 < (int64_t)a.stages ? a.ncb - cb0 : (int64_t)a.stages);
+      uint64_t w = lane < nst ? __ldg(mask + cb0 + lane) : 0ull;
+      const int cnt = __popcll(w);
+      int inc = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int total = __shfl_sync(0xffffffffu, inc, 31);
+      SpEnt* e = ent + bb * SP_W;
+      {  // column offsets, in column order
+        int pos = inc - cnt;
+        const int cbase = (int)((cb0 + lane) * TILE);
+        while (w) {
+          const int j = __ffsll((long long)w) - 1;
+          w &= w - 1;
+          e[pos++].coff = cbase + j * TR;
+        }
+      }
+      __syncwarp();
+      // fold steps, 32 leaves at a time; open-slot set carried across chunks
+      unsigned carry = 0;
+      for (int k0 = 0; k0 < total; k0 += 32) {
+        const int k = k0 + lane;
+        int lvl = 31, sw = 0, jr = 0;
+        double dv = 0.0;
+        if (k < total) {
+          const int co = e[k].coff;
+          const int cbk = co / TILE, j = (co - cbk * TILE) / TR;
+          jr = (int)(cbk - cb0) * TC + j;
+          sw = col_swz(j);
+          dv = __ldg(a.vin + (int64_t)cbk * TC + j);
+          if (k + 1 < total) {
+            const int cn = e[k + 1].coff;
+            const int cbn = cn / TILE, jn = (cn - cbn * TILE) / TR;
+            lvl = 32 - __clz(jr ^ ((int)(cbn - cb0) * TC + jn));
+          }
+        }
+        const unsigned low = (1u << lvl) - 1u;
+        // map f(v) = (v & M) | B; inclusive scan of compositions (earlier maps first)
+        unsigned M = k < total ? ~low : ~0u, B = (k < total && lvl < 31) ? (1u << lvl) : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned Mp = __shfl_up_sync(0xffffffffu, M, o);
+          const unsigned Bp = __shfl_up_sync(0xffffffffu, B, o);
+          if (lane >= o) {  // f_this o f_prev
+            B = (Bp & M) | B;
+            M = Mp & M;
+          }
+        }
+        // open set before leaf k: apply the exclusive prefix to carry
+        unsigned Mx = __shfl_up_sync(0xffffffffu, M, 1), Bx = __shfl_up_sync(0xffffffffu, B, 1);
+        if (lane == 0) {
+          Mx = ~0u;
+          Bx = 0u;
+        }
+        const unsigned open = (carry & Mx) | Bx;
+        if (k < total) {
+          e[k].meta = lvl | (sw << 5) | (int)((open & low) << 9);
+          e[k].d = dv;
+        }
+        carry = (carry & __shfl_sync(0xffffffffu, M, 31)) | __shfl_sync(0xffffffffu, B, 31);
+      }
+      if (rq == 0) {  // telemetry: support columns streamed (proj_profile [18], [19])
+        if (lane == 0) {
+          atomicAdd(&a.st->prof[18], (double)total);
+          if (cr == 0) atomicAdd(&a.st->prof[19], 1.0);
+        }
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) {
+        info[bb].task = t;
+        info[bb].count = total;
+        mbar_arrive(&sfull[bb]);
+      }
+    }
+    return;
+  }
+  // ---- consumers
+  const int cw = warp - 1;
+  double* my = slots + cw * 32 + lane;
+  for (int it = 0;; ++it) {
+    const int bb = it & 1;
+    mbar_wait(&sfull[bb], (uint32_t)((it >> 1) & 1));
+    const int t = info[bb].task;
+    if (t < 0) break;
+    const int L = info[bb].count;
+    const int rq = t / a.ncr, cr = t - rq * a.ncr;
+    const int64_t rb = (int64_t)rq * SP_NCW + cw;
+    const bool live = rb < nrb;
+    const double* kr = a.K + tile_offset(live ? rb : nrb - 1, 0, a.ncb);
+    const SpEnt* e = ent + bb * SP_W;
+    double kv[SP_PF];
+#pragma unroll
+    for (int u = 0; u < SP_PF; ++u)
+      if (u < L) kv[u] = __ldcs(kr + e[u].coff + (lane ^ ((e[u].meta >> 5) & 15)));
+    double x = 0.0;
+    for (int k0 = 0; k0 < L; k0 += SP_PF) {
+#pragma unroll
+      for (int u = 0; u < SP_PF; ++u) {
+        const int k = k0 + u;
+        if (k >= L) break;
+        const int meta = e[k].meta;
+        x = mul(kv[u], e[k].d);
+        const int kn = k + SP_PF;
+        if (kn < L) kv[u] = __ldcs(kr + e[kn].coff + (lane ^ ((e[kn].meta >> 5) & 15)));
+        unsigned pm = (unsigned)meta >> 9;
+        while (pm) {
+          const int lv = __ffs(pm) - 1;
+          x = add(my[lv * SP_NT], x);
+          pm &= pm - 1;
+        }
+        const int lvl = meta & 31;
+        if (lvl < 31) my[lvl * SP_NT] = x;
+      }
+    }
+    if (live) a.part[(int64_t)cr * a.n_pad + rb * TR + lane] = x;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sempty[bb]);
   }
 }
 
@@ -562,6 +760,12 @@ GemvPlan make_plan(int64_t n, int64_t p, int sm_count) {
   while (b > 1 && (b > pl.nrb || pl.ncg * cdiv(pl.nrb, b) < target)) b >>= 1;
   pl.adj_blocks = b;
   pl.nrr = (int)cdiv(pl.nrb, b);
+  // sparse forward: ranges of <= 1024 columns, narrower when that leaves SMs idle
+  const int64_t nrq = cdiv(pl.nrb, SP_NCW);
+  int t = SP_MAXT;
+  while (t > 1 && nrq * cdiv(pl.ncb, t) < 2LL * sm_count) t >>= 1;
+  pl.sp_tiles = t;
+  pl.sp_ncr = (int)cdiv(pl.ncb, t);
   pl.grid = sm_count;
   return pl;
 }
@@ -610,7 +814,7 @@ static void adj_launch(const AdjArgs& a, int grid, cudaStream_t s) {
 }
 
 void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
-                const VecBufs* vb, DevState* st, cudaStream_t s) {
+                const VecBufs* vb, DevState* st, cudaStream_t s, bool sparse) {
   const GemvPlan& pl = op.plan;
   FwdArgs a{};
   a.K = op.K;
@@ -628,6 +832,23 @@ void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, 
   a.cnt_all = ws.counters + pl.nrg + pl.ncg;
   a.st = st;
   if (vb) a.vb = *vb;
+  if (sparse && mode == FWD_ITER && a.vb.dmask) {
+    static bool attr = false;
+    if (!attr) {
+      L1G_CUDA(cudaFuncSetAttribute(fwd_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sp_smem()));
+      attr = true;
+    }
+    a.stages = pl.sp_tiles;
+    a.ncr = pl.sp_ncr;
+    a.task_ctr = ws.counters + pl.nrg + pl.ncg + 2;
+    const int64_t ntasks = (pl.nrb + SP_NCW - 1) / SP_NCW * pl.sp_ncr;
+    fwd_sparse_kernel<<<(int)std::min<int64_t>(pl.grid, ntasks), 32 * (SP_NCW + 1), sp_smem(), s>>>(a);
+    L1G_CUDA(cudaGetLastError());
+    fwd_finish_kernel<<<a.nrg, FIN_T, 0, s>>>(a);
+    L1G_CUDA(cudaGetLastError());
+    return;
+  }
   const int grid = (int)std::min<int64_t>(pl.grid, (int64_t)pl.nrg * pl.ncr);
   switch (split_choice()) {
     case 1: fwd_launch<1>(a, grid, s); break;

@@ -643,14 +643,19 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         const int p = swz<M>((int)j);
         const double h = dyn[p];
         double leaf = 0.0;
+        bool nz = false;
         if (j < lim) {
           const int64_t gj = base + j;
           const double dj = a.mode == PROJ_PLAIN ? h : sub(h, x[gj]);
           lmax = fmax(lmax, fabs(dj));
           a.out[gj] = dj;
           if (a.mode == PROJ_ITER) leaf = mul(g[gj], dj);
+          nz = dj != 0.0;
         }
         dyn[p] = leaf;
+        // support bitmap of d for the sparse forward product (whole warps are in or out)
+        const unsigned bits = __ballot_sync(0xffffffffu, nz);
+        if (a.mode == PROJ_ITER && (tid & 31) == 0 && j < lim) a.vb.dmask[(base + j) >> 5] = bits;
       }
       __syncthreads();
       if (a.mode == PROJ_ITER) {

@@ -105,24 +105,28 @@ __device__ double det_normal(uint64_t seed, uint32_t stream, uint64_t index) {
 }
 
 // ---------------------------------------------------------------- operator construction
-// one thread per padded element, indexed in tiled order (coalesced writes)
-template <class F>
-__global__ void fill_tiled_kernel(double* K, int64_t total, int64_t ncb, int64_t n, int64_t p,
-                                  int64_t row0, int64_t rows, F val) {
-  const int64_t tiles_per_rb = ncb;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t tile = e / TILE;
-    const int pos = (int)(e - tile * TILE);
-    const int64_t rb = tile / tiles_per_rb, cb = tile - rb * tiles_per_rb;
-    // invert in_tile(): pos = ((i*32 + (q ^ (i&7))) << 1) | (j&1)
-    const int u = pos >> 1, h = pos & 1;
-    const int i = u >> 5, qs = u & 31;
-    const int q = qs ^ (i & 7);
-    const int j = 2 * q + h;
-    const int64_t row = row0 + rb * TR + i, col = cb * TC + j;
-    (void)rows;
-    K[e] = (row < n && col < p) ? val(row, col) : 0.0;
+// One CTA per tile (grid-stride): the source is read in its natural order (row-major tile
+// rows, or column-major runs when COLREAD), staged in shared memory, and the tile is written
+// out as one contiguous coalesced 16 KB run in the tiled layout (common.cuh).
+template <bool COLREAD, class F>
+__global__ void __launch_bounds__(256) fill_tiled_kernel(double* K, int64_t ntiles, int64_t ncb,
+                                                         int64_t n, int64_t p, int64_t row0, F val) {
+  __shared__ double t[TR * (TC + 1)];  // row-major staging, padded: conflict-free both ways
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t rb = tile / ncb, cb = tile - rb * ncb;
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+      const int i = COLREAD ? (e & 31) : (e >> 6);
+      const int j = COLREAD ? (e >> 5) : (e & 63);
+      const int64_t row = row0 + rb * TR + i, col = cb * TC + j;
+      t[i * (TC + 1) + j] = (row < n && col < p) ? val(row, col) : 0.0;
+    }
+    __syncthreads();
+    double* dst = K + tile * TILE;
+    for (int e = threadIdx.x; e < TILE; e += blockDim.x) {
+      const int j = e >> 5, i = (e & 31) ^ col_swz(j);  // inverse of in_tile
+      dst[e] = t[i * (TC + 1) + j];
+    }
+    __syncthreads();
   }
 }
 
@@ -156,37 +160,38 @@ static int fill_grid(int64_t total) {
   int64_t b = (total + 255) / 256;
   return (int)(b > 65535 * 8 ? 65535 * 8 : (b < 1 ? 1 : b));
 }
+static int tile_grid(int64_t ntiles) { return (int)(ntiles < 148 * 16 ? (ntiles < 1 ? 1 : ntiles) : 148 * 16); }
 
 // rows [row0, row0+rows) of the padded tiled matrix; row0 and rows multiples of TR
 void tile_rows_from_rowmajor(double* K, const GemvPlan& pl, const double* src_dev, int64_t row0,
                              int64_t rows, cudaStream_t s) {
-  const int64_t total = (rows / TR) * pl.ncb * TILE;
+  const int64_t ntiles = (rows / TR) * pl.ncb;
   double* dst = K + (row0 / TR) * pl.ncb * TILE;
-  fill_tiled_kernel<<<fill_grid(total), 256, 0, s>>>(dst, total, pl.ncb, pl.n, pl.p, row0, rows,
-                                                      RowMajorSrc{src_dev, pl.p, row0});
+  fill_tiled_kernel<false><<<tile_grid(ntiles), 256, 0, s>>>(dst, ntiles, pl.ncb, pl.n, pl.p, row0,
+                                                              RowMajorSrc{src_dev, pl.p, row0});
   L1G_CUDA(cudaGetLastError());
 }
 
 void tile_from_colmajor(double* K, const GemvPlan& pl, const double* src_dev, cudaStream_t s) {
-  const int64_t total = pl.nrb * pl.ncb * TILE;
-  fill_tiled_kernel<<<fill_grid(total), 256, 0, s>>>(K, total, pl.ncb, pl.n, pl.p, 0, pl.n_pad,
-                                                      ColMajorSrc{src_dev, pl.n});
+  const int64_t ntiles = pl.nrb * pl.ncb;
+  fill_tiled_kernel<true><<<tile_grid(ntiles), 256, 0, s>>>(K, ntiles, pl.ncb, pl.n, pl.p, 0,
+                                                             ColMajorSrc{src_dev, pl.n});
   L1G_CUDA(cudaGetLastError());
 }
 
 void generate_gaussian(double* K, const GemvPlan& pl, uint64_t seed, int64_t col_offset,
                        int64_t p_total, cudaStream_t s) {
-  const int64_t total = pl.nrb * pl.ncb * TILE;
-  fill_tiled_kernel<<<fill_grid(total), 256, 0, s>>>(K, total, pl.ncb, pl.n, pl.p, 0, pl.n_pad,
-                                                      GaussSrc{seed, p_total, col_offset});
+  const int64_t ntiles = pl.nrb * pl.ncb;
+  fill_tiled_kernel<true><<<tile_grid(ntiles), 256, 0, s>>>(K, ntiles, pl.ncb, pl.n, pl.p, 0,
+                                                             GaussSrc{seed, p_total, col_offset});
   L1G_CUDA(cudaGetLastError());
 }
 
 void generate_blur(double* K, const GemvPlan& pl, const double* taps_dev, int radius,
                    cudaStream_t s) {
-  const int64_t total = pl.nrb * pl.ncb * TILE;
-  fill_tiled_kernel<<<fill_grid(total), 256, 0, s>>>(K, total, pl.ncb, pl.n, pl.p, 0, pl.n_pad,
-                                                      BlurSrc{taps_dev, radius});
+  const int64_t ntiles = pl.nrb * pl.ncb;
+  fill_tiled_kernel<true><<<tile_grid(ntiles), 256, 0, s>>>(K, ntiles, pl.ncb, pl.n, pl.p, 0,
+                                                             BlurSrc{taps_dev, radius});
   L1G_CUDA(cudaGetLastError());
 }
 

@@ -70,6 +70,10 @@ def main():
         out = (C.c_double * 24)()
         lib.l1g_solver_proj_profile(h, out)
         print("proj profile:", [round(v, 3) for v in out])
+        if out[19] > 0:
+            cols = out[18] / out[19]
+            print(f"sparse forward: {cols:.1f} support columns per call "
+                  f"({cols / spec.p:.3%} of p), {cols * spec.n * 8 / 1e6:.1f} MB of K per call")
     lib.l1g_solver_destroy(h)
 
 
