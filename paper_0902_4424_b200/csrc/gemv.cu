@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) adj_kernel(const AdjA
 // the pairwise tree over all columns equals the tree over the support with the same nesting
 // (bit for bit, up to the sign of an exactly-zero result; K is finite).
 //
-// Task = (16 row blocks = 512 rows, aligned column range of <= 1024 columns), handed out
+// Task = (32 row blocks = 1024 rows, aligned column range of <= 1024 columns), handed out
 // dynamically.  Warp 0 turns the range's support bitmap (written by proj_kernel) into a
 // schedule in shared memory (double-buffered across tasks): per support column its offset
 // in the tiled K, d_j, and its fold step.  The fold is the same for every row: leaf k meets
@@ -555,11 +555,14 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) adj_kernel(const AdjA
 // range), so it first absorbs the pending groups below l_k (increasing level order), then
 // waits in slot l_k; the last leaf absorbs everything.  The open-slot sets come from a warp
 // scan over the maps v -> (v & ~low(l_k)) | bit(l_k), which compose associatively.
-// Consumer warp w owns row block w of the task (lane = row) and streams its 256-byte column
-// runs straight from HBM with a SP_PF-deep register prefetch; slots live in shared memory.
+// Consumer warp w owns row blocks 2w, 2w+1 of the task (lane = a row in each; the fold
+// control is shared) and streams their 256-byte column runs straight from HBM with a
+// SP_PF-deep register prefetch; slots live in shared memory.
 // Range partials go to the dense kernel's buffer, so fwd_finish_kernel is shared.
-constexpr int SP_NCW = 16;     // consumer warps = row blocks per task
-constexpr int SP_NT = SP_NCW * 32;
+constexpr int SP_NCW = 16;     // consumer warps
+constexpr int SP_RPW = 2;      // row blocks per consumer warp (lane = one row in each)
+constexpr int SP_RB = SP_NCW * SP_RPW;  // row blocks per task
+constexpr int SP_NT = SP_NCW * 32 * SP_RPW;  // slot columns (one per row)
 constexpr int SP_MAXT = 16;    // tiles per range (<= 1024 columns, levels 1..10)
 constexpr int SP_W = SP_MAXT * TC;
 constexpr int SP_LVLS = 11;
@@ -595,7 +598,7 @@ __global__ void __launch_bounds__(32 * (SP_NCW + 1), 1) fwd_sparse_kernel(const 
   }
   __syncthreads();
   const int64_t nrb = a.n_pad / TR;
-  const int64_t nrq = (nrb + SP_NCW - 1) / SP_NCW;
+  const int64_t nrq = (nrb + SP_RB - 1) / SP_RB;
   const int ntasks = (int)(nrq * a.ncr);
   if (warp == 0) {  // ---- schedule builder
     const uint64_t* mask = reinterpret_cast<const uint64_t*>(a.vb.dmask);
@@ -696,7 +699,9 @@ __global__ void __launch_bounds__(32 * (SP_NCW + 1), 1) fwd_sparse_kernel(const 
   }
   // ---- consumers
   const int cw = warp - 1;
-  double* my = slots + cw * 32 + lane;
+  double* my0 = slots + cw * 64 + lane;  // slot l of row (block 2cw, lane) at my0[l * SP_NT]
+  double* my1 = my0 + 32;                // row (block 2cw + 1, lane)
+  const int64_t rbs = a.ncb * TILE;      // one row block further in K
   for (int it = 0;; ++it) {
     const int bb = it & 1;
     mbar_wait(&sfull[bb], (uint32_t)((it >> 1) & 1));
@@ -704,35 +709,53 @@ __global__ void __launch_bounds__(32 * (SP_NCW + 1), 1) fwd_sparse_kernel(const 
     if (t < 0) break;
     const int L = info[bb].count;
     const int rq = t / a.ncr, cr = t - rq * a.ncr;
-    const int64_t rb = (int64_t)rq * SP_NCW + cw;
-    const bool live = rb < nrb;
-    const double* kr = a.K + tile_offset(live ? rb : nrb - 1, 0, a.ncb);
+    const int64_t rb = (int64_t)rq * SP_RB + SP_RPW * cw;
+    const bool live0 = rb < nrb, live1 = rb + 1 < nrb;
+    const double* kr0 = a.K + tile_offset(live0 ? rb : nrb - 1, 0, a.ncb);
+    const double* kr1 = live1 ? kr0 + rbs : kr0;
     const SpEnt* e = ent + bb * SP_W;
-    double kv[SP_PF];
+    double kv0[SP_PF], kv1[SP_PF];
 #pragma unroll
-    for (int u = 0; u < SP_PF; ++u)
-      if (u < L) kv[u] = __ldcs(kr + e[u].coff + (lane ^ ((e[u].meta >> 5) & 15)));
-    double x = 0.0;
+    for (int u = 0; u < SP_PF; ++u) {
+      if (u < L) {
+        const int o = e[u].coff + (lane ^ ((e[u].meta >> 5) & 15));
+        kv0[u] = __ldcs(kr0 + o);
+        kv1[u] = __ldcs(kr1 + o);
+      }
+    }
+    double x0 = 0.0, x1 = 0.0;
     for (int k0 = 0; k0 < L; k0 += SP_PF) {
 #pragma unroll
       for (int u = 0; u < SP_PF; ++u) {
         const int k = k0 + u;
         if (k >= L) break;
         const int meta = e[k].meta;
-        x = mul(kv[u], e[k].d);
+        const double dk = e[k].d;
+        x0 = mul(kv0[u], dk);
+        x1 = mul(kv1[u], dk);
         const int kn = k + SP_PF;
-        if (kn < L) kv[u] = __ldcs(kr + e[kn].coff + (lane ^ ((e[kn].meta >> 5) & 15)));
+        if (kn < L) {
+          const int o = e[kn].coff + (lane ^ ((e[kn].meta >> 5) & 15));
+          kv0[u] = __ldcs(kr0 + o);
+          kv1[u] = __ldcs(kr1 + o);
+        }
         unsigned pm = (unsigned)meta >> 9;
         while (pm) {
-          const int lv = __ffs(pm) - 1;
-          x = add(my[lv * SP_NT], x);
+          const int lv = (__ffs(pm) - 1) * SP_NT;
+          x0 = add(my0[lv], x0);
+          x1 = add(my1[lv], x1);
           pm &= pm - 1;
         }
         const int lvl = meta & 31;
-        if (lvl < 31) my[lvl * SP_NT] = x;
+        if (lvl < 31) {
+          my0[lvl * SP_NT] = x0;
+          my1[lvl * SP_NT] = x1;
+        }
       }
     }
-    if (live) a.part[(int64_t)cr * a.n_pad + rb * TR + lane] = x;
+    double* po = a.part + (int64_t)cr * a.n_pad + rb * TR + lane;
+    if (live0) po[0] = x0;
+    if (live1) po[TR] = x1;
     __syncwarp();
     if (lane == 0) mbar_arrive(&sempty[bb]);
   }
@@ -761,9 +784,9 @@ GemvPlan make_plan(int64_t n, int64_t p, int sm_count) {
   pl.adj_blocks = b;
   pl.nrr = (int)cdiv(pl.nrb, b);
   // sparse forward: ranges of <= 1024 columns, narrower when that leaves SMs idle
-  const int64_t nrq = cdiv(pl.nrb, SP_NCW);
+  const int64_t nrq = cdiv(pl.nrb, SP_RB);
   int t = SP_MAXT;
-  while (t > 1 && nrq * cdiv(pl.ncb, t) < 2LL * sm_count) t >>= 1;
+  while (t > 1 && nrq * cdiv(pl.ncb, t) < 3LL * sm_count) t >>= 1;
   pl.sp_tiles = t;
   pl.sp_ncr = (int)cdiv(pl.ncb, t);
   pl.grid = sm_count;
@@ -842,7 +865,7 @@ void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, 
     a.stages = pl.sp_tiles;
     a.ncr = pl.sp_ncr;
     a.task_ctr = ws.counters + pl.nrg + pl.ncg + 2;
-    const int64_t ntasks = (pl.nrb + SP_NCW - 1) / SP_NCW * pl.sp_ncr;
+    const int64_t ntasks = (pl.nrb + SP_RB - 1) / SP_RB * pl.sp_ncr;
     fwd_sparse_kernel<<<(int)std::min<int64_t>(pl.grid, ntasks), 32 * (SP_NCW + 1), sp_smem(), s>>>(a);
     L1G_CUDA(cudaGetLastError());
     fwd_finish_kernel<<<a.nrg, FIN_T, 0, s>>>(a);

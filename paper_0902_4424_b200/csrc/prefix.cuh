@@ -5,9 +5,6 @@
 
 namespace l1g {
 
-#ifndef L1G_PREFIX_PT
-#define L1G_PREFIX_PT 512
-#endif
 
 // The reference's break test  m > fl((S - rho) / k)  (prox.cpp:47-48) without a division on
 // the common path: with a = fl(S - rho), m*k and a are compared with a 2^-50 relative margin
@@ -23,58 +20,123 @@ __device__ __forceinline__ bool passes(double m, double S, double rho, long long
   return m > dvd(a, kd);
 }
 
+
+// Grid count of m >= 0 on the grid of a running sum with biased exponent be (m <= sum):
+// q = round(m / u), u = 2^(be - 1075), by integer shifts of the mantissa; tie = exact half.
+__device__ __forceinline__ long long grid_count(double m, int be, bool* tie) {
+  const long long bits = __double_as_longlong(m);
+  const int bm = (int)(bits >> 52);
+  const long long M = (bits & ((1LL << 52) - 1)) | (1LL << 52);
+  const int sh = be - bm;
+  const int s1 = sh < 1 ? 1 : (sh > 62 ? 62 : sh);
+  const long long rem = M & ((1LL << s1) - 1), half = 1LL << (s1 - 1);
+  const long long q = (M >> s1) + (rem > half ? 1 : 0);
+  // bm == 0: zero or subnormal, far below half a grid step; sh > 53: below half a step
+  const bool zero = bm == 0 || sh > 53;
+  *tie = !zero && sh > 0 && rem == half;
+  return zero ? 0 : (sh == 0 ? M : q);
+}
+// The break test without the division, for a scan: 0 pass, 1 fail, 3 too close to call
+// (resolved afterwards by passes()).
+__device__ __forceinline__ int quick_test(double m, double S, double rho, double kd) {
+  const double a = sub(S, rho);
+  const double t = mul(m, kd);
+  const double margin = mul(fabs(a), 0x1.0p-50);
+  const bool tiny = !(fabs(a) >= 0x1.0p-900);
+  const bool ps = t > add(a, margin), fl = t < sub(a, margin);
+  return tiny ? 3 : (ps ? 0 : (fl ? 1 : 3));
+}
+// the double N * 2^(be - 1075) for N in [2^52, 2^53)
+__device__ __forceinline__ double from_grid(long long N, int be) {
+  return __longlong_as_double(((long long)(be - 1) << 52) + N);
+}
+
+constexpr int PREFIX_HEAD = 256;
+constexpr int PREFIX_MAXW = 32;  // warps per block
+
+struct ScanShared {
+  double head[PREFIX_HEAD];
+  long long wsum[PREFIX_MAXW];
+  long long wev[PREFIX_MAXW];
+  long long ev, nb;
+  int kind;
+  double sb;
+};
+
 // Exact emulation of the reference's sequential cumulative sum (prox.cpp:44-51) over the
 // sorted candidates c[0..L) (descending, >= 0), fused with its break test.  While the
 // running sum S stays inside one binade [2^e, 2^(e+1)), every fl(S + m) is S plus m rounded
 // to the fixed grid u = 2^(e-52) (round-to-nearest), so the prefix sums of an epoch are one
-// exact integer prefix scan of grid counts.  The first position whose sum leaves the binade,
-// or whose rounding is a tie (decided by the parity of S), is done as one IEEE addition and
-// starts the next epoch.  The short epochs at the top are done by a sequential prologue;
-// later epochs scan windows whose size follows the (doubling) epoch lengths.
+// exact integer prefix scan of grid counts (computed from the mantissa bits).  The first
+// position whose sum leaves the binade, or whose rounding is a tie (decided by the parity
+// of S), is done as one IEEE addition and starts the next epoch.  The short epochs at the
+// top are cheaper as the reference's own sequential sum (one dependent add per position);
+// after PREFIX_HEAD positions the block scans windows sized to the (doubling) epochs.
 // Returns the first failing index ff (L if none) and S_{ff-1} (the sum whose candidate is
-// theta).  All threads of the block call it and receive the same result.
-struct ScanShared {
-  long long wsum[L1G_PREFIX_PT / 32];
-  long long ev[L1G_PREFIX_PT / 32][2];
-  double sv[L1G_PREFIX_PT];
-  double pro[2];
-  long long pro_i;
-};
-
-constexpr int PREFIX_PROLOGUE = 64;
-
+// theta).  All threads of the block call it (blockDim a multiple of 32, <= 1024) and
+// receive the same result.
 __device__ long long prefix_break(const double* c, long long L, double rho, ScanShared& ss,
                                   double* s_before) {
-  constexpr int NT = L1G_PREFIX_PT;
-  constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = blockDim.x, NW = NT >> 5;
   constexpr long long TWO53 = 1LL << 53;
-  // ---- sequential prologue (thread 0): S_0 = fl(0 + c_0) = c_0, then IEEE additions
-  if (tid == 0) {
-    const long long lim = L < PREFIX_PROLOGUE ? L : PREFIX_PROLOGUE;
-    double S = 0.0, prev = 0.0;
-    long long i = 0, ff = -1;
-    for (; i < lim; ++i) {
-      prev = S;
-      S = add(S, c[i]);
-      if (!passes(c[i], S, rho, i + 1)) {
-        ff = i;
+  constexpr unsigned FULL = 0xffffffffu;
+  if (L <= 0) {
+    *s_before = 0.0;
+    return 0;
+  }
+  // ---- head: lane 0 of warp 0 adds sequentially, warp 0 tests in parallel
+  const long long H = L < PREFIX_HEAD ? L : PREFIX_HEAD;
+  if (warp == 0) {
+    if (lane == 0) {
+      double run = 0.0, v[8], w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = u < H ? c[u] : 0.0;
+      for (long long i0 = 0; i0 < H; i0 += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = i0 + 8 + u < H ? c[i0 + 8 + u] : 0.0;  // next batch
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (i0 + u < H) {
+            run = add(run, v[u]);
+            ss.head[i0 + u] = run;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = w[u];
+      }
+    }
+    __syncwarp();
+    long long ff = LLONG_MAX;
+    for (long long i = lane; i - lane < H; i += 32) {
+      const bool ok = i < H ? passes(c[i], ss.head[i], rho, i + 1) : true;
+      const unsigned bad = __ballot_sync(FULL, !ok);
+      if (bad) {
+        ff = i - lane + (__ffs(bad) - 1);
         break;
       }
     }
-    ss.pro_i = ff >= 0 ? -(ff + 1) : lim;  // <0: failure at -(pro_i)-1
-    ss.pro[0] = ff >= 0 ? prev : S;
+    if (lane == 0) {
+      ss.ev = ff;
+      ss.sb = ff == LLONG_MAX ? ss.head[H - 1] : (ff > 0 ? ss.head[ff - 1] : 0.0);
+    }
   }
   __syncthreads();
-  const long long pi = ss.pro_i;
-  double S_prev = ss.pro[0];
-  __syncthreads();
-  if (pi < 0) {
-    *s_before = S_prev;
-    return -pi - 1;
+  {
+    const long long ff = ss.ev;
+    const double sb = ss.sb;
+    __syncthreads();
+    if (ff != LLONG_MAX) {
+      *s_before = sb;
+      return ff;
+    }
+    if (H == L) {
+      *s_before = sb;
+      return L;
+    }
   }
-  long long i0 = pi;
-  long long window = NT;
+  double S_prev = ss.head[H - 1];
+  long long i0 = H, window = 2 * H;
   while (i0 < L) {
     if (!(S_prev >= 0x1.0p-960)) {  // (sub)tiny running sum: plain scalar step, uniform
       const double S = add(S_prev, c[i0]);
@@ -91,94 +153,104 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
     const long long wend = i0 + n;
     const long long p0 = i0 + (long long)tid * E;
     const long long p1 = p0 + E < wend ? p0 + E : wend;
-    const long long ebits = (__double_as_longlong(S_prev) >> 52) & 0x7ff;
-    const double u = __longlong_as_double((ebits - 52) << 52);           // 2^(e-52)
-    const double inv_u = __longlong_as_double((2098 - ebits) << 52);    // 2^(52-e)
-    const double hu = 0.5 * u;
-    const long long base_q = (long long)(S_prev * inv_u);               // exact, < 2^53
+    const long long sbits = __double_as_longlong(S_prev);
+    const int be = (int)(sbits >> 52);
+    const long long base_q = (sbits & ((1LL << 52) - 1)) | (1LL << 52);  // S_prev / u
     // pass 1: grid counts of my positions
     long long tot = 0;
+#pragma unroll 4
     for (long long i = p0; i < p1; ++i) {
-      const double m = c[i];
-      const double qd = floor(m * inv_u);
-      tot += (long long)qd + (sub(m, qd * u) > hu ? 1 : 0);
+      bool t;
+      tot += grid_count(c[i], be, &t);
     }
     long long inc = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      const long long y = __shfl_up_sync(FULL, inc, o);
       if (lane >= o) inc += y;
     }
     if (lane == 31) ss.wsum[warp] = inc;
     __syncthreads();
-    long long off = inc - tot, btot = 0;
+    long long off, btot;
+    {  // warp totals: inclusive scan over the warps by shuffles
+      const long long x = lane < NW ? ss.wsum[lane] : 0;
+      long long sc = x;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const long long x = ss.wsum[w];
-      off += w < warp ? x : 0;
-      btot += x;
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(FULL, sc, o);
+        if (lane >= o) sc += y;
+      }
+      btot = __shfl_sync(FULL, sc, 31);
+      off = inc - tot + (warp > 0 ? __shfl_sync(FULL, sc, warp - 1) : 0);
     }
-    // pass 2: exact sums and tests up to my first event (failure or binade exit / tie)
-    long long P = off, my_ff = LLONG_MAX, my_fb = LLONG_MAX;
+    // pass 2: exact sums and tests; my first event (1 failure, 2 binade exit or tie,
+    // 3 test too close to call), branch-free so positions overlap
+    long long N = base_q + off, my_ev = LLONG_MAX, my_n = 0;
+    int kind = 0;
+    double kd = (double)(p0 + 1);
+#pragma unroll 4
     for (long long i = p0; i < p1; ++i) {
       const double m = c[i];
-      const double qd = floor(m * inv_u);
-      const double r = sub(m, qd * u);
-      const long long q = (long long)qd + (r > hu ? 1 : 0);
-      if (r == hu || base_q + P + q >= TWO53) {
-        my_fb = i;
-        ss.sv[tid] = i == i0 ? S_prev : (double)(base_q + P) * u;  // S_{i-1}
-        break;
-      }
-      P += q;
-      if (!passes(m, (double)(base_q + P) * u, rho, i + 1)) {
-        my_ff = i;
-        ss.sv[tid] = i == i0 ? S_prev : (double)(base_q + P - q) * u;  // S_{i-1}
-        break;
-      }
+      bool tie;
+      const long long q = grid_count(m, be, &tie);
+      const long long Nn = N + q;
+      const int stt = (tie || Nn >= TWO53) ? 2 : quick_test(m, from_grid(Nn, be), rho, kd);
+      const bool take = stt != 0 && my_ev == LLONG_MAX;
+      my_ev = take ? i : my_ev;
+      kind = take ? stt : kind;
+      my_n = take ? N : my_n;
+      N = Nn;
+      kd = add(kd, 1.0);
     }
-    long long a0 = my_ff, a1 = my_fb;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a0 = min(a0, __shfl_xor_sync(0xffffffffu, a0, o));
-      a1 = min(a1, __shfl_xor_sync(0xffffffffu, a1, o));
-    }
-    if (lane == 0) {
-      ss.ev[warp][0] = a0;
-      ss.ev[warp][1] = a1;
-    }
+    // first event of the window (positions increase with the thread index)
+    const unsigned have = __ballot_sync(FULL, my_ev != LLONG_MAX);
+    if (lane == 0) ss.wev[warp] = have ? (long long)warp * 32 + (__ffs(have) - 1) : LLONG_MAX;
     __syncthreads();
-    long long FF = LLONG_MAX, FB = LLONG_MAX;
+    long long owner = lane < NW ? ss.wev[lane] : LLONG_MAX;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      FF = min(FF, ss.ev[w][0]);
-      FB = min(FB, ss.ev[w][1]);
-    }
-    if (FF < FB) {  // a failure inside the exact range
-      *s_before = ss.sv[(FF - i0) / E];
-      __syncthreads();
-      return FF;
-    }
-    if (FB == LLONG_MAX) {  // the whole window is exact and passes: same epoch continues
-      S_prev = (double)(base_q + btot) * u;
+    for (int o = 16; o > 0; o >>= 1) owner = min(owner, __shfl_xor_sync(FULL, owner, o));
+    if (owner == LLONG_MAX) {  // the whole window is exact and passes: the epoch continues
+      S_prev = from_grid(base_q + btot, be);
       i0 = wend;
       window *= 2;
       __syncthreads();
       continue;
     }
-    // one IEEE addition at the first binade exit / tie, evaluated by every thread alike
-    const double Sm1 = ss.sv[(FB - i0) / E];
+    if (tid == owner) {
+      ss.ev = my_ev;
+      ss.kind = kind;
+      ss.nb = my_n;
+    }
     __syncthreads();
-    const double S = add(Sm1, c[FB]);
-    if (!passes(c[FB], S, rho, FB + 1)) {
-      *s_before = Sm1;
-      return FB;
+    const long long ev = ss.ev, nb = ss.nb;
+    const int evk = ss.kind;
+    __syncthreads();
+    const double sb = from_grid(nb, be);  // S_{ev-1}
+    if (evk == 1) {
+      *s_before = sb;
+      return ev;
+    }
+    if (evk == 3) {  // exact test with the division; on success the epoch goes on
+      bool t;
+      const double Se = from_grid(nb + grid_count(c[ev], be, &t), be);
+      if (!passes(c[ev], Se, rho, ev + 1)) {
+        *s_before = sb;
+        return ev;
+      }
+      S_prev = Se;
+      i0 = ev + 1;
+      continue;
+    }
+    // one IEEE addition at the binade exit / tie, evaluated by every thread alike
+    const double S = add(sb, c[ev]);
+    if (!passes(c[ev], S, rho, ev + 1)) {
+      *s_before = sb;
+      return ev;
     }
     // the next epoch is about as long as the whole prefix so far: size the window for it
-    const long long len = FB + 1;
-    window = ((len + NT - 1) / NT) * NT;
+    window = ((ev + 1 + 31) >> 5) << 5;
     S_prev = S;
-    i0 = FB + 1;
+    i0 = ev + 1;
   }
   *s_before = S_prev;
   return L;
