@@ -75,7 +75,7 @@ void check_rho(double rho) {  // prox.cpp:11-13
 void alloc_ws(Workspace& ws, const GemvPlan& pl) {
   ws.fwd_part = dalloc<double>((size_t)std::max(pl.ncr, pl.sp_ncr) * pl.n_pad);
   ws.adj_part = dalloc<double>((size_t)pl.nrr * pl.p_pad);
-  ws.grpsum = dalloc<double>((size_t)std::max(2 * pl.nrg, 3 * pl.ncg) + 8);
+  ws.grpsum = dalloc<double>((size_t)std::max(2 * pl.n_pad / 32, 3 * pl.p_pad / 64) + 8);
   ws.counters = dalloc<unsigned>((size_t)(pl.nrg + pl.ncg + 3));
 }
 void free_ws(Workspace& ws) {

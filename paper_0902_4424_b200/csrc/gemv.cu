@@ -71,19 +71,33 @@ __device__ __forceinline__ double2 tree2(const F& leaf, int base = 0) {
   }
 }
 
-// Tree over `count` values v[0..count) (runtime count, absent beyond) by one warp: lane l
-// takes block l of each 32-chunk, the butterfly reduces the chunk, a counter joins chunks.
-__device__ __forceinline__ double warp_tree_array(const double* v, int count, int stride,
-                                                  int lane) {
-  Counter<20> acc;
+// Trees over NA interleaved arrays v[i*stride + j], i < count (runtime count, absent beyond),
+// by one warp: lane l takes block l of each 32-chunk, the butterfly reduces the chunk, a
+// counter joins chunks.  Loads are issued 4 chunks ahead so the L2 latency is paid once
+// per 4 chunks instead of once per chunk.
+template <int NA>
+__device__ __forceinline__ void warp_tree_arrays(const double* v, int count, int stride, int lane,
+                                                 double* out) {
+  Counter<12> acc[NA];  // chunks < 2^12 per warp block
   const int chunks = (count + 31) >> 5;
-  for (int c = 0; c < chunks; ++c) {
-    const int i = c * 32 + lane;
-    double x = i < count ? __ldcg(v + (int64_t)i * stride) : 0.0;
-    x = warp_tree(x);
-    acc.push(x, c);
+  for (int c0 = 0; c0 < chunks; c0 += 4) {
+    double x[4][NA];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = (c0 + u) * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < NA; ++j) x[u][j] = i < count ? __ldcg(v + (int64_t)i * stride + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (c0 + u < chunks) {
+#pragma unroll
+        for (int j = 0; j < NA; ++j) acc[j].push(warp_tree(x[u][j]), (uint32_t)(c0 + u));
+      }
+    }
   }
-  return acc.final_value(chunks);
+#pragma unroll
+  for (int j = 0; j < NA; ++j) out[j] = acc[j].final_value((uint32_t)chunks);
 }
 
 // position of d unit u (16-byte pair) in the padded per-stage slice: the SPLIT lane groups
@@ -98,11 +112,13 @@ __device__ __forceinline__ int d_pos(int u) {
 __device__ __forceinline__ int rs_pos(int i) { return i + (i >> 3); }
 
 // ============================================================================ finish kernels
-// One CTA of 128 threads per group: thread t <-> row (forward) or column pair (adjoint).
-// Tree over the task partials -> fused epilogue -> block tree (4 warp subtrees, joined as
-// ((w0 + w1) + (w2 + w3))) -> the group's subtree; the CTA that counts last joins the
-// groups and runs the scalar part of gp_iterate.
-constexpr int FIN_T = 128;
+// One CTA of 8 warps per 32 rows (forward) or 64 columns (adjoint): the task partials of
+// each output are split over the warps in aligned power-of-two blocks (a binary counter per
+// warp), warp 0 joins the 8 block values pairwise (blocks past the count are absent), runs
+// the fused epilogue and reduces its dot-product leaves with the warp butterfly; the CTA
+// that counts last joins the group values and runs the scalar part of gp_iterate.
+constexpr int FIN_W = 8;
+constexpr int FIN_T = 32 * FIN_W;
 
 // warp-cooperative copy of the device state into shared memory (one coalesced pass)
 __device__ __forceinline__ void snapshot(DevState* dst, const DevState* src, int lane) {
@@ -112,60 +128,113 @@ __device__ __forceinline__ void snapshot(DevState* dst, const DevState* src, int
   __syncwarp();
 }
 
-template <int N>
-__device__ __forceinline__ double block4(double v, double (*ws)[3], int c) {
-  v = warp_tree(v);
-  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5][c] = v;
-  return v;
+__device__ __forceinline__ int fin_block(int cnt) {
+  int B = 1;
+  while (B * FIN_W < cnt) B <<= 1;
+  return B;
+}
+
+// join of the FIN_W block values of one output held in sv[w][lane] (w < nb present)
+__device__ __forceinline__ double fin_join(const double (*sv)[32], int nb, int lane) {
+  double x[FIN_W];
+#pragma unroll
+  for (int w = 0; w < FIN_W; ++w) x[w] = sv[w][lane];
+#pragma unroll
+  for (int h = 1; h < FIN_W; h <<= 1)
+#pragma unroll
+    for (int i = 0; i + h < FIN_W; i += 2 * h)
+      if (i + h < nb) x[i] = add(x[i], x[i + h]);
+  return x[0];
+}
+
+// Canonical trees over NA interleaved group arrays (count groups) by a whole CTA of
+// FIN_W warps: aligned power-of-two blocks per warp, joined pairwise by warp 0.
+template <int NA>
+__device__ __forceinline__ void cta_tree_arrays(const double* v, int count, int stride,
+                                                double (*sv)[FIN_W][32], double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int B = 32;
+  while (B * FIN_W < count) B <<= 1;
+  const int lo = warp * B, hi = lo + B < count ? lo + B : count;
+  double r[NA];
+  if (hi > lo) warp_tree_arrays<NA>(v + (int64_t)lo * stride, hi - lo, stride, lane, r);
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < NA; ++j) sv[j][warp][0] = hi > lo ? r[j] : 0.0;
+  __syncthreads();
+  const int nb = (count + B - 1) / B;
+#pragma unroll
+  for (int j = 0; j < NA; ++j) {
+    double x[FIN_W];
+#pragma unroll
+    for (int w = 0; w < FIN_W; ++w) x[w] = sv[j][w][0];
+#pragma unroll
+    for (int h = 1; h < FIN_W; h <<= 1)
+#pragma unroll
+      for (int i = 0; i + h < FIN_W; i += 2 * h)
+        if (i + h < nb) x[i] = add(x[i], x[i + h]);
+    out[j] = x[0];
+  }
 }
 
 __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
   if (a.mode != FWD_APPLY && a.st->status != RUNNING) return;
-  __shared__ double ws[4][3];
+  __shared__ double sv[FIN_W][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = blockIdx.x, ngrp = gridDim.x;
+  const int64_t row = (int64_t)grp * 32 + lane;
+  {
+    const int B = fin_block(a.ncr);
+    const int lo = warp * B, hi = lo + B < a.ncr ? lo + B : a.ncr;
+    Counter<16> acc;
+    int k = lo;
+    for (; k + 4 <= hi; k += 4) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcg(a.part + (int64_t)(k + u) * a.n_pad + row);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc.push(v[u], (uint32_t)(k + u - lo));
+    }
+    for (; k < hi; ++k) acc.push(__ldcg(a.part + (int64_t)k * a.n_pad + row), (uint32_t)(k - lo));
+    sv[warp][lane] = hi > lo ? acc.final_value((uint32_t)(hi - lo)) : 0.0;
+    __syncthreads();
+  }
   __shared__ unsigned s_last;
-  const int rg = blockIdx.x;
-  const int64_t row = (int64_t)rg * ROW_GROUP + threadIdx.x;
-  Counter<20> acc;
-  int cr = 0;
-  for (; cr + 8 <= a.ncr; cr += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldcg(a.part + (int64_t)(cr + u) * a.n_pad + row);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc.push(v[u], cr + u);
+  if (warp == 0) {
+    const double kd = fin_join(sv, (a.ncr + fin_block(a.ncr) - 1) / fin_block(a.ncr), lane);
+    if (a.mode == FWD_APPLY) {
+      a.vout[row] = kd;
+    } else {
+      const int cur = a.st->cur;
+      double l0, l1 = 0.0;
+      if (a.mode == FWD_INIT) {
+        const double r = sub(kd, a.vb.y[row]);  // Kx0 - y   (gpss.cpp:128)
+        a.vb.r[cur][row] = r;
+        l0 = mul(r, r);                         // ||r||^2   (gpss.cpp:129)
+      } else {
+        a.vb.kd[row] = kd;
+        l0 = mul(a.vb.r[cur][row], kd);         // (Kx-y)'Kd (gpss.cpp:195)
+        l1 = mul(kd, kd);                       // ||Kd||^2  (gpss.cpp:196)
+      }
+      l0 = warp_tree(l0);
+      l1 = warp_tree(l1);
+      if (lane == 0) {
+        a.grpsum[2 * grp + 0] = l0;
+        a.grpsum[2 * grp + 1] = l1;
+        __threadfence();
+        s_last = atomicAdd(a.cnt_all, 1u) == (unsigned)ngrp - 1u;
+      }
+    }
   }
-  for (; cr < a.ncr; ++cr) acc.push(__ldcg(a.part + (int64_t)cr * a.n_pad + row), cr);
-  const double kd = acc.final_value(a.ncr);
-  if (a.mode == FWD_APPLY) {
-    a.vout[row] = kd;
-    return;
-  }
-  const int cur = a.st->cur;
-  double l0, l1 = 0.0;
-  if (a.mode == FWD_INIT) {
-    const double r = sub(kd, a.vb.y[row]);  // Kx0 - y   (gpss.cpp:128)
-    a.vb.r[cur][row] = r;
-    l0 = mul(r, r);                         // ||r||^2   (gpss.cpp:129)
-  } else {
-    a.vb.kd[row] = kd;
-    l0 = mul(a.vb.r[cur][row], kd);         // (Kx-y)'Kd (gpss.cpp:195)
-    l1 = mul(kd, kd);                       // ||Kd||^2  (gpss.cpp:196)
-  }
-  block4<0>(l0, ws, 0);
-  block4<0>(l1, ws, 1);
+  if (a.mode == FWD_APPLY) return;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    a.grpsum[2 * rg + 0] = add(add(ws[0][0], ws[1][0]), add(ws[2][0], ws[3][0]));
-    a.grpsum[2 * rg + 1] = add(add(ws[0][1], ws[1][1]), add(ws[2][1], ws[3][1]));
-    __threadfence();
-    s_last = atomicAdd(a.cnt_all, 1u) == (unsigned)a.nrg - 1u;
-  }
-  __syncthreads();
-  if (!s_last || threadIdx.x >= 32) return;
+  if (!s_last) return;
   __threadfence();
-  const int lane = threadIdx.x;
-  const double A = warp_tree_array(a.grpsum + 0, a.nrg, 2, lane);
-  const double B = warp_tree_array(a.grpsum + 1, a.nrg, 2, lane);
+  __shared__ double tsv[2][FIN_W][32];
+  double AB[2];
+  cta_tree_arrays<2>(a.grpsum, ngrp, 2, tsv, AB);
+  if (warp != 0) return;
+  const double A = AB[0], B = AB[1];
   __shared__ DevState s;
   snapshot(&s, a.st, lane);
   if (lane != 0) return;
@@ -199,68 +268,80 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
 
 __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a) {
   if (a.mode != ADJ_APPLY && a.st->status != RUNNING) return;
-  __shared__ double ws[4][3];
-  __shared__ unsigned s_last;
+  __shared__ double sv[2][FIN_W][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = blockIdx.x, ngrp = gridDim.x;
+  const int64_t col = (int64_t)grp * 64 + 2 * lane;
+  {
+    const int B = fin_block(a.nrr);
+    const int lo = warp * B, hi = lo + B < a.nrr ? lo + B : a.nrr;
+    Counter<16> acc0, acc1;
+    int k = lo;
+    for (; k + 4 <= hi; k += 4) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)(k + u) * a.p_pad + col));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc0.push(v[u].x, (uint32_t)(k + u - lo));
+        acc1.push(v[u].y, (uint32_t)(k + u - lo));
+      }
+    }
+    for (; k < hi; ++k) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)k * a.p_pad + col));
+      acc0.push(v.x, (uint32_t)(k - lo));
+      acc1.push(v.y, (uint32_t)(k - lo));
+    }
+    sv[0][warp][lane] = hi > lo ? acc0.final_value((uint32_t)(hi - lo)) : 0.0;
+    sv[1][warp][lane] = hi > lo ? acc1.final_value((uint32_t)(hi - lo)) : 0.0;
+    __syncthreads();
+  }
   DevState* st = a.st;
-  const int cg = blockIdx.x;
-  const int64_t col = (int64_t)cg * COL_GROUP + 2 * threadIdx.x;
-  Counter<20> acc0, acc1;
-  int rr = 0;
-  for (; rr + 8 <= a.nrr; rr += 8) {
-    double2 v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      v[u] = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)(rr + u) * a.p_pad + col));
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      acc0.push(v[u].x, rr + u);
-      acc1.push(v[u].y, rr + u);
+  __shared__ unsigned s_last;
+  if (warp == 0) {
+    const int nb = (a.nrr + fin_block(a.nrr) - 1) / fin_block(a.nrr);
+    const double s0 = fin_join(sv[0], nb, lane), s1 = fin_join(sv[1], nb, lane);
+    if (a.mode == ADJ_APPLY) {
+      *reinterpret_cast<double2*>(a.vout + col) = make_double2(s0, s1);
+    } else {
+      const int cur = st->cur;
+      const double g0 = mul(2.0, s0), g1 = mul(2.0, s1);  // 2 K^T r (gpss.cpp:130, :211)
+      if (a.mode == ADJ_INIT) {
+        *reinterpret_cast<double2*>(a.vb.g[cur] + col) = make_double2(g0, g1);
+      } else {
+        // x' = x + lambda d (gpss.cpp:208), s = x' - x, z = g' - g (gpss.cpp:150-151)
+        const double lam = st->step;
+        const double2 xo = *reinterpret_cast<const double2*>(a.vb.x[cur] + col);
+        const double2 go = *reinterpret_cast<const double2*>(a.vb.g[cur] + col);
+        const double2 dd = *reinterpret_cast<const double2*>(a.vb.d + col);
+        const double x0n = add(xo.x, mul(lam, dd.x)), x1n = add(xo.y, mul(lam, dd.y));
+        *reinterpret_cast<double2*>(a.vb.x[cur ^ 1] + col) = make_double2(x0n, x1n);
+        *reinterpret_cast<double2*>(a.vb.g[cur ^ 1] + col) = make_double2(g0, g1);
+        const double sa = sub(x0n, xo.x), sb = sub(x1n, xo.y);
+        const double za = sub(g0, go.x), zb = sub(g1, go.y);
+        const double dsz = warp_tree(add(mul(sa, za), mul(sb, zb)));
+        const double dss = warp_tree(add(mul(sa, sa), mul(sb, sb)));
+        const double dzz = warp_tree(add(mul(za, za), mul(zb, zb)));
+        if (lane == 0) {
+          a.grpsum[3 * grp + 0] = dsz;
+          a.grpsum[3 * grp + 1] = dss;
+          a.grpsum[3 * grp + 2] = dzz;
+          __threadfence();
+          s_last = atomicAdd(a.cnt_all, 1u) == (unsigned)ngrp - 1u;
+        }
+      }
     }
   }
-  for (; rr < a.nrr; ++rr) {
-    const double2 v = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)rr * a.p_pad + col));
-    acc0.push(v.x, rr);
-    acc1.push(v.y, rr);
-  }
-  const double s0 = acc0.final_value(a.nrr), s1 = acc1.final_value(a.nrr);
-  if (a.mode == ADJ_APPLY) {
-    *reinterpret_cast<double2*>(a.vout + col) = make_double2(s0, s1);
-    return;
-  }
-  const int cur = st->cur;
-  const double g0 = mul(2.0, s0), g1 = mul(2.0, s1);  // 2 K^T r (gpss.cpp:130, :211)
-  if (a.mode == ADJ_INIT) {
-    *reinterpret_cast<double2*>(a.vb.g[cur] + col) = make_double2(g0, g1);
-    return;
-  }
-  // x' = x + lambda d (gpss.cpp:208), s = x' - x, z = g' - g (gpss.cpp:150-151)
-  const double lam = st->step;
-  const double2 xo = *reinterpret_cast<const double2*>(a.vb.x[cur] + col);
-  const double2 go = *reinterpret_cast<const double2*>(a.vb.g[cur] + col);
-  const double2 dd = *reinterpret_cast<const double2*>(a.vb.d + col);
-  const double x0n = add(xo.x, mul(lam, dd.x)), x1n = add(xo.y, mul(lam, dd.y));
-  *reinterpret_cast<double2*>(a.vb.x[cur ^ 1] + col) = make_double2(x0n, x1n);
-  *reinterpret_cast<double2*>(a.vb.g[cur ^ 1] + col) = make_double2(g0, g1);
-  const double sa = sub(x0n, xo.x), sb = sub(x1n, xo.y);
-  const double za = sub(g0, go.x), zb = sub(g1, go.y);
-  block4<0>(add(mul(sa, za), mul(sb, zb)), ws, 0);
-  block4<0>(add(mul(sa, sa), mul(sb, sb)), ws, 1);
-  block4<0>(add(mul(za, za), mul(zb, zb)), ws, 2);
+  if (a.mode != ADJ_ITER) return;
   __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-      a.grpsum[3 * cg + c] = add(add(ws[0][c], ws[1][c]), add(ws[2][c], ws[3][c]));
-    __threadfence();
-    s_last = atomicAdd(a.cnt_all, 1u) == (unsigned)a.ncg - 1u;
-  }
-  __syncthreads();
-  if (!s_last || threadIdx.x >= 32) return;
+  if (!s_last) return;
   __threadfence();
-  const int lane = threadIdx.x;
-  const double SZ = warp_tree_array(a.grpsum + 0, a.ncg, 3, lane);
-  const double SS = warp_tree_array(a.grpsum + 1, a.ncg, 3, lane);
-  const double ZZ = warp_tree_array(a.grpsum + 2, a.ncg, 3, lane);
+  __shared__ double tsv[3][FIN_W][32];
+  double sums[3];
+  cta_tree_arrays<3>(a.grpsum, ngrp, 3, tsv, sums);
+  if (warp != 0) return;
+  const double SZ = sums[0], SS = sums[1], ZZ = sums[2];
   __shared__ DevState s;
   snapshot(&s, st, lane);
   if (lane != 0) return;
@@ -818,7 +899,7 @@ static void fwd_launch(const FwdArgs& a, int grid, cudaStream_t s) {
   }
   fwd_kernel<SPLIT><<<grid, 32 * (4 * SPLIT + 1), fwd_smem(), s>>>(a);
   L1G_CUDA(cudaGetLastError());
-  fwd_finish_kernel<<<a.nrg, FIN_T, 0, s>>>(a);
+  fwd_finish_kernel<<<(int)(a.n_pad / 32), FIN_T, 0, s>>>(a);
   L1G_CUDA(cudaGetLastError());
 }
 
@@ -832,7 +913,7 @@ static void adj_launch(const AdjArgs& a, int grid, cudaStream_t s) {
   }
   adj_kernel<SPLIT><<<grid, 32 * (4 * SPLIT + 1), adj_smem(), s>>>(a);
   L1G_CUDA(cudaGetLastError());
-  adj_finish_kernel<<<a.ncg, FIN_T, 0, s>>>(a);
+  adj_finish_kernel<<<(int)(a.p_pad / 64), FIN_T, 0, s>>>(a);
   L1G_CUDA(cudaGetLastError());
 }
 
@@ -868,7 +949,7 @@ void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, 
     const int64_t ntasks = (pl.nrb + SP_RB - 1) / SP_RB * pl.sp_ncr;
     fwd_sparse_kernel<<<(int)std::min<int64_t>(pl.grid, ntasks), 32 * (SP_NCW + 1), sp_smem(), s>>>(a);
     L1G_CUDA(cudaGetLastError());
-    fwd_finish_kernel<<<a.nrg, FIN_T, 0, s>>>(a);
+    fwd_finish_kernel<<<(int)(a.n_pad / 32), FIN_T, 0, s>>>(a);
     L1G_CUDA(cudaGetLastError());
     return;
   }
