@@ -178,6 +178,7 @@ __device__ __forceinline__ void cta_tree_arrays(const double* v, int count, int 
 }
 
 __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
+  pdl_wait_and_trigger();
   if (a.mode != FWD_APPLY && a.st->status != RUNNING) return;
   __shared__ double sv[FIN_W][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
 }
 
 __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a) {
+  pdl_wait_and_trigger();
   if (a.mode != ADJ_APPLY && a.st->status != RUNNING) return;
   __shared__ double sv[2][FIN_W][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -404,6 +406,7 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a) {
 // ============================================================================ forward
 template <int SPLIT>
 __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdArgs a) {
+  pdl_wait_and_trigger();
   constexpr int NCONS = 4 * SPLIT;
   constexpr int NQ = 32 / SPLIT;  // column pairs per lane group
   constexpr int RPW = 32 / SPLIT; // rows per warp
@@ -497,6 +500,7 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdA
 // ============================================================================ adjoint
 template <int SPLIT>
 __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) adj_kernel(const AdjArgs a) {
+  pdl_wait_and_trigger();
   constexpr int NCONS = 4 * SPLIT;
   constexpr int NQ = 32 / SPLIT;  // column pairs per warp
   constexpr int RPL = 32 / SPLIT; // rows per lane group
@@ -662,6 +666,7 @@ static size_t sp_smem() {
 }
 
 __global__ void __launch_bounds__(32 * (SP_NCW + 1), 1) fwd_sparse_kernel(const FwdArgs a) {
+  pdl_wait_and_trigger();
   if (a.st->status != RUNNING) return;
   extern __shared__ __align__(128) unsigned char smem[];
   SpEnt* ent = reinterpret_cast<SpEnt*>(smem);  // [2][SP_W]
@@ -897,9 +902,9 @@ static void fwd_launch(const FwdArgs& a, int grid, cudaStream_t s) {
                                   (int)fwd_smem()));
     attr = true;
   }
-  fwd_kernel<SPLIT><<<grid, 32 * (4 * SPLIT + 1), fwd_smem(), s>>>(a);
+  L1G_CUDA(launch_pdl(fwd_kernel<SPLIT>, grid, 32 * (4 * SPLIT + 1), fwd_smem(), s, a));
   L1G_CUDA(cudaGetLastError());
-  fwd_finish_kernel<<<(int)(a.n_pad / 32), FIN_T, 0, s>>>(a);
+  L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)(a.n_pad / 32), FIN_T, 0, s, a));
   L1G_CUDA(cudaGetLastError());
 }
 
@@ -911,9 +916,9 @@ static void adj_launch(const AdjArgs& a, int grid, cudaStream_t s) {
                                   (int)adj_smem()));
     attr = true;
   }
-  adj_kernel<SPLIT><<<grid, 32 * (4 * SPLIT + 1), adj_smem(), s>>>(a);
+  L1G_CUDA(launch_pdl(adj_kernel<SPLIT>, grid, 32 * (4 * SPLIT + 1), adj_smem(), s, a));
   L1G_CUDA(cudaGetLastError());
-  adj_finish_kernel<<<(int)(a.p_pad / 64), FIN_T, 0, s>>>(a);
+  L1G_CUDA(launch_pdl(adj_finish_kernel, (int)(a.p_pad / 64), FIN_T, 0, s, a));
   L1G_CUDA(cudaGetLastError());
 }
 
@@ -947,9 +952,10 @@ void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, 
     a.ncr = pl.sp_ncr;
     a.task_ctr = ws.counters + pl.nrg + pl.ncg + 2;
     const int64_t ntasks = (pl.nrb + SP_RB - 1) / SP_RB * pl.sp_ncr;
-    fwd_sparse_kernel<<<(int)std::min<int64_t>(pl.grid, ntasks), 32 * (SP_NCW + 1), sp_smem(), s>>>(a);
+    L1G_CUDA(launch_pdl(fwd_sparse_kernel, (int)std::min<int64_t>(pl.grid, ntasks), 32 * (SP_NCW + 1),
+                        sp_smem(), s, a));
     L1G_CUDA(cudaGetLastError());
-    fwd_finish_kernel<<<(int)(a.n_pad / 32), FIN_T, 0, s>>>(a);
+    L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)(a.n_pad / 32), FIN_T, 0, s, a));
     L1G_CUDA(cudaGetLastError());
     return;
   }

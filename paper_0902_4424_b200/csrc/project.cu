@@ -209,6 +209,7 @@ __device__ __forceinline__ double soft(double v, double th) {
 // ---------------------------------------------------------------- the kernel
 template <int M>
 __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
+  pdl_wait_and_trigger();
   cg::cluster_group cl = cg::this_cluster();
   const unsigned rank = cl.block_rank();
   const int cs = a.cs;
@@ -772,13 +773,15 @@ static void proj_launch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s) {
   cfg.blockDim = dim3(PT, 1, 1);
   cfg.dynamicSmemBytes = pp.smem;
   cfg.stream = s;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
   attrs[0].val.clusterDim.x = pp.cs;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   L1G_CUDA(cudaLaunchKernelEx(&cfg, proj_kernel<M>, a));
 }
 
