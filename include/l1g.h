@@ -162,6 +162,22 @@ int l1g_solver_stream(l1g_solver* s, void** stream);
 /* per-kernel CUDA-event timing of the device loop (projection / forward / adjoint), summed
  * over completed iterations, and the number of kernels this solver launched */
 int l1g_solver_set_timing(l1g_solver* s, int on);
+/* ---- column-sharded runs (no reference counterpart: the reference is
+ * single-threaded).  Shard r of R holds columns [r*p/R, (r+1)*p/R) of K as its own l1g_op
+ * (p/R a multiple of 256); x, g and d are replicated, and each iteration exchanges the
+ * shard tree values of K d (n doubles per shard) and of K^T r (p/R doubles per shard).
+ * With p/R a power of two the result is bit-identical to the unsharded solve.
+ *   l1g_solver_create_group: R shards in this process on one device, run in lockstep
+ *     (exchange = device copies); the other l1g_solver_* calls take the returned leader.
+ *   l1g_comm_*: an NCCL communicator, one shard per process (rank r owns shard r). */
+typedef struct l1g_comm l1g_comm;
+int l1g_solver_create_group(l1g_op* const* ops, int nshards, const double* y, double rho,
+                            const l1g_gp_config* cfg, l1g_solver** out);
+int l1g_comm_unique_id(void* id128);
+int l1g_comm_create(l1g_ctx* ctx, int rank, int nranks, const void* id128, l1g_comm** out);
+void l1g_comm_destroy(l1g_comm* comm);
+int l1g_solver_create_sharded(l1g_op* op, l1g_comm* comm, const double* y, double rho,
+                              const l1g_gp_config* cfg, l1g_solver** out);
 /* forward product of the iteration (gpss.cpp:194, DenseOperator::do_apply,
  * linear_operator.hpp:45-46): 1 = over the columns where d != 0 only (default; same bits),
  * 0 = dense streaming pass over all of K.  Environment L1G_FWD=dense sets 0 at creation. */

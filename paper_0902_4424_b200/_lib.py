@@ -94,6 +94,13 @@ _SIGS = {
                                            C.POINTER(GpConfigC), _dp]),
     "l1g_solver_create": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(GpConfigC),
                                     C.POINTER(_vp)]),
+    "l1g_solver_create_group": (C.c_int, [C.POINTER(_vp), C.c_int, _vp, C.c_double,
+                                          C.POINTER(GpConfigC), C.POINTER(_vp)]),
+    "l1g_comm_unique_id": (C.c_int, [_vp]),
+    "l1g_comm_create": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.POINTER(_vp)]),
+    "l1g_comm_destroy": (None, [_vp]),
+    "l1g_solver_create_sharded": (C.c_int, [_vp, _vp, _vp, C.c_double, C.POINTER(GpConfigC),
+                                            C.POINTER(_vp)]),
     "l1g_solver_set_y": (C.c_int, [_vp, _vp]),
     "l1g_solver_set_y_dev": (C.c_int, [_vp, _vp]),
     "l1g_solver_init": (C.c_int, [_vp, _vp]),

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/l1g.h"
+#include "comm.h"
 #include "common.cuh"
 #include "engine.h"
 #include "vec.h"
@@ -72,10 +73,13 @@ void check_rho(double rho) {  // prox.cpp:11-13
   if (!(rho >= 0.0)) throw InvalidArgument("L1Ball: radius must be >= 0");
 }
 
-void alloc_ws(Workspace& ws, const GemvPlan& pl) {
+// p_pad_vec: length of the vectors the adjoint epilogue runs over (all columns of a sharded
+// problem, whose per-group dot-product leaves live in grpsum)
+void alloc_ws(Workspace& ws, const GemvPlan& pl, int64_t p_pad_vec = 0) {
+  const int64_t pv = std::max(pl.p_pad, p_pad_vec);
   ws.fwd_part = dalloc<double>((size_t)std::max(pl.ncr, pl.sp_ncr) * pl.n_pad);
   ws.adj_part = dalloc<double>((size_t)pl.nrr * pl.p_pad);
-  ws.grpsum = dalloc<double>((size_t)std::max(2 * pl.n_pad / 32, 3 * pl.p_pad / 64) + 8);
+  ws.grpsum = dalloc<double>((size_t)std::max(2 * pl.n_pad / 32, 3 * pv / 64) + 8);
   ws.counters = dalloc<unsigned>((size_t)(pl.nrg + pl.ncg + 3));
 }
 void free_ws(Workspace& ws) {
@@ -138,9 +142,23 @@ struct l1g_op : Op {
   l1g_solver* cached = nullptr;
 };
 
+struct l1g_comm {
+  Comm* impl = nullptr;
+};
+
 struct l1g_solver {
-  l1g_op* op = nullptr;
+  l1g_op* op = nullptr;  // this shard's columns of K (all of K when unsharded)
   cudaStream_t stream = nullptr;
+  bool own_stream = true;
+  // vectors span all p columns of the problem; the shard holds K[:, col0 : col0 + op->p]
+  int64_t p = 0, p_pad = 0, col0 = 0;
+  // column sharding: an NCCL communicator (one shard per process)
+  // or in-process shards on one device run in lockstep by the leader (group[0] == this)
+  int nranks = 1;
+  l1g_comm* comm = nullptr;
+  std::vector<l1g_solver*> group;
+  double *kd_send = nullptr, *kd_recv = nullptr, *g_send = nullptr, *g_recv = nullptr;
+  bool split() const { return comm != nullptr || group.size() > 1; }
   Workspace ws;
   VecBufs vb{};
   double* y = nullptr;
@@ -192,6 +210,12 @@ DevState host_state(const l1g_gp_config& cfg, double rho) {
 void solver_free(l1g_solver* s) {
   if (!s) return;
   cudaSetDevice(s->op->c->device);
+  for (size_t i = 1; i < s->group.size(); ++i) solver_free(s->group[i]);
+  s->group.clear();
+  dfree(s->kd_send);
+  dfree(s->kd_recv);
+  dfree(s->g_send);
+  dfree(s->g_recv);
   for (auto& g : s->gexec)
     if (g) cudaGraphExecDestroy(g);
   for (auto e : s->tev) cudaEventDestroy(e);
@@ -210,11 +234,14 @@ void solver_free(l1g_solver* s) {
   dfree(s->scal);
   dfree(s->trace);
   if (s->status_host) cudaFreeHost(s->status_host);
-  if (s->stream) cudaStreamDestroy(s->stream);
+  if (s->stream && s->own_stream) cudaStreamDestroy(s->stream);
   delete s;
 }
 
-l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho) {
+// nranks > 1: a shard of a column-sharded problem, p_total = nranks * op->p columns, this
+// shard's columns start at col0; `stream` (if given) is shared and not owned
+l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho, int nranks = 1,
+                       int64_t col0 = 0, cudaStream_t stream = nullptr, bool sharded = false) {
   check_cfg(cfg);
   check_rho(rho);
   set_device(op->c);
@@ -222,16 +249,27 @@ l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho) {
   s->op = op;
   try {
     const GemvPlan& pl = op->plan;
-    L1G_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    alloc_ws(s->ws, pl);
+    if (nranks > 1 && (pl.p != pl.p_pad))
+      throw InvalidArgument("sharded solver: columns per shard must be a multiple of 256");
+    s->nranks = nranks;
+    s->col0 = col0;
+    s->p = nranks > 1 ? pl.p * nranks : pl.p;
+    s->p_pad = nranks > 1 ? pl.p_pad * nranks : pl.p_pad;
+    if (stream) {
+      s->stream = stream;
+      s->own_stream = false;
+    } else {
+      L1G_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    }
+    alloc_ws(s->ws, pl, s->p_pad);
     for (int i = 0; i < 2; ++i) {
-      s->vb.x[i] = dalloc<double>(pl.p_pad);
-      s->vb.g[i] = dalloc<double>(pl.p_pad);
+      s->vb.x[i] = dalloc<double>(s->p_pad);
+      s->vb.g[i] = dalloc<double>(s->p_pad);
       s->vb.r[i] = dalloc<double>(pl.n_pad);
     }
-    s->vb.d = dalloc<double>(pl.p_pad);
+    s->vb.d = dalloc<double>(s->p_pad);
     s->vb.kd = dalloc<double>(pl.n_pad);
-    s->vb.dmask = dalloc<uint32_t>((size_t)pl.p_pad / 32 + 2);
+    s->vb.dmask = dalloc<uint32_t>((size_t)s->p_pad / 32 + 2);
     {
       const char* e = getenv("L1G_FWD");
       s->fwd_sparse = !(e && std::strcmp(e, "dense") == 0);
@@ -239,8 +277,14 @@ l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho) {
     s->y = dalloc<double>(pl.n_pad);
     s->vb.y = s->y;
     s->st = dalloc<DevState>(1);
-    s->pp = make_proj_plan(pl.p_pad);
-    s->pscr = dalloc<double>(proj_scratch_doubles(pl.p_pad));
+    s->pp = make_proj_plan(s->p_pad);
+    s->pscr = dalloc<double>(proj_scratch_doubles(s->p_pad));
+    if (nranks > 1 || sharded) {
+      s->kd_send = dalloc<double>(pl.n_pad);
+      s->kd_recv = dalloc<double>((size_t)pl.n_pad * nranks);
+      s->g_send = dalloc<double>(pl.p_pad);
+      s->g_recv = dalloc<double>((size_t)pl.p_pad * nranks);
+    }
     s->scal = dalloc<double>(16);
     L1G_CUDA(cudaHostAlloc(&s->status_host, 256, cudaHostAllocDefault));
     s->cfg = cfg;
@@ -254,43 +298,117 @@ l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho) {
 
 void solver_set_y(l1g_solver* s, const double* y_host) {
   const GemvPlan& pl = s->op->plan;
-  L1G_CUDA(cudaMemcpyAsync(s->y, y_host, pl.n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  for (l1g_solver* q : (s->group.empty() ? std::vector<l1g_solver*>{s} : s->group))
+    L1G_CUDA(cudaMemcpyAsync(q->y, y_host, pl.n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+}
+
+// members run in lockstep: the solver itself, or its in-process shards
+std::vector<l1g_solver*> members(l1g_solver* s) {
+  if (s->group.empty()) return {s};
+  return s->group;
+}
+
+// allgather of the shard vectors `which` (0: K d tree values, n_pad each; 1: K^T r tree
+// values, the shard's p each) into every member's receive buffer
+void exchange(l1g_solver* s, int which) {
+  const GemvPlan& pl = s->op->plan;
+  const size_t cnt = which == 0 ? (size_t)pl.n_pad : (size_t)pl.p_pad;
+  if (s->comm) {
+    comm_allgather(s->comm->impl, which == 0 ? s->kd_send : s->g_send,
+                   which == 0 ? s->kd_recv : s->g_recv, cnt, s->stream);
+    return;
+  }
+  const auto m = members(s);
+  for (l1g_solver* dst : m)
+    for (size_t r = 0; r < m.size(); ++r)
+      L1G_CUDA(cudaMemcpyAsync((which == 0 ? dst->kd_recv : dst->g_recv) + r * cnt,
+                               which == 0 ? m[r]->kd_send : m[r]->g_send, cnt * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s->stream));
+}
+
+// kernels (and exchanges) one iteration or gp_init enqueues, for launch accounting
+int64_t kernels_per_iteration(l1g_solver* s) {
+  return s->split() ? 7 * (int64_t)members(s).size() + (s->comm ? 2 : 0) : 5;
 }
 
 // gpss.cpp:117-134
 void solver_init(l1g_solver* s, const double* x0_host) {
   set_device(s->op->c);
-  const GemvPlan& pl = s->op->plan;
   s->t0 = std::chrono::steady_clock::now();
-  L1G_CUDA(cudaMemsetAsync(s->vb.x[0], 0, pl.p_pad * sizeof(double), s->stream));
-  if (x0_host) {
-    L1G_CUDA(cudaMemcpyAsync(s->vb.x[0], x0_host, pl.p * sizeof(double), cudaMemcpyHostToDevice,
-                             s->stream));
-    // L1Ball::contains(x0, 1e-12), prox.cpp:15-17 (zero start is always feasible)
-    reduce(s->vb.x[0], nullptr, pl.p_pad, RED_ABS, s->scal, 0, s->stream);
-    double l1 = 0.0;
-    L1G_CUDA(cudaMemcpyAsync(&l1, s->scal, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
-    L1G_CUDA(cudaStreamSynchronize(s->stream));
-    if (!(l1 <= s->rho + 1e-12)) throw InvalidArgument("gp_init: starting point is infeasible");
+  const auto m = members(s);
+  for (l1g_solver* q : m) {
+    L1G_CUDA(cudaMemsetAsync(q->vb.x[0], 0, q->p_pad * sizeof(double), s->stream));
+    if (x0_host) {
+      L1G_CUDA(cudaMemcpyAsync(q->vb.x[0], x0_host, q->p * sizeof(double), cudaMemcpyHostToDevice,
+                               s->stream));
+      // L1Ball::contains(x0, 1e-12), prox.cpp:15-17 (zero start is always feasible)
+      reduce(q->vb.x[0], nullptr, q->p_pad, RED_ABS, q->scal, 0, s->stream);
+      double l1 = 0.0;
+      L1G_CUDA(cudaMemcpyAsync(&l1, q->scal, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+      L1G_CUDA(cudaStreamSynchronize(s->stream));
+      if (!(l1 <= q->rho + 1e-12)) throw InvalidArgument("gp_init: starting point is infeasible");
+    }
+    DevState h = host_state(q->cfg, q->rho);
+    h.matvecs = 2;
+    L1G_CUDA(cudaMemcpyAsync(q->st, &h, sizeof(h), cudaMemcpyHostToDevice, s->stream));
+    state_start(q->st, s->stream);
   }
-  DevState h = host_state(s->cfg, s->rho);
-  h.matvecs = 2;
-  L1G_CUDA(cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, s->stream));
-  state_start(s->st, s->stream);
-  launch_fwd(*s->op, s->ws, FWD_INIT, s->vb.x[0], nullptr, &s->vb, s->st, s->stream);
-  launch_adj(*s->op, s->ws, ADJ_INIT, nullptr, nullptr, &s->vb, s->st, s->stream);
-  launch_proj(s->pp, PROJ_ALPHA0, pl.p, pl.p_pad, s->vb.x[0], s->vb.g[0], nullptr, s->pscr, s->st,
-              &s->vb, s->stream);
-  s->launches += x0_host ? 7 : 6;
+  if (!s->split()) {
+    launch_fwd(*s->op, s->ws, FWD_INIT, s->vb.x[0], nullptr, &s->vb, s->st, s->stream);
+    launch_adj(*s->op, s->ws, ADJ_INIT, nullptr, nullptr, &s->vb, s->st, s->stream);
+  } else {
+    for (l1g_solver* q : m)
+      launch_fwd_part(*q->op, q->ws, q->vb.x[0] + q->col0, nullptr, false, q->kd_send, q->st,
+                      s->stream);
+    exchange(s, 0);
+    for (l1g_solver* q : m)
+      launch_fwd_combine(*q->op, q->ws, FWD_INIT, q->kd_recv, q->nranks, &q->vb, q->st, s->stream);
+    for (l1g_solver* q : m)
+      launch_adj_part(*q->op, q->ws, ADJ_INIT, &q->vb, q->g_send, q->st, s->stream);
+    exchange(s, 1);
+    for (l1g_solver* q : m)
+      launch_adj_combine(*q->op, q->ws, ADJ_INIT, q->g_recv, q->p_pad, &q->vb, q->st, s->stream);
+  }
+  for (l1g_solver* q : m)
+    launch_proj(q->pp, PROJ_ALPHA0, q->p, q->p_pad, q->vb.x[0], q->vb.g[0], nullptr, q->pscr,
+                q->st, &q->vb, s->stream);
+  s->launches += (x0_host ? 7 : 6) * (int64_t)m.size() + (s->split() ? 2 * (int64_t)m.size() : 0);
   s->inited = true;
 }
 
+// one gp_iterate (gpss.cpp:136-219) for every member; mark(j) between the projection (0),
+// forward (1) and adjoint (2) phases and at the end (3), for the per-kernel timing
+template <class Mark>
+void enqueue_iteration(l1g_solver* s, Mark mark) {
+  const auto m = members(s);
+  mark(0);
+  for (l1g_solver* q : m)
+    launch_proj(q->pp, PROJ_ITER, q->p, q->p_pad, nullptr, nullptr, nullptr, q->pscr, q->st,
+                &q->vb, s->stream);
+  mark(1);
+  if (!s->split()) {
+    launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream, s->fwd_sparse);
+    mark(2);
+    launch_adj(*s->op, s->ws, ADJ_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
+    mark(3);
+    return;
+  }
+  for (l1g_solver* q : m)
+    launch_fwd_part(*q->op, q->ws, q->vb.d + q->col0, q->vb.dmask + q->col0 / 32, q->fwd_sparse,
+                    q->kd_send, q->st, s->stream);
+  exchange(s, 0);
+  for (l1g_solver* q : m)
+    launch_fwd_combine(*q->op, q->ws, FWD_ITER, q->kd_recv, q->nranks, &q->vb, q->st, s->stream);
+  mark(2);
+  for (l1g_solver* q : m)
+    launch_adj_part(*q->op, q->ws, ADJ_ITER, &q->vb, q->g_send, q->st, s->stream);
+  exchange(s, 1);
+  for (l1g_solver* q : m)
+    launch_adj_combine(*q->op, q->ws, ADJ_ITER, q->g_recv, q->p_pad, &q->vb, q->st, s->stream);
+  mark(3);
+}
 void enqueue_iteration(l1g_solver* s) {
-  const GemvPlan& pl = s->op->plan;
-  launch_proj(s->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, s->pscr, s->st, &s->vb,
-              s->stream);
-  launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream, s->fwd_sparse);
-  launch_adj(*s->op, s->ws, ADJ_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
+  enqueue_iteration(s, [](int) {});
 }
 
 void drop_graphs(l1g_solver* s) {
@@ -313,7 +431,7 @@ void build_graphs(l1g_solver* s) {
   if (s->gexec[0]) return;
   const GemvPlan& pl = s->op->plan;
   // iterations per graph: ~2 ms of streaming work, between 1 and 64
-  const double bytes = 2.0 * (double)pl.n_pad * (double)pl.p_pad * 8.0;
+  const double bytes = 2.0 * (double)pl.n_pad * (double)pl.p_pad * 8.0 * members(s).size();
   const double est_us = bytes / 6.0e6 + 15.0;
   s->gsize = (int)std::max(1.0, std::min(64.0, 2000.0 / est_us));
   if (s->timing) {
@@ -325,14 +443,9 @@ void build_graphs(l1g_solver* s) {
     L1G_CUDA(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < s->gsize; ++i) {
       if (s->timing) {
-        L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 0), s->stream, cudaEventRecordExternal));
-        launch_proj(s->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, s->pscr, s->st,
-                    &s->vb, s->stream);
-        L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 1), s->stream, cudaEventRecordExternal));
-        launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream, s->fwd_sparse);
-        L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 2), s->stream, cudaEventRecordExternal));
-        launch_adj(*s->op, s->ws, ADJ_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
-        L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, 3), s->stream, cudaEventRecordExternal));
+        enqueue_iteration(s, [&](int j) {
+          L1G_CUDA(cudaEventRecordWithFlags(tev(s, gi, i, j), s->stream, cudaEventRecordExternal));
+        });
       } else {
         enqueue_iteration(s);
       }
@@ -367,8 +480,11 @@ void read_state(l1g_solver* s, DevState* h) {
 
 void configure(l1g_solver* s, const l1g_stop_rule& stop, int single, l1g_iter_record* trace,
                int64_t cap) {
-  configure_kernel<<<1, 1, 0, s->stream>>>(s->st, stop, single, trace, cap);
-  L1G_CUDA(cudaGetLastError());
+  for (l1g_solver* q : members(s)) {  // telemetry is recorded by the leader only
+    configure_kernel<<<1, 1, 0, s->stream>>>(q->st, stop, single, q == s ? trace : nullptr,
+                                             q == s ? cap : 0);
+    L1G_CUDA(cudaGetLastError());
+  }
 }
 
 void finalize(l1g_solver* s, l1g_result* res, l1g_iter_record* trace_host, int64_t cap);
@@ -414,7 +530,7 @@ void solver_run(l1g_solver* s, const l1g_stop_rule& stop, l1g_result* res,
   while (!done) {
     const int slot = (int)(launched & 1);
     L1G_CUDA(cudaGraphLaunch(s->gexec[slot], s->stream));
-    s->launches += 5LL * s->gsize;
+    s->launches += kernels_per_iteration(s) * s->gsize;
     L1G_CUDA(cudaMemcpyAsync((void*)(flag + 16 * slot), &s->st->status, sizeof(int),
                              cudaMemcpyDeviceToHost, s->stream));
     L1G_CUDA(cudaMemcpyAsync((void*)(flag + 16 * slot + 2), &s->st->k, sizeof(int64_t),
@@ -462,19 +578,18 @@ void solver_run_cb(l1g_solver* s, const l1g_stop_rule& stop, l1g_result* res, l1
   if (!s->inited) throw InvalidArgument("solver: gp_init has not been run");
   set_device(s->op->c);
   configure(s, stop, 0, nullptr, 0);
-  const GemvPlan& pl = s->op->plan;
-  std::vector<double> x((size_t)pl.p);
+  std::vector<double> x((size_t)s->p);
   int64_t k_prev = 0;
   for (;;) {
     enqueue_iteration(s);
-    s->launches += 5;
+    s->launches += kernels_per_iteration(s);
     DevState h;
     read_state(s, &h);
     if (h.k > k_prev) {
       k_prev = h.k;
-      download(x.data(), s->vb.x[h.cur], pl.p, s->stream);
+      download(x.data(), s->vb.x[h.cur], s->p, s->stream);
       L1G_CUDA(cudaStreamSynchronize(s->stream));
-      if (cb) cb(&h.last, x.data(), pl.p, user);
+      if (cb) cb(&h.last, x.data(), s->p, user);
     }
     if (h.status != RUNNING) break;
   }
@@ -489,7 +604,7 @@ void solver_iterate(l1g_solver* s, double tol, l1g_iter_record* info, int32_t* s
   st.stationarity_tol = tol;
   configure(s, st, 1, nullptr, 0);
   enqueue_iteration(s);
-  s->launches += 6;
+  s->launches += kernels_per_iteration(s) + 1;
   DevState h;
   read_state(s, &h);
   *stationary = h.stationary;
@@ -924,6 +1039,76 @@ int l1g_solver_create(l1g_op* op, const double* y, double rho, const l1g_gp_conf
   });
 }
 
+int l1g_solver_create_group(l1g_op* const* ops, int nshards, const double* y, double rho,
+                            const l1g_gp_config* cfg, l1g_solver** out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (nshards < 1 || !ops) throw InvalidArgument("solver group: need at least one shard");
+    for (int r = 0; r < nshards; ++r) {
+      if (!ops[r]) throw InvalidArgument("solver group: null operator");
+      if (ops[r]->c != ops[0]->c) throw InvalidArgument("solver group: shards on one context");
+      if (ops[r]->plan.n != ops[0]->plan.n || ops[r]->plan.p != ops[0]->plan.p)
+        throw InvalidArgument("solver group: shards must have equal dimensions");
+    }
+    const int64_t pl = ops[0]->plan.p;
+    l1g_solver* lead = solver_new(ops[0], *cfg, rho, nshards, 0, nullptr, true);
+    try {
+      lead->group.push_back(lead);
+      for (int r = 1; r < nshards; ++r)
+        lead->group.push_back(solver_new(ops[r], *cfg, rho, nshards, r * pl, lead->stream, true));
+      if (y) solver_set_y(lead, y);
+    } catch (...) {
+      solver_free(lead);
+      throw;
+    }
+    *out = lead;
+  });
+}
+
+int l1g_comm_unique_id(void* id) {
+  return guarded([&] { comm_unique_id(id); });
+}
+
+int l1g_comm_create(l1g_ctx* ctx, int rank, int nranks, const void* id, l1g_comm** out) {
+  return guarded([&] {
+    *out = nullptr;
+    auto* c = new l1g_comm();
+    try {
+      c->impl = comm_create(ctx->device, rank, nranks, id);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void l1g_comm_destroy(l1g_comm* c) {
+  if (!c) return;
+  comm_destroy(c->impl);
+  delete c;
+}
+
+int l1g_solver_create_sharded(l1g_op* op, l1g_comm* comm, const double* y, double rho,
+                              const l1g_gp_config* cfg, l1g_solver** out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (!comm || !comm->impl) throw InvalidArgument("sharded solver: no communicator");
+    if (comm->impl->device != op->c->device)
+      throw InvalidArgument("sharded solver: communicator and operator on different devices");
+    const int R = comm->impl->nranks;
+    l1g_solver* s = solver_new(op, *cfg, rho, R, comm->impl->rank * op->plan.p, nullptr, true);
+    s->comm = comm;
+    try {
+      if (y) solver_set_y(s, y);
+    } catch (...) {
+      solver_free(s);
+      throw;
+    }
+    *out = s;
+  });
+}
+
 int l1g_solver_set_y(l1g_solver* s, const double* y) {
   return guarded([&] {
     set_device(s->op->c);
@@ -934,7 +1119,8 @@ int l1g_solver_set_y(l1g_solver* s, const double* y) {
 int l1g_solver_set_y_dev(l1g_solver* s, const double* y_dev) {
   return guarded([&] {
     set_device(s->op->c);
-    L1G_CUDA(cudaMemcpyAsync(s->y, y_dev, s->op->plan.n * 8, cudaMemcpyDeviceToDevice, s->stream));
+    for (l1g_solver* q : (s->group.empty() ? std::vector<l1g_solver*>{s} : s->group))
+      L1G_CUDA(cudaMemcpyAsync(q->y, y_dev, s->op->plan.n * 8, cudaMemcpyDeviceToDevice, s->stream));
   });
 }
 
@@ -963,9 +1149,9 @@ int l1g_solver_get(l1g_solver* s, double* x, double* r, double* g, double* f, in
     DevState h;
     read_state(s, &h);
     const GemvPlan& pl = s->op->plan;
-    download(x, s->vb.x[h.cur], pl.p, s->stream);
+    download(x, s->vb.x[h.cur], s->p, s->stream);
     download(r, s->vb.r[h.cur], pl.n, s->stream);
-    download(g, s->vb.g[h.cur], pl.p, s->stream);
+    download(g, s->vb.g[h.cur], s->p, s->stream);
     L1G_CUDA(cudaStreamSynchronize(s->stream));
     if (f) *f = h.f;
     if (k) *k = h.k;
@@ -996,7 +1182,7 @@ int l1g_solver_set_forward(l1g_solver* s, int sparse) {
     set_device(s->op->c);
     L1G_CUDA(cudaStreamSynchronize(s->stream));
     if (s->fwd_sparse != (sparse != 0)) drop_graphs(s);
-    s->fwd_sparse = sparse != 0;
+    for (l1g_solver* q : members(s)) q->fwd_sparse = sparse != 0;
   });
 }
 

@@ -134,6 +134,16 @@ void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, 
                 DevState* st, cudaStream_t s, bool sparse = false);
 void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
                 DevState* st, cudaStream_t s);
+// column-sharded runs: the shard's tree values (n_pad / p_pad of the shard) and the
+// combination of the gathered rank values with the fused epilogue of `mode`
+void launch_fwd_part(const Op& op, const Workspace& ws, const double* vin, const uint32_t* dmask,
+                     bool sparse, double* out, DevState* st, cudaStream_t s);
+void launch_fwd_combine(const Op& op, const Workspace& ws, int mode, const double* recv, int nr,
+                        const VecBufs* vb, DevState* st, cudaStream_t s);
+void launch_adj_part(const Op& op, const Workspace& ws, int mode, const VecBufs* vb, double* out,
+                     DevState* st, cudaStream_t s);
+void launch_adj_combine(const Op& op, const Workspace& ws, int mode, const double* recv,
+                        int64_t p_pad_total, const VecBufs* vb, DevState* st, cudaStream_t s);
 ProjPlan make_proj_plan(int64_t p_pad);
 void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const double* xin,
                  const double* gin, double* out, double* scratch, DevState* st,

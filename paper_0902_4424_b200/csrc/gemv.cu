@@ -895,7 +895,7 @@ static int split_choice() {
 }
 
 template <int SPLIT>
-static void fwd_launch(const FwdArgs& a, int grid, cudaStream_t s) {
+static void fwd_main_launch(const FwdArgs& a, int grid, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     L1G_CUDA(cudaFuncSetAttribute(fwd_kernel<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -903,13 +903,10 @@ static void fwd_launch(const FwdArgs& a, int grid, cudaStream_t s) {
     attr = true;
   }
   L1G_CUDA(launch_pdl(fwd_kernel<SPLIT>, grid, 32 * (4 * SPLIT + 1), fwd_smem(), s, a));
-  L1G_CUDA(cudaGetLastError());
-  L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)(a.n_pad / 32), FIN_T, 0, s, a));
-  L1G_CUDA(cudaGetLastError());
 }
 
 template <int SPLIT>
-static void adj_launch(const AdjArgs& a, int grid, cudaStream_t s) {
+static void adj_main_launch(const AdjArgs& a, int grid, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     L1G_CUDA(cudaFuncSetAttribute(adj_kernel<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -917,13 +914,10 @@ static void adj_launch(const AdjArgs& a, int grid, cudaStream_t s) {
     attr = true;
   }
   L1G_CUDA(launch_pdl(adj_kernel<SPLIT>, grid, 32 * (4 * SPLIT + 1), adj_smem(), s, a));
-  L1G_CUDA(cudaGetLastError());
-  L1G_CUDA(launch_pdl(adj_finish_kernel, (int)(a.p_pad / 64), FIN_T, 0, s, a));
-  L1G_CUDA(cudaGetLastError());
 }
 
-void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
-                const VecBufs* vb, DevState* st, cudaStream_t s, bool sparse) {
+static FwdArgs fwd_args(const Op& op, const Workspace& ws, int mode, const double* vin,
+                        double* vout, const VecBufs* vb, DevState* st) {
   const GemvPlan& pl = op.plan;
   FwdArgs a{};
   a.K = op.K;
@@ -933,7 +927,7 @@ void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, 
   a.nrg = pl.nrg;
   a.ncr = pl.ncr;
   a.mode = mode;
-  a.vin = (mode == FWD_ITER) ? vb->d : vin;
+  a.vin = vin;
   a.vout = vout;
   a.part = ws.fwd_part;
   a.grpsum = ws.grpsum;
@@ -941,34 +935,11 @@ void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, 
   a.cnt_all = ws.counters + pl.nrg + pl.ncg;
   a.st = st;
   if (vb) a.vb = *vb;
-  if (sparse && mode == FWD_ITER && a.vb.dmask) {
-    static bool attr = false;
-    if (!attr) {
-      L1G_CUDA(cudaFuncSetAttribute(fwd_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)sp_smem()));
-      attr = true;
-    }
-    a.stages = pl.sp_tiles;
-    a.ncr = pl.sp_ncr;
-    a.task_ctr = ws.counters + pl.nrg + pl.ncg + 2;
-    const int64_t ntasks = (pl.nrb + SP_RB - 1) / SP_RB * pl.sp_ncr;
-    L1G_CUDA(launch_pdl(fwd_sparse_kernel, (int)std::min<int64_t>(pl.grid, ntasks), 32 * (SP_NCW + 1),
-                        sp_smem(), s, a));
-    L1G_CUDA(cudaGetLastError());
-    L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)(a.n_pad / 32), FIN_T, 0, s, a));
-    L1G_CUDA(cudaGetLastError());
-    return;
-  }
-  const int grid = (int)std::min<int64_t>(pl.grid, (int64_t)pl.nrg * pl.ncr);
-  switch (split_choice()) {
-    case 1: fwd_launch<1>(a, grid, s); break;
-    case 4: fwd_launch<4>(a, grid, s); break;
-    default: fwd_launch<2>(a, grid, s); break;
-  }
+  return a;
 }
 
-void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
-                const VecBufs* vb, DevState* st, cudaStream_t s) {
+static AdjArgs adj_args(const Op& op, const Workspace& ws, int mode, const double* vin,
+                        double* vout, const VecBufs* vb, DevState* st) {
   const GemvPlan& pl = op.plan;
   AdjArgs a{};
   a.K = op.K;
@@ -987,12 +958,96 @@ void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, 
   a.cnt_all = ws.counters + pl.nrg + pl.ncg + 1;
   a.st = st;
   if (vb) a.vb = *vb;
+  return a;
+}
+
+// main forward kernel over the operator's columns -> range partials in ws.fwd_part;
+// returns the args the finish kernel needs (range count / widths)
+static FwdArgs fwd_main(const Op& op, const Workspace& ws, FwdArgs a, const uint32_t* dmask,
+                        bool sparse, cudaStream_t s) {
+  const GemvPlan& pl = op.plan;
+  if (sparse && dmask) {
+    static bool attr = false;
+    if (!attr) {
+      L1G_CUDA(cudaFuncSetAttribute(fwd_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sp_smem()));
+      attr = true;
+    }
+    a.vb.dmask = const_cast<uint32_t*>(dmask);
+    a.stages = pl.sp_tiles;
+    a.ncr = pl.sp_ncr;
+    a.task_ctr = ws.counters + pl.nrg + pl.ncg + 2;
+    const int64_t ntasks = (pl.nrb + SP_RB - 1) / SP_RB * pl.sp_ncr;
+    L1G_CUDA(launch_pdl(fwd_sparse_kernel, (int)std::min<int64_t>(pl.grid, ntasks),
+                        32 * (SP_NCW + 1), sp_smem(), s, a));
+    return a;
+  }
+  const int grid = (int)std::min<int64_t>(pl.grid, (int64_t)pl.nrg * pl.ncr);
+  switch (split_choice()) {
+    case 1: fwd_main_launch<1>(a, grid, s); break;
+    case 4: fwd_main_launch<4>(a, grid, s); break;
+    default: fwd_main_launch<2>(a, grid, s); break;
+  }
+  return a;
+}
+
+static void adj_main(const Op& op, const AdjArgs& a, cudaStream_t s) {
+  const GemvPlan& pl = op.plan;
   const int grid = (int)std::min<int64_t>(pl.grid, (int64_t)pl.ncg * pl.nrr);
   switch (split_choice()) {
-    case 1: adj_launch<1>(a, grid, s); break;
-    case 4: adj_launch<4>(a, grid, s); break;
-    default: adj_launch<2>(a, grid, s); break;
+    case 1: adj_main_launch<1>(a, grid, s); break;
+    case 4: adj_main_launch<4>(a, grid, s); break;
+    default: adj_main_launch<2>(a, grid, s); break;
   }
+}
+
+void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
+                const VecBufs* vb, DevState* st, cudaStream_t s, bool sparse) {
+  FwdArgs a = fwd_args(op, ws, mode, (mode == FWD_ITER) ? vb->d : vin, vout, vb, st);
+  a = fwd_main(op, ws, a, a.vb.dmask, sparse && mode == FWD_ITER, s);
+  L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)(a.n_pad / 32), FIN_T, 0, s, a));
+}
+
+void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
+                const VecBufs* vb, DevState* st, cudaStream_t s) {
+  const AdjArgs a = adj_args(op, ws, mode, vin, vout, vb, st);
+  adj_main(op, a, s);
+  L1G_CUDA(launch_pdl(adj_finish_kernel, (int)(a.p_pad / 64), FIN_T, 0, s, a));
+}
+
+// ---- column-sharded pieces: rank partials and their combination
+void launch_fwd_part(const Op& op, const Workspace& ws, const double* vin, const uint32_t* dmask,
+                     bool sparse, double* out, DevState* st, cudaStream_t s) {
+  FwdArgs a = fwd_args(op, ws, FWD_APPLY, vin, out, nullptr, st);
+  a = fwd_main(op, ws, a, dmask, sparse, s);
+  a.mode = FWD_APPLY;  // the finish only writes the shard's tree values
+  L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)(a.n_pad / 32), FIN_T, 0, s, a));
+}
+
+void launch_fwd_combine(const Op& op, const Workspace& ws, int mode, const double* recv, int nr,
+                        const VecBufs* vb, DevState* st, cudaStream_t s) {
+  FwdArgs a = fwd_args(op, ws, mode, nullptr, nullptr, vb, st);
+  a.part = const_cast<double*>(recv);
+  a.ncr = nr;
+  a.task_ctr = ws.counters + op.plan.nrg + op.plan.ncg + 2;
+  L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)(a.n_pad / 32), FIN_T, 0, s, a));
+}
+
+void launch_adj_part(const Op& op, const Workspace& ws, int mode, const VecBufs* vb, double* out,
+                     DevState* st, cudaStream_t s) {
+  AdjArgs a = adj_args(op, ws, mode, nullptr, out, vb, st);
+  adj_main(op, a, s);
+  a.mode = ADJ_APPLY;
+  L1G_CUDA(launch_pdl(adj_finish_kernel, (int)(a.p_pad / 64), FIN_T, 0, s, a));
+}
+
+void launch_adj_combine(const Op& op, const Workspace& ws, int mode, const double* recv,
+                        int64_t p_pad_total, const VecBufs* vb, DevState* st, cudaStream_t s) {
+  AdjArgs a = adj_args(op, ws, mode, nullptr, nullptr, vb, st);
+  a.part = const_cast<double*>(recv);
+  a.nrr = 1;
+  a.p_pad = p_pad_total;
+  L1G_CUDA(launch_pdl(adj_finish_kernel, (int)(p_pad_total / 64), FIN_T, 0, s, a));
 }
 
 }  // namespace l1g
