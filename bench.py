@@ -6,6 +6,7 @@ iterations/s and achieved HBM GB/s of K streamed vs peak).
 
 A step is one gpss_solve of the config (C2: 8192x32768, 300 iterations, x0 = 0) with K
 resident in HBM.  K (2 GiB) is larger than L2, so no flush is needed between steps.
+With N > 1 (torchrun) the same problem is column-sharded over the N GPUs (strong scaling).
 `value` = iterations / device time (CUDA events on the solver stream, max over ranks);
 `e2e` = the same metric through the C-ABI call l1g_gpss_solve with host y and x buffers
 (copies inside the timed region).  Prints one JSON line on rank 0.
@@ -208,7 +209,7 @@ def run_reference(args, world, rank, pg):
               f"({'OpenMP Eigen stand-in' if kind == 'reference' else 'C port'})")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Philox Gaussian, oracle generator on the host)",
             "config": {"workload": cfgname, "n": n, "p": p, "iterations_per_step": per_step},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
@@ -238,15 +239,34 @@ def run_b200(args, world, rank, local, pg):
     P = H.build_problem(spec, ctx)
     op, y, rho = P["op"], P["y"], P["rho"]
     n, p = spec.n, spec.p
-    setup_s = time.perf_counter() - t_setup
     lib = L.load()
     cfg = l1.GpConfig()._c()
     stop = l1.StopRule(max_iterations=iters, stationarity_tol=0.0)._c()
-
-    # ---- device-resident solver (inputs already in HBM)
+    comm = None
     h = C.c_void_p()
-    L.check(lib.l1g_solver_create(op.h, L.ptr(np.ascontiguousarray(y)), rho, C.byref(cfg),
-                                  C.byref(h)), "solver_create")
+    sharded = world > 1 or args.force_sharded
+    if sharded:
+        # column sharding over the ranks: this rank keeps only its block of
+        # columns; y and rho come from the full problem built above (identical on all ranks)
+        from paper_0902_4424_b200 import shard as S
+        if spec.sigma_hat is None:
+            spec.sigma_hat = P["sigma_hat"]
+        sh = S.shard_plan(p, world)[rank]
+        op.close()
+        op, _, _ = H.build_operator(spec, ctx, col_offset=sh.col0, p_local=sh.p_local)
+        if pg is not None:
+            uid = S.exchange_id(pg, rank)
+        else:
+            buf = (C.c_uint8 * 128)()
+            L.check(lib.l1g_comm_unique_id(C.cast(buf, C.c_void_p)), "comm_unique_id")
+            uid = bytes(buf)
+        comm = S.Comm(ctx, rank, world, uid)
+        h = S.create_sharded_solver(op, comm, y, rho, l1.GpConfig())
+    else:
+        # ---- device-resident solver (inputs already in HBM)
+        L.check(lib.l1g_solver_create(op.h, L.ptr(np.ascontiguousarray(y)), rho, C.byref(cfg),
+                                      C.byref(h)), "solver_create")
+    setup_s = time.perf_counter() - t_setup
     sp = C.c_void_p()
     lib.l1g_solver_stream(h, C.byref(sp))
     stream = torch.cuda.ExternalStream(sp.value)
@@ -278,7 +298,7 @@ def run_b200(args, world, rank, local, pg):
     tp, tf, ta = C.c_double(), C.c_double(), C.c_double()
     ti, tl = C.c_int64(), C.c_int64()
     lib.l1g_solver_timing(h, None, None, None, None, C.byref(tl), 1)
-    value = world * done_iters / (dev_ms / 1e3)  # whole-job iterations/s (replicas)
+    value = done_iters / (dev_ms / 1e3)  # iterations/s of the one (sharded) problem
     reason = L.REASONS[res.reason]
     # per-kernel breakdown: a separate solve with event nodes between the kernels (they
     # serialise the programmatic launches, so this pass is not the timed one)
@@ -298,6 +318,12 @@ def run_b200(args, world, rank, local, pg):
     res2 = L.ResultC()
 
     def e2e_once():
+        if sharded:  # the sharded solver's public calls, host y in, host x out
+            L.check(lib.l1g_solver_set_y(h, yp), "set_y")
+            L.check(lib.l1g_solver_init(h, None), "init")
+            L.check(lib.l1g_solver_run(h, C.byref(stop), C.byref(res2), None, 0), "run")
+            L.check(lib.l1g_solver_get(h, xp, None, None, None, None, None, None), "get")
+            return res2.iterations
         L.check(lib.l1g_gpss_solve(op.h, yp, rho, C.byref(cfg), C.byref(stop), None, xp,
                                    C.byref(res2), None, 0), "gpss_solve")
         return res2.iterations
@@ -312,7 +338,7 @@ def run_b200(args, world, rank, local, pg):
         e2e_iters += e2e_once()
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(pg, time.perf_counter() - t0)
-    e2e_value = world * e2e_iters / e2e_s
+    e2e_value = e2e_iters / e2e_s
     x_e2e = np.ctypeslib.as_array((C.c_double * p).from_address(xp.value)).copy()
     x_dev = np.empty(p)
     L.check(lib.l1g_solver_get(h, L.ptr(x_dev), None, None, None, None, None, None))
@@ -321,7 +347,7 @@ def run_b200(args, world, rank, local, pg):
 
     # ---- roofline of the dominant kernel (per-launch CUDA events inside the timed loop)
     hbm, peak_src = peaks()
-    k_bytes = n * p * 8.0
+    k_bytes = n * p * 8.0 / world  # this rank's columns
     it = max(ti.value, 1)
     avg = {"proj": tp.value / it, "fwd": tf.value / it, "adj": ta.value / it}
     dom = "adj" if avg["adj"] >= avg["fwd"] else "fwd"
@@ -344,7 +370,7 @@ def run_b200(args, world, rank, local, pg):
                     "GBps_incl_finish": sp_cols * n * 8.0 / (avg["fwd"] / 1e3) / 1e9},
                 "share_of_iteration": {k: round(v / sum(avg.values()), 4)
                                        for k, v in avg.items()},
-                "iteration_GBps_2npx8": 2 * k_bytes * done_iters / (dev_ms / 1e3) / 1e9 / world}
+                "iteration_GBps_2npx8": 2 * k_bytes * done_iters / (dev_ms / 1e3) / 1e9}
 
     # ---- CPU baseline on rank 0 at N=1 (bounded sample of the same workload)
     cpu = None
@@ -368,7 +394,7 @@ def run_b200(args, world, rank, local, pg):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded Philox Gaussian K scaled to ||K||_2=0.9, generated "
                         "on device; BASELINE.json configs[1])",
                 "config": {"workload": f"{args.config}: {spec.kind} {n}x{p}, nnz {spec.nnz}, "
@@ -376,7 +402,9 @@ def run_b200(args, world, rank, local, pg):
                            "n": n, "p": p, "iterations_per_step": done_iters / args.steps,
                            "stop_reason": reason, "rho": rho, "sigma_hat": P["sigma_hat"],
                            "l2": "inputs larger than L2 (K = %.2f GiB)" % (k_bytes / 2**30),
-                           "parallelism": "replicas" if world > 1 else "single",
+                           "parallelism": (f"column-sharded over {world} GPUs (NCCL "
+                                           "allgather of K d / K^T r shard values)")
+                           if sharded else "single",
                            "setup_s": round(setup_s, 3)},
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 8,
                         "d2h_bytes_per_step": p * 8 + C.sizeof(L.ResultC),
@@ -387,12 +415,14 @@ def run_b200(args, world, rank, local, pg):
                 "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)
     lib.l1g_solver_destroy(h)
+    if comm is not None:
+        comm.close()
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--iters", type=int, default=0)
@@ -400,6 +430,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--recompute-sigma", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=0)
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the NCCL-sharded solver path even on one GPU (a 1-rank communicator)")
     args = ap.parse_args()
     world, rank, local, pg = dist_setup(args)
     if args.impl == "reference":
