@@ -118,6 +118,11 @@ int l1g_op_apply_adjoint(l1g_op* op, const double* r, double* out);
 /* device-pointer forms; stream may be NULL (legacy default stream of the context) */
 int l1g_op_apply_dev(l1g_op* op, const double* x_dev, double* out_dev, void* stream);
 int l1g_op_apply_adjoint_dev(l1g_op* op, const double* r_dev, double* out_dev, void* stream);
+/* batched products on the FP64 tensor cores (mma.sync f64): X is B x p, R is B x n,
+ * problem-major; results Y (B x n), G (B x p).  Accumulation order is the tensor core's,
+ * so these agree with l1g_op_apply to rounding (not bit for bit). */
+int l1g_op_apply_batched(l1g_op* op, int B, const double* X, double* Y);
+int l1g_op_apply_adjoint_batched(l1g_op* op, int B, const double* R, double* G);
 int l1g_op_spectral_norm(l1g_op* op, int max_iters, double tol, double* sigma,
                          int64_t* matvecs);
 

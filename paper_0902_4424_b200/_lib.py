@@ -78,6 +78,8 @@ _SIGS = {
     "l1g_op_apply_adjoint": (C.c_int, [_vp, _vp, _vp]),
     "l1g_op_apply_dev": (C.c_int, [_vp, _vp, _vp, _vp]),
     "l1g_op_apply_adjoint_dev": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "l1g_op_apply_batched": (C.c_int, [_vp, C.c_int, _vp, _vp]),
+    "l1g_op_apply_adjoint_batched": (C.c_int, [_vp, C.c_int, _vp, _vp]),
     "l1g_op_spectral_norm": (C.c_int, [_vp, C.c_int, C.c_double, _dp, C.POINTER(_i64)]),
     "l1g_project_l1": (C.c_int, [_vp, _vp, _i64, C.c_double, _vp, _dp, C.POINTER(_i64)]),
     "l1g_soft_threshold": (C.c_int, [_vp, _vp, _i64, C.c_double, _vp]),

@@ -864,6 +864,52 @@ int l1g_op_apply_adjoint(l1g_op* op, const double* r, double* out) {
 }
 
 // linear_operator.cpp:43-60
+// Batched products through the FP64 tensor-core kernels (dmma.cu): X is B x p and R is B x n
+// (problem-major host arrays); each problem counts as one matvec of its own.
+static void batched_product(l1g_op* op, int B, const double* in, double* out, bool adjoint) {
+  if (B < 1) throw InvalidArgument("batched apply: B must be >= 1");
+  std::lock_guard<std::mutex> lk(op->mu);
+  set_device(op->c);
+  const GemvPlan& pl = op->plan;
+  const BatchPlan bp = make_batch_plan(pl, B, op->c->sm_count);
+  const int64_t lin = adjoint ? pl.n : pl.p, lin_pad = adjoint ? pl.n_pad : pl.p_pad;
+  const int64_t lout = adjoint ? pl.p : pl.n, lout_pad = adjoint ? pl.p_pad : pl.n_pad;
+  const int64_t splits = adjoint ? bp.adj_splits : bp.fwd_splits;
+  cudaStream_t s = op->c->stream;
+  double* vin = dalloc<double>((size_t)bp.Bp * lin_pad);
+  double* vout = dalloc<double>((size_t)B * lout_pad);
+  double* part = dalloc<double>((size_t)splits * bp.Bp * lout_pad);
+  try {
+    L1G_CUDA(cudaMemcpy2DAsync(vin, lin_pad * 8, in, lin * 8, lin * 8, B, cudaMemcpyHostToDevice, s));
+    if (adjoint) {
+      launch_badj(*op, bp, vin, part, s);
+      launch_bfinish_adj(*op, bp, ADJ_APPLY, part, vout, nullptr, nullptr, nullptr, nullptr, 0, s);
+    } else {
+      launch_bfwd(*op, bp, vin, part, s);
+      launch_bfinish_fwd(*op, bp, FWD_APPLY, part, vout, nullptr, nullptr, nullptr, nullptr, 0, s);
+    }
+    L1G_CUDA(cudaMemcpy2DAsync(out, lout * 8, vout, lout_pad * 8, lout * 8, B,
+                               cudaMemcpyDeviceToHost, s));
+    L1G_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    dfree(vin);
+    dfree(vout);
+    dfree(part);
+    throw;
+  }
+  dfree(vin);
+  dfree(vout);
+  dfree(part);
+}
+
+int l1g_op_apply_batched(l1g_op* op, int B, const double* X, double* Y) {
+  return guarded([&] { batched_product(op, B, X, Y, false); });
+}
+
+int l1g_op_apply_adjoint_batched(l1g_op* op, int B, const double* R, double* G) {
+  return guarded([&] { batched_product(op, B, R, G, true); });
+}
+
 int l1g_op_spectral_norm(l1g_op* op, int max_iters, double tol, double* sigma, int64_t* matvecs) {
   return guarded([&] {
     if (max_iters < 1) throw InvalidArgument("spectral_norm_estimate: max_iters must be >= 1");

@@ -1,0 +1,257 @@
+// dmma.cu -- batched-RHS products on the FP64 tensor cores (BASELINE config C5).
+//
+// With B problems sharing one K (an isochrone campaign / regularisation path: many y or rho,
+// isochrone.cpp:111-196) the per-problem GEMVs of gp_iterate (gpss.cpp:194, :211) become
+//   forward  Y = K D      (n x B),  D = [d_1 .. d_B]
+//   adjoint  G = K^T R'   (p x B),  R' = [r_1 + l_1 kd_1 .. ]
+// i.e. two DGEMMs with 4 n p B flop per iteration, issued as mma.sync.m8n8k4.f64 (SASS
+// DMMA; tcgen05 has no fp64 kind).  K stays in the tiled layout of the single-RHS kernels;
+// each CTA computes a 64 x 128 (rows or columns x problems) block over one split of the
+// reduction dimension, staged through shared memory with cp.async (2-3 stages); the split
+// partials are joined by the finish kernels (gemv.cu), which also run every problem's
+// epilogue.  DMMA accumulates with fused multiply-adds in its own order, so the batched
+// path matches the per-problem canonical solve to rounding, not bit for bit.
+#include "common.cuh"
+#include "engine.h"
+
+namespace l1g {
+
+namespace {
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+}  // namespace
+
+constexpr int BW = 128;   // problems per CTA (B is padded to a multiple)
+constexpr int BT = 256;   // 8 warps: 2 (rows / columns) x 4 (problems), 32 x 32 each
+constexpr int VPAD = 4;   // row padding (doubles) of staged problem vectors
+
+// forward: K rows 64 (two tiles) x 64 columns, D chunk 128 problems x 64 columns
+constexpr int F_KT = 2 * TILE;
+constexpr int F_VS = BW * (TC + VPAD);
+constexpr int F_STAGE = F_KT + F_VS;
+constexpr int F_STAGES = 2;
+// adjoint: one tile 32 rows x 64 columns, R chunk 128 problems x 32 rows
+constexpr int A_KT = TILE;
+constexpr int A_VS = BW * (TR + VPAD);
+constexpr int A_STAGE = A_KT + A_VS;
+constexpr int A_STAGES = 3;
+
+size_t bfwd_smem() { return (size_t)F_STAGES * F_STAGE * 8; }
+size_t badj_smem() { return (size_t)A_STAGES * A_STAGE * 8; }
+
+// part[split][b][row] = sum over this split's column blocks of K[row, cols] d_b[cols]
+__global__ void __launch_bounds__(BT, 1) bfwd_kernel(const BGemmArgs a) {
+  pdl_wait_and_trigger();
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wr = warp & 1, wc = warp >> 1;
+  const int64_t rb0 = 2LL * blockIdx.x;
+  const int split = blockIdx.y;
+  const int b0 = blockIdx.z * BW;
+  const int c_begin = split * a.per_split;
+  const int c_end = c_begin + a.per_split < a.nblocks ? c_begin + a.per_split : a.nblocks;
+  const int nch = c_end > c_begin ? c_end - c_begin : 0;
+  auto load = [&](int c, int st) {
+    double* ks = sm + st * F_STAGE;
+    double* vs = ks + F_KT;
+    const int64_t cb = c_begin + c;
+    for (int q = tid; q < TILE; q += BT) {  // two tiles = 2 x 1024 chunks of 16 bytes
+      const int tile = q >> 10, off = (q & 1023) * 2;
+      cp16(ks + tile * TILE + off, a.K + tile_offset(rb0 + tile, cb, a.ncb) + off);
+    }
+    for (int q = tid; q < BW * (TC / 2); q += BT) {
+      const int b = q >> 5, kq = (q & 31) * 2;
+      cp16(vs + b * (TC + VPAD) + kq, a.V + (int64_t)(b0 + b) * a.vstride + cb * TC + kq);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (nch > 0) load(0, 0);
+  cp_commit();
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) load(c + 1, (c + 1) & 1);
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    const double* ks = sm + (c & 1) * F_STAGE + wr * TILE;
+    const double* vs = sm + (c & 1) * F_STAGE + F_KT + (wc * 32) * (TC + VPAD);
+#pragma unroll 4
+    for (int kk = 0; kk < TC; kk += 4) {
+      const int col = kk + t;
+      const int sw = col_swz(col);
+      double av[4], bv[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) av[mt] = ks[col * 32 + ((mt * 8 + g) ^ sw)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bv[nt] = vs[(nt * 8 + g) * (TC + VPAD) + col];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av[mt], bv[nt]);
+    }
+    __syncthreads();
+  }
+  double* out = a.part + split * a.pslab;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int64_t row = (rb0 + wr) * TR + mt * 8 + g;
+      const int64_t b = b0 + wc * 32 + nt * 8 + 2 * t;
+      out[b * a.ostride + row] = acc[mt][nt][0];
+      out[(b + 1) * a.ostride + row] = acc[mt][nt][1];
+    }
+}
+
+// part[split][b][col] = sum over this split's row blocks of K[rows, col] r_b[rows]
+__global__ void __launch_bounds__(BT, 1) badj_kernel(const BGemmArgs a) {
+  pdl_wait_and_trigger();
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wc = warp >> 1;
+  const int64_t cb = blockIdx.x;
+  const int split = blockIdx.y;
+  const int b0 = blockIdx.z * BW;
+  const int r_begin = split * a.per_split;
+  const int r_end = r_begin + a.per_split < a.nblocks ? r_begin + a.per_split : a.nblocks;
+  const int nch = r_end > r_begin ? r_end - r_begin : 0;
+  auto load = [&](int c, int st) {
+    double* ks = sm + st * A_STAGE;
+    double* vs = ks + A_KT;
+    const int64_t rb = r_begin + c;
+    for (int q = tid; q < TILE / 2; q += BT) cp16(ks + q * 2, a.K + tile_offset(rb, cb, a.ncb) + q * 2);
+    for (int q = tid; q < BW * (TR / 2); q += BT) {
+      const int b = q >> 4, kq = (q & 15) * 2;
+      cp16(vs + b * (TR + VPAD) + kq, a.V + (int64_t)(b0 + b) * a.vstride + rb * TR + kq);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < A_STAGES - 1; ++s) {
+    if (s < nch) load(s, s);
+    cp_commit();
+  }
+  for (int c = 0; c < nch; ++c) {
+    if (c + A_STAGES - 1 < nch) load(c + A_STAGES - 1, (c + A_STAGES - 1) % A_STAGES);
+    cp_commit();
+    cp_wait<A_STAGES - 1>();
+    __syncthreads();
+    const double* ks = sm + (c % A_STAGES) * A_STAGE;
+    const double* vs = sm + (c % A_STAGES) * A_STAGE + A_KT + (wc * 32) * (TR + VPAD);
+#pragma unroll
+    for (int kk = 0; kk < TR; kk += 4) {
+      const int row = kk + t;
+      double av[4], bv[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int col = wm * 32 + mt * 8 + g;
+        av[mt] = ks[col * 32 + (row ^ col_swz(col))];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bv[nt] = vs[(nt * 8 + g) * (TR + VPAD) + row];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av[mt], bv[nt]);
+    }
+    __syncthreads();
+  }
+  double* out = a.part + split * a.pslab;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int64_t col = cb * TC + wm * 32 + mt * 8 + g;
+      const int64_t b = b0 + wc * 32 + nt * 8 + 2 * t;
+      out[b * a.ostride + col] = acc[mt][nt][0];
+      out[(b + 1) * a.ostride + col] = acc[mt][nt][1];
+    }
+}
+
+static int splits_for(int64_t tiles_out, int64_t nblocks, int sm_count) {
+  // enough CTAs for ~7 waves of one CTA per SM, splits dividing the reduction evenly
+  int s = 1;
+  while (s * 2 <= nblocks && tiles_out * s * 2 <= 7LL * sm_count) s *= 2;
+  return s;
+}
+
+BatchPlan make_batch_plan(const GemvPlan& pl, int B, int sm_count) {
+  BatchPlan bp{};
+  bp.B = B;
+  bp.Bp = (B + BW - 1) / BW * BW;
+  const int64_t bz = bp.Bp / BW;
+  bp.fwd_splits = splits_for((pl.n_pad / 64) * bz, pl.ncb, sm_count);
+  bp.fwd_per = (int)((pl.ncb + bp.fwd_splits - 1) / bp.fwd_splits);
+  bp.adj_splits = splits_for(pl.ncb * bz, pl.nrb, sm_count);
+  bp.adj_per = (int)((pl.nrb + bp.adj_splits - 1) / bp.adj_splits);
+  return bp;
+}
+
+void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* part,
+                 cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    L1G_CUDA(cudaFuncSetAttribute(bfwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)bfwd_smem()));
+    attr = true;
+  }
+  const GemvPlan& pl = op.plan;
+  BGemmArgs a{};
+  a.K = op.K;
+  a.ncb = pl.ncb;
+  a.nrb = pl.nrb;
+  a.V = D;
+  a.vstride = pl.p_pad;
+  a.part = part;
+  a.pslab = (int64_t)bp.Bp * pl.n_pad;
+  a.ostride = pl.n_pad;
+  a.per_split = bp.fwd_per;
+  a.nblocks = (int)pl.ncb;
+  const dim3 grid((unsigned)(pl.n_pad / 64), (unsigned)bp.fwd_splits, (unsigned)(bp.Bp / BW));
+  L1G_CUDA(launch_pdl(bfwd_kernel, grid, BT, bfwd_smem(), s, a));
+}
+
+void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* part,
+                 cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    L1G_CUDA(cudaFuncSetAttribute(badj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)badj_smem()));
+    attr = true;
+  }
+  const GemvPlan& pl = op.plan;
+  BGemmArgs a{};
+  a.K = op.K;
+  a.ncb = pl.ncb;
+  a.nrb = pl.nrb;
+  a.V = R;
+  a.vstride = pl.n_pad;
+  a.part = part;
+  a.pslab = (int64_t)bp.Bp * pl.p_pad;
+  a.ostride = pl.p_pad;
+  a.per_split = bp.adj_per;
+  a.nblocks = (int)pl.nrb;
+  const dim3 grid((unsigned)pl.ncb, (unsigned)bp.adj_splits, (unsigned)(bp.Bp / BW));
+  L1G_CUDA(launch_pdl(badj_kernel, grid, BT, badj_smem(), s, a));
+}
+
+}  // namespace l1g

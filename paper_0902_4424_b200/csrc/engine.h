@@ -128,6 +128,32 @@ struct VecBufs {
   uint32_t* dmask;  // support bitmap of d (bit j of word j/32), written by proj_kernel
 };
 
+// batched-RHS products on the FP64 tensor cores (dmma.cu)
+struct BatchPlan {
+  int B, Bp;                 // problems, padded to the CTA width (128)
+  int fwd_splits, fwd_per;   // column blocks per split of the forward reduction
+  int adj_splits, adj_per;   // row blocks per split of the adjoint reduction
+};
+struct BGemmArgs {
+  const double* K;
+  int64_t ncb, nrb;
+  const double* V;   // forward: D [Bp][p_pad]; adjoint: R [Bp][n_pad]
+  int64_t vstride;
+  double* part;      // [splits][Bp][ostride]
+  int64_t pslab, ostride;
+  int per_split, nblocks;
+};
+BatchPlan make_batch_plan(const GemvPlan& pl, int B, int sm_count);
+void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* part, cudaStream_t s);
+void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* part, cudaStream_t s);
+
+void launch_bfinish_fwd(const Op& op, const BatchPlan& bp, int mode, const double* part,
+                        double* vout, const VecBufs* vb, DevState* st, unsigned* counters,
+                        double* grpsum, int64_t grp_stride, cudaStream_t s);
+void launch_bfinish_adj(const Op& op, const BatchPlan& bp, int mode, const double* part,
+                        double* vout, const VecBufs* vb, DevState* st, unsigned* counters,
+                        double* grpsum, int64_t grp_stride, cudaStream_t s);
+
 // host launchers (gemv.cu, project.cu)
 GemvPlan make_plan(int64_t n, int64_t p, int sm_count);
 void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,

@@ -31,6 +31,13 @@ constexpr int ADJ_MAX_BLOCKS = 16;   // row blocks per adjoint task (counter dep
 constexpr int MAX_TR = ADJ_MAX_BLOCKS * TR;
 constexpr int RS_PAD = MAX_TR / 8;   // padding of the shared r slice (see rs_pos)
 
+// Finish kernels over a batch of problems (gridDim.y = problems): problem b's partials,
+// vectors, state, group sums and counter sit at these offsets from problem 0's.
+struct BatchStrides {
+  int64_t pstride;  // between consecutive partials of one output
+  int64_t bpart, bn, bp, bgrp;
+};
+
 struct FwdArgs {
   const double* K;
   int64_t ncb, n_pad;
@@ -44,6 +51,7 @@ struct FwdArgs {
   unsigned* task_ctr;  // sparse forward: dynamic task counter (reset by fwd_finish)
   DevState* st;
   VecBufs vb;
+  BatchStrides bs;     // finish kernels: partial stride, per-problem offsets (blockIdx.y)
 };
 
 struct AdjArgs {
@@ -58,6 +66,7 @@ struct AdjArgs {
   unsigned* cnt_all;
   DevState* st;
   VecBufs vb;
+  BatchStrides bs;
 };
 
 template <int N, class F>
@@ -128,6 +137,18 @@ __device__ __forceinline__ void snapshot(DevState* dst, const DevState* src, int
   __syncwarp();
 }
 
+template <class A>
+__device__ __forceinline__ A batch_view(const A& a0, int prob) {
+  A a = a0;
+  if (prob == 0) return a;
+  const BatchStrides& b = a0.bs;
+  a.part += prob * b.bpart;
+  a.st += prob;
+  a.grpsum += prob * b.bgrp;
+  a.cnt_all += prob;
+  return a;  // vectors: the kernels add prob * bn / bp to a0.vb (runtime-indexed arrays)
+}
+
 __device__ __forceinline__ int fin_block(int cnt) {
   int B = 1;
   while (B * FIN_W < cnt) B <<= 1;
@@ -177,8 +198,11 @@ __device__ __forceinline__ void cta_tree_arrays(const double* v, int count, int 
   }
 }
 
-__global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
+__global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a0) {
   pdl_wait_and_trigger();
+  FwdArgs a = batch_view(a0, blockIdx.y);
+  if (blockIdx.y && a.vout) a.vout += blockIdx.y * a0.bs.bn;
+  const int64_t on = blockIdx.y * a0.bs.bn;
   if (a.mode != FWD_APPLY && a.st->status != RUNNING) return;
   __shared__ double sv[FIN_W][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -192,11 +216,11 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
     for (; k + 4 <= hi; k += 4) {
       double v[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldcg(a.part + (int64_t)(k + u) * a.n_pad + row);
+      for (int u = 0; u < 4; ++u) v[u] = __ldcg(a.part + (int64_t)(k + u) * a.bs.pstride + row);
 #pragma unroll
       for (int u = 0; u < 4; ++u) acc.push(v[u], (uint32_t)(k + u - lo));
     }
-    for (; k < hi; ++k) acc.push(__ldcg(a.part + (int64_t)k * a.n_pad + row), (uint32_t)(k - lo));
+    for (; k < hi; ++k) acc.push(__ldcg(a.part + (int64_t)k * a.bs.pstride + row), (uint32_t)(k - lo));
     sv[warp][lane] = hi > lo ? acc.final_value((uint32_t)(hi - lo)) : 0.0;
     __syncthreads();
   }
@@ -209,12 +233,12 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
       const int cur = a.st->cur;
       double l0, l1 = 0.0;
       if (a.mode == FWD_INIT) {
-        const double r = sub(kd, a.vb.y[row]);  // Kx0 - y   (gpss.cpp:128)
-        a.vb.r[cur][row] = r;
+        const double r = sub(kd, a0.vb.y[on + row]);  // Kx0 - y   (gpss.cpp:128)
+        a0.vb.r[cur][on + row] = r;
         l0 = mul(r, r);                         // ||r||^2   (gpss.cpp:129)
       } else {
-        a.vb.kd[row] = kd;
-        l0 = mul(a.vb.r[cur][row], kd);         // (Kx-y)'Kd (gpss.cpp:195)
+        a0.vb.kd[on + row] = kd;
+        l0 = mul(a0.vb.r[cur][on + row], kd);         // (Kx-y)'Kd (gpss.cpp:195)
         l1 = mul(kd, kd);                       // ||Kd||^2  (gpss.cpp:196)
       }
       l0 = warp_tree(l0);
@@ -267,8 +291,11 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a) {
+__global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
   pdl_wait_and_trigger();
+  AdjArgs a = batch_view(a0, blockIdx.y);
+  if (blockIdx.y && a.vout) a.vout += blockIdx.y * a0.bs.bp;
+  const int64_t ofp = blockIdx.y * a0.bs.bp;
   if (a.mode != ADJ_APPLY && a.st->status != RUNNING) return;
   __shared__ double sv[2][FIN_W][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -283,7 +310,7 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a) {
       double2 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        v[u] = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)(k + u) * a.p_pad + col));
+        v[u] = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)(k + u) * a.bs.pstride + col));
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         acc0.push(v[u].x, (uint32_t)(k + u - lo));
@@ -291,7 +318,7 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a) {
       }
     }
     for (; k < hi; ++k) {
-      const double2 v = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)k * a.p_pad + col));
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)k * a.bs.pstride + col));
       acc0.push(v.x, (uint32_t)(k - lo));
       acc1.push(v.y, (uint32_t)(k - lo));
     }
@@ -310,16 +337,16 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a) {
       const int cur = st->cur;
       const double g0 = mul(2.0, s0), g1 = mul(2.0, s1);  // 2 K^T r (gpss.cpp:130, :211)
       if (a.mode == ADJ_INIT) {
-        *reinterpret_cast<double2*>(a.vb.g[cur] + col) = make_double2(g0, g1);
+        *reinterpret_cast<double2*>(a0.vb.g[cur] + ofp + col) = make_double2(g0, g1);
       } else {
         // x' = x + lambda d (gpss.cpp:208), s = x' - x, z = g' - g (gpss.cpp:150-151)
         const double lam = st->step;
-        const double2 xo = *reinterpret_cast<const double2*>(a.vb.x[cur] + col);
-        const double2 go = *reinterpret_cast<const double2*>(a.vb.g[cur] + col);
-        const double2 dd = *reinterpret_cast<const double2*>(a.vb.d + col);
+        const double2 xo = *reinterpret_cast<const double2*>(a0.vb.x[cur] + ofp + col);
+        const double2 go = *reinterpret_cast<const double2*>(a0.vb.g[cur] + ofp + col);
+        const double2 dd = *reinterpret_cast<const double2*>(a0.vb.d + ofp + col);
         const double x0n = add(xo.x, mul(lam, dd.x)), x1n = add(xo.y, mul(lam, dd.y));
-        *reinterpret_cast<double2*>(a.vb.x[cur ^ 1] + col) = make_double2(x0n, x1n);
-        *reinterpret_cast<double2*>(a.vb.g[cur ^ 1] + col) = make_double2(g0, g1);
+        *reinterpret_cast<double2*>(a0.vb.x[cur ^ 1] + ofp + col) = make_double2(x0n, x1n);
+        *reinterpret_cast<double2*>(a0.vb.g[cur ^ 1] + ofp + col) = make_double2(g0, g1);
         const double sa = sub(x0n, xo.x), sb = sub(x1n, xo.y);
         const double za = sub(g0, go.x), zb = sub(g1, go.y);
         const double dsz = warp_tree(add(mul(sa, za), mul(sb, zb)));
@@ -935,6 +962,7 @@ static FwdArgs fwd_args(const Op& op, const Workspace& ws, int mode, const doubl
   a.cnt_all = ws.counters + pl.nrg + pl.ncg;
   a.st = st;
   if (vb) a.vb = *vb;
+  a.bs.pstride = pl.n_pad;
   return a;
 }
 
@@ -958,6 +986,7 @@ static AdjArgs adj_args(const Op& op, const Workspace& ws, int mode, const doubl
   a.cnt_all = ws.counters + pl.nrg + pl.ncg + 1;
   a.st = st;
   if (vb) a.vb = *vb;
+  a.bs.pstride = pl.p_pad;
   return a;
 }
 
@@ -1047,7 +1076,44 @@ void launch_adj_combine(const Op& op, const Workspace& ws, int mode, const doubl
   a.part = const_cast<double*>(recv);
   a.nrr = 1;
   a.p_pad = p_pad_total;
+  a.bs.pstride = p_pad_total;
   L1G_CUDA(launch_pdl(adj_finish_kernel, (int)(p_pad_total / 64), FIN_T, 0, s, a));
+}
+
+// ---- batched-RHS finishes (dmma.cu partials): gridDim.y = problems
+void launch_bfinish_fwd(const Op& op, const BatchPlan& bp, int mode, const double* part,
+                        double* vout, const VecBufs* vb, DevState* st, unsigned* counters,
+                        double* grpsum, int64_t grp_stride, cudaStream_t s) {
+  const GemvPlan& pl = op.plan;
+  FwdArgs a = fwd_args(op, Workspace{}, mode, nullptr, vout, vb, st);
+  a.part = const_cast<double*>(part);
+  a.ncr = bp.fwd_splits;
+  a.bs.pstride = (int64_t)bp.Bp * pl.n_pad;
+  a.bs.bpart = pl.n_pad;
+  a.bs.bn = pl.n_pad;
+  a.bs.bgrp = grp_stride;
+  a.grpsum = grpsum;
+  a.cnt_all = counters;
+  a.task_ctr = nullptr;
+  L1G_CUDA(launch_pdl(fwd_finish_kernel, dim3((unsigned)(pl.n_pad / 32), (unsigned)bp.B), FIN_T, 0,
+                      s, a));
+}
+
+void launch_bfinish_adj(const Op& op, const BatchPlan& bp, int mode, const double* part,
+                        double* vout, const VecBufs* vb, DevState* st, unsigned* counters,
+                        double* grpsum, int64_t grp_stride, cudaStream_t s) {
+  const GemvPlan& pl = op.plan;
+  AdjArgs a = adj_args(op, Workspace{}, mode, nullptr, vout, vb, st);
+  a.part = const_cast<double*>(part);
+  a.nrr = bp.adj_splits;
+  a.bs.pstride = (int64_t)bp.Bp * pl.p_pad;
+  a.bs.bpart = pl.p_pad;
+  a.bs.bp = pl.p_pad;
+  a.bs.bgrp = grp_stride;
+  a.grpsum = grpsum;
+  a.cnt_all = counters;
+  L1G_CUDA(launch_pdl(adj_finish_kernel, dim3((unsigned)(pl.p_pad / 64), (unsigned)bp.B), FIN_T, 0,
+                      s, a));
 }
 
 }  // namespace l1g
