@@ -183,6 +183,23 @@ int l1g_comm_create(l1g_ctx* ctx, int rank, int nranks, const void* id128, l1g_c
 void l1g_comm_destroy(l1g_comm* comm);
 int l1g_solver_create_sharded(l1g_op* op, l1g_comm* comm, const double* y, double rho,
                               const l1g_gp_config* cfg, l1g_solver** out);
+/* ---- batched right-hand sides (BASELINE C5): B
+ * problems sharing K, with their own y_b (Y is B x n, problem-major) and rho_b, solved in
+ * lockstep.  Each problem follows gpss_solve (gpss.cpp:221-292) and counts its matvecs as if
+ * solved alone; the products run on the FP64 tensor cores, so iterates agree with the
+ * per-problem solve to rounding.  X0 / X are B x p. */
+typedef struct l1g_batch l1g_batch;
+int l1g_batch_create(l1g_op* op, int B, const double* Y, const double* rho,
+                     const l1g_gp_config* cfg, l1g_batch** out);
+int l1g_batch_init(l1g_batch* b, const double* X0);
+int l1g_batch_run(l1g_batch* b, const l1g_stop_rule* stop, l1g_result* results);
+int l1g_batch_get_x(l1g_batch* b, double* X);
+int l1g_batch_stream(l1g_batch* b, void** stream);
+int l1g_batch_launches(l1g_batch* b, int64_t* launches, int reset);
+void l1g_batch_destroy(l1g_batch* b);
+int l1g_gpss_solve_batched(l1g_op* op, int B, const double* Y, const double* rho,
+                           const l1g_gp_config* cfg, const l1g_stop_rule* stop, double* X_out,
+                           l1g_result* results);
 /* forward product of the iteration (gpss.cpp:194, DenseOperator::do_apply,
  * linear_operator.hpp:45-46): 1 = over the columns where d != 0 only (default; same bits),
  * 0 = dense streaming pass over all of K.  Environment L1G_FWD=dense sets 0 at creation. */

@@ -103,6 +103,15 @@ _SIGS = {
     "l1g_comm_destroy": (None, [_vp]),
     "l1g_solver_create_sharded": (C.c_int, [_vp, _vp, _vp, C.c_double, C.POINTER(GpConfigC),
                                             C.POINTER(_vp)]),
+    "l1g_batch_create": (C.c_int, [_vp, C.c_int, _vp, _vp, C.POINTER(GpConfigC), C.POINTER(_vp)]),
+    "l1g_batch_init": (C.c_int, [_vp, _vp]),
+    "l1g_batch_run": (C.c_int, [_vp, C.POINTER(StopRuleC), _vp]),
+    "l1g_batch_get_x": (C.c_int, [_vp, _vp]),
+    "l1g_batch_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "l1g_batch_launches": (C.c_int, [_vp, C.POINTER(_i64), C.c_int]),
+    "l1g_batch_destroy": (None, [_vp]),
+    "l1g_gpss_solve_batched": (C.c_int, [_vp, C.c_int, _vp, _vp, C.POINTER(GpConfigC),
+                                         C.POINTER(StopRuleC), _vp, _vp]),
     "l1g_solver_set_y": (C.c_int, [_vp, _vp]),
     "l1g_solver_set_y_dev": (C.c_int, [_vp, _vp]),
     "l1g_solver_init": (C.c_int, [_vp, _vp]),

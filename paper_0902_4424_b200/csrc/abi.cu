@@ -648,6 +648,248 @@ l1g_op* op_alloc(l1g_ctx* ctx, int64_t n, int64_t p) {
 
 }  // namespace
 
+// =============================================================================== batched
+// B problems sharing one K (BASELINE C5; the isochrone campaigns of the reference,
+// isochrone.cpp:111-196, are this shape): every per-problem vector is a [Bp][len] slab,
+// every problem has its own DevState, and the loop runs all problems in lockstep:
+//   proj (one CTA / cluster per problem) -> DMMA K D -> finish (per-problem epilogue and
+//   backtracking) -> r' = r + l Kd -> DMMA K^T R' -> finish (x', g', BB dots, bookkeeping)
+// A stopped problem's kernels return early; the host stops when no problem is live.
+struct l1g_batch {
+  l1g_op* op = nullptr;
+  int B = 0;
+  BatchPlan bp{};
+  ProjPlan pp{};
+  cudaStream_t stream = nullptr;
+  l1g_gp_config cfg{};
+  std::vector<double> rho;
+  VecBufs vb{};
+  double *y = nullptr, *rn = nullptr, *part = nullptr, *pscr = nullptr, *grpsum = nullptr;
+  int64_t grp_stride = 0, scr_stride = 0;
+  DevState* st = nullptr;
+  unsigned* counters = nullptr;
+  int* nrun = nullptr;
+  int* nrun_host = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int gsize = 0;
+  int64_t launches = 0;
+  bool inited = false;
+  std::chrono::steady_clock::time_point t0;
+};
+
+namespace {
+
+void batch_free(l1g_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->op->c->device);
+  if (b->gexec) cudaGraphExecDestroy(b->gexec);
+  for (int i = 0; i < 2; ++i) {
+    dfree(b->vb.x[i]);
+    dfree(b->vb.g[i]);
+    dfree(b->vb.r[i]);
+  }
+  dfree(b->vb.d);
+  dfree(b->vb.kd);
+  dfree(b->vb.dmask);
+  dfree(b->y);
+  dfree(b->rn);
+  dfree(b->part);
+  dfree(b->pscr);
+  dfree(b->grpsum);
+  dfree(b->st);
+  dfree(b->counters);
+  dfree(b->nrun);
+  if (b->nrun_host) cudaFreeHost(b->nrun_host);
+  if (b->stream) cudaStreamDestroy(b->stream);
+  delete b;
+}
+
+l1g_batch* batch_new(l1g_op* op, int B, const double* Y, const double* rho,
+                     const l1g_gp_config& cfg) {
+  check_cfg(cfg);
+  if (B < 1) throw InvalidArgument("batched solve: B must be >= 1");
+  for (int i = 0; i < B; ++i) check_rho(rho[i]);
+  set_device(op->c);
+  auto* b = new l1g_batch();
+  b->op = op;
+  try {
+    const GemvPlan& pl = op->plan;
+    b->B = B;
+    b->cfg = cfg;
+    b->rho.assign(rho, rho + B);
+    b->bp = make_batch_plan(pl, B, op->c->sm_count);
+    b->pp = make_proj_plan_single(pl.p_pad);
+    const size_t Bp = (size_t)b->bp.Bp;
+    L1G_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      b->vb.x[i] = dalloc<double>(Bp * pl.p_pad);
+      b->vb.g[i] = dalloc<double>(Bp * pl.p_pad);
+      b->vb.r[i] = dalloc<double>(Bp * pl.n_pad);
+    }
+    b->vb.d = dalloc<double>(Bp * pl.p_pad);
+    b->vb.kd = dalloc<double>(Bp * pl.n_pad);
+    b->vb.dmask = dalloc<uint32_t>(Bp * pl.p_pad / 32 + 2);
+    b->y = dalloc<double>(Bp * pl.n_pad);
+    b->vb.y = b->y;
+    b->rn = dalloc<double>(Bp * pl.n_pad);
+    b->part = dalloc<double>(std::max((size_t)b->bp.fwd_splits * Bp * pl.n_pad,
+                                      (size_t)b->bp.adj_splits * Bp * pl.p_pad));
+    b->scr_stride = (int64_t)proj_scratch_doubles(pl.p_pad);
+    b->pscr = dalloc<double>((size_t)B * b->scr_stride);
+    b->grp_stride = std::max(2 * pl.n_pad / 32, 3 * pl.p_pad / 64) + 8;
+    b->grpsum = dalloc<double>((size_t)B * b->grp_stride);
+    b->st = dalloc<DevState>(B);
+    b->counters = dalloc<unsigned>(B);
+    b->nrun = dalloc<int>(1);
+    L1G_CUDA(cudaHostAlloc(&b->nrun_host, 64, cudaHostAllocDefault));
+    L1G_CUDA(cudaMemcpy2DAsync(b->y, pl.n_pad * 8, Y, pl.n * 8, pl.n * 8, B,
+                               cudaMemcpyHostToDevice, b->stream));
+    L1G_CUDA(cudaStreamSynchronize(b->stream));
+  } catch (...) {
+    batch_free(b);
+    throw;
+  }
+  return b;
+}
+
+BFinArgs bfin_args(l1g_batch* b, int mode, bool adjoint) {
+  const GemvPlan& pl = b->op->plan;
+  BFinArgs a{};
+  a.mode = mode;
+  a.B = b->B;
+  a.splits = adjoint ? b->bp.adj_splits : b->bp.fwd_splits;
+  a.part = b->part;
+  a.ostride = adjoint ? pl.p_pad : pl.n_pad;
+  a.pslab = (int64_t)b->bp.Bp * a.ostride;
+  a.vb = b->vb;
+  a.st = b->st;
+  a.counters = b->counters;
+  a.grpsum = b->grpsum;
+  a.grp_stride = b->grp_stride;
+  return a;
+}
+
+void batch_products(l1g_batch* b, int fmode, const double* D, int amode, const double* R,
+                    bool rupdate, bool proj_first) {
+  const GemvPlan& pl = b->op->plan;
+  cudaStream_t s = b->stream;
+  if (proj_first)
+    launch_proj(b->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, b->pscr, b->st,
+                &b->vb, s, b->B, b->scr_stride);
+  launch_bfwd(*b->op, b->bp, D, b->part, s);
+  launch_bfin(bfin_args(b, fmode, false), false, pl.n_pad, s);
+  if (rupdate) launch_brupdate(bfin_args(b, fmode, false), b->rn, s);
+  launch_badj(*b->op, b->bp, R, b->part, s);
+  launch_bfin(bfin_args(b, amode, true), true, pl.p_pad, s);
+}
+
+// gpss.cpp:117-134 for every problem
+void batch_init(l1g_batch* b, const double* X0) {
+  set_device(b->op->c);
+  const GemvPlan& pl = b->op->plan;
+  cudaStream_t s = b->stream;
+  b->t0 = std::chrono::steady_clock::now();
+  L1G_CUDA(cudaMemsetAsync(b->vb.x[0], 0, (size_t)b->bp.Bp * pl.p_pad * 8, s));
+  if (X0) {
+    L1G_CUDA(cudaMemcpy2DAsync(b->vb.x[0], pl.p_pad * 8, X0, pl.p * 8, pl.p * 8, b->B,
+                               cudaMemcpyHostToDevice, s));
+    for (int i = 0; i < b->B; ++i) {  // L1Ball::contains(x0, 1e-12), prox.cpp:15-17
+      double l1 = 0.0;
+      for (int64_t j = 0; j < pl.p; ++j) l1 += std::fabs(X0[(size_t)i * pl.p + j]);
+      if (!(l1 <= b->rho[i] + 1e-12))
+        throw InvalidArgument("gp_init: starting point is infeasible");
+    }
+  }
+  std::vector<DevState> hs((size_t)b->B);
+  for (int i = 0; i < b->B; ++i) {
+    hs[i] = host_state(b->cfg, b->rho[i]);
+    hs[i].matvecs = 2;
+    hs[i].nrun = b->nrun;
+  }
+  L1G_CUDA(cudaMemcpyAsync(b->st, hs.data(), sizeof(DevState) * b->B, cudaMemcpyHostToDevice, s));
+  for (int i = 0; i < b->B; ++i) state_start(b->st + i, s);
+  batch_products(b, FWD_INIT, b->vb.x[0], ADJ_INIT, b->vb.r[0], false, false);
+  launch_proj(b->pp, PROJ_ALPHA0, pl.p, pl.p_pad, b->vb.x[0], b->vb.g[0], nullptr, b->pscr, b->st,
+              &b->vb, s, b->B, b->scr_stride);
+  b->launches += 5 + b->B;
+  b->inited = true;
+}
+
+void batch_enqueue_iteration(l1g_batch* b) {
+  batch_products(b, FWD_ITER, b->vb.d, ADJ_ITER, b->rn, true, true);
+}
+
+// gpss.cpp:221-292 for every problem, in lockstep
+void batch_run(l1g_batch* b, const l1g_stop_rule& stop, l1g_result* res) {
+  check_stop(stop);
+  if (!b->inited) throw InvalidArgument("batched solve: gp_init has not been run");
+  set_device(b->op->c);
+  cudaStream_t s = b->stream;
+  for (int i = 0; i < b->B; ++i) {
+    configure_kernel<<<1, 1, 0, s>>>(b->st + i, stop, 0, nullptr, 0);
+    L1G_CUDA(cudaGetLastError());
+  }
+  const int B = b->B;
+  L1G_CUDA(cudaMemcpyAsync(b->nrun, &B, sizeof(int), cudaMemcpyHostToDevice, s));
+  L1G_CUDA(cudaStreamSynchronize(s));
+  if (!b->gexec) {
+    const GemvPlan& pl = b->op->plan;
+    const double est_us = 4.0 * pl.n_pad * pl.p_pad * b->bp.Bp / 25e6 + 200.0;
+    b->gsize = (int)std::max(1.0, std::min(16.0, 4000.0 / est_us));
+    cudaGraph_t g;
+    L1G_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < b->gsize; ++i) batch_enqueue_iteration(b);
+    L1G_CUDA(cudaStreamEndCapture(s, &g));
+    L1G_CUDA(cudaGraphInstantiate(&b->gexec, g, 0));
+    cudaGraphDestroy(g);
+  }
+  const int64_t cap = stop.max_iterations > 0 ? stop.max_iterations / b->gsize + 3 : INT64_MAX;
+  volatile int* flag = b->nrun_host;
+  for (int64_t launched = 0;;) {
+    L1G_CUDA(cudaGraphLaunch(b->gexec, s));
+    b->launches += 6LL * b->gsize;
+    L1G_CUDA(cudaMemcpyAsync((void*)flag, b->nrun, sizeof(int), cudaMemcpyDeviceToHost, s));
+    L1G_CUDA(cudaStreamSynchronize(s));
+    ++launched;
+    if (*flag <= 0 || launched >= cap) break;
+  }
+  std::vector<DevState> hs((size_t)B);
+  L1G_CUDA(cudaMemcpyAsync(hs.data(), b->st, sizeof(DevState) * B, cudaMemcpyDeviceToHost, s));
+  L1G_CUDA(cudaStreamSynchronize(s));
+  const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - b->t0).count();
+  for (int i = 0; i < B; ++i) {
+    const DevState& h = hs[i];
+    if (h.status == FAILED)
+      throw RuntimeFailure("backtracking_search: no acceptable step after 60 shrink steps");
+    if (h.status == RUNNING) throw RuntimeFailure("batched solve: a run did not reach a stop rule");
+    l1g_result& r = res[i];
+    std::memset(&r, 0, sizeof(r));
+    r.iterations = h.k;
+    r.matvecs = h.matvecs;
+    r.objective = h.f;
+    r.stationarity = h.out_stationarity;
+    r.elapsed_seconds = el;
+    r.reason = h.reason;
+    r.f_history_len = h.fh_len;
+    std::memcpy(r.f_history, h.fh, sizeof(double) * h.fh_len);
+  }
+}
+
+void batch_get_x(l1g_batch* b, double* X) {
+  set_device(b->op->c);
+  const GemvPlan& pl = b->op->plan;
+  std::vector<DevState> hs((size_t)b->B);
+  L1G_CUDA(cudaMemcpyAsync(hs.data(), b->st, sizeof(DevState) * b->B, cudaMemcpyDeviceToHost,
+                           b->stream));
+  L1G_CUDA(cudaStreamSynchronize(b->stream));
+  for (int i = 0; i < b->B; ++i)
+    L1G_CUDA(cudaMemcpyAsync(X + (size_t)i * pl.p, b->vb.x[hs[i].cur] + (size_t)i * pl.p_pad,
+                             pl.p * 8, cudaMemcpyDeviceToHost, b->stream));
+  L1G_CUDA(cudaStreamSynchronize(b->stream));
+}
+
+}  // namespace
+
 // =============================================================================== C ABI
 extern "C" {
 
@@ -881,13 +1123,17 @@ static void batched_product(l1g_op* op, int B, const double* in, double* out, bo
   double* part = dalloc<double>((size_t)splits * bp.Bp * lout_pad);
   try {
     L1G_CUDA(cudaMemcpy2DAsync(vin, lin_pad * 8, in, lin * 8, lin * 8, B, cudaMemcpyHostToDevice, s));
-    if (adjoint) {
-      launch_badj(*op, bp, vin, part, s);
-      launch_bfinish_adj(*op, bp, ADJ_APPLY, part, vout, nullptr, nullptr, nullptr, nullptr, 0, s);
-    } else {
-      launch_bfwd(*op, bp, vin, part, s);
-      launch_bfinish_fwd(*op, bp, FWD_APPLY, part, vout, nullptr, nullptr, nullptr, nullptr, 0, s);
-    }
+    BFinArgs fa{};
+    fa.mode = adjoint ? ADJ_APPLY : FWD_APPLY;
+    fa.B = B;
+    fa.splits = (int)splits;
+    fa.part = part;
+    fa.pslab = (int64_t)bp.Bp * lout_pad;
+    fa.ostride = lout_pad;
+    fa.vout = vout;
+    if (adjoint) launch_badj(*op, bp, vin, part, s);
+    else launch_bfwd(*op, bp, vin, part, s);
+    launch_bfin(fa, adjoint, lout_pad, s);
     L1G_CUDA(cudaMemcpy2DAsync(out, lout * 8, vout, lout_pad * 8, lout * 8, B,
                                cudaMemcpyDeviceToHost, s));
     L1G_CUDA(cudaStreamSynchronize(s));
@@ -1309,6 +1555,57 @@ int l1g_rng_fill(l1g_ctx* c, int kind, uint64_t seed, uint32_t stream, uint64_t 
     rng_fill(kind, seed, stream, first, count, c->o, c->stream);
     download(out, c->o, count, c->stream);
     L1G_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int l1g_batch_create(l1g_op* op, int B, const double* Y, const double* rho,
+                     const l1g_gp_config* cfg, l1g_batch** out) {
+  return guarded([&] {
+    *out = nullptr;
+    *out = batch_new(op, B, Y, rho, *cfg);
+  });
+}
+
+int l1g_batch_init(l1g_batch* b, const double* X0) {
+  return guarded([&] { batch_init(b, X0); });
+}
+
+int l1g_batch_run(l1g_batch* b, const l1g_stop_rule* stop, l1g_result* results) {
+  return guarded([&] { batch_run(b, *stop, results); });
+}
+
+int l1g_batch_get_x(l1g_batch* b, double* X) {
+  return guarded([&] { batch_get_x(b, X); });
+}
+
+int l1g_batch_stream(l1g_batch* b, void** stream) {
+  *stream = b->stream;
+  return L1G_OK;
+}
+
+int l1g_batch_launches(l1g_batch* b, int64_t* launches, int reset) {
+  *launches = b->launches;
+  if (reset) b->launches = 0;
+  return L1G_OK;
+}
+
+void l1g_batch_destroy(l1g_batch* b) { batch_free(b); }
+
+int l1g_gpss_solve_batched(l1g_op* op, int B, const double* Y, const double* rho,
+                           const l1g_gp_config* cfg, const l1g_stop_rule* stop, double* X_out,
+                           l1g_result* results) {
+  return guarded([&] {
+    check_stop(*stop);
+    l1g_batch* b = batch_new(op, B, Y, rho, *cfg);
+    try {
+      batch_init(b, nullptr);
+      batch_run(b, *stop, results);
+      if (X_out) batch_get_x(b, X_out);
+    } catch (...) {
+      batch_free(b);
+      throw;
+    }
+    batch_free(b);
   });
 }
 

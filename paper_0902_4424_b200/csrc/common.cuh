@@ -174,9 +174,9 @@ __device__ __forceinline__ void pdl_wait_and_trigger() {
 }
 
 // launch with programmatic stream serialization (see pdl_wait_and_trigger)
-template <class Kern, class Args>
+template <class Kern, class... Args>
 inline cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              const Args& a) {
+                              const Args&... a) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -187,7 +187,7 @@ inline cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cud
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a);
+  return cudaLaunchKernelEx(&cfg, kern, a...);
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {

@@ -13,6 +13,7 @@
 // path matches the per-problem canonical solve to rounding, not bit for bit.
 #include "common.cuh"
 #include "engine.h"
+#include "steps.cuh"
 
 namespace l1g {
 
@@ -187,6 +188,182 @@ __global__ void __launch_bounds__(BT, 1) badj_kernel(const BGemmArgs a) {
     }
 }
 
+template <int NA>
+__device__ __forceinline__ void warp_tree_arrays_b(const double* v, int count, int stride,
+                                                   int lane, double* out) {
+  Counter<14> acc[NA];
+  const int chunks = (count + 31) >> 5;
+  for (int c0 = 0; c0 < chunks; c0 += 4) {
+    double x[4][NA];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = (c0 + u) * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < NA; ++j) x[u][j] = i < count ? __ldcg(v + (int64_t)i * stride + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c0 + u < chunks)
+#pragma unroll
+        for (int j = 0; j < NA; ++j) acc[j].push(warp_tree(x[u][j]), (uint32_t)(c0 + u));
+  }
+#pragma unroll
+  for (int j = 0; j < NA; ++j) out[j] = acc[j].final_value((uint32_t)chunks);
+}
+
+// ---------------------------------------------------------------- batched finishes
+// One warp per (problem, 32 rows | 64 columns): the split partials are joined in split
+// order by a binary counter (pairwise), then the problem's epilogue runs as in the
+// single-RHS finish kernels; the problem's last warp (per-problem counter) joins the group
+// values and runs the scalar tail (steps.cuh).
+constexpr int BF_W = 8;  // warps (problems) per CTA
+
+__global__ void __launch_bounds__(32 * BF_W) bfin_fwd_kernel(const BFinArgs a) {
+  pdl_wait_and_trigger();
+  __shared__ DevState snap[BF_W];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.y * BF_W + warp;
+  if (b >= a.B) return;
+  DevState* st = a.st ? a.st + b : nullptr;
+  if (a.mode != FWD_APPLY && st->status != RUNNING) return;
+  const int64_t row = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t ob = (int64_t)b * a.ostride;
+  Counter<12> acc;
+  int k = 0;
+  for (; k + 4 <= a.splits; k += 4) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcg(a.part + (k + u) * a.pslab + ob + row);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc.push(v[u], (uint32_t)(k + u));
+  }
+  for (; k < a.splits; ++k) acc.push(__ldcg(a.part + k * a.pslab + ob + row), (uint32_t)k);
+  const double kd = acc.final_value((uint32_t)a.splits);
+  if (a.mode == FWD_APPLY) {
+    a.vout[ob + row] = kd;
+    return;
+  }
+  const int cur = st->cur;
+  double l0, l1 = 0.0;
+  if (a.mode == FWD_INIT) {
+    const double r = sub(kd, a.vb.y[ob + row]);  // Kx0 - y   (gpss.cpp:128)
+    a.vb.r[cur][ob + row] = r;
+    l0 = mul(r, r);
+  } else {
+    a.vb.kd[ob + row] = kd;
+    l0 = mul(a.vb.r[cur][ob + row], kd);           // (Kx-y)'Kd (gpss.cpp:195)
+    l1 = mul(kd, kd);                              // ||Kd||^2  (gpss.cpp:196)
+  }
+  l0 = warp_tree(l0);
+  l1 = warp_tree(l1);
+  const int ngrp = gridDim.x;
+  double* grp = a.grpsum + (int64_t)b * a.grp_stride;
+  unsigned last = 0;
+  if (lane == 0) {
+    grp[2 * blockIdx.x + 0] = l0;
+    grp[2 * blockIdx.x + 1] = l1;
+    __threadfence();
+    last = atomicAdd(a.counters + b, 1u) == (unsigned)ngrp - 1u;
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  __threadfence();
+  double AB[2];
+  warp_tree_arrays_b<2>(grp, ngrp, 2, lane, AB);
+  snapshot(&snap[warp], st, lane);
+  if (lane != 0) return;
+  a.counters[b] = 0;
+  fwd_tail(st, snap[warp], a.mode, AB[0], AB[1]);
+}
+
+__global__ void __launch_bounds__(32 * BF_W) bfin_adj_kernel(const BFinArgs a) {
+  pdl_wait_and_trigger();
+  __shared__ DevState snap[BF_W];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.y * BF_W + warp;
+  if (b >= a.B) return;
+  DevState* st = a.st ? a.st + b : nullptr;
+  if (a.mode != ADJ_APPLY && st->status != RUNNING) return;
+  const int64_t col = (int64_t)blockIdx.x * 64 + 2 * lane;
+  const int64_t ob = (int64_t)b * a.ostride;
+  Counter<12> acc0, acc1;
+  int k = 0;
+  for (; k + 4 <= a.splits; k += 4) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = __ldcg(reinterpret_cast<const double2*>(a.part + (k + u) * a.pslab + ob + col));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc0.push(v[u].x, (uint32_t)(k + u));
+      acc1.push(v[u].y, (uint32_t)(k + u));
+    }
+  }
+  for (; k < a.splits; ++k) {
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(a.part + k * a.pslab + ob + col));
+    acc0.push(v.x, (uint32_t)k);
+    acc1.push(v.y, (uint32_t)k);
+  }
+  const double s0 = acc0.final_value((uint32_t)a.splits), s1 = acc1.final_value((uint32_t)a.splits);
+  if (a.mode == ADJ_APPLY) {
+    *reinterpret_cast<double2*>(a.vout + ob + col) = make_double2(s0, s1);
+    return;
+  }
+  const int cur = st->cur;
+  const double g0 = mul(2.0, s0), g1 = mul(2.0, s1);  // 2 K^T r (gpss.cpp:130, :211)
+  if (a.mode == ADJ_INIT) {
+    *reinterpret_cast<double2*>(a.vb.g[cur] + ob + col) = make_double2(g0, g1);
+    return;
+  }
+  const double lam = st->step;
+  const double2 xo = *reinterpret_cast<const double2*>(a.vb.x[cur] + ob + col);
+  const double2 go = *reinterpret_cast<const double2*>(a.vb.g[cur] + ob + col);
+  const double2 dd = *reinterpret_cast<const double2*>(a.vb.d + ob + col);
+  const double x0n = add(xo.x, mul(lam, dd.x)), x1n = add(xo.y, mul(lam, dd.y));
+  *reinterpret_cast<double2*>(a.vb.x[cur ^ 1] + ob + col) = make_double2(x0n, x1n);
+  *reinterpret_cast<double2*>(a.vb.g[cur ^ 1] + ob + col) = make_double2(g0, g1);
+  const double sa = sub(x0n, xo.x), sb = sub(x1n, xo.y);
+  const double za = sub(g0, go.x), zb = sub(g1, go.y);
+  const double dsz = warp_tree(add(mul(sa, za), mul(sb, zb)));
+  const double dss = warp_tree(add(mul(sa, sa), mul(sb, sb)));
+  const double dzz = warp_tree(add(mul(za, za), mul(zb, zb)));
+  const int ngrp = gridDim.x;
+  double* grp = a.grpsum + (int64_t)b * a.grp_stride;
+  unsigned last = 0;
+  if (lane == 0) {
+    grp[3 * blockIdx.x + 0] = dsz;
+    grp[3 * blockIdx.x + 1] = dss;
+    grp[3 * blockIdx.x + 2] = dzz;
+    __threadfence();
+    last = atomicAdd(a.counters + b, 1u) == (unsigned)ngrp - 1u;
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  __threadfence();
+  double sums[3];
+  warp_tree_arrays_b<3>(grp, ngrp, 3, lane, sums);
+  snapshot(&snap[warp], st, lane);
+  if (lane != 0) return;
+  a.counters[b] = 0;
+  adj_tail(st, snap[warp], sums[0], sums[1], sums[2]);
+}
+
+// r' = r + lambda kd for every live problem (gpss.cpp:209) into r[cur^1] and the staging
+// matrix the adjoint DMMA reads
+__global__ void brupdate_kernel(const BFinArgs a, double* rn) {
+  pdl_wait_and_trigger();
+  const int b = blockIdx.y;
+  const DevState* st = a.st + b;
+  if (st->status != RUNNING) return;
+  const int cur = st->cur;
+  const double lam = st->step;
+  const int64_t ob = (int64_t)b * a.ostride;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.ostride;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double r = add(a.vb.r[cur][ob + i], mul(lam, a.vb.kd[ob + i]));
+    a.vb.r[cur ^ 1][ob + i] = r;
+    rn[ob + i] = r;
+  }
+}
+
 static int splits_for(int64_t tiles_out, int64_t nblocks, int sm_count) {
   // enough CTAs for ~7 waves of one CTA per SM, splits dividing the reduction evenly
   int s = 1;
@@ -252,6 +429,18 @@ void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* par
   a.nblocks = (int)pl.nrb;
   const dim3 grid((unsigned)pl.ncb, (unsigned)bp.adj_splits, (unsigned)(bp.Bp / BW));
   L1G_CUDA(launch_pdl(badj_kernel, grid, BT, badj_smem(), s, a));
+}
+
+void launch_bfin(const BFinArgs& a, bool adjoint, int64_t len_pad, cudaStream_t s) {
+  const dim3 grid((unsigned)(len_pad / (adjoint ? 64 : 32)), (unsigned)((a.B + BF_W - 1) / BF_W));
+  if (adjoint) L1G_CUDA(launch_pdl(bfin_adj_kernel, grid, 32 * BF_W, 0, s, a));
+  else L1G_CUDA(launch_pdl(bfin_fwd_kernel, grid, 32 * BF_W, 0, s, a));
+}
+
+void launch_brupdate(const BFinArgs& a, double* rn, cudaStream_t s) {
+  const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(a.ostride / 256, 16)),
+                  (unsigned)a.B);
+  L1G_CUDA(launch_pdl(brupdate_kernel, grid, 256, 0, s, a, rn));
 }
 
 }  // namespace l1g

@@ -66,6 +66,8 @@ struct DevState {
   double h_inf;  // alpha0 projection inf-norm
   // projection phase profile (SM cycles of CTA 0 / event counts), see project.cu
   double prof[24];
+  // batched runs: live-problem counter, decremented when this problem stops (steps.cuh)
+  int* nrun;
 };
 static_assert(sizeof(DevState) % 8 == 0, "DevState is copied as 8-byte words");
 
@@ -143,16 +145,22 @@ struct BGemmArgs {
   int64_t pslab, ostride;
   int per_split, nblocks;
 };
+struct BFinArgs {  // batched finishes (dmma.cu): problem b's vectors at b * ostride
+  int mode, B, splits;
+  const double* part;
+  int64_t pslab, ostride;
+  double* vout;
+  VecBufs vb;
+  DevState* st;
+  unsigned* counters;
+  double* grpsum;
+  int64_t grp_stride;
+};
+void launch_bfin(const BFinArgs& a, bool adjoint, int64_t len_pad, cudaStream_t s);
+void launch_brupdate(const BFinArgs& a, double* rn, cudaStream_t s);
 BatchPlan make_batch_plan(const GemvPlan& pl, int B, int sm_count);
 void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* part, cudaStream_t s);
 void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* part, cudaStream_t s);
-
-void launch_bfinish_fwd(const Op& op, const BatchPlan& bp, int mode, const double* part,
-                        double* vout, const VecBufs* vb, DevState* st, unsigned* counters,
-                        double* grpsum, int64_t grp_stride, cudaStream_t s);
-void launch_bfinish_adj(const Op& op, const BatchPlan& bp, int mode, const double* part,
-                        double* vout, const VecBufs* vb, DevState* st, unsigned* counters,
-                        double* grpsum, int64_t grp_stride, cudaStream_t s);
 
 // host launchers (gemv.cu, project.cu)
 GemvPlan make_plan(int64_t n, int64_t p, int sm_count);
@@ -173,7 +181,8 @@ void launch_adj_combine(const Op& op, const Workspace& ws, int mode, const doubl
 ProjPlan make_proj_plan(int64_t p_pad);
 void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const double* xin,
                  const double* gin, double* out, double* scratch, DevState* st,
-                 const VecBufs* vb, cudaStream_t s);
+                 const VecBufs* vb, cudaStream_t s, int nprob = 1, int64_t scr_stride = 0);
+ProjPlan make_proj_plan_single(int64_t p_pad);
 size_t proj_scratch_doubles(int64_t p_pad);
 
 }  // namespace l1g

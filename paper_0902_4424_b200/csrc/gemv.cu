@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "engine.h"
 #include "scalar.cuh"
+#include "steps.cuh"
 
 namespace l1g {
 
@@ -129,13 +130,6 @@ __device__ __forceinline__ int rs_pos(int i) { return i + (i >> 3); }
 constexpr int FIN_W = 8;
 constexpr int FIN_T = 32 * FIN_W;
 
-// warp-cooperative copy of the device state into shared memory (one coalesced pass)
-__device__ __forceinline__ void snapshot(DevState* dst, const DevState* src, int lane) {
-  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
-  unsigned long long* d = reinterpret_cast<unsigned long long*>(dst);
-  for (int i = lane; i < (int)(sizeof(DevState) / 8); i += 32) d[i] = __ldcg(s + i);
-  __syncwarp();
-}
 
 template <class A>
 __device__ __forceinline__ A batch_view(const A& a0, int prob) {
@@ -263,32 +257,9 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a0) {
   __shared__ DevState s;
   snapshot(&s, a.st, lane);
   if (lane != 0) return;
-  DevState* st = a.st;
   *a.cnt_all = 0;
   if (a.task_ctr) *a.task_ctr = 0;
-  if (a.mode == FWD_INIT) {
-    st->f = A;
-    st->f_prev = A;
-    st->fh[0] = A;
-    st->fh_len = 1;
-    return;
-  }
-  // gpss.cpp:199-203 -- nonmonotone reference value and quadratic backtracking
-  st->a = A;
-  st->b = B;
-  double f_max = s.fh[0];
-  for (int i = 1; i < s.fh_len; ++i) f_max = s.fh[i] > f_max ? s.fh[i] : f_max;
-  st->f_max = f_max;
-  double step, f_new;
-  int h;
-  if (backtrack_quadratic(s.f, A, B, f_max, s.gd, s.cfg, &step, &f_new, &h)) {
-    st->step = step;
-    st->f_new = f_new;
-    st->halvings = h;
-  } else {
-    st->status = FAILED;
-    st->failure = FAIL_BACKTRACK;
-  }
+  fwd_tail(a.st, s, a.mode, A, B);
 }
 
 __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
@@ -375,59 +346,7 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
   snapshot(&s, st, lane);
   if (lane != 0) return;
   *a.cnt_all = 0;
-  // gpss.cpp:206-217 state advance, gpss.cpp:255-283 loop bookkeeping (on the snapshot,
-  // then written back field by field)
-  st->sz = SZ;
-  st->ss = SS;
-  st->zz = ZZ;
-  const double f = s.f_new;
-  st->f = f;
-  int fl = s.fh_len;
-  if (fl < kMaxHist) {
-    s.fh[fl++] = f;
-  } else {
-    for (int i = 0; i + 1 < fl; ++i) s.fh[i] = s.fh[i + 1];
-    s.fh[fl - 1] = f;
-  }
-  while (fl > s.cfg.memory) {
-    for (int i = 0; i + 1 < fl; ++i) s.fh[i] = s.fh[i + 1];
-    --fl;
-  }
-  for (int i = 0; i < fl; ++i) st->fh[i] = s.fh[i];
-  st->fh_len = fl;
-  const int64_t k = s.k;
-  st->k = k + 1;
-  const int64_t mv = s.matvecs + 2;
-  st->matvecs = mv;
-  l1g_iter_record rec;
-  rec.k = k;
-  rec.f = f;
-  rec.stationarity = s.stat;
-  rec.alpha = s.alpha_used;
-  rec.step = s.step;
-  rec.matvecs = mv;
-  rec.elapsed_seconds = elapsed_s(&s);
-  rec.bb_active = s.choice.bb_active;
-  rec.halvings = s.halvings;
-  rec.bb1_raw = s.choice.bb1_raw;
-  rec.bb2_raw = s.choice.bb2_raw;
-  rec.tau_before = s.choice.tau_before;
-  rec.tau_after = s.choice.tau_after;
-  rec.f_max = s.f_max;
-  rec.dir_derivative = s.gd;
-  rec.theta = s.theta;
-  rec.support = s.support;
-  st->last = rec;
-  if (s.trace && k < s.trace_cap) s.trace[k] = rec;
-  if (!s.single_step && s.objective_tol > 0.0) {
-    const double af = fabs(f);
-    if (fabs(sub(s.f_prev, f)) <= mul(s.objective_tol, af > 1.0 ? af : 1.0)) {
-      st->status = STOPPED;
-      st->reason = L1G_OBJECTIVE_TOL;
-    }
-  }
-  st->f_prev = f;
-  st->cur = s.cur ^ 1;
+  adj_tail(st, s, SZ, SS, ZZ);
 }
 
 // ============================================================================ forward
@@ -1078,42 +997,6 @@ void launch_adj_combine(const Op& op, const Workspace& ws, int mode, const doubl
   a.p_pad = p_pad_total;
   a.bs.pstride = p_pad_total;
   L1G_CUDA(launch_pdl(adj_finish_kernel, (int)(p_pad_total / 64), FIN_T, 0, s, a));
-}
-
-// ---- batched-RHS finishes (dmma.cu partials): gridDim.y = problems
-void launch_bfinish_fwd(const Op& op, const BatchPlan& bp, int mode, const double* part,
-                        double* vout, const VecBufs* vb, DevState* st, unsigned* counters,
-                        double* grpsum, int64_t grp_stride, cudaStream_t s) {
-  const GemvPlan& pl = op.plan;
-  FwdArgs a = fwd_args(op, Workspace{}, mode, nullptr, vout, vb, st);
-  a.part = const_cast<double*>(part);
-  a.ncr = bp.fwd_splits;
-  a.bs.pstride = (int64_t)bp.Bp * pl.n_pad;
-  a.bs.bpart = pl.n_pad;
-  a.bs.bn = pl.n_pad;
-  a.bs.bgrp = grp_stride;
-  a.grpsum = grpsum;
-  a.cnt_all = counters;
-  a.task_ctr = nullptr;
-  L1G_CUDA(launch_pdl(fwd_finish_kernel, dim3((unsigned)(pl.n_pad / 32), (unsigned)bp.B), FIN_T, 0,
-                      s, a));
-}
-
-void launch_bfinish_adj(const Op& op, const BatchPlan& bp, int mode, const double* part,
-                        double* vout, const VecBufs* vb, DevState* st, unsigned* counters,
-                        double* grpsum, int64_t grp_stride, cudaStream_t s) {
-  const GemvPlan& pl = op.plan;
-  AdjArgs a = adj_args(op, Workspace{}, mode, nullptr, vout, vb, st);
-  a.part = const_cast<double*>(part);
-  a.nrr = bp.adj_splits;
-  a.bs.pstride = (int64_t)bp.Bp * pl.p_pad;
-  a.bs.bpart = pl.p_pad;
-  a.bs.bp = pl.p_pad;
-  a.bs.bgrp = grp_stride;
-  a.grpsum = grpsum;
-  a.cnt_all = counters;
-  L1G_CUDA(launch_pdl(adj_finish_kernel, dim3((unsigned)(pl.p_pad / 64), (unsigned)bp.B), FIN_T, 0,
-                      s, a));
 }
 
 }  // namespace l1g

@@ -23,6 +23,7 @@
 #include "engine.h"
 #include "scalar.cuh"
 #include "prefix.cuh"
+#include "steps.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -46,6 +47,8 @@ struct ProjArgs {
   double* gpre;   // global scratch: sequential prefix sums (p_pad + 2)
   DevState* st;
   VecBufs vb;
+  // batched runs: cluster k projects problem k (vectors bstride apart, states consecutive)
+  int64_t bstride, scr_stride;
 };
 
 struct ProjShared {
@@ -219,7 +222,9 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   __shared__ ScanShared scan_sh;
   __shared__ DevState sst;
   __shared__ SortShared srt;
-  DevState* st = a.st;
+  const int prob = (int)(blockIdx.x / (unsigned)a.cs);
+  const int64_t pofs = prob * a.bstride;
+  DevState* st = a.st + prob;
   const int tid = threadIdx.x;
   if (tid == 0) sh.red_par = 0;
   const bool prof = (a.mode == PROJ_ITER) && rank == 0 && tid == 0;
@@ -245,8 +250,10 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   const l1g_gp_config cfg = sst.cfg;
   const double rho = sst.rho;
   const int cur = a.mode == PROJ_ITER ? sst.cur : 0;
-  const double* x = a.mode == PROJ_ITER ? a.vb.x[cur] : a.xin;
-  const double* g = a.mode == PROJ_ITER ? a.vb.g[cur] : a.gin;
+  const double* x = (a.mode == PROJ_ITER ? a.vb.x[cur] : a.xin) + pofs;
+  const double* g = (a.mode == PROJ_ITER ? a.vb.g[cur] : a.gin) + pofs;
+  double* const dout = a.out + pofs;
+  double* const gcand = a.gcand + prob * a.scr_stride;
   const int64_t base = (int64_t)rank * LS;
   const int64_t lim = a.p_pad - base < LS ? (a.p_pad - base > 0 ? a.p_pad - base : 0) : LS;
 
@@ -278,8 +285,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         st->choice = c;
         al = c.alpha;
       } else {
-        st->status = STOPPED;
         st->reason = dec - 1;
+        leave_run(st, STOPPED);
         if (dec - 1 == L1G_STATIONARY) {
           st->last.stationarity = 0.0;
           st->out_stationarity = 0.0;
@@ -561,7 +568,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         int64_t n2 = 1;
         while (n2 < total) n2 <<= 1;
         const bool in_smem = (n2 + 1 <= a.cand_cap);
-        double* cbuf = in_smem ? cl.map_shared_rank(dyn, 0) : a.gcand;
+        double* cbuf = in_smem ? cl.map_shared_rank(dyn, 0) : gcand;
         long long pos = before + off;
 #pragma unroll
         for (int k = 0; k < M; ++k) {
@@ -573,7 +580,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         mark(3);
         count(11, (double)total);
         if (rank == 0) {
-          double* c = in_smem ? dyn : a.gcand;
+          double* c = in_smem ? dyn : gcand;
           for (int64_t i = total + tid; i < n2; i += PT) c[i] = 0.0;
           __syncthreads();
           bitonic_desc(c, (int)n2);
@@ -649,14 +656,15 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           const int64_t gj = base + j;
           const double dj = a.mode == PROJ_PLAIN ? h : sub(h, x[gj]);
           lmax = fmax(lmax, fabs(dj));
-          a.out[gj] = dj;
+          dout[gj] = dj;
           if (a.mode == PROJ_ITER) leaf = mul(g[gj], dj);
           nz = dj != 0.0;
         }
         dyn[p] = leaf;
         // support bitmap of d for the sparse forward product (whole warps are in or out)
         const unsigned bits = __ballot_sync(0xffffffffu, nz);
-        if (a.mode == PROJ_ITER && (tid & 31) == 0 && j < lim) a.vb.dmask[(base + j) >> 5] = bits;
+        if (a.mode == PROJ_ITER && (tid & 31) == 0 && j < lim)
+          a.vb.dmask[(pofs + base + j) >> 5] = bits;
       }
       __syncthreads();
       if (a.mode == PROJ_ITER) {
@@ -706,8 +714,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         st->support = support;
       } else {
         st->stationary = 1;
-        st->status = STOPPED;
         st->reason = L1G_STATIONARY;
+        leave_run(st, STOPPED);
         l1g_iter_record& r = st->last;
         r.k = sst.k;
         r.f = sst.f;
@@ -760,7 +768,7 @@ size_t proj_scratch_doubles(int64_t p_pad) {
 }
 
 template <int M>
-static void proj_launch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s) {
+static void proj_launch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s, int nprob) {
   static bool attr = false;
   if (!attr) {
     L1G_CUDA(cudaFuncSetAttribute(proj_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -769,7 +777,7 @@ static void proj_launch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s) {
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pp.cs, 1, 1);
+  cfg.gridDim = dim3(pp.cs * nprob, 1, 1);
   cfg.blockDim = dim3(PT, 1, 1);
   cfg.dynamicSmemBytes = pp.smem;
   cfg.stream = s;
@@ -785,9 +793,21 @@ static void proj_launch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s) {
   L1G_CUDA(cudaLaunchKernelEx(&cfg, proj_kernel<M>, a));
 }
 
+static void proj_dispatch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s, int nprob) {
+  switch (pp.ls / PT) {
+    case 1: proj_launch<1>(pp, a, s, nprob); break;
+    case 2: proj_launch<2>(pp, a, s, nprob); break;
+    case 4: proj_launch<4>(pp, a, s, nprob); break;
+    case 8: proj_launch<8>(pp, a, s, nprob); break;
+    case 16: proj_launch<16>(pp, a, s, nprob); break;
+    case 32: proj_launch<32>(pp, a, s, nprob); break;
+    default: throw InvalidArgument("projection: unsupported slice length");
+  }
+}
+
 void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const double* xin,
                  const double* gin, double* out, double* scratch, DevState* st,
-                 const VecBufs* vb, cudaStream_t s) {
+                 const VecBufs* vb, cudaStream_t s, int nprob, int64_t scr_stride) {
   ProjArgs a{};
   a.mode = mode;
   a.p = p;
@@ -802,15 +822,22 @@ void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const d
   a.gpre = scratch + pow2_at_least(p_pad) + 1;
   a.st = st;
   if (vb) a.vb = *vb;
-  switch (pp.ls / PT) {
-    case 1: proj_launch<1>(pp, a, s); break;
-    case 2: proj_launch<2>(pp, a, s); break;
-    case 4: proj_launch<4>(pp, a, s); break;
-    case 8: proj_launch<8>(pp, a, s); break;
-    case 16: proj_launch<16>(pp, a, s); break;
-    case 32: proj_launch<32>(pp, a, s); break;
-    default: throw InvalidArgument("projection: unsupported slice length");
-  }
+  a.bstride = nprob > 1 ? p_pad : 0;
+  a.scr_stride = scr_stride;
+  proj_dispatch(pp, a, s, nprob);
+}
+
+// one CTA per problem (batched runs): the whole vector in registers of one CTA
+ProjPlan make_proj_plan_single(int64_t p_pad) {
+  ProjPlan pp{};
+  int64_t m = 1;
+  while (PT * m < p_pad) m <<= 1;
+  if (m > MAX_M) return make_proj_plan(p_pad);
+  pp.cs = 1;
+  pp.ls = PT * m;
+  pp.cand_cap = pp.ls + 1;
+  pp.smem = (size_t)pp.cand_cap * 8;
+  return pp;
 }
 
 }  // namespace l1g

@@ -45,3 +45,55 @@ def test_batched_products(n, p, B):
         refg = O.apply_adjoint(K, R[b])
         boundg = np.abs(K).T @ np.abs(R[b])
         assert np.all(np.abs(G[b] - refg) <= TOL * boundg + 1e-300), b
+
+
+def batch_problems(n, p, B, seed):
+    """B problems on one Gaussian K: distinct sparse x_true, y = K x_true + noise, rho_b
+    spaced from 0.2 to 1.0 of ||x_true_b||_1 (the C5 recipe at a small size)."""
+    K = O.gaussian_matrix(seed, n, p)
+    sig, _ = O.spectral_norm(K, 200, 1e-10)
+    K *= 0.9 / sig
+    rng = np.random.default_rng(seed)
+    Y, rho, xt = [], [], []
+    for b in range(B):
+        x = np.zeros(p)
+        idx = rng.choice(p, size=max(3, p // 60), replace=False)
+        x[idx] = rng.normal(size=idx.size)
+        y = O.apply(K, x) + 1e-3 * rng.normal(size=n)
+        Y.append(y)
+        rho.append((0.2 + 0.8 * b / max(B - 1, 1)) * float(np.abs(x).sum()))
+        xt.append(x)
+    return K, np.array(Y), np.array(rho)
+
+
+@pytest.mark.parametrize("n,p,B,iters,strict", [
+    (256, 1024, 6, 15, True), (200, 2048, 130, 15, True), (1024, 4096, 16, 20, True),
+    (512, 2048, 16, 80, False), (256, 1024, 6, 60, False)])
+def test_batched_solve_matches_single(n, p, B, iters, strict):
+    """Every problem of the batch against its own canonical solve.  Away from the arithmetic
+    floor the iterates agree to ~1e-15 (tolerance 1e-9, equal steps); once a run reaches the
+    floor (gpss.cpp:180-189: no descent left at rounding level) the stop iteration may differ
+    by a few steps and the iterates agree to the floor's own resolution (1e-7 here), the
+    objective to 1e-9."""
+    K, Y, rho = batch_problems(n, p, B, 31 + B)
+    op = l1.DenseOperator(K)
+    lib = L.load()
+    cfg = l1.GpConfig()._c()
+    stop = l1.StopRule(max_iterations=iters, stationarity_tol=0.0)._c()
+    X = np.empty((B, p))
+    res = (L.ResultC * B)()
+    L.check(lib.l1g_gpss_solve_batched(op.h, B, L.ptr(np.ascontiguousarray(Y)), L.ptr(rho),
+                                       C.byref(cfg), C.byref(stop), L.ptr(X), res), "batched")
+    for b in range(0, B, max(1, B // 8)):
+        sol = l1.gpss_solve(l1.Objective(op, Y[b]), l1.L1Ball(rho[b]), l1.GpConfig(),
+                            l1.StopRule(max_iterations=iters, stationarity_tol=0.0))
+        scale = max(1.0, np.abs(sol.x).max())
+        if strict:
+            assert res[b].iterations == sol.iterations == iters, b
+            assert res[b].reason == int(sol.reason), b
+            assert res[b].matvecs == sol.matvecs.count, b
+            assert np.abs(X[b] - sol.x).max() <= 1e-9 * scale, (b, np.abs(X[b] - sol.x).max())
+        else:
+            assert np.abs(X[b] - sol.x).max() <= 1e-7 * scale, (b, np.abs(X[b] - sol.x).max())
+        assert abs(res[b].objective - sol.objective) <= 1e-9 * abs(sol.objective), b
+        assert np.abs(X[b]).sum() <= rho[b] * (1 + 1e-12) + 1e-12
