@@ -219,6 +219,145 @@ def run_reference(args, world, rank, pg):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ C5: batched RHS
+def fp64_peak():
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            return float(json.load(f)["dmma_m8n8k4_tflops"]), "measured (tools/fp64_peak.cu)"
+    except Exception:
+        return 37.0, "fallback"
+
+
+def run_batch(args, world, rank, local, pg):
+    """BASELINE configs[4]: 128 problems on one 4096x16384 K, solved in lockstep; the
+    products run on the FP64 tensor cores.  A step is one batched gpss_solve (all problems
+    to their stop rule, at most 300 lockstep iterations)."""
+    import ctypes as C
+
+    import paper_0902_4424_b200 as l1
+    from paper_0902_4424_b200 import _lib as L
+    from paper_0902_4424_b200 import harness as H
+
+    import torch
+    torch.cuda.set_device(local)
+    c = dict(H.C5)
+    B, n, p = c["batch"], c["n"], c["p"]
+    iters = args.iters or H.ITERATIONS["C5"]
+    t_setup = time.perf_counter()
+    P = H.build_batch_problem(**c, sigma_hat=sigma_fixture("C5"))
+    setup_s = time.perf_counter() - t_setup
+    lib = L.load()
+    cfg = l1.GpConfig()._c()
+    stop = l1.StopRule(max_iterations=iters, stationarity_tol=0.0)._c()
+    Y = np.ascontiguousarray(P["Y"])
+    rho = np.ascontiguousarray(P["rho"])
+    h = C.c_void_p()
+    L.check(lib.l1g_batch_create(P["op"].h, B, L.ptr(Y), L.ptr(rho), C.byref(cfg), C.byref(h)))
+    sp = C.c_void_p()
+    lib.l1g_batch_stream(h, C.byref(sp))
+    stream = torch.cuda.ExternalStream(sp.value)
+    res = (L.ResultC * B)()
+
+    def solve_once():
+        L.check(lib.l1g_batch_init(h, None), "batch_init")
+        L.check(lib.l1g_batch_run(h, C.byref(stop), res), "batch_run")
+        its = [res[i].iterations for i in range(B)]
+        return max(its), sum(its)
+
+    for _ in range(args.warmup):
+        solve_once()
+    tl = C.c_int64()
+    lib.l1g_batch_launches(h, C.byref(tl), 1)
+    barrier(pg)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lock_its = prob_its = 0
+    with clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            a, b = solve_once()
+            lock_its += a
+            prob_its += b
+        e1.record(stream)
+        e1.synchronize()
+    dev_ms = max_over_ranks(pg, e0.elapsed_time(e1))
+    lib.l1g_batch_launches(h, C.byref(tl), 1)
+    value = world * lock_its / (dev_ms / 1e3)
+    tf, ta = C.c_double(), C.c_double()
+    L.check(lib.l1g_batch_time_products(h, 10, C.byref(tf), C.byref(ta)))
+    X_dev = np.empty((B, p))
+    L.check(lib.l1g_batch_get_x(h, L.ptr(X_dev)))
+    lib.l1g_batch_destroy(h)
+
+    # end to end: l1g_gpss_solve_batched with host Y / rho in and X / results out
+    X = np.empty((B, p))
+    res2 = (L.ResultC * B)()
+
+    def e2e_once():
+        L.check(lib.l1g_gpss_solve_batched(P["op"].h, B, L.ptr(Y), L.ptr(rho), C.byref(cfg),
+                                           C.byref(stop), L.ptr(X), res2), "solve_batched")
+        return max(res2[i].iterations for i in range(B))
+
+    e2e_once()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_its = sum(e2e_once() for _ in range(max(1, args.steps // 2)))
+    e2e_s = max_over_ranks(pg, time.perf_counter() - t0)
+
+    peak, peak_src = fp64_peak()
+    flop = 2.0 * n * p * B  # one product
+    dom = "adj" if ta.value >= tf.value else "fwd"
+    ms = {"fwd": tf.value, "adj": ta.value}[dom]
+    achieved = flop / (ms / 1e3) / 1e12
+    roofline = {"bound": "tensor", "kernel": {"adj": "badj_kernel (K^T R', DMMA)",
+                                              "fwd": "bfwd_kernel (K D, DMMA)"}[dom],
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "peak_source": peak_src, "traffic": None,
+                "algorithmic_flops_per_launch": flop,
+                "avg_launch_ms": {"bfwd": round(tf.value, 4), "badj": round(ta.value, 4)},
+                "iteration_TFLOPs_4npB": 2 * flop * lock_its / (dev_ms / 1e3) / 1e12}
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            K = P["op"].matrix()
+            per = 20
+            dt, itn, kind, cores = ref_time(K, Y[0], float(rho[0]), per)
+            cpu = {"value": itn / dt / B, "unit": UNIT, "cores": cores, "kind": kind,
+                   "sample": f"{itn} GPSS iterations of problem 0 of C5 solved alone "
+                             f"(reference sources), scaled to lockstep iterations of {B} "
+                             f"problems (/{B})"}
+            del K
+        except Exception as ex:
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {ex}"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64",
+                "data": "synthetic (seeded Philox Gaussian K scaled to ||K||_2=0.9 on device, "
+                        "128 seeded x_true; BASELINE.json configs[4])",
+                "config": {"workload": f"C5: batched {B} problems on gaussian {n}x{p}, nnz 150 "
+                                       f"each, rho_j = (0.2..1.0)||x_true_j||_1, up to {iters} "
+                                       "lockstep iterations, x0=0, stationarity_tol=0",
+                           "n": n, "p": p, "batch": B,
+                           "lockstep_iterations_per_step": lock_its / args.steps,
+                           "problem_iterations_per_s": world * prob_its / (dev_ms / 1e3),
+                           "l2": "inputs larger than L2 (K = 0.5 GiB, partials 67 MB)",
+                           "parallelism": "replicas" if world > 1 else "single",
+                           "setup_s": round(setup_s, 3)},
+                "e2e": {"value": world * e2e_its / e2e_s, "unit": UNIT,
+                        "h2d_bytes_per_step": Y.nbytes + rho.nbytes,
+                        "d2h_bytes_per_step": X.nbytes + B * C.sizeof(L.ResultC),
+                        "x_matches_device_run": bool(np.array_equal(X, X_dev))},
+                "gpu_launches": int(tl.value),
+                "roofline": roofline,
+                "cpu_baseline": cpu,
+                "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ B200 arm
 def run_b200(args, world, rank, local, pg):
     import ctypes as C
@@ -436,6 +575,8 @@ def main():
     world, rank, local, pg = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank, pg)
+    elif args.config == "C5":
+        run_batch(args, world, rank, local, pg)
     else:
         run_b200(args, world, rank, local, pg)
     if pg is not None:

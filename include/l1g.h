@@ -196,6 +196,7 @@ int l1g_batch_run(l1g_batch* b, const l1g_stop_rule* stop, l1g_result* results);
 int l1g_batch_get_x(l1g_batch* b, double* X);
 int l1g_batch_stream(l1g_batch* b, void** stream);
 int l1g_batch_launches(l1g_batch* b, int64_t* launches, int reset);
+int l1g_batch_time_products(l1g_batch* b, int reps, double* fwd_ms, double* adj_ms);
 void l1g_batch_destroy(l1g_batch* b);
 int l1g_gpss_solve_batched(l1g_op* op, int B, const double* Y, const double* rho,
                            const l1g_gp_config* cfg, const l1g_stop_rule* stop, double* X_out,

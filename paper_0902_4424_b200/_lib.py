@@ -110,6 +110,7 @@ _SIGS = {
     "l1g_batch_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "l1g_batch_launches": (C.c_int, [_vp, C.POINTER(_i64), C.c_int]),
     "l1g_batch_destroy": (None, [_vp]),
+    "l1g_batch_time_products": (C.c_int, [_vp, C.c_int, _dp, _dp]),
     "l1g_gpss_solve_batched": (C.c_int, [_vp, C.c_int, _vp, _vp, C.POINTER(GpConfigC),
                                          C.POINTER(StopRuleC), _vp, _vp]),
     "l1g_solver_set_y": (C.c_int, [_vp, _vp]),

@@ -1583,6 +1583,33 @@ int l1g_batch_stream(l1g_batch* b, void** stream) {
   return L1G_OK;
 }
 
+// average duration of the two DMMA products over `reps` launches on the batch stream
+// (inputs: the current d and r' slabs), for the roofline of the tensor-core kernels
+int l1g_batch_time_products(l1g_batch* b, int reps, double* fwd_ms, double* adj_ms) {
+  return guarded([&] {
+    set_device(b->op->c);
+    cudaEvent_t e[3];
+    for (auto& x : e) L1G_CUDA(cudaEventCreate(&x));
+    float tf = 0.f, ta = 0.f;
+    for (int i = 0; i < reps; ++i) {
+      L1G_CUDA(cudaEventRecord(e[0], b->stream));
+      launch_bfwd(*b->op, b->bp, b->vb.d, b->part, b->stream);
+      L1G_CUDA(cudaEventRecord(e[1], b->stream));
+      launch_badj(*b->op, b->bp, b->rn, b->part, b->stream);
+      L1G_CUDA(cudaEventRecord(e[2], b->stream));
+      L1G_CUDA(cudaEventSynchronize(e[2]));
+      float x = 0.f, y = 0.f;
+      L1G_CUDA(cudaEventElapsedTime(&x, e[0], e[1]));
+      L1G_CUDA(cudaEventElapsedTime(&y, e[1], e[2]));
+      tf += x;
+      ta += y;
+    }
+    for (auto& x : e) cudaEventDestroy(x);
+    *fwd_ms = tf / std::max(reps, 1);
+    *adj_ms = ta / std::max(reps, 1);
+  });
+}
+
 int l1g_batch_launches(l1g_batch* b, int64_t* launches, int reset) {
   *launches = b->launches;
   if (reset) b->launches = 0;

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(BT, 1) badj_kernel(const BGemmArgs a) {
 template <int NA>
 __device__ __forceinline__ void warp_tree_arrays_b(const double* v, int count, int stride,
                                                    int lane, double* out) {
-  Counter<14> acc[NA];
+  Counter<11> acc[NA];  // groups < 2^16
   const int chunks = (count + 31) >> 5;
   for (int c0 = 0; c0 < chunks; c0 += 4) {
     double x[4][NA];
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(32 * BF_W) bfin_fwd_kernel(const BFinArgs a) {
   if (a.mode != FWD_APPLY && st->status != RUNNING) return;
   const int64_t row = (int64_t)blockIdx.x * 32 + lane;
   const int64_t ob = (int64_t)b * a.ostride;
-  Counter<12> acc;
+  Counter<8> acc;  // splits < 256
   int k = 0;
   for (; k + 4 <= a.splits; k += 4) {
     double v[4];
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(32 * BF_W) bfin_adj_kernel(const BFinArgs a) {
   if (a.mode != ADJ_APPLY && st->status != RUNNING) return;
   const int64_t col = (int64_t)blockIdx.x * 64 + 2 * lane;
   const int64_t ob = (int64_t)b * a.ostride;
-  Counter<12> acc0, acc1;
+  Counter<8> acc0, acc1;
   int k = 0;
   for (; k + 4 <= a.splits; k += 4) {
     double2 v[4];
@@ -339,7 +339,8 @@ __global__ void __launch_bounds__(32 * BF_W) bfin_adj_kernel(const BFinArgs a) {
   if (!__shfl_sync(0xffffffffu, last, 0)) return;
   __threadfence();
   double sums[3];
-  warp_tree_arrays_b<3>(grp, ngrp, 3, lane, sums);
+#pragma unroll 1
+  for (int j = 0; j < 3; ++j) warp_tree_arrays_b<1>(grp + j, ngrp, 3, lane, sums + j);
   snapshot(&snap[warp], st, lane);
   if (lane != 0) return;
   a.counters[b] = 0;

@@ -48,6 +48,9 @@ CONFIGS = {
 }
 ITERATIONS = {"C1": 500, "C2": 300, "C3": 2000, "C4": 200, "C5": 300}
 
+# C5: one Gaussian K shared by B problems (BASELINE.json configs[4])
+C5 = dict(n=4096, p=16384, batch=128, nnz=150, seed=5, noise=1e-3)
+
 
 def rng(ctx, kind, seed, stream, first, count) -> np.ndarray:
     out = np.empty(max(count, 1))
@@ -142,3 +145,27 @@ def build_problem(spec: ProblemSpec, ctx=None):
     d = build_vectors(spec, op, ctx)
     d.update(op=op, sigma_hat=sigma_hat, scale=scale)
     return d
+
+
+def build_batch_problem(n, p, batch, nnz, seed, noise, ctx=None, sigma_hat=None,
+                        power_iters=1000, power_tol=1e-8):
+    """BASELINE C5 recipe: K iid N(0,1) (Philox stream 0 of `seed`) scaled to ||K||_2 = 0.9;
+    problem j has its own x_true (nnz N(0,1) values at positions sampled from seed
+    1000*seed + j), y_j = K x_true_j + noise * e_j, rho_j = (0.2 + 0.8 j/(B-1)) ||x_true_j||_1.
+    Returns dict(op, Y (B x n), rho (B,), X_true (B x p), sigma_hat)."""
+    ctx = ctx or api.default_context()
+    spec = ProblemSpec("gaussian", n, p, nnz, seed, "normal", noise, "abs",
+                       sigma_hat=sigma_hat, power_iters=power_iters, power_tol=power_tol)
+    op, sig, _ = build_operator(spec, ctx)
+    Y = np.empty((batch, n))
+    X = np.zeros((batch, p))
+    rho = np.empty(batch)
+    for j in range(batch):
+        sj = 1000 * seed + j
+        sub = ProblemSpec("gaussian", n, p, nnz, sj, "normal", noise, "abs")
+        sup = sample_support(ctx, sj, 1, p, nnz)
+        X[j, sup] = x_true_values(ctx, sub, nnz)
+        clean = op.apply(X[j])
+        Y[j] = clean + noise * rng(ctx, 0, sj, 2, 0, n)
+        rho[j] = (0.2 + 0.8 * j / max(batch - 1, 1)) * api.l1_norm(X[j], ctx)
+    return dict(op=op, Y=Y, rho=rho, X_true=X, sigma_hat=sig)
