@@ -423,9 +423,10 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         }
         const long long L = total + (next >= 0.0 ? 1 : 0);
         mark(14);
-        if (cs > 1 && total + 1 <= a.cand_cap && lo >= 0.0) {
+        if (cs > 1 && lo >= 0.0) {
           // ---- cluster bucket sort: bins on the key bits (~log scale), whole bins to CTAs,
-          //      DSMEM scatter, local bitonic sorts, gather of the sorted ranges into CTA 0
+          //      DSMEM scatter, local bitonic sorts, then the sorted ranges are gathered into
+          //      CTA 0's shared memory (or, beyond its capacity, into the global scratch)
           const long long kmin = __double_as_longlong(lo);
           const long long kspan = __double_as_longlong(vinf) - kmin;  // candidates: key > kmin
           if (tid == 0) {
@@ -529,19 +530,28 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
             __syncthreads();
             cl.sync();  // every range sorted before CTA 0's buffer receives the others
             mark(17);
-            if (rank != 0) {
-              double* dst = cl.map_shared_rank(dyn, 0) + srt.base[rank];
+            const bool gather_smem = total + 1 <= a.cand_cap;
+            if (gather_smem) {
+              if (rank != 0) {
+                double* dst = cl.map_shared_rank(dyn, 0) + srt.base[rank];
+                for (int i = tid; i < cnt; i += PT) dst[i] = dyn[i];
+              }
+            } else {
+              double* dst = gcand + srt.base[rank];
               for (int i = tid; i < cnt; i += PT) dst[i] = dyn[i];
+              __threadfence();
             }
             cl.sync();
             mark(3);
             count(11, (double)total);
             if (rank == 0) {
-              if (tid == 0 && next >= 0.0) dyn[total] = next;
+              double* const c = gather_smem ? dyn : gcand;
+              if (tid == 0 && next >= 0.0) c[total] = next;
+              if (!gather_smem) __threadfence_block();
               __syncthreads();
               mark(4);
               double s_before = 0.0;
-              const long long ff = prefix_break(dyn, L, rho, scan_sh, &s_before);
+              const long long ff = prefix_break(c, L, rho, scan_sh, &s_before);
               if (tid == 0) {
                 sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
                 sh.dec = (ff == L && next >= 0.0) ? 1 : 0;

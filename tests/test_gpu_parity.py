@@ -79,13 +79,16 @@ def test_projection_bit_identical():
 def test_projection_large(p):
     """Cluster path (cs > 1) and the global-memory sort for large candidate sets."""
     rng = np.random.default_rng(p)
-    x = rng.normal(size=p)
-    for frac in (0.9, 0.3, 0.01):
-        rho = frac * float(np.abs(x).sum())
-        u, th, sup = O.project_l1(x, rho)
-        pr = l1.project_l1_ball_with_threshold(x, l1.L1Ball(rho))
-        assert pr.threshold == th and pr.support == sup
-        assert np.array_equal(pr.point, u)
+    vectors = [rng.normal(size=p),
+               # few distinct magnitudes: whole key bins collide (unbalanced bucket ranges)
+               rng.choice([-1.0, 1.0, 0.5, -0.25, 2.0], size=p) * (rng.random(p) < 0.7)]
+    for x in vectors:
+        for frac in (0.9, 0.3, 0.01):
+            rho = frac * float(np.abs(x).sum())
+            u, th, sup = O.project_l1(x, rho)
+            pr = l1.project_l1_ball_with_threshold(x, l1.L1Ball(rho))
+            assert pr.threshold == th and pr.support == sup
+            assert np.array_equal(pr.point, u)
 
 
 def test_generators_bit_identical():
