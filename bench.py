@@ -310,10 +310,17 @@ def run_batch(args, world, rank, local, pg):
     dom = "adj" if ta.value >= tf.value else "fwd"
     ms = {"fwd": tf.value, "adj": ta.value}[dom]
     achieved = flop / (ms / 1e3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get({"adj": "C5_badj", "fwd": "C5_bfwd"}[dom])
+    except Exception:
+        pass
     roofline = {"bound": "tensor", "kernel": {"adj": "badj_kernel (K^T R', DMMA)",
                                               "fwd": "bfwd_kernel (K D, DMMA)"}[dom],
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "peak_source": peak_src, "traffic": None,
+                "peak_source": peak_src, "traffic": traffic,
+                "traffic_unit": "bytes per launch (K 512 MiB + vectors + split partials)",
                 "algorithmic_flops_per_launch": flop,
                 "avg_launch_ms": {"bfwd": round(tf.value, 4), "badj": round(ta.value, 4)},
                 "iteration_TFLOPs_4npB": 2 * flop * lock_its / (dev_ms / 1e3) / 1e12}

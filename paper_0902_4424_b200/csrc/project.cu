@@ -29,6 +29,13 @@ namespace cg = cooperative_groups;
 
 namespace l1g {
 
+#ifndef L1G_PROJ_KEEP  // keep x, g in registers between the first and the last pass up to this M
+#define L1G_PROJ_KEEP 2
+#endif
+#ifndef L1G_PROJ_WARM
+#define L1G_PROJ_WARM 0
+#endif
+
 constexpr int PT = 512;
 constexpr int PW = PT / 32;
 constexpr int MAX_M = 32;
@@ -123,6 +130,32 @@ __device__ __forceinline__ double block_sum_any(double v, ProjShared& sh) {  // 
   for (int w = 0; w < PW; ++w) r += sh.wv[w][2];
   __syncthreads();
   return r;
+}
+
+// Several block reductions with one barrier pair.  kinds[c]: 0 = canonical tree over the
+// threads' aligned runs (warp butterfly, then butterfly over warp index: same bits as
+// block_tree), 1 = max, 2 = plain sum.  Every thread receives the results.
+template <int N>
+__device__ __forceinline__ void block_reduce(double (&v)[N], const int (&kinds)[N],
+                                             ProjShared& sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    const double x = kinds[c] == 1 ? warp_max(v[c]) : warp_tree(v[c]);
+    if (lane == 0) sh.wv[warp][c] = x;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    double x = lane < PW ? sh.wv[lane][c] : (kinds[c] == 1 ? -1.0 : 0.0);
+#pragma unroll
+    for (int o = 1; o < PW; o <<= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, x, o);
+      x = kinds[c] == 1 ? fmax(x, y) : add(x, y);
+    }
+    v[c] = __shfl_sync(0xffffffffu, x, 0);
+  }
+  __syncthreads();
 }
 
 __device__ __forceinline__ long long block_excl_scan(long long v, ProjShared& sh,
@@ -310,17 +343,33 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   count(8, 1.0);
   mark(0);
   double v[M];
+  // x and g in the coalesced order (j = tid + PT*i), kept for the final pass when small
+  constexpr bool KEEP = M <= L1G_PROJ_KEEP;
+  double xr[KEEP ? M : 1], gr[KEEP ? M : 1];
+  if (KEEP) {
+#pragma unroll
+    for (int i = 0; i < (KEEP ? M : 1); ++i) {
+      const int64_t j = tid + (int64_t)PT * i;
+      const bool in = j < lim;
+      xr[i] = in ? x[base + j] : 0.0;
+      gr[i] = in && a.mode != PROJ_PLAIN ? g[base + j] : 0.0;
+    }
+  }
   for (int attempt = 0;; ++attempt) {
     count(9, 1.0);
     // ---- v = x - alpha g  (gpss.cpp:167; alpha0: x0 - grad, gpss.cpp:95): coalesced
     //      loads, staged through shared memory into per-thread registers
-    for (int64_t j = tid; j < LS; j += PT) {
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      const int64_t j = tid + (int64_t)PT * i;
       double val = 0.0;
       if (j < lim) {
         const int64_t gj = base + j;
-        if (a.mode == PROJ_PLAIN) val = x[gj];
-        else if (a.mode == PROJ_ALPHA0) val = sub(x[gj], g[gj]);
-        else val = sub(x[gj], mul(alpha, g[gj]));
+        const double xv = KEEP ? xr[KEEP ? i : 0] : x[gj];
+        const double gv = KEEP ? gr[KEEP ? i : 0] : (a.mode != PROJ_PLAIN ? g[gj] : 0.0);
+        if (a.mode == PROJ_PLAIN) val = xv;
+        else if (a.mode == PROJ_ALPHA0) val = sub(xv, gv);
+        else val = sub(xv, mul(alpha, gv));
       }
       dyn[swz<M>((int)j)] = val;
     }
@@ -334,9 +383,10 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       double m = 0.0;
 #pragma unroll
       for (int k = 0; k < M; ++k) m = fmax(m, fabs(v[k]));
-      red[0] = block_tree(t, sh, 0);
-      red[1] = block_max(m, sh);
+      red[0] = t;
+      red[1] = m;
       const int kinds[2] = {0, 1};
+      block_reduce<2>(red, kinds, sh);
       cluster_combine(red, kinds, 2, sh, cl, cs);
     }
     const double l1v = red[0], vinf = red[1];
@@ -353,22 +403,41 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     } else {
       branch = 2;
       // Michelot pivot iteration from below: th_{t+1} = (sum_{|v|>th_t} |v| - rho) / count
-      double th = dvd(sub(l1v, rho), (double)a.p_pad);
+      // Warm start from the previous iteration's theta: each update is a Newton step on
+      // the convex f(t) = sum max(|v|-t, 0) - rho, so a start above theta* lands at or below
+      // it in one step and the iteration then climbs monotonically.  Only the bracket
+      // depends on this; the exact sort-and-scan below decides theta.
+      const double th_cold = dvd(sub(l1v, rho), (double)a.p_pad);
+      bool warm = L1G_PROJ_WARM && a.mode == PROJ_ITER && sst.k > 0 && sst.theta > th_cold &&
+                  sst.theta < vinf;
+      double th = warm ? sst.theta : th_cold;
       double cnt_prev = (double)a.p_pad + 1.0;
       const int kinds_cs[2] = {2, 2};
       for (int it = 0; it < 64; ++it) {
-        double c = 0.0, s = 0.0;
+        double v2[2] = {0.0, 0.0};
 #pragma unroll
         for (int k = 0; k < M; ++k) {
           const double m = fabs(v[k]);
           if (m > th) {
-            c += 1.0;
-            s += m;
+            v2[0] += 1.0;
+            v2[1] += m;
           }
         }
-        double v2[2] = {block_sum_any(c, sh), block_sum_any(s, sh)};
+        block_reduce<2>(v2, kinds_cs, sh);
         cluster_combine(v2, kinds_cs, 2, sh, cl, cs);
         count(10, 1.0);
+        if (warm) {  // first step from the previous theta
+          warm = false;
+          if (v2[0] == 0.0) {
+            th = th_cold;
+            continue;
+          }
+          const double thn = dvd(sub(v2[1], rho), v2[0]);
+          if (thn < th) {  // started above theta*: restart the monotone climb from thn
+            th = thn;
+            continue;
+          }
+        }
         if (v2[0] == 0.0 || v2[0] >= cnt_prev) break;
         const double shrink = cnt_prev - v2[0];
         cnt_prev = v2[0];
@@ -657,17 +726,20 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
 #pragma unroll
       for (int k = 0; k < M; ++k) dyn[swz<M>(tid * M + k)] = v[k];
       __syncthreads();
-      for (int64_t j = tid; j < LS; j += PT) {
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        const int64_t j = tid + (int64_t)PT * i;
         const int p = swz<M>((int)j);
         const double h = dyn[p];
         double leaf = 0.0;
         bool nz = false;
         if (j < lim) {
           const int64_t gj = base + j;
-          const double dj = a.mode == PROJ_PLAIN ? h : sub(h, x[gj]);
+          const double xv = KEEP ? xr[KEEP ? i : 0] : x[gj];
+          const double dj = a.mode == PROJ_PLAIN ? h : sub(h, xv);
           lmax = fmax(lmax, fabs(dj));
           dout[gj] = dj;
-          if (a.mode == PROJ_ITER) leaf = mul(g[gj], dj);
+          if (a.mode == PROJ_ITER) leaf = mul(KEEP ? gr[KEEP ? i : 0] : g[gj], dj);
           nz = dj != 0.0;
         }
         dyn[p] = leaf;
@@ -680,13 +752,12 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       if (a.mode == PROJ_ITER) {
 #pragma unroll
         for (int k = 0; k < M; ++k) v[k] = dyn[swz<M>(tid * M + k)];
-        gdl = block_tree(tree<M>([&](int k) { return v[k]; }), sh, 2);
+        gdl = tree<M>([&](int k) { return v[k]; });
       }
-      __syncthreads();
     }
-    double red2[4] = {gdl, block_max(lmax, sh), block_max(hmax, sh),
-                      block_sum_any((double)sup, sh)};
+    double red2[4] = {gdl, lmax, hmax, (double)sup};
     const int kinds2[4] = {0, 1, 1, 2};
+    block_reduce<4>(red2, kinds2, sh);
     cluster_combine(red2, kinds2, 4, sh, cl, cs);
     const double gd = red2[0], stat = red2[1], hinf = red2[2];
     const long long support = (long long)red2[3];
