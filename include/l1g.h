@@ -167,6 +167,17 @@ int l1g_solver_stream(l1g_solver* s, void** stream);
 /* per-kernel CUDA-event timing of the device loop (projection / forward / adjoint), summed
  * over completed iterations, and the number of kernels this solver launched */
 int l1g_solver_set_timing(l1g_solver* s, int on);
+/* ---- the reference's other solvers of the problem family, on the same
+ * device kernels; trace may be NULL.  x0 = 0 as in the reference.
+ *   l1g_psd_solve       -> psd_solve    psd.cpp:14-93  (projected steepest descent)
+ *   l1g_shrinkage_solve -> ista_solve / fista_solve (accelerated = 1) shrinkage.cpp:41-118 */
+int l1g_psd_solve(l1g_op* op, const double* y, double rho, const l1g_stop_rule* stop,
+                  double* x_out, l1g_result* res, l1g_iter_record* trace, int64_t cap,
+                  l1g_iter_cb cb, void* user);
+int l1g_shrinkage_solve(l1g_op* op, const double* y, double lambda, int accelerated,
+                        const l1g_stop_rule* stop, double* x_out, l1g_result* res,
+                        l1g_iter_record* trace, int64_t cap, l1g_iter_cb cb, void* user);
+
 /* ---- column-sharded runs (no reference counterpart: the reference is
  * single-threaded).  Shard r of R holds columns [r*p/R, (r+1)*p/R) of K as its own l1g_op
  * (p/R a multiple of 256); x, g and d are replicated, and each iteration exchanges the

@@ -798,3 +798,190 @@ int orc_sample_support(uint64_t seed, uint32_t stream, int64_t p, int64_t k, int
   free(pool);
   return ORC_OK;
 }
+
+/* ======================================================================== PSD, ISTA, FISTA */
+/* f_history of these solvers keeps the newest 10 values (psd.cpp:68, shrinkage.cpp:33-36) */
+static void hist_push10(orc_result* res, double f) {
+  if (res->f_history_len < 10) {
+    res->f_history[res->f_history_len++] = f;
+  } else {
+    for (int i = 0; i + 1 < 10; ++i) res->f_history[i] = res->f_history[i + 1];
+    res->f_history[9] = f;
+  }
+}
+
+/* budget checks at the top of an iteration (psd.cpp:24-35, shrinkage.cpp:16-31) */
+static int budget_stop(const orc_stop_rule* stop, int64_t k, int64_t matvecs, double elapsed,
+                       int32_t* reason) {
+  if (stop->max_iterations > 0 && k >= stop->max_iterations) {
+    *reason = ORC_MAX_ITERATIONS;
+    return 1;
+  }
+  if (stop->max_matvecs > 0 && matvecs >= stop->max_matvecs) {
+    *reason = ORC_MAX_MATVECS;
+    return 1;
+  }
+  if (stop->max_seconds > 0.0 && elapsed >= stop->max_seconds) {
+    *reason = ORC_MAX_SECONDS;
+    return 1;
+  }
+  return 0;
+}
+
+/* ||a - b||_inf of two vectors (element differences first, as the Eigen expression) */
+static double linf_diff(const double* a, const double* b, int64_t m, double* tmp) {
+  for (int64_t i = 0; i < m; ++i) tmp[i] = a[i] - b[i];
+  return orc_linf(tmp, m);
+}
+
+int orc_psd_solve(const double* K, int64_t n, int64_t p, const double* y, double rho,
+                  const orc_stop_rule* stop, double* x_out, orc_result* res,
+                  orc_iter_record* trace, int64_t trace_cap) {
+  memset(res, 0, sizeof(*res));
+  if (orc_stop_validate(stop)) return (res->status = ORC_EINVAL);
+  if (!(rho >= 0.0)) return (res->status = ORC_EINVAL);
+  const double t0 = now_seconds();
+  double *x = dalloc(p), *xn = dalloc(p), *v = dalloc(p), *r = dalloc(p), *tmp = dalloc(p);
+  double *kx = dalloc(n), *mis = dalloc(n), *kr = dalloc(n);
+  int64_t mv = 0;
+  double f_prev = INFINITY;
+  res->reason = ORC_MAX_ITERATIONS;
+  res->objective = NAN;
+  res->stationarity = INFINITY;
+  for (int64_t k = 0;; ++k) {
+    if (budget_stop(stop, k, mv, now_seconds() - t0, &res->reason)) break;
+    orc_apply(K, n, p, x, kx);  /* misfit = y - K x */
+    ++mv;
+    for (int64_t i = 0; i < n; ++i) mis[i] = y[i] - kx[i];
+    const double f = orc_sqnorm(mis, n);
+    orc_apply_adjoint(K, n, p, mis, r);
+    ++mv;
+    if (orc_linf(r, p) == 0.0) {
+      res->objective = f;
+      res->stationarity = 0.0;
+      res->reason = ORC_STATIONARY;
+      break;
+    }
+    orc_apply(K, n, p, r, kr);
+    ++mv;
+    const double denom = orc_sqnorm(kr, n);
+    if (denom == 0.0) {
+      res->objective = f;
+      res->stationarity = 0.0;
+      res->reason = ORC_STATIONARY;
+      break;
+    }
+    const double beta = orc_sqnorm(r, p) / denom; /* exact line-search step */
+    for (int64_t j = 0; j < p; ++j) v[j] = x[j] + beta * r[j];
+    double th;
+    int64_t sup;
+    orc_project_l1(v, p, rho, xn, &th, &sup);
+    const double stat = linf_diff(xn, x, p, tmp);
+    memcpy(x, xn, sizeof(double) * (size_t)p);
+    res->iterations = k + 1;
+    res->objective = f;
+    res->stationarity = stat;
+    res->elapsed_seconds = now_seconds() - t0;
+    hist_push10(res, f);
+    if (trace && k < trace_cap) {
+      orc_iter_record* t = &trace[k];
+      memset(t, 0, sizeof(*t));
+      t->k = k;
+      t->f = f;
+      t->stationarity = stat;
+      t->alpha = beta;
+      t->step = 1.0;
+      t->matvecs = mv;
+      t->elapsed_seconds = res->elapsed_seconds;
+      t->theta = th;
+      t->support = sup;
+    }
+    if (stop->stationarity_tol > 0.0 && stat <= stop->stationarity_tol) {
+      res->reason = ORC_STATIONARY;
+      break;
+    }
+    if (stop->objective_tol > 0.0 &&
+        fabs(f_prev - f) <= stop->objective_tol * (fabs(f) > 1.0 ? fabs(f) : 1.0)) {
+      res->reason = ORC_OBJECTIVE_TOL;
+      break;
+    }
+    f_prev = f;
+  }
+  res->matvecs = mv;
+  res->elapsed_seconds = now_seconds() - t0;
+  memcpy(x_out, x, sizeof(double) * (size_t)p);
+  free(x); free(xn); free(v); free(r); free(tmp); free(kx); free(mis); free(kr);
+  return ORC_OK;
+}
+
+int orc_shrinkage_solve(const double* K, int64_t n, int64_t p, const double* y, double lambda,
+                        int accelerated, const orc_stop_rule* stop, double* x_out,
+                        orc_result* res, orc_iter_record* trace, int64_t trace_cap) {
+  memset(res, 0, sizeof(*res));
+  if (orc_stop_validate(stop)) return (res->status = ORC_EINVAL);
+  if (!(lambda >= 0.0)) return (res->status = ORC_EINVAL); /* PenaltyWeight, prox.cpp */
+  const double t0 = now_seconds();
+  const double c = 0.999; /* kShrinkageOperatorScale, solver.hpp:128 */
+  const double c2 = c * c;
+  const double lam_eff = lambda * c2;
+  double *x = dalloc(p), *xprev = dalloc(p), *pt = dalloc(p), *r = dalloc(p), *v = dalloc(p);
+  double *xn = dalloc(p), *tmp = dalloc(p), *kp = dalloc(n), *mis = dalloc(n);
+  int64_t mv = 0;
+  double t = 1.0, f_prev = INFINITY;
+  res->reason = ORC_MAX_ITERATIONS;
+  res->objective = NAN;
+  res->stationarity = INFINITY;
+  for (int64_t k = 0;; ++k) {
+    if (budget_stop(stop, k, mv, now_seconds() - t0, &res->reason)) break;
+    memcpy(pt, x, sizeof(double) * (size_t)p);
+    double t_next = t;
+    if (accelerated) {
+      t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t)); /* fista_t_next, solver.hpp:118 */
+      const double coef = (t - 1.0) / t_next;
+      for (int64_t j = 0; j < p; ++j) pt[j] += coef * (x[j] - xprev[j]);
+    }
+    orc_apply(K, n, p, pt, kp);  /* misfit = K point - y */
+    ++mv;
+    for (int64_t i = 0; i < n; ++i) mis[i] = kp[i] - y[i];
+    const double f = orc_sqnorm(mis, n);
+    orc_apply_adjoint(K, n, p, mis, r);
+    ++mv;
+    for (int64_t j = 0; j < p; ++j) v[j] = pt[j] - c2 * r[j];
+    orc_soft_threshold(v, p, lam_eff, xn);
+    const double stat = linf_diff(xn, pt, p, tmp);
+    memcpy(xprev, x, sizeof(double) * (size_t)p);
+    memcpy(x, xn, sizeof(double) * (size_t)p);
+    t = t_next;
+    res->iterations = k + 1;
+    res->objective = f;
+    res->stationarity = stat;
+    res->elapsed_seconds = now_seconds() - t0;
+    hist_push10(res, f);
+    if (trace && k < trace_cap) {
+      orc_iter_record* tr = &trace[k];
+      memset(tr, 0, sizeof(*tr));
+      tr->k = k;
+      tr->f = f;
+      tr->stationarity = stat;
+      tr->alpha = 1.0;
+      tr->step = 1.0;
+      tr->matvecs = mv;
+      tr->elapsed_seconds = res->elapsed_seconds;
+    }
+    if (stop->stationarity_tol > 0.0 && stat <= stop->stationarity_tol) {
+      res->reason = ORC_STATIONARY;
+      break;
+    }
+    if (stop->objective_tol > 0.0 &&
+        fabs(f_prev - f) <= stop->objective_tol * (fabs(f) > 1.0 ? fabs(f) : 1.0)) {
+      res->reason = ORC_OBJECTIVE_TOL;
+      break;
+    }
+    f_prev = f;
+  }
+  res->matvecs = mv;
+  res->elapsed_seconds = now_seconds() - t0;
+  memcpy(x_out, x, sizeof(double) * (size_t)p);
+  free(x); free(xprev); free(pt); free(r); free(v); free(xn); free(tmp); free(kp); free(mis);
+  return ORC_OK;
+}

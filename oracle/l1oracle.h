@@ -130,6 +130,16 @@ int orc_gpss_solve(const double* K, int64_t n, int64_t p, const double* y, doubl
                    double* x_out, orc_result* res, orc_iter_record* trace, int64_t trace_cap,
                    double* x_trace /* iterations x p, optional */);
 
+/* Projected steepest descent, psd.cpp:14-93 (3 matvecs per iteration, x0 = 0). */
+int orc_psd_solve(const double* K, int64_t n, int64_t p, const double* y, double rho,
+                  const orc_stop_rule* stop, double* x_out, orc_result* res,
+                  orc_iter_record* trace, int64_t trace_cap);
+/* ISTA (accelerated = 0) / FISTA (accelerated = 1), shrinkage.cpp:41-118, on the rescaled
+ * problem (c = 0.999, solver.hpp:128), x0 = 0. */
+int orc_shrinkage_solve(const double* K, int64_t n, int64_t p, const double* y, double lambda,
+                        int accelerated, const orc_stop_rule* stop, double* x_out,
+                        orc_result* res, orc_iter_record* trace, int64_t trace_cap);
+
 /* Stateful single-step interface (gp_init / gp_iterate) for step-level tests. */
 typedef struct orc_gp orc_gp;
 int orc_gp_init(const double* K, int64_t n, int64_t p, const double* y, double rho,

@@ -120,6 +120,10 @@ def lib():
             "orc_gpss_solve": (i32, [_dp, i64, i64, _dp, dbl, C.POINTER(GpConfig),
                                      C.POINTER(StopRule), C.c_void_p, _dp, C.POINTER(Result),
                                      C.c_void_p, i64, C.c_void_p]),
+            "orc_psd_solve": (i32, [_dp, i64, i64, _dp, dbl, C.POINTER(StopRule), _dp,
+                                    C.POINTER(Result), C.c_void_p, i64]),
+            "orc_shrinkage_solve": (i32, [_dp, i64, i64, _dp, dbl, i32, C.POINTER(StopRule), _dp,
+                                          C.POINTER(Result), C.c_void_p, i64]),
             "orc_gp_init": (i32, [_dp, i64, i64, _dp, dbl, C.POINTER(GpConfig), C.c_void_p,
                                   C.POINTER(C.c_void_p)]),
             "orc_gp_iterate": (i32, [C.c_void_p, dbl, C.POINTER(IterRecord),
@@ -309,6 +313,40 @@ def gpss_solve(K, y, rho, cfg=None, stop=None, x0=None, trace=True, x_trace=Fals
     rec = records_to_dicts(recs, min(cap, res.iterations)) if cap else []
     xh = xs[: res.iterations] if xs is not None else None
     return x, out, rec, xh
+
+
+def _result_dict(res):
+    out = {f: getattr(res, f) for f, _ in Result._fields_ if f not in ("f_history",)}
+    out["f_history"] = [res.f_history[i] for i in range(res.f_history_len)]
+    out["reason_name"] = REASONS[res.reason]
+    return out
+
+
+def psd_solve(K, y, rho, stop=None, trace=True):
+    """psd.cpp:14-93.  Returns (x, result-dict, records)."""
+    stop = stop or StopRule()
+    K, y = _a(K), _a(y)
+    n, p = K.shape
+    x, res = np.zeros(p), Result()
+    cap = int(stop.max_iterations) if (trace and stop.max_iterations > 0) else 0
+    recs = (IterRecord * max(cap, 1))()
+    _check(lib().orc_psd_solve(K, n, p, y, rho, C.byref(stop), x, C.byref(res),
+                               C.addressof(recs) if cap else None, cap), "psd_solve")
+    return x, _result_dict(res), (records_to_dicts(recs, min(cap, res.iterations)) if cap else [])
+
+
+def shrinkage_solve(K, y, lam, accelerated, stop=None, trace=True):
+    """ista_solve / fista_solve, shrinkage.cpp:41-118.  Returns (x, result-dict, records)."""
+    stop = stop or StopRule()
+    K, y = _a(K), _a(y)
+    n, p = K.shape
+    x, res = np.zeros(p), Result()
+    cap = int(stop.max_iterations) if (trace and stop.max_iterations > 0) else 0
+    recs = (IterRecord * max(cap, 1))()
+    _check(lib().orc_shrinkage_solve(K, n, p, y, lam, int(accelerated), C.byref(stop), x,
+                                     C.byref(res), C.addressof(recs) if cap else None, cap),
+           "fista_solve" if accelerated else "ista_solve")
+    return x, _result_dict(res), (records_to_dicts(recs, min(cap, res.iterations)) if cap else [])
 
 
 class GpState:

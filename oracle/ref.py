@@ -42,6 +42,13 @@ def lib(kind="canon"):
         L.ref_gpss_solve.argtypes = [C.c_void_p, _dp, C.c_double, C.POINTER(O.GpConfig),
                                      C.POINTER(O.StopRule), C.c_void_p, _dp,
                                      C.POINTER(O.Result), C.c_void_p, C.c_long]
+        L.ref_psd_solve.restype = C.c_int
+        L.ref_psd_solve.argtypes = [C.c_void_p, _dp, C.c_double, C.POINTER(O.StopRule), _dp,
+                                    C.POINTER(O.Result), C.c_void_p, C.c_long]
+        L.ref_shrinkage_solve.restype = C.c_int
+        L.ref_shrinkage_solve.argtypes = [C.c_void_p, _dp, C.c_double, C.c_int,
+                                          C.POINTER(O.StopRule), _dp, C.POINTER(O.Result),
+                                          C.c_void_p, C.c_long]
         _libs[kind] = L
     return _libs[kind]
 
@@ -87,6 +94,28 @@ class RefOperator:
         out["reason_name"] = O.REASONS[res.reason]
         rec = O.records_to_dicts(recs, min(cap, res.iterations)) if cap else []
         return x, out, rec
+
+
+def _solve_other(op, fn, args, stop, trace):
+    cap = int(stop.max_iterations) if (trace and stop.max_iterations > 0) else 0
+    recs = (O.IterRecord * max(cap, 1))()
+    x, res = np.zeros(op.p), O.Result()
+    O._check(fn(op.h, *args, C.byref(stop), x, C.byref(res), C.addressof(recs) if cap else None,
+                cap), "solve")
+    return x, O._result_dict(res), (O.records_to_dicts(recs, min(cap, res.iterations)) if cap else [])
+
+
+def psd_solve(op: "RefOperator", y, rho, stop=None, trace=True):
+    stop = stop or O.StopRule()
+    return _solve_other(op, op.L.ref_psd_solve, (np.ascontiguousarray(y, dtype=np.float64), rho),
+                        stop, trace)
+
+
+def shrinkage_solve(op: "RefOperator", y, lam, accelerated, stop=None, trace=True):
+    stop = stop or O.StopRule()
+    return _solve_other(op, op.L.ref_shrinkage_solve,
+                        (np.ascontiguousarray(y, dtype=np.float64), lam, int(accelerated)),
+                        stop, trace)
 
 
 def project_l1(x, rho, kind="canon"):

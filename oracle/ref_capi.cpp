@@ -1,7 +1,8 @@
 // C entry points into the reference's own solver sources (TEST INFRASTRUCTURE ONLY).
 //
 // oracle/build_ref.sh compiles this file together with the UNMODIFIED reference sources
-// /root/reference/proj/core/src/{gpss,prox,linear_operator,objective}.cpp against the
+// /root/reference/proj/core/src/{gpss,prox,linear_operator,objective,psd,shrinkage}.cpp
+// against the
 // Eigen stand-in in oracle/eigen_shim, producing oracle/_ref/libref_canon.so (canonical
 // reductions, parity) and oracle/_ref/libref_fast.so (OpenMP GEMVs, CPU timing baseline).
 // Structs are layout-compatible with oracle/l1oracle.h.
@@ -12,6 +13,7 @@
 #include "../oracle/l1oracle.h"
 #include "l1solve/gpss.hpp"
 #include "l1solve/prox.hpp"
+#include "l1solve/solver.hpp"
 
 using namespace l1solve;
 
@@ -140,6 +142,76 @@ int ref_gpss_solve(ref_op* o, const double* y, double rho, const orc_gp_config* 
     for (double f : s.f_history)
       if (i < 64) res->f_history[i++] = f;
     res->f_history_len = i;
+    return 0;
+  } catch (const std::exception& e) {
+    return res->status = code(e);
+  }
+}
+
+static StopRule conv_stop(const orc_stop_rule* s) {
+  StopRule stop;
+  stop.max_iterations = s->max_iterations;
+  stop.max_matvecs = s->max_matvecs;
+  stop.max_seconds = s->max_seconds;
+  stop.stationarity_tol = s->stationarity_tol;
+  stop.objective_tol = s->objective_tol;
+  return stop;
+}
+
+static void fill_result(const SolverState& st, long p, double* x_out, orc_result* res) {
+  std::memcpy(x_out, st.x.data(), sizeof(double) * static_cast<size_t>(p));
+  res->iterations = st.iterations;
+  res->matvecs = st.matvecs.count;
+  res->objective = st.objective;
+  res->stationarity = st.stationarity;
+  res->elapsed_seconds = st.elapsed_seconds;
+  res->reason = static_cast<int>(st.reason);
+  int i = 0;
+  for (double f : st.f_history)
+    if (i < 64) res->f_history[i++] = f;
+  res->f_history_len = i;
+}
+
+static IterationCallback record_cb(orc_iter_record* trace, long cap) {
+  if (!trace || cap <= 0) return {};
+  return [trace, cap](const IterationRecord& r, const Vector&) {
+    if (r.k >= cap) return;
+    orc_iter_record& t = trace[r.k];
+    std::memset(&t, 0, sizeof(t));
+    t.k = r.k;
+    t.f = r.f;
+    t.stationarity = r.stationarity;
+    t.alpha = r.alpha;
+    t.step = r.step;
+    t.matvecs = r.matvecs;
+    t.elapsed_seconds = r.elapsed_seconds;
+  };
+}
+
+int ref_psd_solve(ref_op* o, const double* y, double rho, const orc_stop_rule* stop_in,
+                  double* x_out, orc_result* res, orc_iter_record* trace, long trace_cap) {
+  std::memset(res, 0, sizeof(*res));
+  try {
+    const Objective obj(o->op, vec(y, o->op.rows()));
+    const SolverState s = psd_solve(obj, L1Ball(rho), conv_stop(stop_in), record_cb(trace, trace_cap));
+    fill_result(s, o->op.cols(), x_out, res);
+    return 0;
+  } catch (const std::exception& e) {
+    return res->status = code(e);
+  }
+}
+
+int ref_shrinkage_solve(ref_op* o, const double* y, double lambda, int accelerated,
+                        const orc_stop_rule* stop_in, double* x_out, orc_result* res,
+                        orc_iter_record* trace, long trace_cap) {
+  std::memset(res, 0, sizeof(*res));
+  try {
+    const Objective obj(o->op, vec(y, o->op.rows()));
+    const auto cb = record_cb(trace, trace_cap);
+    const SolverState s = accelerated
+                              ? fista_solve(obj, PenaltyWeight(lambda), conv_stop(stop_in), cb)
+                              : ista_solve(obj, PenaltyWeight(lambda), conv_stop(stop_in), cb);
+    fill_result(s, o->op.cols(), x_out, res);
     return 0;
   } catch (const std::exception& e) {
     return res->status = code(e);

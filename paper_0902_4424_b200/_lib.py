@@ -134,6 +134,10 @@ _SIGS = {
     "l1g_gpss_solve": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(GpConfigC),
                                  C.POINTER(StopRuleC), _vp, _vp, C.POINTER(ResultC), _vp, _i64]),
     "l1g_rng_fill": (C.c_int, [_vp, C.c_int, C.c_uint64, C.c_uint32, C.c_uint64, _i64, _vp]),
+    "l1g_psd_solve": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(StopRuleC), _vp,
+                                C.POINTER(ResultC), _vp, _i64, ITER_CB, _vp]),
+    "l1g_shrinkage_solve": (C.c_int, [_vp, _vp, C.c_double, C.c_int, C.POINTER(StopRuleC), _vp,
+                                      C.POINTER(ResultC), _vp, _i64, ITER_CB, _vp]),
     "l1g_host_alloc": (C.c_int, [_i64, C.POINTER(_vp)]),
     "l1g_host_free": (None, [_vp]),
 }

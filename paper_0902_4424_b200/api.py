@@ -665,3 +665,61 @@ def gpss_solve(prob: Objective, ball: L1Ball, cfg: GpConfig, stop: StopRule,
     if err:
         raise err[0]
     return _state_from(res, x)
+
+
+# ------------------------------------------------------------------ PSD, ISTA, FISTA
+def _other_solve(prob: Objective, param: float, kind: int, stop: StopRule,
+                 cb: Optional[IterationCallback], trace: Optional[list]) -> SolverState:
+    stop.validate()
+    op = _require_dense(prob)
+    lib = L.load()
+    y = prob.y()
+    res = L.ResultC()
+    s = stop._c()
+    x = np.empty(op.cols())
+    cap = stop.max_iterations if (trace is not None and stop.max_iterations > 0) else 0
+    recs = (L.IterRecordC * max(cap, 1))()
+    err = []
+
+    def _cb(rec_p, x_p, p, user):
+        try:
+            cb(IterationRecord.from_c(rec_p.contents),
+               np.ctypeslib.as_array(x_p, shape=(p,)).copy())
+        except Exception as e:  # surfaced after the run
+            err.append(e)
+
+    cfun = L.ITER_CB(_cb) if cb is not None else L.ITER_CB()
+    if kind == 0:
+        rc = lib.l1g_psd_solve(op.h, ptr(y), param, C.byref(s), ptr(x), C.byref(res),
+                               C.addressof(recs) if cap else None, cap, cfun, None)
+    else:
+        rc = lib.l1g_shrinkage_solve(op.h, ptr(y), param, int(kind == 2), C.byref(s), ptr(x),
+                                     C.byref(res), C.addressof(recs) if cap else None, cap,
+                                     cfun, None)
+    check(rc, ["psd_solve", "ista_solve", "fista_solve"][kind])
+    if err:
+        raise err[0]
+    if trace is not None:
+        trace.extend(IterationRecord.from_c(recs[i]) for i in range(min(cap, res.iterations)))
+    return _state_from(res, x)
+
+
+def psd_solve(prob: Objective, ball: L1Ball, stop: StopRule,
+              cb: Optional[IterationCallback] = None,
+              trace: Optional[list] = None) -> SolverState:
+    """Projected steepest descent, psd.cpp:14-93 (3 matvecs per iteration)."""
+    return _other_solve(prob, ball.radius(), 0, stop, cb, trace)
+
+
+def ista_solve(prob: Objective, lam: PenaltyWeight, stop: StopRule,
+               cb: Optional[IterationCallback] = None,
+               trace: Optional[list] = None) -> SolverState:
+    """Iterative soft thresholding, shrinkage.cpp:41-112 (c = 0.999 rescaling)."""
+    return _other_solve(prob, lam.value(), 1, stop, cb, trace)
+
+
+def fista_solve(prob: Objective, lam: PenaltyWeight, stop: StopRule,
+                cb: Optional[IterationCallback] = None,
+                trace: Optional[list] = None) -> SolverState:
+    """Accelerated soft thresholding, shrinkage.cpp:41-118."""
+    return _other_solve(prob, lam.value(), 2, stop, cb, trace)

@@ -44,6 +44,9 @@ T* dalloc(size_t count) {
   void* p = nullptr;
   L1G_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
   L1G_CUDA(cudaMemset(p, 0, std::max<size_t>(count, 1) * sizeof(T)));
+  // the zero fill runs on the legacy stream, which does not order against the library's
+  // non-blocking streams: finish it before the buffer is handed out
+  L1G_CUDA(cudaStreamSynchronize(0));
   return static_cast<T*>(p);
 }
 void dfree(void* p) {
@@ -890,6 +893,216 @@ void batch_get_x(l1g_batch* b, double* X) {
 
 }  // namespace
 
+// =============================================================================== PSD, ISTA, FISTA
+// The reference's other solvers of the same problem family (psd.cpp:14-93,
+// shrinkage.cpp:41-118): host-driven loops (one synchronisation per reduction batch) over
+// the same device kernels -- canonical GEMVs, the exact projection, element-wise kernels
+// with rounded products -- so they reproduce the oracle bit for bit.
+namespace {
+
+struct LoopBufs {
+  cudaStream_t s = nullptr;
+  Workspace ws;
+  std::vector<double*> bufs;
+  double* scal = nullptr;
+  DevState* st = nullptr;
+  double* pscr = nullptr;
+  double* get(int64_t m) {
+    bufs.push_back(dalloc<double>((size_t)m));
+    return bufs.back();
+  }
+  ~LoopBufs() {
+    for (double* b : bufs) dfree(b);
+    free_ws(ws);
+    dfree(scal);
+    dfree(st);
+    dfree(pscr);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+double fetch(LoopBufs& lb, int i) {
+  double v = 0.0;
+  L1G_CUDA(cudaMemcpyAsync(&v, lb.scal + i, sizeof(double), cudaMemcpyDeviceToHost, lb.s));
+  L1G_CUDA(cudaStreamSynchronize(lb.s));
+  return v;
+}
+
+void hist_push10(l1g_result* res, double f) {
+  if (res->f_history_len < 10) {
+    res->f_history[res->f_history_len++] = f;
+  } else {
+    for (int i = 0; i + 1 < 10; ++i) res->f_history[i] = res->f_history[i + 1];
+    res->f_history[9] = f;
+  }
+}
+
+bool budget_stop(const l1g_stop_rule& stop, int64_t k, int64_t mv, double el, int32_t* reason) {
+  if (stop.max_iterations > 0 && k >= stop.max_iterations) {
+    *reason = L1G_MAX_ITERATIONS;
+    return true;
+  }
+  if (stop.max_matvecs > 0 && mv >= stop.max_matvecs) {
+    *reason = L1G_MAX_MATVECS;
+    return true;
+  }
+  if (stop.max_seconds > 0.0 && el >= stop.max_seconds) {
+    *reason = L1G_MAX_SECONDS;
+    return true;
+  }
+  return false;
+}
+
+bool objective_stop(const l1g_stop_rule& stop, double f_prev, double f) {
+  return stop.objective_tol > 0.0 &&
+         std::fabs(f_prev - f) <= stop.objective_tol * std::max(1.0, std::fabs(f));
+}
+
+// kind 0: psd_solve (constraint rho), 1: ista_solve, 2: fista_solve (penalty lambda)
+void other_solve(l1g_op* op, const double* y_host, double param, int kind,
+                 const l1g_stop_rule& stop, double* x_out, l1g_result* res,
+                 l1g_iter_record* trace, int64_t cap, l1g_iter_cb cb, void* user) {
+  check_stop(stop);
+  if (kind == 0) check_rho(param);
+  else if (!(param >= 0.0)) throw InvalidArgument("PenaltyWeight: lambda must be >= 0");
+  set_device(op->c);
+  const GemvPlan& pl = op->plan;
+  LoopBufs lb;
+  L1G_CUDA(cudaStreamCreateWithFlags(&lb.s, cudaStreamNonBlocking));
+  alloc_ws(lb.ws, pl);
+  lb.scal = dalloc<double>(8);
+  double *x = lb.get(pl.p_pad), *xn = lb.get(pl.p_pad), *v = lb.get(pl.p_pad),
+         *r = lb.get(pl.p_pad), *tmp = lb.get(pl.p_pad), *xp = lb.get(pl.p_pad),
+         *pt = lb.get(pl.p_pad);
+  double *y = lb.get(pl.n_pad), *kx = lb.get(pl.n_pad), *mis = lb.get(pl.n_pad),
+         *kr = lb.get(pl.n_pad);
+  L1G_CUDA(cudaMemcpyAsync(y, y_host, pl.n * 8, cudaMemcpyHostToDevice, lb.s));
+  ProjPlan pp = make_proj_plan(pl.p_pad);
+  lb.pscr = dalloc<double>(proj_scratch_doubles(pl.p_pad));
+  lb.st = dalloc<DevState>(1);
+  if (kind == 0) {
+    l1g_gp_config cfg{1e-4, 0.5, 1, 2, 1e-10, 1e10, 0.5};
+    DevState h = host_state(cfg, param);
+    L1G_CUDA(cudaMemcpyAsync(lb.st, &h, sizeof(h), cudaMemcpyHostToDevice, lb.s));
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  auto elapsed = [&] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  const double c = 0.999, c2 = c * c, lam_eff = param * c2;  // solver.hpp:128
+  std::memset(res, 0, sizeof(*res));
+  res->reason = L1G_MAX_ITERATIONS;
+  res->objective = std::nan("");
+  res->stationarity = INFINITY;
+  int64_t mv = 0;
+  double t = 1.0, f_prev = INFINITY;
+  cudaStream_t s = lb.s;
+  for (int64_t k = 0;; ++k) {
+    if (budget_stop(stop, k, mv, elapsed(), &res->reason)) break;
+    double f, stat, alpha = 1.0, theta = 0.0;
+    int64_t support = 0;
+    if (kind == 0) {
+      launch_fwd(*op, lb.ws, FWD_APPLY, x, kx, nullptr, nullptr, s);  // misfit = y - K x
+      vsub(y, kx, mis, pl.n_pad, s);
+      launch_adj(*op, lb.ws, ADJ_APPLY, mis, r, nullptr, nullptr, s);
+      mv += 2;
+      reduce(mis, nullptr, pl.n_pad, RED_SQ, lb.scal + 0, 0, s);
+      reduce(r, nullptr, pl.p_pad, RED_MAX, lb.scal + 1, 0, s);
+      f = fetch(lb, 0);
+      if (fetch(lb, 1) == 0.0) {
+        res->objective = f;
+        res->stationarity = 0.0;
+        res->reason = L1G_STATIONARY;
+        break;
+      }
+      launch_fwd(*op, lb.ws, FWD_APPLY, r, kr, nullptr, nullptr, s);
+      ++mv;
+      reduce(kr, nullptr, pl.n_pad, RED_SQ, lb.scal + 2, 0, s);
+      reduce(r, nullptr, pl.p_pad, RED_SQ, lb.scal + 3, 0, s);
+      const double denom = fetch(lb, 2);
+      if (denom == 0.0) {
+        res->objective = f;
+        res->stationarity = 0.0;
+        res->reason = L1G_STATIONARY;
+        break;
+      }
+      const double beta = fetch(lb, 3) / denom;  // exact line-search step
+      alpha = beta;
+      lincomb(x, beta, r, v, pl.p_pad, s);
+      launch_proj(pp, PROJ_PLAIN, pl.p, pl.p_pad, v, nullptr, xn, lb.pscr, lb.st, nullptr, s);
+      vsub(xn, x, tmp, pl.p_pad, s);
+      reduce(tmp, nullptr, pl.p_pad, RED_MAX, lb.scal + 4, 0, s);
+      stat = fetch(lb, 4);
+      DevState h;
+      L1G_CUDA(cudaMemcpyAsync(&h, lb.st, sizeof(h), cudaMemcpyDeviceToHost, s));
+      L1G_CUDA(cudaStreamSynchronize(s));
+      theta = h.theta;
+      support = h.support;
+      std::swap(x, xn);
+    } else {
+      const double* point = x;
+      double t_next = t;
+      if (kind == 2) {
+        t_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));  // fista_t_next, solver.hpp:118
+        extrap(x, xp, (t - 1.0) / t_next, pt, pl.p_pad, s);
+        point = pt;
+      }
+      launch_fwd(*op, lb.ws, FWD_APPLY, point, kx, nullptr, nullptr, s);  // K point - y
+      vsub(kx, y, mis, pl.n_pad, s);
+      launch_adj(*op, lb.ws, ADJ_APPLY, mis, r, nullptr, nullptr, s);
+      mv += 2;
+      reduce(mis, nullptr, pl.n_pad, RED_SQ, lb.scal + 0, 0, s);
+      lincomb(point, -c2, r, v, pl.p_pad, s);
+      soft_threshold(v, xn, pl.p_pad, lam_eff, s);
+      vsub(xn, point, tmp, pl.p_pad, s);
+      reduce(tmp, nullptr, pl.p_pad, RED_MAX, lb.scal + 1, 0, s);
+      f = fetch(lb, 0);
+      stat = fetch(lb, 1);
+      std::swap(xp, x);  // x_prev = x
+      std::swap(x, xn);  // x = x_new
+      t = t_next;
+    }
+    res->iterations = k + 1;
+    res->objective = f;
+    res->stationarity = stat;
+    res->elapsed_seconds = elapsed();
+    hist_push10(res, f);
+    l1g_iter_record rc;
+    std::memset(&rc, 0, sizeof(rc));
+    rc.k = k;
+    rc.f = f;
+    rc.stationarity = stat;
+    rc.alpha = alpha;
+    rc.step = 1.0;
+    rc.matvecs = mv;
+    rc.elapsed_seconds = res->elapsed_seconds;
+    rc.theta = theta;
+    rc.support = support;
+    if (trace && k < cap) trace[k] = rc;
+    if (cb) {  // IterationCallback (solver.hpp:86-88): the record and the new iterate
+      std::vector<double> xh((size_t)pl.p);
+      download(xh.data(), x, pl.p, s);
+      L1G_CUDA(cudaStreamSynchronize(s));
+      cb(&rc, xh.data(), pl.p, user);
+    }
+    if (stop.stationarity_tol > 0.0 && stat <= stop.stationarity_tol) {
+      res->reason = L1G_STATIONARY;
+      break;
+    }
+    if (objective_stop(stop, f_prev, f)) {
+      res->reason = L1G_OBJECTIVE_TOL;
+      break;
+    }
+    f_prev = f;
+  }
+  res->matvecs = mv;
+  res->elapsed_seconds = elapsed();
+  download(x_out, x, pl.p, s);
+  L1G_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
 // =============================================================================== C ABI
 extern "C" {
 
@@ -1633,6 +1846,20 @@ int l1g_gpss_solve_batched(l1g_op* op, int B, const double* Y, const double* rho
       throw;
     }
     batch_free(b);
+  });
+}
+
+int l1g_psd_solve(l1g_op* op, const double* y, double rho, const l1g_stop_rule* stop,
+                  double* x_out, l1g_result* res, l1g_iter_record* trace, int64_t cap,
+                  l1g_iter_cb cb, void* user) {
+  return guarded([&] { other_solve(op, y, rho, 0, *stop, x_out, res, trace, cap, cb, user); });
+}
+
+int l1g_shrinkage_solve(l1g_op* op, const double* y, double lambda, int accelerated,
+                        const l1g_stop_rule* stop, double* x_out, l1g_result* res,
+                        l1g_iter_record* trace, int64_t cap, l1g_iter_cb cb, void* user) {
+  return guarded([&] {
+    other_solve(op, y, lambda, accelerated ? 2 : 1, *stop, x_out, res, trace, cap, cb, user);
   });
 }
 

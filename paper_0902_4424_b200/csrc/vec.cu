@@ -318,6 +318,32 @@ void vsub(const double* a, const double* b, double* out, int64_t m, cudaStream_t
   L1G_CUDA(cudaGetLastError());
 }
 
+// out = a + alpha * b (product rounded, then the sum: Eigen's `a + alpha * b`)
+__global__ void lincomb_kernel(const double* a, double alpha, const double* b, double* out,
+                               int64_t m) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = add(a[e], mul(alpha, b[e]));
+}
+void lincomb(const double* a, double alpha, const double* b, double* out, int64_t m,
+             cudaStream_t s) {
+  lincomb_kernel<<<fill_grid(m), 256, 0, s>>>(a, alpha, b, out, m);
+  L1G_CUDA(cudaGetLastError());
+}
+
+// out = x + coef * (x - xprev)  (FISTA extrapolation, shrinkage.cpp:61-63)
+__global__ void extrap_kernel(const double* x, const double* xp, double coef, double* out,
+                              int64_t m) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = add(x[e], mul(coef, sub(x[e], xp[e])));
+}
+void extrap(const double* x, const double* xprev, double coef, double* out, int64_t m,
+            cudaStream_t s) {
+  extrap_kernel<<<fill_grid(m), 256, 0, s>>>(x, xprev, coef, out, m);
+  L1G_CUDA(cudaGetLastError());
+}
+
 // ---------------------------------------------------------------- scalar kernels
 __global__ void steplength_kernel(l1g_sl_state* sl, const double* dots, l1g_gp_config cfg,
                                   l1g_sl_choice* out) {

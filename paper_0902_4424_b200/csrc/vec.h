@@ -25,6 +25,10 @@ void fill(double* a, int64_t m, int64_t valid, double c, cudaStream_t s);
 void div_by(const double* w, double* v, int64_t m, const double* nrm, cudaStream_t s);
 void soft_threshold(const double* x, double* out, int64_t m, double t, cudaStream_t s);
 void vsub(const double* a, const double* b, double* out, int64_t m, cudaStream_t s);
+void lincomb(const double* a, double alpha, const double* b, double* out, int64_t m,
+             cudaStream_t s);
+void extrap(const double* x, const double* xprev, double coef, double* out, int64_t m,
+            cudaStream_t s);
 void steplength_device(l1g_sl_state* sl, const double* dots, const l1g_gp_config& cfg,
                        l1g_sl_choice* out, cudaStream_t s);
 void backtrack_device(const double* in, const l1g_gp_config& cfg, double* out, cudaStream_t s);

@@ -74,3 +74,33 @@ def test_literal_mode_within_tolerance():
         xl, rl, recl, _ = O.gpss_solve(P["K"], P["y"], P["rho"], cfg, stop)
     assert np.linalg.norm(xc - xl) <= 1e-9 * np.linalg.norm(xc)
     assert abs(rc["objective"] - rl["objective"]) <= 1e-9 * abs(rc["objective"])
+
+
+OTHER_FIELDS = ["k", "f", "stationarity", "alpha", "step", "matvecs"]
+
+
+@pytest.mark.parametrize("spec,iters", [(PB.C1, 120), (PB.C2_MINI, 60), (PB.RAGGED, 80),
+                                        (PB.TINY, 30)], ids=lambda v: getattr(v, "name", str(v)))
+@pytest.mark.parametrize("solver", ["psd", "ista", "fista"])
+def test_psd_ista_fista_bit_identical(spec, iters, solver):
+    """psd.cpp / shrinkage.cpp: the restatement against the reference sources."""
+    P = O.build_problem(spec)
+    op = R.RefOperator(P["K"])
+    for tol in (0.0, 1e-7):
+        stop = O.StopRule(iters, 0, 0, tol, 1e-12 if tol else 0.0)
+        if solver == "psd":
+            xo, ro, reco = O.psd_solve(P["K"], P["y"], P["rho"], stop)
+            xr, rr, recr = R.psd_solve(op, P["y"], P["rho"], stop)
+        else:
+            lam = 0.05 * float(np.abs(O.apply_adjoint(P["K"], P["y"])).max())
+            acc = solver == "fista"
+            xo, ro, reco = O.shrinkage_solve(P["K"], P["y"], lam, acc, stop)
+            xr, rr, recr = R.shrinkage_solve(op, P["y"], lam, acc, stop)
+        assert ro["iterations"] == rr["iterations"] and ro["reason"] == rr["reason"]
+        assert ro["matvecs"] == rr["matvecs"]
+        assert np.array_equal(xo, xr)
+        assert ro["objective"] == rr["objective"] and ro["f_history"] == rr["f_history"]
+        assert ro["stationarity"] == rr["stationarity"]
+        for a, b in zip(reco, recr):
+            for f in OTHER_FIELDS:
+                assert same(a[f], b[f]), (a["k"], f, a[f], b[f])
