@@ -92,3 +92,8 @@ struct MatvecCounter {
 };
 
 }  // namespace l1solve
+
+// source compatibility with callers written against Eigen (x.lpNorm<Eigen::Infinity>())
+namespace Eigen {
+using l1solve::Infinity;
+}

@@ -645,4 +645,46 @@ SolverState gpss_solve(const Objective& prob, const L1Ball& ball, const GpConfig
   return state_from(res, std::move(x));
 }
 
+namespace {
+// psd / ista / fista through the device drivers (l1g_psd_solve, l1g_shrinkage_solve)
+SolverState other_solve(const Objective& prob, double param, int kind, const StopRule& stop,
+                        const IterationCallback& cb, const char* name) {
+  stop.validate();
+  auto* dense = dynamic_cast<const DenseOperator*>(&prob.op());
+  if (!dense) throw std::invalid_argument(std::string(name) + ": needs a DenseOperator here");
+  const l1g_stop_rule s = conv(stop);
+  l1g_result res;
+  Vector x(prob.dim());
+  CbCtx cc{&cb, nullptr};
+  const l1g_iter_cb fn = cb ? &trampoline : nullptr;
+  const int rc = kind == 0
+                     ? l1g_psd_solve(dense->handle(), prob.y().data(), param, &s, x.data(), &res,
+                                     nullptr, 0, fn, &cc)
+                     : l1g_shrinkage_solve(dense->handle(), prob.y().data(), param, kind == 2, &s,
+                                           x.data(), &res, nullptr, 0, fn, &cc);
+  if (cc.err) std::rethrow_exception(cc.err);
+  if (rc) {
+    const std::string msg = l1g_last_error();
+    if (rc == L1G_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+  }
+  return state_from(res, std::move(x));
+}
+}  // namespace
+
+SolverState psd_solve(const Objective& prob, const L1Ball& ball, const StopRule& stop,
+                      const IterationCallback& cb) {
+  return other_solve(prob, ball.radius(), 0, stop, cb, "psd_solve");
+}
+
+SolverState ista_solve(const Objective& prob, const PenaltyWeight& lambda, const StopRule& stop,
+                       const IterationCallback& cb) {
+  return other_solve(prob, lambda.value(), 1, stop, cb, "ista_solve");
+}
+
+SolverState fista_solve(const Objective& prob, const PenaltyWeight& lambda, const StopRule& stop,
+                        const IterationCallback& cb) {
+  return other_solve(prob, lambda.value(), 2, stop, cb, "fista_solve");
+}
+
 }  // namespace l1solve

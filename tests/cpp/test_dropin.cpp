@@ -131,6 +131,25 @@ int main() {
   dg(1, 1) = 5.0;
   EXPECT(near(spectral_norm_estimate(DenseOperator(dg)), 5.0, 1e-10));
 
+  // psd / ista / fista (psd.cpp, shrinkage.cpp): feasibility, matvec accounting, callbacks
+  {
+    StopRule st3;
+    st3.max_iterations = 40;
+    st3.stationarity_tol = 0.0;
+    long ncb = 0;
+    const SolverState sp = psd_solve(obj, ball, st3, [&](const IterationRecord&, const Vector&) { ++ncb; });
+    EXPECT(sp.iterations == 40 && ncb == 40 && sp.matvecs.count == 3 * 40);
+    EXPECT(sp.x.lpNorm<1>() <= ball.radius() * (1 + 1e-12) + 1e-12);
+    EXPECT(sp.f_history.size() == 10);
+    MatvecCounter mvx;
+    const double lam = 0.05 * obj.op().apply_adjoint(obj.y(), mvx).lpNorm<Eigen::Infinity>();
+    const SolverState si = ista_solve(obj, PenaltyWeight(lam), st3);
+    const SolverState sf = fista_solve(obj, PenaltyWeight(lam), st3);
+    EXPECT(si.matvecs.count == 80 && sf.matvecs.count == 80);
+    EXPECT(sf.objective <= si.objective * 1.5);
+    EXPECT_THROW(ista_solve(obj, PenaltyWeight(-1.0), st3), std::invalid_argument);
+  }
+
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }
