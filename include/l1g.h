@@ -167,6 +167,20 @@ int l1g_solver_stream(l1g_solver* s, void** stream);
 /* per-kernel CUDA-event timing of the device loop (projection / forward / adjoint), summed
  * over completed iterations, and the number of kernels this solver launched */
 int l1g_solver_set_timing(l1g_solver* s, int on);
+/* ---- L1PROBv1 problem files (problem_io.cpp, docs/problem_format.md):
+ *   l1g_problem_info  -> header of a file (n, p, seed, noise_level)
+ *   l1g_problem_load  -> load_problem: K streamed into a new device operator; y (n) and
+ *                        x_true (p) into caller buffers (either may be NULL)
+ *   l1g_problem_save  -> save_problem (K read back from the device)
+ *   l1g_problem_hash  -> problem_hash: FNV-1a 64 of the serialized bytes */
+int l1g_problem_info(const char* path, int64_t* n, int64_t* p, uint64_t* seed, double* noise);
+int l1g_problem_load(l1g_ctx* ctx, const char* path, double* y, double* x_true, uint64_t* seed,
+                     double* noise, l1g_op** out);
+int l1g_problem_save(const char* path, l1g_op* op, const double* y, const double* x_true,
+                     uint64_t seed, double noise);
+int l1g_problem_hash(l1g_op* op, const double* y, const double* x_true, uint64_t seed,
+                     double noise, uint64_t* hash);
+
 /* ---- the reference's other solvers of the problem family, on the same
  * device kernels; trace may be NULL.  x0 = 0 as in the reference.
  *   l1g_psd_solve       -> psd_solve    psd.cpp:14-93  (projected steepest descent)

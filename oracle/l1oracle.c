@@ -985,3 +985,14 @@ int orc_shrinkage_solve(const double* K, int64_t n, int64_t p, const double* y, 
   free(x); free(xprev); free(pt); free(r); free(v); free(xn); free(tmp); free(kp); free(mis);
   return ORC_OK;
 }
+
+/* ======================================================================== L1PROBv1 hash */
+/* problem_io.cpp:115-125: FNV-1a 64 (offset basis 1469598103934665603, prime 1099511628211) */
+uint64_t orc_fnv1a(const void* data, int64_t bytes, uint64_t h) {
+  const unsigned char* c = (const unsigned char*)data;
+  for (int64_t i = 0; i < bytes; ++i) {
+    h ^= c[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}

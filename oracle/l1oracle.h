@@ -150,6 +150,9 @@ void orc_gp_get(const orc_gp* st, double* x, double* kx_minus_y, double* grad, d
                 int64_t* k, double* alpha0, int64_t* matvecs);
 void orc_gp_free(orc_gp* st);
 
+/* ---- L1PROBv1 (problem_io.cpp): FNV-1a 64 over serialized bytes, chained from h */
+uint64_t orc_fnv1a(const void* data, int64_t bytes, uint64_t h);
+
 /* ---- harness generators (deterministic, bit-identical to the device generators) ---- */
 void orc_philox4x32(uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 double orc_det_log(double u);

@@ -124,6 +124,7 @@ def lib():
                                     C.POINTER(Result), C.c_void_p, i64]),
             "orc_shrinkage_solve": (i32, [_dp, i64, i64, _dp, dbl, i32, C.POINTER(StopRule), _dp,
                                           C.POINTER(Result), C.c_void_p, i64]),
+            "orc_fnv1a": (C.c_uint64, [C.c_void_p, i64, C.c_uint64]),
             "orc_gp_init": (i32, [_dp, i64, i64, _dp, dbl, C.POINTER(GpConfig), C.c_void_p,
                                   C.POINTER(C.c_void_p)]),
             "orc_gp_iterate": (i32, [C.c_void_p, dbl, C.POINTER(IterRecord),
@@ -493,3 +494,43 @@ def build_problem(spec: ProblemSpec):
         rho = spec.rho_factor * l1norm(x_true)
     return dict(K=K, y=y, x_true=x_true, rho=rho, sigma_hat=sigma_hat, scale=scale,
                 noise_sigma=sig, support=sup)
+
+
+# ------------------------------------------------------------------ L1PROBv1 (problem_io.cpp)
+L1PROB_MAGIC = b"L1PROBv1"
+FNV_BASIS = 1469598103934665603
+
+
+def problem_bytes(K, y, x_true, seed, noise):
+    """The serialized L1PROBv1 bytes (problem_io.cpp:43-60, docs/problem_format.md)."""
+    K = np.ascontiguousarray(K, dtype="<f8")
+    n, p = K.shape
+    head = L1PROB_MAGIC + np.array([n, p, seed], dtype="<u8").tobytes() + \
+        np.array([noise], dtype="<f8").tobytes()
+    return head + K.tobytes() + np.ascontiguousarray(y, dtype="<f8").tobytes() + \
+        np.ascontiguousarray(x_true, dtype="<f8").tobytes()
+
+
+def save_problem(path, K, y, x_true, seed, noise):
+    with open(path, "wb") as f:
+        f.write(problem_bytes(K, y, x_true, seed, noise))
+
+
+def load_problem(path):
+    raw = open(path, "rb").read()
+    if raw[:8] != L1PROB_MAGIC:
+        raise RuntimeError(f"not an L1PROBv1 problem file: {path}")
+    n, p, seed = (int(v) for v in np.frombuffer(raw, dtype="<u8", count=3, offset=8))
+    noise = float(np.frombuffer(raw, dtype="<f8", count=1, offset=32)[0])
+    if n < 1 or p < 1 or len(raw) < 40 + 8 * (n * p + n + p):
+        raise RuntimeError(f"corrupt or truncated problem file: {path}")
+    K = np.frombuffer(raw, dtype="<f8", count=n * p, offset=40).reshape(n, p).copy()
+    y = np.frombuffer(raw, dtype="<f8", count=n, offset=40 + 8 * n * p).copy()
+    x = np.frombuffer(raw, dtype="<f8", count=p, offset=40 + 8 * (n * p + n)).copy()
+    return dict(K=K, y=y, x_true=x, seed=seed, noise_level=noise)
+
+
+def problem_hash(K, y, x_true, seed, noise):
+    b = problem_bytes(K, y, x_true, seed, noise)
+    buf = C.create_string_buffer(b, len(b))
+    return int(lib().orc_fnv1a(C.addressof(buf), len(b), FNV_BASIS))

@@ -49,6 +49,15 @@ def lib(kind="canon"):
         L.ref_shrinkage_solve.argtypes = [C.c_void_p, _dp, C.c_double, C.c_int,
                                           C.POINTER(O.StopRule), _dp, C.POINTER(O.Result),
                                           C.c_void_p, C.c_long]
+        L.ref_problem_save.restype = C.c_int
+        L.ref_problem_save.argtypes = [C.c_char_p, _dp, C.c_long, C.c_long, _dp, _dp,
+                                       C.c_uint64, C.c_double]
+        L.ref_problem_load.restype = C.c_int
+        L.ref_problem_load.argtypes = [C.c_char_p, C.c_long, C.c_long, _dp, _dp, _dp,
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        L.ref_problem_hash.restype = C.c_int
+        L.ref_problem_hash.argtypes = [_dp, C.c_long, C.c_long, _dp, _dp, C.c_uint64,
+                                       C.c_double, C.POINTER(C.c_uint64)]
         _libs[kind] = L
     return _libs[kind]
 
@@ -124,3 +133,29 @@ def project_l1(x, rho, kind="canon"):
     th = C.c_double()
     O._check(lib(kind).ref_project_l1(x, x.size, rho, out, C.byref(th)), "project_l1_ball")
     return out, th.value
+
+
+def problem_save(path, K, y, x_true, seed, noise):
+    K = np.ascontiguousarray(K, dtype=np.float64)
+    n, p = K.shape
+    O._check(lib().ref_problem_save(str(path).encode(), K, n, p, np.ascontiguousarray(y, dtype=np.float64),
+                                    np.ascontiguousarray(x_true, dtype=np.float64), seed, noise),
+             "save_problem")
+
+
+def problem_load(path, n, p):
+    K, y, x = np.empty((n, p)), np.empty(n), np.empty(p)
+    seed, noise = C.c_uint64(), C.c_double()
+    O._check(lib().ref_problem_load(str(path).encode(), n, p, K, y, x, C.byref(seed),
+                                    C.byref(noise)), "load_problem")
+    return dict(K=K, y=y, x_true=x, seed=seed.value, noise_level=noise.value)
+
+
+def problem_hash(K, y, x_true, seed, noise):
+    K = np.ascontiguousarray(K, dtype=np.float64)
+    n, p = K.shape
+    h = C.c_uint64()
+    O._check(lib().ref_problem_hash(K, n, p, np.ascontiguousarray(y, dtype=np.float64),
+                                    np.ascontiguousarray(x_true, dtype=np.float64), seed, noise,
+                                    C.byref(h)), "problem_hash")
+    return h.value

@@ -6,13 +6,16 @@
 // Eigen stand-in in oracle/eigen_shim, producing oracle/_ref/libref_canon.so (canonical
 // reductions, parity) and oracle/_ref/libref_fast.so (OpenMP GEMVs, CPU timing baseline).
 // Structs are layout-compatible with oracle/l1oracle.h.
+#include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <stdexcept>
 
 #include "../oracle/l1oracle.h"
 #include "l1solve/gpss.hpp"
 #include "l1solve/prox.hpp"
+#include "l1solve/problem_io.hpp"
 #include "l1solve/solver.hpp"
 
 using namespace l1solve;
@@ -215,6 +218,56 @@ int ref_shrinkage_solve(ref_op* o, const double* y, double lambda, int accelerat
     return 0;
   } catch (const std::exception& e) {
     return res->status = code(e);
+  }
+}
+
+static GeneratedProblem make_problem(const double* K, long n, long p, const double* y,
+                                     const double* x_true, std::uint64_t seed, double noise) {
+  GeneratedProblem g;
+  g.op = std::make_shared<DenseOperator>(from_row_major(K, n, p));
+  g.y = vec(y, n);
+  g.x_true = vec(x_true, p);
+  g.seed = seed;
+  g.noise_level = noise;
+  return g;
+}
+
+// problem_io.cpp: save / load / hash (L1PROBv1)
+int ref_problem_save(const char* path, const double* K, long n, long p, const double* y,
+                     const double* x_true, std::uint64_t seed, double noise) {
+  try {
+    save_problem(make_problem(K, n, p, y, x_true, seed, noise), path);
+    return 0;
+  } catch (const std::exception& e) {
+    return code(e);
+  }
+}
+
+int ref_problem_load(const char* path, long n, long p, double* K, double* y, double* x_true,
+                     std::uint64_t* seed, double* noise) {
+  try {
+    const GeneratedProblem g = load_problem(path);
+    const Matrix& m = g.op->matrix();
+    if (m.rows() != n || m.cols() != p) return 1;
+    for (long i = 0; i < n; ++i)
+      for (long j = 0; j < p; ++j) K[i * p + j] = m(i, j);
+    std::memcpy(y, g.y.data(), sizeof(double) * static_cast<size_t>(n));
+    std::memcpy(x_true, g.x_true.data(), sizeof(double) * static_cast<size_t>(p));
+    *seed = g.seed;
+    *noise = g.noise_level;
+    return 0;
+  } catch (const std::exception& e) {
+    return code(e);
+  }
+}
+
+int ref_problem_hash(const double* K, long n, long p, const double* y, const double* x_true,
+                     std::uint64_t seed, double noise, std::uint64_t* h) {
+  try {
+    *h = problem_hash(make_problem(K, n, p, y, x_true, seed, noise));
+    return 0;
+  } catch (const std::exception& e) {
+    return code(e);
   }
 }
 

@@ -5,8 +5,9 @@ from .api import (  # noqa: F401
     BacktrackResult, Context, DenseOperator, GpConfig, GpIterationState, GpStepInfo,
     IterationRecord, L1Ball, L1Projection, LinearOperator, MatvecCounter, Objective,
     PenaltyWeight, SolverState, SteplengthChoice, SteplengthState, StopReason, StopRule,
-    alpha0_from_gradient, alpha0_init, backtracking_search, default_context, dot, fista_solve,
-    gp_init, gp_iterate, gpss_solve, ista_solve, psd_solve, l1_norm, lambda_from_rho, lambda_max, linf_norm,
+    GeneratedProblem, alpha0_from_gradient, alpha0_init, backtracking_search, default_context, dot, fista_solve,
+    gp_init, gp_iterate, gpss_solve, ista_solve, load_problem, problem_hash, psd_solve,
+    save_problem, l1_norm, lambda_from_rho, lambda_max, linf_norm,
     project_l1_ball, project_l1_ball_with_threshold, rho_from_lambda, soft_threshold,
     spectral_norm_estimate, squared_norm, steplength_init, steplength_select, to_string)
 

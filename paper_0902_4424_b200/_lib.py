@@ -138,6 +138,13 @@ _SIGS = {
                                 C.POINTER(ResultC), _vp, _i64, ITER_CB, _vp]),
     "l1g_shrinkage_solve": (C.c_int, [_vp, _vp, C.c_double, C.c_int, C.POINTER(StopRuleC), _vp,
                                       C.POINTER(ResultC), _vp, _i64, ITER_CB, _vp]),
+    "l1g_problem_info": (C.c_int, [C.c_char_p, C.POINTER(_i64), C.POINTER(_i64),
+                                   C.POINTER(C.c_uint64), _dp]),
+    "l1g_problem_load": (C.c_int, [_vp, C.c_char_p, _vp, _vp, C.POINTER(C.c_uint64), _dp,
+                                   C.POINTER(_vp)]),
+    "l1g_problem_save": (C.c_int, [C.c_char_p, _vp, _vp, _vp, C.c_uint64, C.c_double]),
+    "l1g_problem_hash": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_double,
+                                   C.POINTER(C.c_uint64)]),
     "l1g_host_alloc": (C.c_int, [_i64, C.POINTER(_vp)]),
     "l1g_host_free": (None, [_vp]),
 }

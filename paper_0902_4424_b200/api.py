@@ -723,3 +723,46 @@ def fista_solve(prob: Objective, lam: PenaltyWeight, stop: StopRule,
                 trace: Optional[list] = None) -> SolverState:
     """Accelerated soft thresholding, shrinkage.cpp:41-118."""
     return _other_solve(prob, lam.value(), 2, stop, cb, trace)
+
+
+# ------------------------------------------------------------------ L1PROBv1 problem files
+@dataclass
+class GeneratedProblem:  # generators.hpp:14-20
+    op: DenseOperator
+    y: np.ndarray
+    x_true: np.ndarray
+    noise_level: float = 0.0
+    seed: int = 0
+
+
+def load_problem(path, ctx: Optional[Context] = None) -> GeneratedProblem:
+    """problem_io.cpp load_problem: K goes straight into the device tiled layout."""
+    ctx = ctx or default_context()
+    lib = L.load()
+    n, p = C.c_int64(), C.c_int64()
+    check(lib.l1g_problem_info(str(path).encode(), C.byref(n), C.byref(p), None, None),
+          "load_problem")
+    y, x = np.empty(n.value), np.empty(p.value)
+    seed, noise, h = C.c_uint64(), C.c_double(), C.c_void_p()
+    check(lib.l1g_problem_load(ctx.h, str(path).encode(), ptr(y), ptr(x), C.byref(seed),
+                               C.byref(noise), C.byref(h)), "load_problem")
+    op = DenseOperator(ctx=ctx, _handle=h.value, _dims=(n.value, p.value))
+    return GeneratedProblem(op, y, x, noise.value, seed.value)
+
+
+def save_problem(prob: GeneratedProblem, path):
+    """problem_io.cpp save_problem (K read back from the device)."""
+    y, x = _f64(prob.y), _f64(prob.x_true)
+    if y.size != prob.op.rows() or x.size != prob.op.cols():
+        raise ValueError("save_problem: inconsistent problem dimensions")
+    check(L.load().l1g_problem_save(str(path).encode(), prob.op.h, ptr(y), ptr(x),
+                                    int(prob.seed), float(prob.noise_level)), "save_problem")
+
+
+def problem_hash(prob: GeneratedProblem) -> int:
+    """problem_io.cpp problem_hash: FNV-1a 64 of the serialized L1PROBv1 bytes."""
+    h = C.c_uint64()
+    check(L.load().l1g_problem_hash(prob.op.h, ptr(_f64(prob.y)), ptr(_f64(prob.x_true)),
+                                    int(prob.seed), float(prob.noise_level), C.byref(h)),
+          "problem_hash")
+    return h.value

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -1103,6 +1104,85 @@ void other_solve(l1g_op* op, const double* y_host, double param, int kind,
 
 }  // namespace
 
+// =============================================================================== L1PROBv1
+// The reference's problem container (problem_io.cpp, docs/problem_format.md): 40-byte header
+// (magic, n, p, seed, noise_level), K row-major, y, x_true; little-endian fp64. Loading
+// streams K straight into the tiled device layout through a pinned double buffer (file read
+// of block i+1 overlaps the copy / tiling of block i); saving and hashing stream it back.
+namespace {
+
+constexpr char kProbMagic[8] = {'L', '1', 'P', 'R', 'O', 'B', 'v', '1'};
+constexpr uint64_t kFnvBasis = 1469598103934665603ull;
+
+uint64_t fnv1a(const void* data, size_t bytes, uint64_t h) {
+  const unsigned char* c = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < bytes; ++i) {
+    h ^= c[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+struct File {
+  FILE* f = nullptr;
+  File(const char* path, const char* mode) : f(std::fopen(path, mode)) {}
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+
+struct ProbHeader {
+  uint64_t n, p, seed;
+  double noise;
+};
+
+ProbHeader read_header(FILE* f, const char* path) {
+  char magic[8];
+  ProbHeader h{};
+  if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, kProbMagic, 8) != 0)
+    throw RuntimeFailure(std::string("not an L1PROBv1 problem file: ") + path);
+  if (std::fread(&h.n, 8, 1, f) != 1 || std::fread(&h.p, 8, 1, f) != 1 ||
+      std::fread(&h.seed, 8, 1, f) != 1 || std::fread(&h.noise, 8, 1, f) != 1 || h.n < 1 ||
+      h.p < 1)
+    throw RuntimeFailure(std::string("corrupt problem header: ") + path);
+  return h;
+}
+
+void header_bytes(const ProbHeader& h, unsigned char out[40]) {
+  std::memcpy(out, kProbMagic, 8);
+  std::memcpy(out + 8, &h.n, 8);
+  std::memcpy(out + 16, &h.p, 8);
+  std::memcpy(out + 24, &h.seed, 8);
+  std::memcpy(out + 32, &h.noise, 8);
+}
+
+// K row blocks of `op` in row-major order, handed to `sink(rows_ptr, r0, rows)` on the host
+template <class Sink>
+void stream_rows_out(l1g_op* op, Sink sink) {
+  const GemvPlan& pl = op->plan;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(pl.n, (int64_t)(64 << 20) / (pl.p * 8)));
+  double* dev = dalloc<double>((size_t)chunk * pl.p);
+  double* host = nullptr;
+  L1G_CUDA(cudaHostAlloc(&host, (size_t)chunk * pl.p * 8, cudaHostAllocDefault));
+  try {
+    for (int64_t r0 = 0; r0 < pl.n; r0 += chunk) {
+      const int64_t rows = std::min<int64_t>(chunk, pl.n - r0);
+      untile_rows(op->K, pl, dev, r0, rows, op->c->stream);
+      L1G_CUDA(cudaMemcpyAsync(host, dev, rows * pl.p * 8, cudaMemcpyDeviceToHost, op->c->stream));
+      L1G_CUDA(cudaStreamSynchronize(op->c->stream));
+      sink(host, r0, rows);
+    }
+  } catch (...) {
+    cudaFreeHost(host);
+    dfree(dev);
+    throw;
+  }
+  cudaFreeHost(host);
+  dfree(dev);
+}
+
+}  // namespace
+
 // =============================================================================== C ABI
 extern "C" {
 
@@ -1860,6 +1940,127 @@ int l1g_shrinkage_solve(l1g_op* op, const double* y, double lambda, int accelera
                         l1g_iter_record* trace, int64_t cap, l1g_iter_cb cb, void* user) {
   return guarded([&] {
     other_solve(op, y, lambda, accelerated ? 2 : 1, *stop, x_out, res, trace, cap, cb, user);
+  });
+}
+
+int l1g_problem_info(const char* path, int64_t* n, int64_t* p, uint64_t* seed, double* noise) {
+  return guarded([&] {
+    File f(path, "rb");
+    if (!f.f) throw RuntimeFailure(std::string("cannot open problem file: ") + path);
+    const ProbHeader h = read_header(f.f, path);
+    if (n) *n = (int64_t)h.n;
+    if (p) *p = (int64_t)h.p;
+    if (seed) *seed = h.seed;
+    if (noise) *noise = h.noise;
+  });
+}
+
+int l1g_problem_load(l1g_ctx* c, const char* path, double* y, double* x_true, uint64_t* seed,
+                     double* noise, l1g_op** out) {
+  return guarded([&] {
+    *out = nullptr;
+    File f(path, "rb");
+    if (!f.f) throw RuntimeFailure(std::string("cannot open problem file: ") + path);
+    const ProbHeader h = read_header(f.f, path);
+    const int64_t n = (int64_t)h.n, p = (int64_t)h.p;
+    std::fseek(f.f, 0, SEEK_END);
+    const long long size = std::ftell(f.f);
+    if (size < 40 + 8LL * (n * p + n + p))
+      throw RuntimeFailure(std::string("truncated problem file: ") + path);
+    std::fseek(f.f, 40, SEEK_SET);
+    l1g_op* op = op_alloc(c, n, p);
+    double *host[2] = {nullptr, nullptr}, *dev[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    try {
+      const GemvPlan& pl = op->plan;
+      const int64_t chunk = std::max<int64_t>(TR, ((int64_t)(64 << 20) / (p * 8)) / TR * TR);
+      for (int i = 0; i < 2; ++i) {
+        L1G_CUDA(cudaHostAlloc(&host[i], (size_t)chunk * p * 8, cudaHostAllocDefault));
+        dev[i] = dalloc<double>((size_t)chunk * p);
+        L1G_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+      }
+      int b = 0;
+      for (int64_t r0 = 0; r0 < n; r0 += chunk, b ^= 1) {
+        const int64_t rows = std::min<int64_t>(chunk, n - r0);
+        L1G_CUDA(cudaEventSynchronize(done[b]));  // buffer b's previous copy has finished
+        if (std::fread(host[b], 8, (size_t)(rows * p), f.f) != (size_t)(rows * p))
+          throw RuntimeFailure(std::string("short read of K: ") + path);
+        L1G_CUDA(cudaMemcpyAsync(dev[b], host[b], rows * p * 8, cudaMemcpyHostToDevice, c->stream));
+        tile_rows_from_rowmajor(op->K, pl, dev[b], r0, pad_to(rows, TR), c->stream);
+        L1G_CUDA(cudaEventRecord(done[b], c->stream));
+      }
+      L1G_CUDA(cudaStreamSynchronize(c->stream));
+      std::vector<double> tmp;
+      double* yy = y;
+      double* xx = x_true;
+      if (!yy) {
+        tmp.resize((size_t)n);
+        yy = tmp.data();
+      }
+      if (std::fread(yy, 8, (size_t)n, f.f) != (size_t)n)
+        throw RuntimeFailure(std::string("truncated problem file: ") + path);
+      std::vector<double> tmp2;
+      if (!xx) {
+        tmp2.resize((size_t)p);
+        xx = tmp2.data();
+      }
+      if (std::fread(xx, 8, (size_t)p, f.f) != (size_t)p)
+        throw RuntimeFailure(std::string("truncated problem file: ") + path);
+    } catch (...) {
+      for (int i = 0; i < 2; ++i) {
+        if (host[i]) cudaFreeHost(host[i]);
+        dfree(dev[i]);
+        if (done[i]) cudaEventDestroy(done[i]);
+      }
+      l1g_op_destroy(op);
+      throw;
+    }
+    for (int i = 0; i < 2; ++i) {
+      cudaFreeHost(host[i]);
+      dfree(dev[i]);
+      cudaEventDestroy(done[i]);
+    }
+    if (seed) *seed = h.seed;
+    if (noise) *noise = h.noise;
+    *out = op;
+  });
+}
+
+int l1g_problem_save(const char* path, l1g_op* op, const double* y, const double* x_true,
+                     uint64_t seed, double noise) {
+  return guarded([&] {
+    if (!op) throw InvalidArgument("save_problem: problem has no operator");
+    set_device(op->c);
+    File f(path, "wb");
+    if (!f.f) throw RuntimeFailure(std::string("cannot open problem file for writing: ") + path);
+    const GemvPlan& pl = op->plan;
+    unsigned char head[40];
+    header_bytes(ProbHeader{(uint64_t)pl.n, (uint64_t)pl.p, seed, noise}, head);
+    bool ok = std::fwrite(head, 1, 40, f.f) == 40;
+    stream_rows_out(op, [&](const double* rows, int64_t, int64_t cnt) {
+      ok = ok && std::fwrite(rows, 8, (size_t)(cnt * pl.p), f.f) == (size_t)(cnt * pl.p);
+    });
+    ok = ok && std::fwrite(y, 8, (size_t)pl.n, f.f) == (size_t)pl.n;
+    ok = ok && std::fwrite(x_true, 8, (size_t)pl.p, f.f) == (size_t)pl.p;
+    ok = ok && std::fflush(f.f) == 0;
+    if (!ok) throw RuntimeFailure(std::string("short write while saving problem: ") + path);
+  });
+}
+
+int l1g_problem_hash(l1g_op* op, const double* y, const double* x_true, uint64_t seed,
+                     double noise, uint64_t* hash) {
+  return guarded([&] {
+    set_device(op->c);
+    const GemvPlan& pl = op->plan;
+    unsigned char head[40];
+    header_bytes(ProbHeader{(uint64_t)pl.n, (uint64_t)pl.p, seed, noise}, head);
+    uint64_t h = fnv1a(head, 40, kFnvBasis);
+    stream_rows_out(op, [&](const double* rows, int64_t, int64_t cnt) {
+      h = fnv1a(rows, (size_t)(cnt * pl.p) * 8, h);
+    });
+    h = fnv1a(y, (size_t)pl.n * 8, h);
+    h = fnv1a(x_true, (size_t)pl.p * 8, h);
+    *hash = h;
   });
 }
 

@@ -14,6 +14,7 @@
 
 #include "l1g.h"
 #include "l1solve/gpss.hpp"
+#include "l1solve/problem_io.hpp"
 
 namespace l1solve {
 
@@ -671,6 +672,34 @@ SolverState other_solve(const Objective& prob, double param, int kind, const Sto
   return state_from(res, std::move(x));
 }
 }  // namespace
+
+void save_problem(const GeneratedProblem& prob, const std::filesystem::path& path) {
+  if (!prob.op) throw std::invalid_argument("save_problem: problem has no operator");
+  if (prob.y.size() != prob.op->rows() || prob.x_true.size() != prob.op->cols())
+    throw std::invalid_argument("save_problem: inconsistent problem dimensions");
+  check(l1g_problem_save(path.string().c_str(), prob.op->handle(), prob.y.data(),
+                         prob.x_true.data(), prob.seed, prob.noise_level));
+}
+
+GeneratedProblem load_problem(const std::filesystem::path& path) {
+  int64_t n = 0, p = 0;
+  check(l1g_problem_info(path.string().c_str(), &n, &p, nullptr, nullptr));
+  GeneratedProblem g;
+  g.y = Vector(n);
+  g.x_true = Vector(p);
+  l1g_op* op = nullptr;
+  check(l1g_problem_load(ctx(), path.string().c_str(), g.y.data(), g.x_true.data(), &g.seed,
+                         &g.noise_level, &op));
+  g.op = std::make_shared<DenseOperator>(op, n, p);
+  return g;
+}
+
+std::uint64_t problem_hash(const GeneratedProblem& prob) {
+  std::uint64_t h = 0;
+  check(l1g_problem_hash(prob.op->handle(), prob.y.data(), prob.x_true.data(), prob.seed,
+                         prob.noise_level, &h));
+  return h;
+}
 
 SolverState psd_solve(const Objective& prob, const L1Ball& ball, const StopRule& stop,
                       const IterationCallback& cb) {

@@ -4,10 +4,12 @@
 // each checked against closed forms or against the other entry points.
 #include <cmath>
 #include <cstdio>
+#include <filesystem>
 #include <stdexcept>
 #include <vector>
 
 #include "l1solve/gpss.hpp"
+#include "l1solve/problem_io.hpp"
 
 using namespace l1solve;
 
@@ -148,6 +150,30 @@ int main() {
     EXPECT(si.matvecs.count == 80 && sf.matvecs.count == 80);
     EXPECT(sf.objective <= si.objective * 1.5);
     EXPECT_THROW(ista_solve(obj, PenaltyWeight(-1.0), st3), std::invalid_argument);
+  }
+
+  // L1PROBv1 round trip through the drop-in problem_io (problem_io.cpp)
+  {
+    GeneratedProblem g;
+    Matrix km = Matrix::Zero(3, 4);
+    for (Index i = 0; i < 3; ++i)
+      for (Index j = 0; j < 4; ++j) km(i, j) = 1.0 + i * 4 + j;
+    g.op = std::make_shared<DenseOperator>(km);
+    g.y = Vector{1.0, 2.0, 3.0};
+    g.x_true = Vector{0.0, 0.5, 0.0, -1.0};
+    g.seed = 123;
+    g.noise_level = 0.25;
+    const std::filesystem::path path = std::filesystem::temp_directory_path() / "l1g_dropin.l1prob";
+    save_problem(g, path);
+    EXPECT(std::filesystem::file_size(path) == 40 + 8 * (12 + 3 + 4));
+    const GeneratedProblem b = load_problem(path);
+    const Matrix kb = b.op->matrix();
+    bool same = kb.rows() == 3 && kb.cols() == 4;
+    for (Index i = 0; same && i < 3; ++i)
+      for (Index j = 0; j < 4; ++j) same = same && kb(i, j) == km(i, j);
+    EXPECT(same && b.seed == 123 && b.noise_level == 0.25 && b.y[2] == 3.0 && b.x_true[3] == -1.0);
+    EXPECT(problem_hash(b) == problem_hash(g));
+    std::filesystem::remove(path);
   }
 
   std::printf("%d passed, %d failed\n", g_pass, g_fail);

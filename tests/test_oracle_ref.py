@@ -104,3 +104,29 @@ def test_psd_ista_fista_bit_identical(spec, iters, solver):
         for a, b in zip(reco, recr):
             for f in OTHER_FIELDS:
                 assert same(a[f], b[f]), (a["k"], f, a[f], b[f])
+
+
+def test_l1prob_format_matches_reference(tmp_path):
+    """problem_io.cpp: the oracle's L1PROBv1 writer / reader / FNV-1a hash against the
+    reference's own save_problem / load_problem / problem_hash."""
+    rng = np.random.default_rng(9)
+    for (n, p) in [(3, 4), (9, 21), (77, 301)]:
+        K, y, x = rng.normal(size=(n, p)), rng.normal(size=n), rng.normal(size=p)
+        seed, noise = int(rng.integers(0, 2**63)), float(rng.random())
+        a, b = tmp_path / "a.l1prob", tmp_path / "b.l1prob"
+        O.save_problem(a, K, y, x, seed, noise)
+        R.problem_save(b, K, y, x, seed, noise)
+        assert a.read_bytes() == b.read_bytes()
+        assert len(a.read_bytes()) == 40 + 8 * (n * p + n + p)
+        back = R.problem_load(a, n, p)
+        assert np.array_equal(back["K"], K) and np.array_equal(back["y"], y)
+        assert np.array_equal(back["x_true"], x)
+        assert back["seed"] == seed and back["noise_level"] == noise
+        mine = O.load_problem(b)
+        assert np.array_equal(mine["K"], K) and mine["seed"] == seed
+        assert O.problem_hash(K, y, x, seed, noise) == R.problem_hash(K, y, x, seed, noise)
+    # documented offsets (test_operator.cpp:176-200): K(0,1) at byte 48
+    K = np.arange(12.0).reshape(3, 4)
+    O.save_problem(tmp_path / "c.l1prob", K, np.zeros(3), np.zeros(4), 123, 0.0)
+    raw = (tmp_path / "c.l1prob").read_bytes()
+    assert raw[:8] == b"L1PROBv1" and np.frombuffer(raw, "<f8", 1, 48)[0] == K[0, 1]
