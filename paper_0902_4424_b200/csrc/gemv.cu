@@ -597,7 +597,7 @@ constexpr int SP_NT = SP_NCW * 32 * SP_RPW;  // slot columns (one per row)
 constexpr int SP_MAXT = 16;    // tiles per range (<= 1024 columns, levels 1..10)
 constexpr int SP_W = SP_MAXT * TC;
 constexpr int SP_LVLS = 11;
-constexpr int SP_PF = 8;       // loads in flight per consumer thread
+constexpr int SP_PF = 16;      // loads in flight per consumer thread
 struct SpEnt {
   int coff;  // (tile column block) * TILE + j * 32
   int meta;  // [0,5) level (31 = last leaf), [5,9) column swizzle, [9,20) open slots absorbed
@@ -817,8 +817,13 @@ GemvPlan make_plan(int64_t n, int64_t p, int sm_count) {
   pl.nrr = (int)cdiv(pl.nrb, b);
   // sparse forward: ranges of <= 1024 columns, narrower when that leaves SMs idle
   const int64_t nrq = cdiv(pl.nrb, SP_RB);
+  static const int sp_waves = [] {
+    const char* e = getenv("L1G_SP_WAVES");
+    const int v = e ? atoi(e) : 3;
+    return v > 0 ? v : 3;
+  }();
   int t = SP_MAXT;
-  while (t > 1 && nrq * cdiv(pl.ncb, t) < 3LL * sm_count) t >>= 1;
+  while (t > 1 && nrq * cdiv(pl.ncb, t) < (int64_t)sp_waves * sm_count) t >>= 1;
   pl.sp_tiles = t;
   pl.sp_ncr = (int)cdiv(pl.ncb, t);
   pl.grid = sm_count;
