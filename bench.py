@@ -184,12 +184,36 @@ def host_problem(spec_name):
     return K, y, float(np.abs(x_true).sum())
 
 
+def host_batch_problem0():
+    """C5 (BASELINE configs[4]) problem 0 on the host with the oracle generators (the same
+    streams harness.build_batch_problem uses on the device)."""
+    from oracle import oracle as O
+    from paper_0902_4424_b200 import harness as H
+    c = H.C5
+    n, p, seed = c["n"], c["p"], c["seed"]
+    K = O.gaussian_matrix(seed, n, p)
+    sigma = sigma_fixture("C5")
+    if sigma is None:
+        sigma, _ = O.spectral_norm(K, 8, 1e-8)
+    O.lib().orc_scale(K, K.size, 0.9 / sigma)
+    sj = 1000 * seed
+    spec = O.ProblemSpec("gaussian", n, p, c["nnz"], sj, "normal", c["noise"], "abs")
+    x = np.zeros(p)
+    x[O.sample_support(sj, 1, p, c["nnz"])] = O.x_true_values(spec, c["nnz"])
+    y = O.apply(K, x) + c["noise"] * O.fill_normal(sj, 2, 0, n)
+    return K, y, 0.2 * O.l1norm(x), c["batch"]
+
+
 def run_reference(args, world, rank, pg):
     """--impl reference: the reference CPU path on this box's host cores."""
     if rank != 0:
         return
     cfgname = args.config
-    K, y, rho = host_problem(cfgname)
+    scale = 1
+    if cfgname == "C5":  # problems are solved one by one there: lockstep unit = B problems
+        K, y, rho, scale = host_batch_problem0()
+    else:
+        K, y, rho = host_problem(cfgname)
     from oracle import ref as R
     n, p = K.shape
     # bounded sample per step: enough iterations for ~5 s of CPU work
@@ -203,8 +227,10 @@ def run_reference(args, world, rank, pg):
         times.append(dt)
         total_it += itn
     total_t = sum(times)
-    v = total_it / total_t
+    v = total_it / total_t / scale
     sample = (f"{per_step} GPSS iterations per step of {cfgname} ({n}x{p}) from x0=0, "
+              + (f"problem 0 of {scale} solved alone, scaled to lockstep iterations (/{scale}), "
+                 if scale > 1 else "") +
               f"reference gpss.cpp/prox.cpp/linear_operator.cpp via oracle/_ref "
               f"({'OpenMP Eigen stand-in' if kind == 'reference' else 'C port'})")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,

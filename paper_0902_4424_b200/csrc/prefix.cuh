@@ -137,7 +137,18 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
   }
   double S_prev = ss.head[H - 1];
   long long i0 = H, window = 2 * H;
+#ifdef L1G_PREFIX_TRACE
+  int ntr = 0;
+#endif
   while (i0 < L) {
+#ifdef L1G_PREFIX_TRACE
+    if (threadIdx.x == 0 && ntr < 64) {
+      L1G_PREFIX_TRACE[3 * ntr] = clock64();
+      L1G_PREFIX_TRACE[3 * ntr + 1] = i0;
+      L1G_PREFIX_TRACE[3 * ntr + 2] = window;
+      ++ntr;
+    }
+#endif
     if (!(S_prev >= 0x1.0p-960)) {  // (sub)tiny running sum: plain scalar step, uniform
       const double S = add(S_prev, c[i0]);
       if (!passes(c[i0], S, rho, i0 + 1)) {

@@ -10,6 +10,10 @@
 #include <random>
 #include <vector>
 
+#ifdef TRACE
+__device__ long long g_trace[192];
+#define L1G_PREFIX_TRACE g_trace
+#endif
 #include "prefix.cuh"
 
 using namespace l1g;
@@ -89,6 +93,16 @@ int main() {
       cudaMemcpy(&ff2, dff, 8, cudaMemcpyDeviceToHost);
       cudaMemcpy(&s2, dsb, 8, cudaMemcpyDeviceToHost);
       cudaMemcpy(&cy2, dcy, 8, cudaMemcpyDeviceToHost);
+#ifdef TRACE
+      {
+        long long tr[192];
+        cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr));
+        for (int e = 0; e < 64 && tr[3 * e] != 0; ++e)
+          std::printf("   epoch %d: t=%lld i0=%lld window=%lld\n", e, tr[3 * e] - tr[0], tr[3 * e + 1], tr[3 * e + 2]);
+        long long z[192] = {0};
+        cudaMemcpyToSymbol(g_trace, z, sizeof(z));
+      }
+#endif
       std::printf("L=%6lld rho=%.2f*sum  parallel: ff=%lld cycles=%lld | sequential: ff=%lld cycles=%lld | %s\n",
                   L, frac, ff1, cy1, ff2, cy2, (ff1 == ff2 && s1 == s2) ? "equal" : "MISMATCH");
       cudaFree(dc);
