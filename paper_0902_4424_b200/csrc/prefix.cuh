@@ -57,19 +57,68 @@ constexpr int PREFIX_MAXW = 32;  // warps per block
 struct ScanShared {
   double head[PREFIX_HEAD];
   long long wsum[PREFIX_MAXW];
+  long long wd0[PREFIX_MAXW], wd1[PREFIX_MAXW];
+  int wp[PREFIX_MAXW];
   long long wev[PREFIX_MAXW];
   long long ev, nb;
   int kind;
   double sb;
+  int epochs;  // telemetry: windows scanned by the last call
 };
+
+// A run of positions as a function of the parity of the running grid count N it starts
+// from: a rounding tie (m an odd multiple of half a grid step) rounds N + q + 1/2 to the
+// even neighbour, so it adds q or q + 1 depending on N's parity and always leaves N even;
+// other positions add their fixed q.  (d0, p0) / (d1, p1): increment and final parity for
+// an even / odd start.  Composition is associative, so ties ride along the prefix scan.
+struct ParSeg {
+  long long d0, d1;
+  int p0, p1;
+};
+__device__ __forceinline__ ParSeg seg_then(const ParSeg& A, const ParSeg& B) {
+  ParSeg C;
+  C.d0 = A.d0 + (A.p0 ? B.d1 : B.d0);
+  C.p0 = A.p0 ? B.p1 : B.p0;
+  C.d1 = A.d1 + (A.p1 ? B.d1 : B.d0);
+  C.p1 = A.p1 ? B.p1 : B.p0;
+  return C;
+}
+__device__ __forceinline__ ParSeg seg_shfl_up(const ParSeg& v, int o) {
+  ParSeg r;
+  r.d0 = __shfl_up_sync(0xffffffffu, v.d0, o);
+  r.d1 = __shfl_up_sync(0xffffffffu, v.d1, o);
+  const int pk = __shfl_up_sync(0xffffffffu, v.p0 | (v.p1 << 1), o);
+  r.p0 = pk & 1;
+  r.p1 = pk >> 1;
+  return r;
+}
+__device__ __forceinline__ ParSeg seg_shfl(const ParSeg& v, int src) {
+  ParSeg r;
+  r.d0 = __shfl_sync(0xffffffffu, v.d0, src);
+  r.d1 = __shfl_sync(0xffffffffu, v.d1, src);
+  const int pk = __shfl_sync(0xffffffffu, v.p0 | (v.p1 << 1), src);
+  r.p0 = pk & 1;
+  r.p1 = pk >> 1;
+  return r;
+}
+// inclusive scan of per-lane segments over the warp (earlier lanes first)
+__device__ __forceinline__ ParSeg seg_warp_scan(ParSeg v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const ParSeg y = seg_shfl_up(v, o);
+    if (lane >= o) v = seg_then(y, v);
+  }
+  return v;
+}
 
 // Exact emulation of the reference's sequential cumulative sum (prox.cpp:44-51) over the
 // sorted candidates c[0..L) (descending, >= 0), fused with its break test.  While the
 // running sum S stays inside one binade [2^e, 2^(e+1)), every fl(S + m) is S plus m rounded
 // to the fixed grid u = 2^(e-52) (round-to-nearest), so the prefix sums of an epoch are one
-// exact integer prefix scan of grid counts (computed from the mantissa bits).  The first
-// position whose sum leaves the binade, or whose rounding is a tie (decided by the parity
-// of S), is done as one IEEE addition and starts the next epoch.  The short epochs at the
+// exact integer prefix scan of grid counts (computed from the mantissa bits; rounding ties,
+// decided by the parity of the running count, ride along the scan as parity-dependent
+// segments).  The first position whose sum leaves the binade is done as one IEEE addition
+// and starts the next epoch.  The short epochs at the
 // top are cheaper as the reference's own sequential sum (one dependent add per position);
 // after PREFIX_HEAD positions the block scans windows sized to the (doubling) epochs.
 // Returns the first failing index ff (L if none) and S_{ff-1} (the sum whose candidate is
@@ -140,7 +189,9 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
 #ifdef L1G_PREFIX_TRACE
   int ntr = 0;
 #endif
+  if (threadIdx.x == 0) ss.epochs = 0;
   while (i0 < L) {
+    if (threadIdx.x == 0) ++ss.epochs;
 #ifdef L1G_PREFIX_TRACE
     if (threadIdx.x == 0 && ntr < 64) {
       L1G_PREFIX_TRACE[3 * ntr] = clock64();
@@ -167,12 +218,14 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
     const long long sbits = __double_as_longlong(S_prev);
     const int be = (int)(sbits >> 52);
     const long long base_q = (sbits & ((1LL << 52) - 1)) | (1LL << 52);  // S_prev / u
-    // pass 1: grid counts of my positions
+    // pass 1: grid counts of my positions (a tie counted at its floor)
     long long tot = 0;
+    int tie_here = 0;
 #pragma unroll 4
     for (long long i = p0; i < p1; ++i) {
       bool t;
       tot += grid_count(c[i], be, &t);
+      tie_here |= t;
     }
     long long inc = tot;
 #pragma unroll
@@ -181,9 +234,10 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
       if (lane >= o) inc += y;
     }
     if (lane == 31) ss.wsum[warp] = inc;
-    __syncthreads();
-    long long off, btot;
-    {  // warp totals: inclusive scan over the warps by shuffles
+    const int any_tie = __syncthreads_or(tie_here);
+    const int par0 = (int)(base_q & 1);
+    long long start, btot;
+    if (!any_tie) {  // warp totals: inclusive scan over the warps by shuffles
       const long long x = lane < NW ? ss.wsum[lane] : 0;
       long long sc = x;
 #pragma unroll
@@ -192,11 +246,51 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
         if (lane >= o) sc += y;
       }
       btot = __shfl_sync(FULL, sc, 31);
-      off = inc - tot + (warp > 0 ? __shfl_sync(FULL, sc, warp - 1) : 0);
+      start = inc - tot + (warp > 0 ? __shfl_sync(FULL, sc, warp - 1) : 0);
+    } else {  // rounding ties in the window: scan parity-dependent segments instead
+      ParSeg me = {0, 0, 0, 1};
+      for (long long i = p0; i < p1; ++i) {
+        bool tie;
+        const long long q = grid_count(c[i], be, &tie);
+        if (!tie) {
+          me.d0 += q;
+          me.d1 += q;
+          me.p0 ^= (int)(q & 1);
+          me.p1 ^= (int)(q & 1);
+        } else {
+          me.d0 += q + ((me.p0 + q) & 1);
+          me.d1 += q + ((me.p1 + q) & 1);
+          me.p0 = 0;
+          me.p1 = 0;
+        }
+      }
+      const ParSeg incl = seg_warp_scan(me, lane);
+      if (lane == 31) {
+        ss.wd0[warp] = incl.d0;
+        ss.wd1[warp] = incl.d1;
+        ss.wp[warp] = incl.p0 | (incl.p1 << 1);
+      }
+      __syncthreads();
+      ParSeg t = {0, 0, 0, 1};
+      if (lane < NW) {
+        t.d0 = ss.wd0[lane];
+        t.d1 = ss.wd1[lane];
+        t.p0 = ss.wp[lane] & 1;
+        t.p1 = ss.wp[lane] >> 1;
+      }
+      const ParSeg ti = seg_warp_scan(t, lane);
+      const ParSeg total = seg_shfl(ti, 31);
+      const ParSeg wx = seg_shfl(ti, warp > 0 ? warp - 1 : 0);
+      const ParSeg wpre = warp > 0 ? wx : ParSeg{0, 0, 0, 1};
+      ParSeg lx = seg_shfl_up(incl, 1);
+      if (lane == 0) lx = ParSeg{0, 0, 0, 1};
+      const ParSeg before = seg_then(wpre, lx);
+      btot = par0 ? total.d1 : total.d0;
+      start = par0 ? before.d1 : before.d0;
     }
-    // pass 2: exact sums and tests; my first event (1 failure, 2 binade exit or tie,
+    // pass 2: exact sums and tests; my first event (1 failure, 2 binade exit,
     // 3 test too close to call), branch-free so positions overlap
-    long long N = base_q + off, my_ev = LLONG_MAX, my_n = 0;
+    long long N = base_q + start, my_ev = LLONG_MAX, my_n = 0;
     int kind = 0;
     double kd = (double)(p0 + 1);
 #pragma unroll 4
@@ -204,8 +298,8 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
       const double m = c[i];
       bool tie;
       const long long q = grid_count(m, be, &tie);
-      const long long Nn = N + q;
-      const int stt = (tie || Nn >= TWO53) ? 2 : quick_test(m, from_grid(Nn, be), rho, kd);
+      const long long Nn = N + q + (tie ? ((N + q) & 1) : 0);
+      const int stt = Nn >= TWO53 ? 2 : quick_test(m, from_grid(Nn, be), rho, kd);
       const bool take = stt != 0 && my_ev == LLONG_MAX;
       my_ev = take ? i : my_ev;
       kind = take ? stt : kind;
@@ -236,6 +330,9 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
     const long long ev = ss.ev, nb = ss.nb;
     const int evk = ss.kind;
     __syncthreads();
+#ifdef L1G_PREFIX_TRACE
+    if (threadIdx.x == 0 && ntr > 0 && ntr <= 64) L1G_PREFIX_TRACE[3 * (ntr - 1) + 2] += 1000000LL * evk;
+#endif
     const double sb = from_grid(nb, be);  // S_{ev-1}
     if (evk == 1) {
       *s_before = sb;
@@ -243,7 +340,8 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
     }
     if (evk == 3) {  // exact test with the division; on success the epoch goes on
       bool t;
-      const double Se = from_grid(nb + grid_count(c[ev], be, &t), be);
+      const long long qe = grid_count(c[ev], be, &t);
+      const double Se = from_grid(nb + qe + (t ? ((nb + qe) & 1) : 0), be);
       if (!passes(c[ev], Se, rho, ev + 1)) {
         *s_before = sb;
         return ev;
@@ -252,14 +350,15 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
       i0 = ev + 1;
       continue;
     }
-    // one IEEE addition at the binade exit / tie, evaluated by every thread alike
+    // one IEEE addition at the binade exit, evaluated by every thread alike
     const double S = add(sb, c[ev]);
     if (!passes(c[ev], S, rho, ev + 1)) {
       *s_before = sb;
       return ev;
     }
-    // the next epoch is about as long as the whole prefix so far: size the window for it
-    window = ((ev + 1 + 31) >> 5) << 5;
+    // the running sum doubles again after a bit more than the prefix so far (candidates
+    // decrease): size the window to twice the prefix, overshooting rather than re-scanning
+    window = ((2 * (ev + 1) + 31) >> 5) << 5;
     S_prev = S;
     i0 = ev + 1;
   }

@@ -621,6 +621,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
               mark(4);
               double s_before = 0.0;
               const long long ff = prefix_break(c, L, rho, scan_sh, &s_before);
+              count(20, (double)scan_sh.epochs);
               if (tid == 0) {
                 sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
                 sh.dec = (ff == L && next >= 0.0) ? 1 : 0;
@@ -669,6 +670,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           mark(4);
           double s_before = 0.0;
           const long long ff = prefix_break(c, L, rho, scan_sh, &s_before);
+          count(20, (double)scan_sh.epochs);
           if (tid == 0) {
             // theta = candidate of the last passing index (prox.cpp:47-50); 0 if none passed
             sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
