@@ -38,13 +38,27 @@ constexpr int BW = 128;   // problems per CTA (B is padded to a multiple)
 constexpr int BT = 256;   // 8 warps: 2 (rows / columns) x 4 (problems), 32 x 32 each
 constexpr int VPAD = 4;   // row padding (doubles) of staged problem vectors
 
+// K tiles are restaged column-major with a 36-double column pitch: element (i, j) of a
+// tile sits at j*KP + (i ^ (col_swz(j) & 1)).  The 16-byte cp.async chunks of the global
+// column runs (two adjacent rows) land whole, and both fragment patterns -- 8 rows x 4
+// columns (forward) and 8 columns x 4 rows (adjoint) -- touch every 8-byte bank pair at
+// most twice (KP = 36 = 4 mod 16), the minimum for 32 64-bit lanes.
+constexpr int KP = 36;
+constexpr int KT_S = TC * KP;  // doubles per restaged tile
+__device__ __forceinline__ int kpos(int i, int j) { return j * KP + (i ^ (col_swz(j) & 1)); }
+// 16-byte chunk q (0..1023) of a tile: global offset 2q, restaged offset
+__device__ __forceinline__ int kchunk_dst(int q) {
+  const int j = q >> 4, k2 = (q & 15) * 2;
+  return j * KP + (k2 ^ (col_swz(j) & ~1));
+}
+
 // forward: K rows 64 (two tiles) x 64 columns, D chunk 128 problems x 64 columns
-constexpr int F_KT = 2 * TILE;
+constexpr int F_KT = 2 * KT_S;
 constexpr int F_VS = BW * (TC + VPAD);
 constexpr int F_STAGE = F_KT + F_VS;
 constexpr int F_STAGES = 2;
 // adjoint: one tile 32 rows x 64 columns, R chunk 128 problems x 32 rows
-constexpr int A_KT = TILE;
+constexpr int A_KT = KT_S;
 constexpr int A_VS = BW * (TR + VPAD);
 constexpr int A_STAGE = A_KT + A_VS;
 constexpr int A_STAGES = 3;
@@ -69,8 +83,8 @@ __global__ void __launch_bounds__(BT, 1) bfwd_kernel(const BGemmArgs a) {
     double* vs = ks + F_KT;
     const int64_t cb = c_begin + c;
     for (int q = tid; q < TILE; q += BT) {  // two tiles = 2 x 1024 chunks of 16 bytes
-      const int tile = q >> 10, off = (q & 1023) * 2;
-      cp16(ks + tile * TILE + off, a.K + tile_offset(rb0 + tile, cb, a.ncb) + off);
+      const int tile = q >> 10, c = q & 1023;
+      cp16(ks + tile * KT_S + kchunk_dst(c), a.K + tile_offset(rb0 + tile, cb, a.ncb) + 2 * c);
     }
     for (int q = tid; q < BW * (TC / 2); q += BT) {
       const int b = q >> 5, kq = (q & 31) * 2;
@@ -89,15 +103,14 @@ __global__ void __launch_bounds__(BT, 1) bfwd_kernel(const BGemmArgs a) {
     cp_commit();
     cp_wait<1>();
     __syncthreads();
-    const double* ks = sm + (c & 1) * F_STAGE + wr * TILE;
+    const double* ks = sm + (c & 1) * F_STAGE + wr * KT_S;
     const double* vs = sm + (c & 1) * F_STAGE + F_KT + (wc * 32) * (TC + VPAD);
 #pragma unroll 4
     for (int kk = 0; kk < TC; kk += 4) {
       const int col = kk + t;
-      const int sw = col_swz(col);
       double av[4], bv[4];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) av[mt] = ks[col * 32 + ((mt * 8 + g) ^ sw)];
+      for (int mt = 0; mt < 4; ++mt) av[mt] = ks[kpos(mt * 8 + g, col)];
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) bv[nt] = vs[(nt * 8 + g) * (TC + VPAD) + col];
 #pragma unroll
@@ -135,7 +148,8 @@ __global__ void __launch_bounds__(BT, 1) badj_kernel(const BGemmArgs a) {
     double* ks = sm + st * A_STAGE;
     double* vs = ks + A_KT;
     const int64_t rb = r_begin + c;
-    for (int q = tid; q < TILE / 2; q += BT) cp16(ks + q * 2, a.K + tile_offset(rb, cb, a.ncb) + q * 2);
+    for (int q = tid; q < TILE / 2; q += BT)
+      cp16(ks + kchunk_dst(q), a.K + tile_offset(rb, cb, a.ncb) + q * 2);
     for (int q = tid; q < BW * (TR / 2); q += BT) {
       const int b = q >> 4, kq = (q & 15) * 2;
       cp16(vs + b * (TR + VPAD) + kq, a.V + (int64_t)(b0 + b) * a.vstride + rb * TR + kq);
@@ -164,8 +178,7 @@ __global__ void __launch_bounds__(BT, 1) badj_kernel(const BGemmArgs a) {
       double av[4], bv[4];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) {
-        const int col = wm * 32 + mt * 8 + g;
-        av[mt] = ks[col * 32 + (row ^ col_swz(col))];
+        av[mt] = ks[kpos(row, wm * 32 + mt * 8 + g)];
       }
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) bv[nt] = vs[(nt * 8 + g) * (TR + VPAD) + row];
