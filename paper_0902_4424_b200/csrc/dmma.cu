@@ -57,11 +57,12 @@ constexpr int F_KT = 2 * KT_S;
 constexpr int F_VS = BW * (TC + VPAD);
 constexpr int F_STAGE = F_KT + F_VS;
 constexpr int F_STAGES = 2;
-// adjoint: one tile 32 rows x 64 columns, R chunk 128 problems x 32 rows
-constexpr int A_KT = KT_S;
-constexpr int A_VS = BW * (TR + VPAD);
+// adjoint: two tiles 64 rows x 64 columns, R chunk 128 problems x 64 rows
+constexpr int A_RB = 2;  // row blocks per stage
+constexpr int A_KT = A_RB * KT_S;
+constexpr int A_VS = BW * (A_RB * TR + VPAD);
 constexpr int A_STAGE = A_KT + A_VS;
-constexpr int A_STAGES = 3;
+constexpr int A_STAGES = 2;
 
 size_t bfwd_smem() { return (size_t)F_STAGES * F_STAGE * 8; }
 size_t badj_smem() { return (size_t)A_STAGES * A_STAGE * 8; }
@@ -141,18 +142,21 @@ __global__ void __launch_bounds__(BT, 1) badj_kernel(const BGemmArgs a) {
   const int64_t cb = blockIdx.x;
   const int split = blockIdx.y;
   const int b0 = blockIdx.z * BW;
-  const int r_begin = split * a.per_split;
+  constexpr int RS = A_RB * TR + VPAD;  // row pitch of the staged R chunk
+  const int r_begin = split * a.per_split;  // in row blocks (per_split is a multiple of A_RB)
   const int r_end = r_begin + a.per_split < a.nblocks ? r_begin + a.per_split : a.nblocks;
-  const int nch = r_end > r_begin ? r_end - r_begin : 0;
+  const int nch = r_end > r_begin ? (r_end - r_begin + A_RB - 1) / A_RB : 0;
   auto load = [&](int c, int st) {
     double* ks = sm + st * A_STAGE;
     double* vs = ks + A_KT;
-    const int64_t rb = r_begin + c;
-    for (int q = tid; q < TILE / 2; q += BT)
-      cp16(ks + kchunk_dst(q), a.K + tile_offset(rb, cb, a.ncb) + q * 2);
-    for (int q = tid; q < BW * (TR / 2); q += BT) {
-      const int b = q >> 4, kq = (q & 15) * 2;
-      cp16(vs + b * (TR + VPAD) + kq, a.V + (int64_t)(b0 + b) * a.vstride + rb * TR + kq);
+    const int64_t rb = r_begin + (int64_t)c * A_RB;
+    for (int q = tid; q < A_RB * TILE / 2; q += BT) {
+      const int tl = q >> 10, cq = q & 1023;
+      cp16(ks + tl * KT_S + kchunk_dst(cq), a.K + tile_offset(rb + tl, cb, a.ncb) + 2 * cq);
+    }
+    for (int q = tid; q < BW * (A_RB * TR / 2); q += BT) {
+      const int b = q >> 5, kq = (q & 31) * 2;
+      cp16(vs + b * RS + kq, a.V + (int64_t)(b0 + b) * a.vstride + rb * TR + kq);
     }
   };
   double acc[4][4][2];
@@ -160,28 +164,24 @@ __global__ void __launch_bounds__(BT, 1) badj_kernel(const BGemmArgs a) {
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll
-  for (int s = 0; s < A_STAGES - 1; ++s) {
-    if (s < nch) load(s, s);
-    cp_commit();
-  }
+  if (nch > 0) load(0, 0);
+  cp_commit();
   for (int c = 0; c < nch; ++c) {
-    if (c + A_STAGES - 1 < nch) load(c + A_STAGES - 1, (c + A_STAGES - 1) % A_STAGES);
+    if (c + 1 < nch) load(c + 1, (c + 1) & 1);
     cp_commit();
-    cp_wait<A_STAGES - 1>();
+    cp_wait<1>();
     __syncthreads();
-    const double* ks = sm + (c % A_STAGES) * A_STAGE;
-    const double* vs = sm + (c % A_STAGES) * A_STAGE + A_KT + (wc * 32) * (TR + VPAD);
-#pragma unroll
-    for (int kk = 0; kk < TR; kk += 4) {
+    const double* ks = sm + (c & 1) * A_STAGE;
+    const double* vs = sm + (c & 1) * A_STAGE + A_KT + (wc * 32) * RS;
+#pragma unroll 4
+    for (int kk = 0; kk < A_RB * TR; kk += 4) {
       const int row = kk + t;
+      const double* kt = ks + (row >> 5) * KT_S;
       double av[4], bv[4];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        av[mt] = ks[kpos(row, wm * 32 + mt * 8 + g)];
-      }
+      for (int mt = 0; mt < 4; ++mt) av[mt] = kt[kpos(row & 31, wm * 32 + mt * 8 + g)];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bv[nt] = vs[(nt * 8 + g) * (TR + VPAD) + row];
+      for (int nt = 0; nt < 4; ++nt) bv[nt] = vs[(nt * 8 + g) * RS + row];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -394,6 +394,7 @@ BatchPlan make_batch_plan(const GemvPlan& pl, int B, int sm_count) {
   bp.fwd_per = (int)((pl.ncb + bp.fwd_splits - 1) / bp.fwd_splits);
   bp.adj_splits = splits_for(pl.ncb * bz, pl.nrb, sm_count);
   bp.adj_per = (int)((pl.nrb + bp.adj_splits - 1) / bp.adj_splits);
+  bp.adj_per = (bp.adj_per + A_RB - 1) / A_RB * A_RB;  // whole stages per split
   return bp;
 }
 
