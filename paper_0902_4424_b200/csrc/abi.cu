@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -722,7 +723,11 @@ l1g_batch* batch_new(l1g_op* op, int B, const double* Y, const double* rho,
     b->cfg = cfg;
     b->rho.assign(rho, rho + B);
     b->bp = make_batch_plan(pl, B, op->c->sm_count);
-    b->pp = make_proj_plan_single(pl.p_pad);
+    {  // a small cluster per problem (>= 4096 elements per CTA): C5 measured best at 4
+      int cs = 1;
+      while (cs < 4 && pl.p_pad / (cs * 2) >= 4096) cs *= 2;
+      b->pp = make_proj_plan_single(pl.p_pad, cs);
+    }
     const size_t Bp = (size_t)b->bp.Bp;
     L1G_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {

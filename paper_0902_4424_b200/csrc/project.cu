@@ -910,15 +910,16 @@ void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const d
   proj_dispatch(pp, a, s, nprob);
 }
 
-// one CTA per problem (batched runs): the whole vector in registers of one CTA
-ProjPlan make_proj_plan_single(int64_t p_pad) {
+// batched runs: a cluster of `cs` CTAs per problem (1: the whole vector in one CTA)
+ProjPlan make_proj_plan_single(int64_t p_pad, int cs) {
   ProjPlan pp{};
   int64_t m = 1;
-  while (PT * m < p_pad) m <<= 1;
+  while (PT * m * cs < p_pad) m <<= 1;
   if (m > MAX_M) return make_proj_plan(p_pad);
-  pp.cs = 1;
+  pp.cs = cs;
   pp.ls = PT * m;
-  pp.cand_cap = pp.ls + 1;
+  pp.cand_cap = (pp.ls > SMEM_CAND ? pp.ls : SMEM_CAND) + 1;
+  if (cs == 1) pp.cand_cap = pp.ls + 1;
   pp.smem = (size_t)pp.cand_cap * 8;
   return pp;
 }
