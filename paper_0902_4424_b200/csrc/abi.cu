@@ -145,6 +145,7 @@ struct l1g_op : Op {
   double *vin = nullptr, *vout = nullptr, *vtmp = nullptr, *scal = nullptr;
   std::mutex solver_mu;
   l1g_solver* cached = nullptr;
+  l1g_batch* cached_batch = nullptr;  // workspace of l1g_gpss_solve_batched, reused per B
 };
 
 struct l1g_comm {
@@ -1340,6 +1341,7 @@ void l1g_op_destroy(l1g_op* op) {
   if (!op) return;
   cudaSetDevice(op->c->device);
   if (op->cached) solver_free(op->cached);
+  if (op->cached_batch) batch_free(op->cached_batch);
   dfree(op->K);
   free_ws(op->ws);
   dfree(op->vin);
@@ -1921,16 +1923,39 @@ int l1g_gpss_solve_batched(l1g_op* op, int B, const double* Y, const double* rho
                            l1g_result* results) {
   return guarded([&] {
     check_stop(*stop);
-    l1g_batch* b = batch_new(op, B, Y, rho, *cfg);
+    check_cfg(*cfg);
+    for (int i = 0; i < B; ++i) check_rho(rho[i]);
+    // reuse the operator's cached batch workspace (and its captured graph) when the batch
+    // size matches and no other thread holds it
+    std::unique_lock<std::mutex> lk(op->solver_mu, std::try_to_lock);
+    l1g_batch* b = nullptr;
+    bool temp = true;
+    if (lk.owns_lock() && op->cached_batch && op->cached_batch->B == B) {
+      b = op->cached_batch;
+      temp = false;
+      set_device(op->c);
+      const GemvPlan& pl = op->plan;
+      b->cfg = *cfg;
+      b->rho.assign(rho, rho + B);
+      L1G_CUDA(cudaMemcpy2DAsync(b->y, pl.n_pad * 8, Y, pl.n * 8, pl.n * 8, B,
+                                 cudaMemcpyHostToDevice, b->stream));
+    } else {
+      b = batch_new(op, B, Y, rho, *cfg);
+      if (lk.owns_lock()) {
+        if (op->cached_batch) batch_free(op->cached_batch);
+        op->cached_batch = b;
+        temp = false;
+      }
+    }
     try {
       batch_init(b, nullptr);
       batch_run(b, *stop, results);
       if (X_out) batch_get_x(b, X_out);
     } catch (...) {
-      batch_free(b);
+      if (temp) batch_free(b);
       throw;
     }
-    batch_free(b);
+    if (temp) batch_free(b);
   });
 }
 
