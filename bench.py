@@ -478,6 +478,14 @@ def run_b200(args, world, rank, local, pg):
     solve_once()
     lib.l1g_solver_timing(h, C.byref(tp), C.byref(tf), C.byref(ta), C.byref(ti), None, 1)
     L.check(lib.l1g_solver_set_timing(h, 0))
+    nccl = None
+    if sharded:  # the two allgathers of an iteration, timed alone on the solver stream
+        xk, xg = C.c_double(), C.c_double()
+        L.check(lib.l1g_solver_time_exchange(h, 20, C.byref(xk), C.byref(xg)), "time_exchange")
+        nccl = {"allgather_Kd_ms": round(max_over_ranks(pg, xk.value), 5),
+                "allgather_KTr_ms": round(max_over_ranks(pg, xg.value), 5),
+                "share_of_iteration": round((xk.value + xg.value) /
+                                            (dev_ms / max(done_iters, 1)), 4)}
     prof = (C.c_double * 24)()
     lib.l1g_solver_proj_profile(h, prof)
     sp_cols = prof[18] / prof[19] if prof[19] > 0 else None
@@ -585,6 +593,8 @@ def run_b200(args, world, rank, local, pg):
                 "roofline": roofline,
                 "cpu_baseline": cpu,
                 "clocks": clocks.summary()}
+        if nccl is not None:
+            line["nccl"] = nccl
         print(json.dumps(line), flush=True)
     lib.l1g_solver_destroy(h)
     if comm is not None:

@@ -208,6 +208,9 @@ int l1g_comm_create(l1g_ctx* ctx, int rank, int nranks, const void* id128, l1g_c
 void l1g_comm_destroy(l1g_comm* comm);
 int l1g_solver_create_sharded(l1g_op* op, l1g_comm* comm, const double* y, double rho,
                               const l1g_gp_config* cfg, l1g_solver** out);
+/* average duration of the two per-iteration exchanges (K d values, K^T r values) over `reps`
+ * standalone launches on the solver stream (NCCL time, reported next to the solve) */
+int l1g_solver_time_exchange(l1g_solver* s, int reps, double* kd_ms, double* g_ms);
 /* ---- batched right-hand sides (BASELINE C5): B
  * problems sharing K, with their own y_b (Y is B x n, problem-major) and rho_b, solved in
  * lockstep.  Each problem follows gpss_solve (gpss.cpp:221-292) and counts its matvecs as if

@@ -113,6 +113,7 @@ _SIGS = {
     "l1g_batch_time_products": (C.c_int, [_vp, C.c_int, _dp, _dp]),
     "l1g_gpss_solve_batched": (C.c_int, [_vp, C.c_int, _vp, _vp, C.POINTER(GpConfigC),
                                          C.POINTER(StopRuleC), _vp, _vp]),
+    "l1g_solver_time_exchange": (C.c_int, [_vp, C.c_int, _dp, _dp]),
     "l1g_solver_set_y": (C.c_int, [_vp, _vp]),
     "l1g_solver_set_y_dev": (C.c_int, [_vp, _vp]),
     "l1g_solver_init": (C.c_int, [_vp, _vp]),

@@ -1778,6 +1778,32 @@ int l1g_solver_set_forward(l1g_solver* s, int sparse) {
   });
 }
 
+int l1g_solver_time_exchange(l1g_solver* s, int reps, double* kd_ms, double* g_ms) {
+  return guarded([&] {
+    if (!s->split()) throw InvalidArgument("time_exchange: not a sharded solver");
+    set_device(s->op->c);
+    cudaEvent_t e[3];
+    for (auto& x : e) L1G_CUDA(cudaEventCreate(&x));
+    float a = 0.f, b = 0.f;
+    for (int i = 0; i < reps; ++i) {
+      L1G_CUDA(cudaEventRecord(e[0], s->stream));
+      exchange(s, 0);
+      L1G_CUDA(cudaEventRecord(e[1], s->stream));
+      exchange(s, 1);
+      L1G_CUDA(cudaEventRecord(e[2], s->stream));
+      L1G_CUDA(cudaEventSynchronize(e[2]));
+      float x = 0.f, y = 0.f;
+      L1G_CUDA(cudaEventElapsedTime(&x, e[0], e[1]));
+      L1G_CUDA(cudaEventElapsedTime(&y, e[1], e[2]));
+      a += x;
+      b += y;
+    }
+    for (auto& x : e) cudaEventDestroy(x);
+    *kd_ms = a / std::max(reps, 1);
+    *g_ms = b / std::max(reps, 1);
+  });
+}
+
 int l1g_solver_timing(l1g_solver* s, double* proj_ms, double* fwd_ms, double* adj_ms,
                       int64_t* iterations, int64_t* launches, int reset) {
   if (proj_ms) *proj_ms = s->t_proj;
