@@ -159,7 +159,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("L1G_LIB_PATH", LIB_PATH)  # L1G_LIB_PATH: debug builds
     if not os.path.exists(p):
         raise ImportError(f"{p} is missing: build the CUDA extension first "
                           "(python -c 'import __graft_entry__ as g; g.build()')")

@@ -51,55 +51,61 @@ __device__ __forceinline__ double from_grid(long long N, int be) {
   return __longlong_as_double(((long long)(be - 1) << 52) + N);
 }
 
-constexpr int PREFIX_HEAD = 256;
-constexpr int PREFIX_MAXW = 32;  // warps per block
+#ifdef L1G_PREFIX_STAMPS  // sub-epoch clock stamps (tools/bench_prefix.cu)
+#define L1G_PSTAMP(k) \
+  if (threadIdx.x == 0 && ntr > 0 && ntr <= 64) L1G_PREFIX_STAMPS[(ntr - 1) * 8 + (k)] = clock64();
+#define L1G_HSTAMP(k) \
+  if (threadIdx.x == 0) L1G_PREFIX_STAMPS[64 * 8 + (k)] = clock64();
+#else
+#define L1G_PSTAMP(k)
+#define L1G_HSTAMP(k)
+#endif
 
-struct ScanShared {
-  double head[PREFIX_HEAD];
-  long long wsum[PREFIX_MAXW];
-  long long wd0[PREFIX_MAXW], wd1[PREFIX_MAXW];
-  int wp[PREFIX_MAXW];
-  long long wev[PREFIX_MAXW];
-  long long ev, nb;
-  int kind;
-  double sb;
-  int epochs;  // telemetry: windows scanned by the last call
-};
+#ifndef L1G_PREFIX_HEAD
+#define L1G_PREFIX_HEAD 256
+#endif
+constexpr int PREFIX_HEAD = L1G_PREFIX_HEAD;
+constexpr int PREFIX_MAXW = 32;  // warps per block
 
 // A run of positions as a function of the parity of the running grid count N it starts
 // from: a rounding tie (m an odd multiple of half a grid step) rounds N + q + 1/2 to the
 // even neighbour, so it adds q or q + 1 depending on N's parity and always leaves N even;
-// other positions add their fixed q.  (d0, p0) / (d1, p1): increment and final parity for
-// an even / odd start.  Composition is associative, so ties ride along the prefix scan.
+// other positions add their fixed q.  d0 / p0: increment and final parity from an even
+// start; from an odd start the increment is d0 + dl (dl in {-1, 0, 1}) and the final parity
+// p1.  Composition is associative, so ties ride along the prefix scan.
 struct ParSeg {
-  long long d0, d1;
-  int p0, p1;
+  long long d0;
+  int dl, p0, p1;
 };
+__device__ __forceinline__ ParSeg seg_id() { return ParSeg{0, 0, 0, 1}; }
 __device__ __forceinline__ ParSeg seg_then(const ParSeg& A, const ParSeg& B) {
   ParSeg C;
-  C.d0 = A.d0 + (A.p0 ? B.d1 : B.d0);
+  const int b0 = A.p0 ? B.dl : 0, b1 = A.p1 ? B.dl : 0;
+  C.d0 = A.d0 + B.d0 + b0;
+  C.dl = A.dl + b1 - b0;
   C.p0 = A.p0 ? B.p1 : B.p0;
-  C.d1 = A.d1 + (A.p1 ? B.d1 : B.d0);
   C.p1 = A.p1 ? B.p1 : B.p0;
   return C;
 }
-__device__ __forceinline__ ParSeg seg_shfl_up(const ParSeg& v, int o) {
-  ParSeg r;
-  r.d0 = __shfl_up_sync(0xffffffffu, v.d0, o);
-  r.d1 = __shfl_up_sync(0xffffffffu, v.d1, o);
-  const int pk = __shfl_up_sync(0xffffffffu, v.p0 | (v.p1 << 1), o);
-  r.p0 = pk & 1;
-  r.p1 = pk >> 1;
-  return r;
+// one position: grid count q, tie or not
+__device__ __forceinline__ ParSeg seg_elem(long long q, bool tie) {
+  const int odd = (int)(q & 1);
+  if (!tie) return ParSeg{q, 0, odd, odd ^ 1};
+  return ParSeg{q + odd, odd ? -1 : 1, 0, 0};
 }
-__device__ __forceinline__ ParSeg seg_shfl(const ParSeg& v, int src) {
-  ParSeg r;
-  r.d0 = __shfl_sync(0xffffffffu, v.d0, src);
-  r.d1 = __shfl_sync(0xffffffffu, v.d1, src);
-  const int pk = __shfl_sync(0xffffffffu, v.p0 | (v.p1 << 1), src);
-  r.p0 = pk & 1;
-  r.p1 = pk >> 1;
-  return r;
+// the running count after the segment, from the concrete count N
+__device__ __forceinline__ long long seg_apply(const ParSeg& s, long long N) {
+  return N + s.d0 + ((N & 1) ? s.dl : 0);
+}
+__device__ __forceinline__ int seg_pack(const ParSeg& v) {
+  return (v.dl + 1) | (v.p0 << 2) | (v.p1 << 3);
+}
+__device__ __forceinline__ ParSeg seg_unpack(long long d0, int pk) {
+  return ParSeg{d0, (pk & 3) - 1, (pk >> 2) & 1, (pk >> 3) & 1};
+}
+__device__ __forceinline__ ParSeg seg_shfl_up(const ParSeg& v, int o) {
+  return seg_unpack(__shfl_up_sync(0xffffffffu, v.d0, o),
+                    __shfl_up_sync(0xffffffffu, seg_pack(v), o));
 }
 // inclusive scan of per-lane segments over the warp (earlier lanes first)
 __device__ __forceinline__ ParSeg seg_warp_scan(ParSeg v, int lane) {
@@ -111,6 +117,17 @@ __device__ __forceinline__ ParSeg seg_warp_scan(ParSeg v, int lane) {
   return v;
 }
 
+struct ScanShared {
+  alignas(16) double head[PREFIX_HEAD];
+  long long wd0[2][PREFIX_MAXW];  // warp segments (double-buffered by epoch parity)
+  int wpk[2][PREFIX_MAXW];
+  int epos[2][PREFIX_MAXW];       // per warp: first event (position, kind, count before)
+  int ekind[2][PREFIX_MAXW];
+  long long en[2][PREFIX_MAXW];
+  int hbad[PREFIX_MAXW];
+  int epochs;  // telemetry: windows scanned by the last call
+};
+
 // Exact emulation of the reference's sequential cumulative sum (prox.cpp:44-51) over the
 // sorted candidates c[0..L) (descending, >= 0), fused with its break test.  While the
 // running sum S stays inside one binade [2^e, 2^(e+1)), every fl(S + m) is S plus m rounded
@@ -118,80 +135,86 @@ __device__ __forceinline__ ParSeg seg_warp_scan(ParSeg v, int lane) {
 // exact integer prefix scan of grid counts (computed from the mantissa bits; rounding ties,
 // decided by the parity of the running count, ride along the scan as parity-dependent
 // segments).  The first position whose sum leaves the binade is done as one IEEE addition
-// and starts the next epoch.  The short epochs at the
-// top are cheaper as the reference's own sequential sum (one dependent add per position);
-// after PREFIX_HEAD positions the block scans windows sized to the (doubling) epochs.
-// Returns the first failing index ff (L if none) and S_{ff-1} (the sum whose candidate is
-// theta).  All threads of the block call it (blockDim a multiple of 32, <= 1024) and
-// receive the same result.
-__device__ long long prefix_break(const double* c, long long L, double rho, ScanShared& ss,
+// and starts the next epoch.  The short epochs at the top are cheaper as the reference's
+// own sequential sum (one dependent add per position); after PREFIX_HEAD positions the
+// block scans windows sized to the (doubling) epochs.  Returns the first failing index ff
+// (L if none) and S_{ff-1} (the sum whose candidate is theta).  All NT threads of the block
+// call it and receive the same result.
+template <int NT = 512>
+__device__ long long prefix_break(const double* c, long long Ll, double rho, ScanShared& ss,
                                   double* s_before) {
+  static_assert(NT % 32 == 0 && NT <= 32 * PREFIX_MAXW && PREFIX_HEAD <= NT && PREFIX_HEAD % 32 == 0, "prefix_break block shape");
+  constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NT = blockDim.x, NW = NT >> 5;
   constexpr long long TWO53 = 1LL << 53;
   constexpr unsigned FULL = 0xffffffffu;
+  const int L = (int)Ll;
   if (L <= 0) {
     *s_before = 0.0;
     return 0;
   }
-  // ---- head: lane 0 of warp 0 adds sequentially, warp 0 tests in parallel
-  const long long H = L < PREFIX_HEAD ? L : PREFIX_HEAD;
+  // ---- head: warp 0 stages c[0..H) in shared memory, one thread adds sequentially (vector
+  //      loads one batch ahead, each sum in its own register), then every thread tests one
+  //      position
+  const int H = L < PREFIX_HEAD ? L : PREFIX_HEAD;
+  L1G_HSTAMP(0)
   if (warp == 0) {
+    for (int i = lane; i < PREFIX_HEAD; i += 32) ss.head[i] = i < H ? c[i] : 0.0;
+    __syncwarp();
     if (lane == 0) {
-      double run = 0.0, v[8], w[8];
+      double2* hp = reinterpret_cast<double2*>(ss.head);
+      double run = 0.0;
+      double2 v[4], w[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = u < H ? c[u] : 0.0;
-      for (long long i0 = 0; i0 < H; i0 += 8) {
+      for (int u = 0; u < 4; ++u) v[u] = hp[u];
+      for (int i0 = 0; i0 < H; i0 += 8) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) w[u] = i0 + 8 + u < H ? c[i0 + 8 + u] : 0.0;  // next batch
+        for (int u = 0; u < 4; ++u)
+          w[u] = i0 + 8 < PREFIX_HEAD ? hp[(i0 + 8) / 2 + u] : make_double2(0.0, 0.0);
+        double hs[8];
+        hs[0] = add(run, v[0].x);
+        hs[1] = add(hs[0], v[0].y);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (i0 + u < H) {
-            run = add(run, v[u]);
-            ss.head[i0 + u] = run;
-          }
+        for (int u = 1; u < 4; ++u) {
+          hs[2 * u] = add(hs[2 * u - 1], v[u].x);
+          hs[2 * u + 1] = add(hs[2 * u], v[u].y);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = w[u];
+        for (int u = 0; u < 4; ++u) hp[i0 / 2 + u] = make_double2(hs[2 * u], hs[2 * u + 1]);
+        run = hs[7];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = w[u];
       }
-    }
-    __syncwarp();
-    long long ff = LLONG_MAX;
-    for (long long i = lane; i - lane < H; i += 32) {
-      const bool ok = i < H ? passes(c[i], ss.head[i], rho, i + 1) : true;
-      const unsigned bad = __ballot_sync(FULL, !ok);
-      if (bad) {
-        ff = i - lane + (__ffs(bad) - 1);
-        break;
-      }
-    }
-    if (lane == 0) {
-      ss.ev = ff;
-      ss.sb = ff == LLONG_MAX ? ss.head[H - 1] : (ff > 0 ? ss.head[ff - 1] : 0.0);
     }
   }
+  L1G_HSTAMP(1)
   __syncthreads();
   {
-    const long long ff = ss.ev;
-    const double sb = ss.sb;
-    __syncthreads();
-    if (ff != LLONG_MAX) {
-      *s_before = sb;
-      return ff;
-    }
-    if (H == L) {
-      *s_before = sb;
-      return L;
+    const bool bad = tid < H && !passes(c[tid], ss.head[tid], rho, tid + 1);
+    const unsigned bb = __ballot_sync(FULL, bad);
+    if (lane == 0) ss.hbad[warp] = bb ? warp * 32 + __ffs(bb) - 1 : INT_MAX;
+  }
+  L1G_HSTAMP(2)
+  __syncthreads();
+  L1G_HSTAMP(3)
+  {
+    int ff = INT_MAX;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) ff = min(ff, ss.hbad[w]);
+    if (ff != INT_MAX || H == L) {
+      if (tid == 0) ss.epochs = 0;
+      *s_before = ff == INT_MAX ? ss.head[H - 1] : (ff > 0 ? ss.head[ff - 1] : 0.0);
+      return ff == INT_MAX ? L : ff;
     }
   }
   double S_prev = ss.head[H - 1];
-  long long i0 = H, window = 2 * H;
+  int i0 = H, window = 2 * H, par = 0;
 #ifdef L1G_PREFIX_TRACE
   int ntr = 0;
 #endif
-  if (threadIdx.x == 0) ss.epochs = 0;
+  int nep = 0;
   while (i0 < L) {
-    if (threadIdx.x == 0) ++ss.epochs;
+    ++nep;
 #ifdef L1G_PREFIX_TRACE
     if (threadIdx.x == 0 && ntr < 64) {
       L1G_PREFIX_TRACE[3 * ntr] = clock64();
@@ -204,138 +227,109 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
       const double S = add(S_prev, c[i0]);
       if (!passes(c[i0], S, rho, i0 + 1)) {
         *s_before = S_prev;
+        if (tid == 0) ss.epochs = nep;
         return i0;
       }
       S_prev = S;
       ++i0;
       continue;
     }
-    const long long n = (L - i0) < window ? (L - i0) : window;
-    const long long E = (n + NT - 1) / NT;
-    const long long wend = i0 + n;
-    const long long p0 = i0 + (long long)tid * E;
-    const long long p1 = p0 + E < wend ? p0 + E : wend;
+    const int n = (L - i0) < window ? (L - i0) : window;
+    const int E = (n + NT - 1) / NT;
+    const int wend = i0 + n;
+    const int p0 = min(i0 + tid * E, wend);
+    const int p1 = min(p0 + E, wend);
     const long long sbits = __double_as_longlong(S_prev);
     const int be = (int)(sbits >> 52);
     const long long base_q = (sbits & ((1LL << 52) - 1)) | (1LL << 52);  // S_prev / u
-    // pass 1: grid counts of my positions (a tie counted at its floor)
-    long long tot = 0;
-    int tie_here = 0;
+    // pass 1: this thread's run as a parity segment; warp scan; warp totals to shared
+    ParSeg me = seg_id();
 #pragma unroll 4
-    for (long long i = p0; i < p1; ++i) {
+    for (int i = p0; i < p1; ++i) {
       bool t;
-      tot += grid_count(c[i], be, &t);
-      tie_here |= t;
+      const long long q = grid_count(c[i], be, &t);
+      me = seg_then(me, seg_elem(q, t));
     }
-    long long inc = tot;
+    L1G_PSTAMP(0)
+    const ParSeg incl = seg_warp_scan(me, lane);
+    if (lane == 31) {
+      ss.wd0[par][warp] = incl.d0;
+      ss.wpk[par][warp] = seg_pack(incl);
+    }
+    __syncthreads();
+    L1G_PSTAMP(1)
+    // concrete counts: the warps' starts by applying the warp segments in order (the
+    // parity chain is a 1-bit select per warp; increments add up independently)
+    long long Nw = base_q, accd = base_q;
+    int accl = 0, pb = (int)(base_q & 1);
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long y = __shfl_up_sync(FULL, inc, o);
-      if (lane >= o) inc += y;
+    for (int w = 0; w < NW; ++w) {
+      const long long d0 = ss.wd0[par][w];
+      const int pk = ss.wpk[par][w];
+      Nw = w == warp ? accd + accl : Nw;
+      accl += pb ? (pk & 3) - 1 : 0;
+      accd += d0;
+      pb = pb ? (pk >> 3) & 1 : (pk >> 2) & 1;
     }
-    if (lane == 31) ss.wsum[warp] = inc;
-    const int any_tie = __syncthreads_or(tie_here);
-    const int par0 = (int)(base_q & 1);
-    long long start, btot;
-    if (!any_tie) {  // warp totals: inclusive scan over the warps by shuffles
-      const long long x = lane < NW ? ss.wsum[lane] : 0;
-      long long sc = x;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long y = __shfl_up_sync(FULL, sc, o);
-        if (lane >= o) sc += y;
-      }
-      btot = __shfl_sync(FULL, sc, 31);
-      start = inc - tot + (warp > 0 ? __shfl_sync(FULL, sc, warp - 1) : 0);
-    } else {  // rounding ties in the window: scan parity-dependent segments instead
-      ParSeg me = {0, 0, 0, 1};
-      for (long long i = p0; i < p1; ++i) {
-        bool tie;
-        const long long q = grid_count(c[i], be, &tie);
-        if (!tie) {
-          me.d0 += q;
-          me.d1 += q;
-          me.p0 ^= (int)(q & 1);
-          me.p1 ^= (int)(q & 1);
-        } else {
-          me.d0 += q + ((me.p0 + q) & 1);
-          me.d1 += q + ((me.p1 + q) & 1);
-          me.p0 = 0;
-          me.p1 = 0;
-        }
-      }
-      const ParSeg incl = seg_warp_scan(me, lane);
-      if (lane == 31) {
-        ss.wd0[warp] = incl.d0;
-        ss.wd1[warp] = incl.d1;
-        ss.wp[warp] = incl.p0 | (incl.p1 << 1);
-      }
-      __syncthreads();
-      ParSeg t = {0, 0, 0, 1};
-      if (lane < NW) {
-        t.d0 = ss.wd0[lane];
-        t.d1 = ss.wd1[lane];
-        t.p0 = ss.wp[lane] & 1;
-        t.p1 = ss.wp[lane] >> 1;
-      }
-      const ParSeg ti = seg_warp_scan(t, lane);
-      const ParSeg total = seg_shfl(ti, 31);
-      const ParSeg wx = seg_shfl(ti, warp > 0 ? warp - 1 : 0);
-      const ParSeg wpre = warp > 0 ? wx : ParSeg{0, 0, 0, 1};
-      ParSeg lx = seg_shfl_up(incl, 1);
-      if (lane == 0) lx = ParSeg{0, 0, 0, 1};
-      const ParSeg before = seg_then(wpre, lx);
-      btot = par0 ? total.d1 : total.d0;
-      start = par0 ? before.d1 : before.d0;
-    }
+    const long long Nend = accd + accl;
+    ParSeg ex = seg_shfl_up(incl, 1);
+    if (lane == 0) ex = seg_id();
+    long long N = seg_apply(ex, Nw);
+    L1G_PSTAMP(2)
     // pass 2: exact sums and tests; my first event (1 failure, 2 binade exit,
     // 3 test too close to call), branch-free so positions overlap
-    long long N = base_q + start, my_ev = LLONG_MAX, my_n = 0;
-    int kind = 0;
+    int my_ev = INT_MAX, kind = 0;
+    long long my_n = 0;
     double kd = (double)(p0 + 1);
 #pragma unroll 4
-    for (long long i = p0; i < p1; ++i) {
+    for (int i = p0; i < p1; ++i) {
       const double m = c[i];
       bool tie;
       const long long q = grid_count(m, be, &tie);
       const long long Nn = N + q + (tie ? ((N + q) & 1) : 0);
       const int stt = Nn >= TWO53 ? 2 : quick_test(m, from_grid(Nn, be), rho, kd);
-      const bool take = stt != 0 && my_ev == LLONG_MAX;
+      const bool take = stt != 0 && my_ev == INT_MAX;
       my_ev = take ? i : my_ev;
       kind = take ? stt : kind;
       my_n = take ? N : my_n;
       N = Nn;
       kd = add(kd, 1.0);
     }
-    // first event of the window (positions increase with the thread index)
-    const unsigned have = __ballot_sync(FULL, my_ev != LLONG_MAX);
-    if (lane == 0) ss.wev[warp] = have ? (long long)warp * 32 + (__ffs(have) - 1) : LLONG_MAX;
+    L1G_PSTAMP(3)
+    // first event of the window: per warp (positions increase with the lane), then over
+    // the warps in order
+    const unsigned have = __ballot_sync(FULL, my_ev != INT_MAX);
+    if (have) {
+      if (lane == __ffs(have) - 1) {
+        ss.epos[par][warp] = my_ev;
+        ss.ekind[par][warp] = kind;
+        ss.en[par][warp] = my_n;
+      }
+    } else if (lane == 0) {
+      ss.epos[par][warp] = INT_MAX;
+    }
     __syncthreads();
-    long long owner = lane < NW ? ss.wev[lane] : LLONG_MAX;
+    int ew = -1;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) owner = min(owner, __shfl_xor_sync(FULL, owner, o));
-    if (owner == LLONG_MAX) {  // the whole window is exact and passes: the epoch continues
-      S_prev = from_grid(base_q + btot, be);
+    for (int w = NW - 1; w >= 0; --w) ew = ss.epos[par][w] != INT_MAX ? w : ew;
+    L1G_PSTAMP(4)
+    if (ew < 0) {  // the whole window is exact and passes: the epoch continues
+      S_prev = from_grid(Nend, be);
       i0 = wend;
       window *= 2;
-      __syncthreads();
+      par ^= 1;
       continue;
     }
-    if (tid == owner) {
-      ss.ev = my_ev;
-      ss.kind = kind;
-      ss.nb = my_n;
-    }
-    __syncthreads();
-    const long long ev = ss.ev, nb = ss.nb;
-    const int evk = ss.kind;
-    __syncthreads();
+    const int ev = ss.epos[par][ew], evk = ss.ekind[par][ew];
+    const long long nb = ss.en[par][ew];
+    par ^= 1;
 #ifdef L1G_PREFIX_TRACE
     if (threadIdx.x == 0 && ntr > 0 && ntr <= 64) L1G_PREFIX_TRACE[3 * (ntr - 1) + 2] += 1000000LL * evk;
 #endif
     const double sb = from_grid(nb, be);  // S_{ev-1}
     if (evk == 1) {
       *s_before = sb;
+      if (tid == 0) ss.epochs = nep;
       return ev;
     }
     if (evk == 3) {  // exact test with the division; on success the epoch goes on
@@ -344,6 +338,7 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
       const double Se = from_grid(nb + qe + (t ? ((nb + qe) & 1) : 0), be);
       if (!passes(c[ev], Se, rho, ev + 1)) {
         *s_before = sb;
+        if (tid == 0) ss.epochs = nep;
         return ev;
       }
       S_prev = Se;
@@ -354,8 +349,10 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
     const double S = add(sb, c[ev]);
     if (!passes(c[ev], S, rho, ev + 1)) {
       *s_before = sb;
+      if (tid == 0) ss.epochs = nep;
       return ev;
     }
+    L1G_PSTAMP(5)
     // the running sum doubles again after a bit more than the prefix so far (candidates
     // decrease): size the window to twice the prefix, overshooting rather than re-scanning
     window = ((2 * (ev + 1) + 31) >> 5) << 5;
@@ -363,6 +360,7 @@ __device__ long long prefix_break(const double* c, long long L, double rho, Scan
     i0 = ev + 1;
   }
   *s_before = S_prev;
+  if (tid == 0) ss.epochs = nep;
   return L;
 }
 

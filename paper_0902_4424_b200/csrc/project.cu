@@ -22,6 +22,12 @@
 #include "common.cuh"
 #include "engine.h"
 #include "scalar.cuh"
+#ifdef L1G_PROJ_TRACE  // debug builds only (tools/prof_solve.py --prefix-trace)
+__device__ long long g_ptrace[192];
+__device__ long long g_pstamp[65 * 8];
+#define L1G_PREFIX_TRACE g_ptrace
+#define L1G_PREFIX_STAMPS g_pstamp
+#endif
 #include "prefix.cuh"
 #include "steps.cuh"
 
@@ -70,6 +76,7 @@ struct ProjShared {
 
 // ---------------------------------------------------------------- distributed sort state
 constexpr int NB = 256;  // key-bit bins of the cluster bucket sort
+constexpr int RANK_MAXBIN = 256;  // largest bin the rank sort takes (else bitonic sorts)
 struct SortShared {
   int hist[NB];    // this CTA's candidates per bin
   int gcnt[NB];    // cluster-wide candidates per bin
@@ -79,7 +86,7 @@ struct SortShared {
   int dest[NB];
   int base[MAX_CS + 1];
   double next;
-  int total, shift, ok;
+  int total, shift, ok, maxbin;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -532,10 +539,11 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           __syncthreads();
           if (tid < 32) {  // descending exclusive scan over bins, destination CTAs
             const int lane = tid;
-            int carry = 0;
+            int carry = 0, mx = 0;
             for (int c0 = NB - 32; c0 >= 0; c0 -= 32) {
               const int b = c0 + 31 - lane;  // lane 0 takes the highest bin of the chunk
               int x = srt.gcnt[b], inc = x;
+              mx = max(mx, x);
 #pragma unroll
               for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, inc, o);
@@ -549,7 +557,12 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
               const int d = share > 0 ? srt.start[b] / share : 0;
               srt.dest[b] = d < cs ? d : cs - 1;
             }
-            if (lane == 0) srt.total = carry;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (lane == 0) {
+              srt.total = carry;
+              srt.maxbin = mx;
+            }
           }
           __syncthreads();
           {  // base[d] = first position owned by CTA d: one warp per d, min over bins
@@ -591,24 +604,59 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           mark(16);
           if (srt.ok) {
             const int cnt = srt.base[rank + 1] - srt.base[rank];
-            int m2 = 1;
-            while (m2 < cnt) m2 <<= 1;
-            for (int i = cnt + tid; i < m2; i += PT) dyn[i] = 0.0;
-            __syncthreads();
-            if (cnt > 1) bitonic_desc(dyn, m2);
-            __syncthreads();
-            cl.sync();  // every range sorted before CTA 0's buffer receives the others
-            mark(17);
             const bool gather_smem = total + 1 <= a.cand_cap;
-            if (gather_smem) {
-              if (rank != 0) {
-                double* dst = cl.map_shared_rank(dyn, 0) + srt.base[rank];
-                for (int i = tid; i < cnt; i += PT) dst[i] = dyn[i];
+            constexpr int RK = M >= 16 ? 8 : 2;  // candidates per thread on the rank path
+            if (cnt <= RK * PT && srt.maxbin <= RANK_MAXBIN) {
+              // rank sort: bins are narrow, so an element's place is its bin's start plus the
+              // number of larger bin mates (equal ones ordered by position); each element is
+              // written straight to its final place in CTA 0 (or the global scratch)
+              const int b0 = srt.base[rank];
+              double mv[RK];
+              int pos[RK];
+#pragma unroll
+              for (int k = 0; k < RK; ++k) {
+                const int i = tid + k * PT;
+                pos[k] = -1;
+                mv[k] = 0.0;
+                if (i < cnt) {
+                  const double m = dyn[i];
+                  const int b = (int)((__double_as_longlong(m) - kmin) >> shft);
+                  const int s0 = srt.start[b] - b0, s1 = s0 + srt.gcnt[b];
+                  int r = 0;
+                  for (int j = s0; j < s1; ++j) {
+                    const double y = dyn[j];
+                    r += (y > m) | ((y == m) & (j < i));
+                  }
+                  mv[k] = m;
+                  pos[k] = srt.start[b] + r;
+                }
               }
+              __syncthreads();  // CTA 0 overwrites its own unsorted range
+              mark(17);
+              double* dst = gather_smem ? cl.map_shared_rank(dyn, 0) : gcand;
+#pragma unroll
+              for (int k = 0; k < RK; ++k)
+                if (pos[k] >= 0) dst[pos[k]] = mv[k];
+              if (!gather_smem) __threadfence();
             } else {
-              double* dst = gcand + srt.base[rank];
-              for (int i = tid; i < cnt; i += PT) dst[i] = dyn[i];
-              __threadfence();
+              int m2 = 1;
+              while (m2 < cnt) m2 <<= 1;
+              for (int i = cnt + tid; i < m2; i += PT) dyn[i] = 0.0;
+              __syncthreads();
+              if (cnt > 1) bitonic_desc(dyn, m2);
+              __syncthreads();
+              cl.sync();  // every range sorted before CTA 0's buffer receives the others
+              mark(17);
+              if (gather_smem) {
+                if (rank != 0) {
+                  double* dst = cl.map_shared_rank(dyn, 0) + srt.base[rank];
+                  for (int i = tid; i < cnt; i += PT) dst[i] = dyn[i];
+                }
+              } else {
+                double* dst = gcand + srt.base[rank];
+                for (int i = tid; i < cnt; i += PT) dst[i] = dyn[i];
+                __threadfence();
+              }
             }
             cl.sync();
             mark(3);
@@ -622,6 +670,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
               double s_before = 0.0;
               const long long ff = prefix_break(c, L, rho, scan_sh, &s_before);
               count(20, (double)scan_sh.epochs);
+              count(21, (double)ff);
               if (tid == 0) {
                 sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
                 sh.dec = (ff == L && next >= 0.0) ? 1 : 0;
@@ -671,6 +720,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           double s_before = 0.0;
           const long long ff = prefix_break(c, L, rho, scan_sh, &s_before);
           count(20, (double)scan_sh.epochs);
+              count(21, (double)ff);
           if (tid == 0) {
             // theta = candidate of the last passing index (prox.cpp:47-50); 0 if none passed
             sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
@@ -925,3 +975,11 @@ ProjPlan make_proj_plan_single(int64_t p_pad, int cs) {
 }
 
 }  // namespace l1g
+
+#ifdef L1G_PROJ_TRACE
+extern "C" int l1g_debug_prefix_trace(long long* trace192, long long* stamps520) {
+  cudaMemcpyFromSymbol(trace192, g_ptrace, sizeof(long long) * 192);
+  cudaMemcpyFromSymbol(stamps520, g_pstamp, sizeof(long long) * 65 * 8);
+  return 0;
+}
+#endif

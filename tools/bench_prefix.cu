@@ -13,6 +13,8 @@
 #ifdef TRACE
 __device__ long long g_trace[192];
 #define L1G_PREFIX_TRACE g_trace
+__device__ long long g_stamp[65 * 8];
+#define L1G_PREFIX_STAMPS g_stamp
 #endif
 #include "prefix.cuh"
 
@@ -22,11 +24,13 @@ __global__ void k_parallel(const double* c, long long L, double rho, long long* 
                            long long* cycles) {
   __shared__ ScanShared ss;
   extern __shared__ double sc[];
-  for (long long i = threadIdx.x; i < L; i += blockDim.x) sc[i] = c[i];
+  const bool smem = L * 8 <= 200000;  // else straight from global memory (L2), as project.cu
+  if (smem)
+    for (long long i = threadIdx.x; i < L; i += blockDim.x) sc[i] = c[i];
   __syncthreads();
   const long long t0 = clock64();
   double s = 0;
-  const long long f = prefix_break(sc, L, rho, ss, &s);
+  const long long f = prefix_break(smem ? (const double*)sc : c, L, rho, ss, &s);
   __syncthreads();
   const long long t1 = clock64();
   if (threadIdx.x == 0) {
@@ -38,8 +42,11 @@ __global__ void k_parallel(const double* c, long long L, double rho, long long* 
 
 __global__ void k_sequential(const double* c, long long L, double rho, long long* ff, double* sb,
                              long long* cycles) {
-  extern __shared__ double sc[];
-  for (long long i = threadIdx.x; i < L; i += blockDim.x) sc[i] = c[i];
+  extern __shared__ double sc_[];
+  const bool smem = L * 8 <= 200000;
+  if (smem)
+    for (long long i = threadIdx.x; i < L; i += blockDim.x) sc_[i] = c[i];
+  const double* sc = smem ? (const double*)sc_ : c;
   __syncthreads();
   const long long t0 = clock64();
   if (threadIdx.x == 0) {
@@ -90,7 +97,7 @@ int main() {
       cudaMalloc(&dff, 8);
       cudaMalloc(&dcy, 8);
       cudaMemcpy(dc, c.data(), L * 8, cudaMemcpyHostToDevice);
-      const size_t sm = L * 8;
+      const size_t sm = L * 8 <= 200000 ? L * 8 : 0;
       cudaFuncSetAttribute(k_parallel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
       cudaFuncSetAttribute(k_sequential, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
       long long ff1, ff2, cy1, cy2;
@@ -109,6 +116,15 @@ int main() {
         cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr));
         for (int e = 0; e < 64 && tr[3 * e] != 0; ++e)
           std::printf("   epoch %d: t=%lld i0=%lld window=%lld\n", e, tr[3 * e] - tr[0], tr[3 * e + 1], tr[3 * e + 2]);
+        long long stp[65 * 8];
+        cudaMemcpyFromSymbol(stp, g_stamp, sizeof(stp));
+        std::printf("   head: seq %lld test %lld sync %lld\n", stp[513] - stp[512], stp[514] - stp[513],
+                    stp[515] - stp[514]);
+        for (int e = 0; e < 64 && tr[3 * e] != 0; ++e) {
+          std::printf("   epoch %d stamps:", e);
+          for (int k = 0; k < 6; ++k) std::printf(" %lld", stp[e * 8 + k] ? stp[e * 8 + k] - tr[3 * e] : -1LL);
+          std::printf("\n");
+        }
         long long z[192] = {0};
         cudaMemcpyToSymbol(g_trace, z, sizeof(z));
       }

@@ -74,6 +74,17 @@ def main():
             cols = out[18] / out[19]
             print(f"sparse forward: {cols:.1f} support columns per call "
                   f"({cols / spec.p:.3%} of p), {cols * spec.n * 8 / 1e6:.1f} MB of K per call")
+    if hasattr(lib, "l1g_debug_prefix_trace"):  # L1G_PROJ_TRACE builds: the last prefix call
+        tr, stp = (C.c_longlong * 192)(), (C.c_longlong * 520)()
+        lib.l1g_debug_prefix_trace(tr, stp)
+        print("prefix head: seq %d test %d sync %d" % (stp[513] - stp[512], stp[514] - stp[513],
+                                                      stp[515] - stp[514]))
+        for e in range(64):
+            if tr[3 * e] == 0:
+                break
+            st = [stp[e * 8 + k] - tr[3 * e] if stp[e * 8 + k] else -1 for k in range(6)]
+            print(f"  epoch {e}: t={tr[3 * e] - tr[0]} i0={tr[3 * e + 1]} window={tr[3 * e + 2]}"
+                  f" stamps={st}")
     lib.l1g_solver_destroy(h)
 
 
