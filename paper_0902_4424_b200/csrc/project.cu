@@ -67,10 +67,9 @@ struct ProjArgs {
 struct ProjShared {
   double slot[2][MAX_CS][4];  // cluster reduction slots (double-buffered)
   long long slotl[2][MAX_CS];
-  double wv[PW][4];
+  double wv[2][PW][4];         // warp partials (double-buffered)
   long long wl[PW][2];
   double bc[8];
-  int red_par;
   int dec;
 };
 
@@ -97,64 +96,29 @@ __device__ __forceinline__ int swz(int e) {  // bank-conflict-free thread-run la
   return t * M + (k ^ (t & C));
 }
 
-// canonical block tree of one value per thread (threads own consecutive aligned runs)
-__device__ __forceinline__ double block_tree(double v, ProjShared& sh, int c) {
-  v = warp_tree(v);
-  if ((threadIdx.x & 31) == 0) sh.wv[threadIdx.x >> 5][c] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (threadIdx.x < 32) {
-    double x = threadIdx.x < PW ? sh.wv[threadIdx.x][c] : 0.0;
-#pragma unroll
-    for (int o = 1; o < PW; o <<= 1) x = add(x, __shfl_xor_sync(0xffffffffu, x, o));
-    r = x;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) sh.wv[0][c] = r;
-  __syncthreads();
-  r = sh.wv[0][c];
-  __syncthreads();
-  return r;
-}
+// Parities of the double-buffered reduction buffers.  Every thread keeps its own copy (all
+// threads run the same sequence of reductions), so no barrier is spent on flipping them, and
+// a buffer is rewritten only after the barrier of the reduction in between.
+struct RedPar {
+  int b, c;  // block (warp partials), cluster (rank slots)
+};
 
-__device__ __forceinline__ double block_max(double v, ProjShared& sh) {
-  v = warp_max(v);
-  if ((threadIdx.x & 31) == 0) sh.wv[threadIdx.x >> 5][3] = v;
-  __syncthreads();
-  double r = -1.0;
-#pragma unroll
-  for (int w = 0; w < PW; ++w) r = fmax(r, sh.wv[w][3]);
-  __syncthreads();
-  return r;
-}
-
-__device__ __forceinline__ double block_sum_any(double v, ProjShared& sh) {  // order-free
-  v = warp_tree(v);
-  if ((threadIdx.x & 31) == 0) sh.wv[threadIdx.x >> 5][2] = v;
-  __syncthreads();
-  double r = 0.0;
-#pragma unroll
-  for (int w = 0; w < PW; ++w) r += sh.wv[w][2];
-  __syncthreads();
-  return r;
-}
-
-// Several block reductions with one barrier pair.  kinds[c]: 0 = canonical tree over the
-// threads' aligned runs (warp butterfly, then butterfly over warp index: same bits as
-// block_tree), 1 = max, 2 = plain sum.  Every thread receives the results.
+// Several block reductions with one barrier.  kinds[c]: 0 = canonical tree over the threads'
+// aligned runs (warp butterfly, then butterfly over the warp index), 1 = max, 2 = plain sum.
+// Every thread receives the results.
 template <int N>
 __device__ __forceinline__ void block_reduce(double (&v)[N], const int (&kinds)[N],
-                                             ProjShared& sh) {
+                                             ProjShared& sh, RedPar& rp) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int c = 0; c < N; ++c) {
     const double x = kinds[c] == 1 ? warp_max(v[c]) : warp_tree(v[c]);
-    if (lane == 0) sh.wv[warp][c] = x;
+    if (lane == 0) sh.wv[rp.b][warp][c] = x;
   }
   __syncthreads();
 #pragma unroll
   for (int c = 0; c < N; ++c) {
-    double x = lane < PW ? sh.wv[lane][c] : (kinds[c] == 1 ? -1.0 : 0.0);
+    double x = lane < PW ? sh.wv[rp.b][lane][c] : (kinds[c] == 1 ? -1.0 : 0.0);
 #pragma unroll
     for (int o = 1; o < PW; o <<= 1) {
       const double y = __shfl_xor_sync(0xffffffffu, x, o);
@@ -162,7 +126,7 @@ __device__ __forceinline__ void block_reduce(double (&v)[N], const int (&kinds)[
     }
     v[c] = __shfl_sync(0xffffffffu, x, 0);
   }
-  __syncthreads();
+  rp.b ^= 1;
 }
 
 __device__ __forceinline__ long long block_excl_scan(long long v, ProjShared& sh,
@@ -188,36 +152,30 @@ __device__ __forceinline__ long long block_excl_scan(long long v, ProjShared& sh
   return base + inc - v;
 }
 
-// Cluster-wide combine of per-CTA values.  kinds[c]: 0 = canonical tree over ranks,
-// 1 = max, 2 = plain sum.  Every CTA must call it in the same order.
-__device__ void cluster_combine(double* vals, const int* kinds, int nv, ProjShared& sh,
-                                cg::cluster_group& cl, int cs) {
+// Cluster-wide combine of per-CTA values (identical in every thread of a CTA).  kinds[c]:
+// 0 = canonical tree over ranks, 1 = max, 2 = plain sum.  Each CTA pushes its values into
+// every CTA's slots (DSMEM stores ahead of the cluster barrier), then every warp combines the
+// local slots by a butterfly over the rank.  Every CTA must call it in the same order.
+__device__ __forceinline__ void cluster_combine(double* vals, const int* kinds, int nv,
+                                                ProjShared& sh, cg::cluster_group& cl, int cs,
+                                                RedPar& rp) {
   if (cs == 1) return;
-  const int par = sh.red_par;
   const unsigned rank = cl.block_rank();
-  if (threadIdx.x == 0)
-    for (int c = 0; c < nv; ++c) sh.slot[par][rank][c] = vals[c];
-  cl.sync();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    double x[4] = {0.0, 0.0, 0.0, 0.0};
-    if (lane < cs) {
-      const ProjShared* rem = cl.map_shared_rank(&sh, lane);
-      for (int c = 0; c < nv; ++c) x[c] = rem->slot[par][lane][c];
-    }
-    for (int c = 0; c < nv; ++c) {
-      for (int o = 1; o < cs; o <<= 1) {
-        const double y = __shfl_xor_sync(0xffffffffu, x[c], o);
-        x[c] = kinds[c] == 1 ? fmax(x[c], y) : add(x[c], y);
-      }
-      if (lane == 0) sh.bc[c] = x[c];
-    }
+  if ((int)threadIdx.x < cs) {
+    ProjShared* dst = cl.map_shared_rank(&sh, (int)threadIdx.x);
+    for (int c = 0; c < nv; ++c) dst->slot[rp.c][rank][c] = vals[c];
   }
-  __syncthreads();
-  for (int c = 0; c < nv; ++c) vals[c] = sh.bc[c];
-  __syncthreads();
-  if (threadIdx.x == 0) sh.red_par = par ^ 1;
-  __syncthreads();
+  cl.sync();
+  const int lane = threadIdx.x & 31;
+  for (int c = 0; c < nv; ++c) {
+    double x = lane < cs ? sh.slot[rp.c][lane][c] : (kinds[c] == 1 ? -1.0 : 0.0);
+    for (int o = 1; o < cs; o <<= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, x, o);
+      x = kinds[c] == 1 ? fmax(x, y) : add(x, y);
+    }
+    vals[c] = __shfl_sync(0xffffffffu, x, 0);
+  }
+  rp.c ^= 1;
 }
 
 // descending bitonic sort of n2 (power of two) values by the first min(PT, n2/2) threads
@@ -266,7 +224,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   const int64_t pofs = prob * a.bstride;
   DevState* st = a.st + prob;
   const int tid = threadIdx.x;
-  if (tid == 0) sh.red_par = 0;
+  RedPar rp{0, 0};
   const bool prof = (a.mode == PROJ_ITER) && rank == 0 && tid == 0;
   long long t_last = clock64();
   auto mark = [&](int idx) {
@@ -341,8 +299,11 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       sh.bc[6] = r0->bc[6];
       sh.dec = r0->dec;
     }
-    cl.sync();
-    if (sh.dec != 0) return;
+    __syncthreads();  // (CTA 0 rewrites bc / dec only after later cluster barriers)
+    if (sh.dec != 0) {
+      cl.sync();  // no CTA leaves while another may still read its shared memory
+      return;
+    }
     alpha = first_alpha = sh.bc[6];
   }
 
@@ -393,8 +354,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       red[0] = t;
       red[1] = m;
       const int kinds[2] = {0, 1};
-      block_reduce<2>(red, kinds, sh);
-      cluster_combine(red, kinds, 2, sh, cl, cs);
+      block_reduce<2>(red, kinds, sh, rp);
+      cluster_combine(red, kinds, 2, sh, cl, cs, rp);
     }
     const double l1v = red[0], vinf = red[1];
     mark(1);
@@ -430,8 +391,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
             v2[1] += m;
           }
         }
-        block_reduce<2>(v2, kinds_cs, sh);
-        cluster_combine(v2, kinds_cs, 2, sh, cl, cs);
+        block_reduce<2>(v2, kinds_cs, sh, rp);
+        cluster_combine(v2, kinds_cs, 2, sh, cl, cs, rp);
         count(10, 1.0);
         if (warm) {  // first step from the previous theta
           warm = false;
@@ -465,37 +426,31 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         }
         long long ctot;
         const long long off = block_excl_scan(myc, sh, &ctot);
-        const double bnext = block_max(mynext, sh);
+        double bnx[1] = {mynext};
+        const int k_max[1] = {1};
+        block_reduce<1>(bnx, k_max, sh, rp);
+        const double bnext = bnx[0];
         long long before = 0, total = ctot;
         double next = bnext;
-        if (cs > 1) {
-          if (tid == 0) {
-            sh.slotl[sh.red_par][rank] = ctot;
-            sh.slot[sh.red_par][rank][0] = bnext;
+        if (cs > 1) {  // counts and the next value below the bracket, pushed to every CTA
+          if (tid < cs) {
+            ProjShared* dst = cl.map_shared_rank(&sh, tid);
+            dst->slotl[rp.c][rank] = ctot;
+            dst->slot[rp.c][rank][0] = bnext;
           }
           cl.sync();
-          if (tid == 0) {
-            long long b = 0, tt = 0;
-            double nx = -1.0;
-            const int par = sh.red_par;
-            for (int r = 0; r < cs; ++r) {
-              const ProjShared* rem = cl.map_shared_rank(&sh, r);
-              const long long cr = rem->slotl[par][r];
-              b += r < (int)rank ? cr : 0;
-              tt += cr;
-              nx = fmax(nx, rem->slot[par][r][0]);
-            }
-            sh.wl[0][0] = b;
-            sh.wl[0][1] = tt;
-            sh.bc[5] = nx;
+          long long b = 0, tt = 0;
+          double nx = -1.0;
+          for (int r = 0; r < cs; ++r) {
+            const long long cr = sh.slotl[rp.c][r];
+            b += r < (int)rank ? cr : 0;
+            tt += cr;
+            nx = fmax(nx, sh.slot[rp.c][r][0]);
           }
-          __syncthreads();
-          before = sh.wl[0][0];
-          total = sh.wl[0][1];
-          next = sh.bc[5];
-          __syncthreads();
-          if (tid == 0) sh.red_par ^= 1;
-          __syncthreads();
+          before = b;
+          total = tt;
+          next = nx;
+          rp.c ^= 1;
         }
         const long long L = total + (next >= 0.0 ? 1 : 0);
         mark(14);
@@ -670,18 +625,17 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
               double s_before = 0.0;
               const long long ff = prefix_break(c, L, rho, scan_sh, &s_before);
               count(20, (double)scan_sh.epochs);
-              count(21, (double)ff);
               if (tid == 0) {
                 sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
                 sh.dec = (ff == L && next >= 0.0) ? 1 : 0;
               }
               mark(5);
-            }
-            cl.sync();
-            if (tid == 0 && rank != 0) {
-              const ProjShared* r0 = cl.map_shared_rank(&sh, 0);
-              sh.bc[4] = r0->bc[4];
-              sh.dec = r0->dec;
+              __syncthreads();
+              if (tid > 0 && tid < cs) {  // push theta and the decision to the other CTAs
+                ProjShared* dst = cl.map_shared_rank(&sh, tid);
+                dst->bc[4] = sh.bc[4];
+                dst->dec = sh.dec;
+              }
             }
             cl.sync();
             if (!sh.dec) {
@@ -720,7 +674,6 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           double s_before = 0.0;
           const long long ff = prefix_break(c, L, rho, scan_sh, &s_before);
           count(20, (double)scan_sh.epochs);
-              count(21, (double)ff);
           if (tid == 0) {
             // theta = candidate of the last passing index (prox.cpp:47-50); 0 if none passed
             sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
@@ -728,12 +681,12 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
             sh.dec = (ff == L && next >= 0.0) ? 1 : 0;
           }
           mark(5);
-        }
-        cl.sync();
-        if (tid == 0 && rank != 0) {
-          const ProjShared* r0 = cl.map_shared_rank(&sh, 0);
-          sh.bc[4] = r0->bc[4];
-          sh.dec = r0->dec;
+          __syncthreads();
+          if (tid > 0 && tid < cs) {  // push theta and the decision to the other CTAs
+            ProjShared* dst = cl.map_shared_rank(&sh, tid);
+            dst->bc[4] = sh.bc[4];
+            dst->dec = sh.dec;
+          }
         }
         if (cs > 1) cl.sync();
         else __syncthreads();
@@ -751,8 +704,9 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       int guard = 0;
       for (;;) {
         const double thc = theta;
-        double l1u[1] = {block_tree(tree<M>([&](int k) { return fabs(soft(v[k], thc)); }), sh, 1)};
-        cluster_combine(l1u, k_sum, 1, sh, cl, cs);
+        double l1u[1] = {tree<M>([&](int k) { return fabs(soft(v[k], thc)); })};
+        block_reduce<1>(l1u, k_sum, sh, rp);
+        cluster_combine(l1u, k_sum, 1, sh, cl, cs, rp);
         if (!(l1u[0] > rho && guard++ < 64)) break;
         count(12, 1.0);
         theta = add(theta, bump);
@@ -809,8 +763,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     }
     double red2[4] = {gdl, lmax, hmax, (double)sup};
     const int kinds2[4] = {0, 1, 1, 2};
-    block_reduce<4>(red2, kinds2, sh);
-    cluster_combine(red2, kinds2, 4, sh, cl, cs);
+    block_reduce<4>(red2, kinds2, sh, rp);
+    cluster_combine(red2, kinds2, 4, sh, cl, cs, rp);
     const double gd = red2[0], stat = red2[1], hinf = red2[2];
     const long long support = (long long)red2[3];
     mark(7);
