@@ -78,6 +78,21 @@ struct Counter {
       open = open && bit;
     }
   }
+  // a whole aligned subtree of 2^S leaves whose first leaf is idx << S (same carries as its
+  // leaves pushed one by one)
+  template <int S>
+  __device__ __forceinline__ void push_node(double v, uint32_t idx) {
+    bool open = true;
+#pragma unroll
+    for (int l = S; l < L; ++l) {
+      const bool bit = (idx >> (l - S)) & 1u;
+      const double merged = add(lvl[l], v);
+      const bool store = open && !bit;
+      lvl[l] = store ? v : lvl[l];
+      v = (open && bit) ? merged : v;
+      open = open && bit;
+    }
+  }
   __device__ __forceinline__ double final_value(uint32_t count) const {
     double acc = 0.0;
     bool have = false;

@@ -53,6 +53,7 @@ struct FwdArgs {
   DevState* st;
   VecBufs vb;
   BatchStrides bs;     // finish kernels: partial stride, per-problem offsets (blockIdx.y)
+  int wpg;             // finish kernels: warps per output group (fin_wpg)
 };
 
 struct AdjArgs {
@@ -68,6 +69,7 @@ struct AdjArgs {
   DevState* st;
   VecBufs vb;
   BatchStrides bs;
+  int wpg;  // finish kernel: warps per output group (fin_wpg)
 };
 
 template <int N, class F>
@@ -122,6 +124,71 @@ __device__ __forceinline__ int d_pos(int u) {
 __device__ __forceinline__ int rs_pos(int i) { return i + (i >> 3); }
 
 // ============================================================================ finish kernels
+// The finish kernels are chains of dependent memory round trips (partials, vectors, state,
+// group sums); every load that does not depend on an earlier one is issued up front.
+
+// canonical tree over partials k in [lo, hi) of one output (p + k * stride), lo a multiple
+// of 16 or the block start: chunks of 16 loads in flight at once, each chunk a register tree
+// (absent leaves past hi read as +0.0, which leaves every sum unchanged) pushed into the
+// binary counter as one level-4 node.  Returns the block value.
+template <int L>
+__device__ __forceinline__ double tree16(const double (&v)[16]) {
+  double t[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) t[i] = add(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t[i] = add(t[2 * i], t[2 * i + 1]);
+  return add(add(t[0], t[1]), add(t[2], t[3]));
+}
+template <int NA>
+__device__ __forceinline__ void chunk_trees(const double* p, int64_t stride, int lo, int hi,
+                                            double* out) {
+  Counter<16> acc[NA];
+  for (int k0 = lo; k0 < hi; k0 += 16) {
+    const int n = hi - k0 < 16 ? hi - k0 : 16;
+    double v[NA][16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      if (NA == 2) {
+        const double2 w = u < n ? __ldcg(reinterpret_cast<const double2*>(p + (int64_t)(k0 + u) * stride))
+                                : make_double2(0.0, 0.0);
+        v[0][u] = w.x;
+        v[NA - 1][u] = w.y;
+      } else {
+        v[0][u] = u < n ? __ldcg(p + (int64_t)(k0 + u) * stride) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NA; ++j) acc[j].template push_node<4>(tree16<0>(v[j]), (uint32_t)((k0 - lo) >> 4));
+  }
+  const uint32_t cnt = (uint32_t)(((hi - lo) + 15) & ~15);
+#pragma unroll
+  for (int j = 0; j < NA; ++j) out[j] = acc[j].final_value(cnt);
+}
+
+// the state words, loaded by warp 0 into registers ahead of other loads, stored to shared
+constexpr int DS_WORDS = (int)(sizeof(DevState) / 8);
+constexpr int DS_PER_LANE = (DS_WORDS + 31) / 32;
+__device__ __forceinline__ void state_prefetch(const DevState* st, int lane,
+                                               unsigned long long (&w)[DS_PER_LANE]) {
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(st);
+#pragma unroll
+  for (int i = 0; i < DS_PER_LANE; ++i) {
+    const int j = lane + 32 * i;
+    w[i] = j < DS_WORDS ? __ldcg(s + j) : 0ull;
+  }
+}
+__device__ __forceinline__ void state_store(DevState* dst, int lane,
+                                            const unsigned long long (&w)[DS_PER_LANE]) {
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(dst);
+#pragma unroll
+  for (int i = 0; i < DS_PER_LANE; ++i) {
+    const int j = lane + 32 * i;
+    if (j < DS_WORDS) d[j] = w[i];
+  }
+  __syncwarp();
+}
+
 // One CTA of 8 warps per 32 rows (forward) or 64 columns (adjoint): the task partials of
 // each output are split over the warps in aligned power-of-two blocks (a binary counter per
 // warp), warp 0 joins the 8 block values pairwise (blocks past the count are absent), runs
@@ -192,47 +259,80 @@ __device__ __forceinline__ void cta_tree_arrays(const double* v, int count, int 
   }
 }
 
+// warps per output group: enough that each warp's aligned block of partials is <= 16 loads
+// (all in flight at once); a CTA of FIN_W warps finishes FIN_W / wpg groups
+static inline int fin_wpg(int cnt) {
+  int w = 1;
+  while (w < FIN_W && w * 16 < cnt) w <<= 1;
+  return w;
+}
+__device__ __forceinline__ int fin_block_w(int cnt, int wpg) {
+  int B = 1;
+  while (B * wpg < cnt) B <<= 1;
+  return B;
+}
+// join of the wpg block values of one output (nb of them present)
+__device__ __forceinline__ double fin_join_w(const double (*sv)[32], int wpg, int nb, int lane) {
+  double x[FIN_W];
+#pragma unroll
+  for (int w = 0; w < FIN_W; ++w) x[w] = w < wpg ? sv[w][lane] : 0.0;
+#pragma unroll
+  for (int h = 1; h < FIN_W; h <<= 1)
+#pragma unroll
+    for (int i = 0; i + h < FIN_W; i += 2 * h)
+      if (i + h < nb) x[i] = add(x[i], x[i + h]);
+  return x[0];
+}
+
 __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a0) {
   pdl_wait_and_trigger();
   FwdArgs a = batch_view(a0, blockIdx.y);
   if (blockIdx.y && a.vout) a.vout += blockIdx.y * a0.bs.bn;
   const int64_t on = blockIdx.y * a0.bs.bn;
-  if (a.mode != FWD_APPLY && a.st->status != RUNNING) return;
   __shared__ double sv[FIN_W][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = blockIdx.x, ngrp = gridDim.x;
-  const int64_t row = (int64_t)grp * 32 + lane;
-  {
-    const int B = fin_block(a.ncr);
-    const int lo = warp * B, hi = lo + B < a.ncr ? lo + B : a.ncr;
-    Counter<16> acc;
-    int k = lo;
-    for (; k + 4 <= hi; k += 4) {
-      double v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = __ldcg(a.part + (int64_t)(k + u) * a.bs.pstride + row);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc.push(v[u], (uint32_t)(k + u - lo));
+  const int wpg = a.wpg, gl = warp / wpg, wi = warp - gl * wpg;
+  const int ngrp = (int)(a.n_pad / 32);
+  const int grp = blockIdx.x * (FIN_W / wpg) + gl;
+  const bool live = grp < ngrp;
+  const int64_t row = (int64_t)(live ? grp : 0) * 32 + lane;
+  // independent loads first: the state words the group leader needs, y or both r buffers
+  int status = RUNNING, cur = 0;
+  double pre0 = 0.0, pre1 = 0.0;
+  if (a.mode != FWD_APPLY) {
+    status = __ldcg(&a.st->status);
+    if (wi == 0 && live) {
+      cur = __ldcg(&a.st->cur);
+      if (a.mode == FWD_INIT) {
+        pre0 = __ldcg(a0.vb.y + on + row);
+      } else {
+        pre0 = __ldcg(a0.vb.r[0] + on + row);
+        pre1 = __ldcg(a0.vb.r[1] + on + row);
+      }
     }
-    for (; k < hi; ++k) acc.push(__ldcg(a.part + (int64_t)k * a.bs.pstride + row), (uint32_t)(k - lo));
-    sv[warp][lane] = hi > lo ? acc.final_value((uint32_t)(hi - lo)) : 0.0;
+  }
+  const int B = fin_block_w(a.ncr, wpg);
+  {
+    const int lo = wi * B, hi = lo + B < a.ncr ? lo + B : a.ncr;
+    double bv[1] = {0.0};
+    if (live && hi > lo) chunk_trees<1>(a.part + row, a.bs.pstride, lo, hi, bv);
+    sv[warp][lane] = bv[0];
     __syncthreads();
   }
-  __shared__ unsigned s_last;
-  if (warp == 0) {
-    const double kd = fin_join(sv, (a.ncr + fin_block(a.ncr) - 1) / fin_block(a.ncr), lane);
+  if (status != RUNNING) return;
+  if (wi == 0 && live) {
+    const double kd = fin_join_w(sv + gl * wpg, wpg, (a.ncr + B - 1) / B, lane);
     if (a.mode == FWD_APPLY) {
       a.vout[row] = kd;
     } else {
-      const int cur = a.st->cur;
       double l0, l1 = 0.0;
       if (a.mode == FWD_INIT) {
-        const double r = sub(kd, a0.vb.y[on + row]);  // Kx0 - y   (gpss.cpp:128)
+        const double r = sub(kd, pre0);  // Kx0 - y   (gpss.cpp:128)
         a0.vb.r[cur][on + row] = r;
         l0 = mul(r, r);                         // ||r||^2   (gpss.cpp:129)
       } else {
         a0.vb.kd[on + row] = kd;
-        l0 = mul(a0.vb.r[cur][on + row], kd);         // (Kx-y)'Kd (gpss.cpp:195)
+        l0 = mul(cur ? pre1 : pre0, kd);        // (Kx-y)'Kd (gpss.cpp:195)
         l1 = mul(kd, kd);                       // ||Kd||^2  (gpss.cpp:196)
       }
       l0 = warp_tree(l0);
@@ -241,25 +341,29 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a0) {
         a.grpsum[2 * grp + 0] = l0;
         a.grpsum[2 * grp + 1] = l1;
         __threadfence();
-        s_last = atomicAdd(a.cnt_all, 1u) == (unsigned)ngrp - 1u;
       }
     }
   }
   if (a.mode == FWD_APPLY) return;
+  __shared__ unsigned s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.cnt_all, 1u) == gridDim.x - 1u;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  unsigned long long sw[DS_PER_LANE];
+  if (warp == 0) state_prefetch(a.st, lane, sw);  // in flight with the group sums
   __shared__ double tsv[2][FIN_W][32];
   double AB[2];
   cta_tree_arrays<2>(a.grpsum, ngrp, 2, tsv, AB);
   if (warp != 0) return;
-  const double A = AB[0], B = AB[1];
+  const double A = AB[0], Bv = AB[1];
   __shared__ DevState s;
-  snapshot(&s, a.st, lane);
+  state_store(&s, lane, sw);
   if (lane != 0) return;
   *a.cnt_all = 0;
   if (a.task_ctr) *a.task_ctr = 0;
-  fwd_tail(a.st, s, a.mode, A, B);
+  fwd_tail(a.st, s, a.mode, A, Bv);
 }
 
 __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
@@ -267,54 +371,57 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
   AdjArgs a = batch_view(a0, blockIdx.y);
   if (blockIdx.y && a.vout) a.vout += blockIdx.y * a0.bs.bp;
   const int64_t ofp = blockIdx.y * a0.bs.bp;
-  if (a.mode != ADJ_APPLY && a.st->status != RUNNING) return;
   __shared__ double sv[2][FIN_W][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = blockIdx.x, ngrp = gridDim.x;
-  const int64_t col = (int64_t)grp * 64 + 2 * lane;
-  {
-    const int B = fin_block(a.nrr);
-    const int lo = warp * B, hi = lo + B < a.nrr ? lo + B : a.nrr;
-    Counter<16> acc0, acc1;
-    int k = lo;
-    for (; k + 4 <= hi; k += 4) {
-      double2 v[4];
+  const int wpg = a.wpg, gl = warp / wpg, wi = warp - gl * wpg;
+  const int ngrp = (int)(a.p_pad / 64);
+  const int grp = blockIdx.x * (FIN_W / wpg) + gl;
+  const bool live = grp < ngrp;
+  const int64_t col = (int64_t)(live ? grp : 0) * 64 + 2 * lane;
+  DevState* st = a.st;
+  // independent loads first: state words, and (ITER) x, g of both buffers and d
+  int status = RUNNING, cur = 0;
+  double lam = 0.0;
+  double2 xb[2], gb[2], dd;
+  if (a.mode != ADJ_APPLY) {
+    status = __ldcg(&st->status);
+    if (wi == 0 && live) {
+      cur = __ldcg(&st->cur);
+      if (a.mode == ADJ_ITER) {
+        lam = __ldcg(&st->step);
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        v[u] = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)(k + u) * a.bs.pstride + col));
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        acc0.push(v[u].x, (uint32_t)(k + u - lo));
-        acc1.push(v[u].y, (uint32_t)(k + u - lo));
+        for (int b = 0; b < 2; ++b) {
+          xb[b] = __ldcg(reinterpret_cast<const double2*>(a0.vb.x[b] + ofp + col));
+          gb[b] = __ldcg(reinterpret_cast<const double2*>(a0.vb.g[b] + ofp + col));
+        }
+        dd = __ldcg(reinterpret_cast<const double2*>(a0.vb.d + ofp + col));
       }
     }
-    for (; k < hi; ++k) {
-      const double2 v = __ldcg(reinterpret_cast<const double2*>(a.part + (int64_t)k * a.bs.pstride + col));
-      acc0.push(v.x, (uint32_t)(k - lo));
-      acc1.push(v.y, (uint32_t)(k - lo));
-    }
-    sv[0][warp][lane] = hi > lo ? acc0.final_value((uint32_t)(hi - lo)) : 0.0;
-    sv[1][warp][lane] = hi > lo ? acc1.final_value((uint32_t)(hi - lo)) : 0.0;
+  }
+  const int B = fin_block_w(a.nrr, wpg);
+  {
+    const int lo = wi * B, hi = lo + B < a.nrr ? lo + B : a.nrr;
+    double bv[2] = {0.0, 0.0};
+    if (live && hi > lo) chunk_trees<2>(a.part + col, a.bs.pstride, lo, hi, bv);
+    sv[0][warp][lane] = bv[0];
+    sv[1][warp][lane] = bv[1];
     __syncthreads();
   }
-  DevState* st = a.st;
-  __shared__ unsigned s_last;
-  if (warp == 0) {
-    const int nb = (a.nrr + fin_block(a.nrr) - 1) / fin_block(a.nrr);
-    const double s0 = fin_join(sv[0], nb, lane), s1 = fin_join(sv[1], nb, lane);
+  if (status != RUNNING) return;
+  if (wi == 0 && live) {
+    const int nb = (a.nrr + B - 1) / B;
+    const double s0 = fin_join_w(sv[0] + gl * wpg, wpg, nb, lane);
+    const double s1 = fin_join_w(sv[1] + gl * wpg, wpg, nb, lane);
     if (a.mode == ADJ_APPLY) {
       *reinterpret_cast<double2*>(a.vout + col) = make_double2(s0, s1);
     } else {
-      const int cur = st->cur;
       const double g0 = mul(2.0, s0), g1 = mul(2.0, s1);  // 2 K^T r (gpss.cpp:130, :211)
       if (a.mode == ADJ_INIT) {
         *reinterpret_cast<double2*>(a0.vb.g[cur] + ofp + col) = make_double2(g0, g1);
       } else {
         // x' = x + lambda d (gpss.cpp:208), s = x' - x, z = g' - g (gpss.cpp:150-151)
-        const double lam = st->step;
-        const double2 xo = *reinterpret_cast<const double2*>(a0.vb.x[cur] + ofp + col);
-        const double2 go = *reinterpret_cast<const double2*>(a0.vb.g[cur] + ofp + col);
-        const double2 dd = *reinterpret_cast<const double2*>(a0.vb.d + ofp + col);
+        const double2 xo = cur ? xb[1] : xb[0];
+        const double2 go = cur ? gb[1] : gb[0];
         const double x0n = add(xo.x, mul(lam, dd.x)), x1n = add(xo.y, mul(lam, dd.y));
         *reinterpret_cast<double2*>(a0.vb.x[cur ^ 1] + ofp + col) = make_double2(x0n, x1n);
         *reinterpret_cast<double2*>(a0.vb.g[cur ^ 1] + ofp + col) = make_double2(g0, g1);
@@ -328,22 +435,26 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
           a.grpsum[3 * grp + 1] = dss;
           a.grpsum[3 * grp + 2] = dzz;
           __threadfence();
-          s_last = atomicAdd(a.cnt_all, 1u) == (unsigned)ngrp - 1u;
         }
       }
     }
   }
   if (a.mode != ADJ_ITER) return;
+  __shared__ unsigned s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.cnt_all, 1u) == gridDim.x - 1u;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  unsigned long long sw[DS_PER_LANE];
+  if (warp == 0) state_prefetch(st, lane, sw);  // in flight with the group sums
   __shared__ double tsv[3][FIN_W][32];
   double sums[3];
   cta_tree_arrays<3>(a.grpsum, ngrp, 3, tsv, sums);
   if (warp != 0) return;
   const double SZ = sums[0], SS = sums[1], ZZ = sums[2];
   __shared__ DevState s;
-  snapshot(&s, st, lane);
+  state_store(&s, lane, sw);
   if (lane != 0) return;
   *a.cnt_all = 0;
   adj_tail(st, s, SZ, SS, ZZ);
@@ -954,18 +1065,29 @@ static void adj_main(const Op& op, const AdjArgs& a, cudaStream_t s) {
   }
 }
 
+static void fin_launch(FwdArgs a, cudaStream_t s) {
+  a.wpg = fin_wpg(a.ncr);
+  const int64_t ngrp = a.n_pad / 32, gpc = FIN_W / a.wpg;
+  L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)((ngrp + gpc - 1) / gpc), FIN_T, 0, s, a));
+}
+static void fin_launch(AdjArgs a, cudaStream_t s) {
+  a.wpg = fin_wpg(a.nrr);
+  const int64_t ngrp = a.p_pad / 64, gpc = FIN_W / a.wpg;
+  L1G_CUDA(launch_pdl(adj_finish_kernel, (int)((ngrp + gpc - 1) / gpc), FIN_T, 0, s, a));
+}
+
 void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
                 const VecBufs* vb, DevState* st, cudaStream_t s, bool sparse) {
   FwdArgs a = fwd_args(op, ws, mode, (mode == FWD_ITER) ? vb->d : vin, vout, vb, st);
   a = fwd_main(op, ws, a, a.vb.dmask, sparse && mode == FWD_ITER, s);
-  L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)(a.n_pad / 32), FIN_T, 0, s, a));
+  fin_launch(a, s);
 }
 
 void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
                 const VecBufs* vb, DevState* st, cudaStream_t s) {
   const AdjArgs a = adj_args(op, ws, mode, vin, vout, vb, st);
   adj_main(op, a, s);
-  L1G_CUDA(launch_pdl(adj_finish_kernel, (int)(a.p_pad / 64), FIN_T, 0, s, a));
+  fin_launch(a, s);
 }
 
 // ---- column-sharded pieces: rank partials and their combination
@@ -974,7 +1096,7 @@ void launch_fwd_part(const Op& op, const Workspace& ws, const double* vin, const
   FwdArgs a = fwd_args(op, ws, FWD_APPLY, vin, out, nullptr, st);
   a = fwd_main(op, ws, a, dmask, sparse, s);
   a.mode = FWD_APPLY;  // the finish only writes the shard's tree values
-  L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)(a.n_pad / 32), FIN_T, 0, s, a));
+  fin_launch(a, s);
 }
 
 void launch_fwd_combine(const Op& op, const Workspace& ws, int mode, const double* recv, int nr,
@@ -983,7 +1105,7 @@ void launch_fwd_combine(const Op& op, const Workspace& ws, int mode, const doubl
   a.part = const_cast<double*>(recv);
   a.ncr = nr;
   a.task_ctr = ws.counters + op.plan.nrg + op.plan.ncg + 2;
-  L1G_CUDA(launch_pdl(fwd_finish_kernel, (int)(a.n_pad / 32), FIN_T, 0, s, a));
+  fin_launch(a, s);
 }
 
 void launch_adj_part(const Op& op, const Workspace& ws, int mode, const VecBufs* vb, double* out,
@@ -991,7 +1113,7 @@ void launch_adj_part(const Op& op, const Workspace& ws, int mode, const VecBufs*
   AdjArgs a = adj_args(op, ws, mode, nullptr, out, vb, st);
   adj_main(op, a, s);
   a.mode = ADJ_APPLY;
-  L1G_CUDA(launch_pdl(adj_finish_kernel, (int)(a.p_pad / 64), FIN_T, 0, s, a));
+  fin_launch(a, s);
 }
 
 void launch_adj_combine(const Op& op, const Workspace& ws, int mode, const double* recv,
@@ -1001,7 +1123,7 @@ void launch_adj_combine(const Op& op, const Workspace& ws, int mode, const doubl
   a.nrr = 1;
   a.p_pad = p_pad_total;
   a.bs.pstride = p_pad_total;
-  L1G_CUDA(launch_pdl(adj_finish_kernel, (int)(p_pad_total / 64), FIN_T, 0, s, a));
+  fin_launch(a, s);
 }
 
 }  // namespace l1g

@@ -245,6 +245,9 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   }
   __syncthreads();
   if (a.mode == PROJ_ITER && sst.status != RUNNING) return;  // uniform over the cluster
+  // every CTA of the cluster is running before any DSMEM access (PROJ_ITER: the barrier of
+  // the steplength broadcast below)
+  if (a.mode != PROJ_ITER && cs > 1) cl.sync();
   const l1g_gp_config cfg = sst.cfg;
   const double rho = sst.rho;
   const int cur = a.mode == PROJ_ITER ? sst.cur : 0;
