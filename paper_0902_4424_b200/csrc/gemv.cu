@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a0) {
   __threadfence();
   unsigned long long sw[DS_PER_LANE];
   if (warp == 0) state_prefetch(a.st, lane, sw);  // in flight with the group sums
-  __shared__ double tsv[2][FIN_W][32];
+  __shared__ double tsv[2][FIN_W][32];  // (sv is one array: the tree needs two)
   double AB[2];
   cta_tree_arrays<2>(a.grpsum, ngrp, 2, tsv, AB);
   if (warp != 0) return;
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
   AdjArgs a = batch_view(a0, blockIdx.y);
   if (blockIdx.y && a.vout) a.vout += blockIdx.y * a0.bs.bp;
   const int64_t ofp = blockIdx.y * a0.bs.bp;
-  __shared__ double sv[2][FIN_W][32];
+  __shared__ double sv[3][FIN_W][32];  // [2] only for the group-sum tree of the last CTA
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wpg = a.wpg, gl = warp / wpg, wi = warp - gl * wpg;
   const int ngrp = (int)(a.p_pad / 64);
@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
   __threadfence();
   unsigned long long sw[DS_PER_LANE];
   if (warp == 0) state_prefetch(st, lane, sw);  // in flight with the group sums
-  __shared__ double tsv[3][FIN_W][32];
+  __syncthreads();  // sv is free: the group-sum tree reuses it
+  double (*tsv)[FIN_W][32] = reinterpret_cast<double (*)[FIN_W][32]>(&sv[0][0][0]);
   double sums[3];
   cta_tree_arrays<3>(a.grpsum, ngrp, 3, tsv, sums);
   if (warp != 0) return;
