@@ -564,7 +564,9 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
             const int cnt = srt.base[rank + 1] - srt.base[rank];
             const bool gather_smem = total + 1 <= a.cand_cap;
             constexpr int RK = M >= 16 ? 8 : 2;  // candidates per thread on the rank path
-            if (cnt <= RK * PT && srt.maxbin <= RANK_MAXBIN) {
+            int maxcnt = 0;  // the path must be the same in every CTA (cluster barriers)
+            for (int d = 0; d < cs; ++d) maxcnt = max(maxcnt, srt.base[d + 1] - srt.base[d]);
+            if (maxcnt <= RK * PT && srt.maxbin <= RANK_MAXBIN) {
               // rank sort: bins are narrow, so an element's place is its bin's start plus the
               // number of larger bin mates (equal ones ordered by position); each element is
               // written straight to its final place in CTA 0 (or the global scratch)
