@@ -56,5 +56,16 @@ def build(force: bool = False, verbose: bool = False):
     return lib_path()
 
 
+def build_variant(name: str, defines: list[str], verbose: bool = False) -> str:
+    """Debug variants (e.g. -DL1G_TIMELINE) as lib<name>.so next to libl1g.so; loaded through
+    L1G_LIB_PATH by the profiling tools only."""
+    out = os.path.join(HERE, f"lib{name}.so")
+    cmd = [NVCC, *FLAGS, *defines, "-o", out, *[os.path.join(CSRC, s) for s in SOURCES]]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    return out
+
+
 if __name__ == "__main__":
     build(force=True, verbose=True)

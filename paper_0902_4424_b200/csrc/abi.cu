@@ -95,6 +95,15 @@ void free_ws(Workspace& ws) {
   ws = Workspace{};
 }
 
+// loop condition of the run graph (build_loop_graph): another body while the run is live
+__global__ void loop_cond_kernel(const DevState* st, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, st->status == RUNNING ? 1u : 0u);
+}
+void loop_cond(const DevState* st, cudaGraphConditionalHandle h, cudaStream_t s) {
+  loop_cond_kernel<<<1, 1, 0, s>>>(st, h);
+  L1G_CUDA(cudaGetLastError());
+}
+
 __global__ void configure_kernel(DevState* st, l1g_stop_rule stop, int single_step,
                                  l1g_iter_record* trace, int64_t cap) {
   st->max_iterations = stop.max_iterations;
@@ -178,6 +187,11 @@ struct l1g_solver {
   int64_t trace_cap = 0;
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   int gsize = 0;
+  // the whole run as one launch: a device-side WHILE loop over gsize iterations
+  // (conditional graph node), when the driver supports it; else the chunked gexec pair
+  cudaGraphExec_t gloop = nullptr;
+  int lsize = 0;  // iterations per loop body (~8 ms of streaming work, 1..64)
+  bool gloop_tried = false;
   // optional per-kernel timing: events [graph][iteration][4] around proj / fwd / adj
   bool timing = false;
   bool fwd_sparse = true;  // forward product over the support of d only (gemv.cu)
@@ -224,6 +238,7 @@ void solver_free(l1g_solver* s) {
   dfree(s->g_recv);
   for (auto& g : s->gexec)
     if (g) cudaGraphExecDestroy(g);
+  if (s->gloop) cudaGraphExecDestroy(s->gloop);
   for (auto e : s->tev) cudaEventDestroy(e);
   free_ws(s->ws);
   for (int i = 0; i < 2; ++i) {
@@ -423,6 +438,9 @@ void drop_graphs(l1g_solver* s) {
       cudaGraphExecDestroy(g);
       g = nullptr;
     }
+  if (s->gloop) cudaGraphExecDestroy(s->gloop);
+  s->gloop = nullptr;
+  s->gloop_tried = false;
   for (auto e : s->tev) cudaEventDestroy(e);
   s->tev.clear();
 }
@@ -460,6 +478,73 @@ void build_graphs(l1g_solver* s) {
     L1G_CUDA(cudaGraphInstantiate(&s->gexec[gi], g, 0));
     cudaGraphDestroy(g);
   }
+}
+
+// One graph for the whole run: WHILE (status == RUNNING) { gsize iterations }.  The loop
+// condition is set on the device after every body, so the host launches once and waits; no
+// graph boundary (a host round trip, ~15-20 us) sits between chunks of iterations.  Returns
+// false (and leaves the chunked graphs in charge) if the driver rejects the construction.
+bool build_loop_graph(l1g_solver* s) {
+  if (s->gloop || s->gloop_tried) return s->gloop != nullptr;
+  s->gloop_tried = true;
+  {
+    const char* e = getenv("L1G_LOOP_GRAPH");
+    if (e && std::strcmp(e, "0") == 0) return false;
+  }
+  {
+    const GemvPlan& pl = s->op->plan;
+    const double bytes = 2.0 * (double)pl.n_pad * (double)pl.p_pad * 8.0 * members(s).size();
+    const double est_us = bytes / 6.0e6 + 15.0;
+    const char* e = getenv("L1G_LOOP_US");
+    const double target = e ? atof(e) : 8000.0;
+    s->lsize = (int)std::max(1.0, std::min(64.0, target / est_us));
+  }
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  bool capturing = false;
+  auto fail = [&](cudaError_t) {
+    if (capturing) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(s->stream, &junk);
+      if (junk) cudaGraphDestroy(junk);
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return false;
+  };
+  cudaError_t e = cudaGraphCreate(&g, 0);
+  if (e != cudaSuccess) return fail(e);
+  cudaGraphConditionalHandle h;
+  e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  if (e != cudaSuccess) return fail(e);
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+  if (e != cudaSuccess) return fail(e);
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  e = cudaStreamBeginCaptureToGraph(s->stream, body, nullptr, nullptr, 0,
+                                    cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return fail(e);
+  capturing = true;
+  try {
+    for (int i = 0; i < s->lsize; ++i) enqueue_iteration(s);
+    loop_cond(s->st, h, s->stream);
+  } catch (const CudaError&) {
+    return fail(cudaErrorUnknown);
+  }
+  cudaGraph_t body_out = nullptr;
+  capturing = false;
+  e = cudaStreamEndCapture(s->stream, &body_out);
+  if (e != cudaSuccess) return fail(e);
+  e = cudaGraphInstantiate(&ex, g, 0);
+  if (e != cudaSuccess) return fail(e);
+  cudaGraphDestroy(g);
+  s->gloop = ex;
+  return true;
 }
 
 void accumulate_timing(l1g_solver* s, int gi, int64_t real_iters) {
@@ -509,6 +594,18 @@ void solver_run(l1g_solver* s, const l1g_stop_rule& stop, l1g_result* res,
   configure(s, stop, 0, trace_host && cap > 0 ? s->trace : nullptr, trace_host ? cap : 0);
   build_graphs(s);
   s->launches += 1;
+  if (!s->timing && build_loop_graph(s)) {
+    int64_t k0 = 0, k1 = 0;
+    L1G_CUDA(cudaMemcpyAsync(&k0, &s->st->k, sizeof(int64_t), cudaMemcpyDeviceToHost, s->stream));
+    L1G_CUDA(cudaGraphLaunch(s->gloop, s->stream));
+    L1G_CUDA(cudaMemcpyAsync(&k1, &s->st->k, sizeof(int64_t), cudaMemcpyDeviceToHost, s->stream));
+    L1G_CUDA(cudaStreamSynchronize(s->stream));
+    // bodies run: the iterations done plus the one whose projection stopped the run
+    const int64_t bodies = (k1 - k0) / s->lsize + 1;
+    s->launches += bodies * (kernels_per_iteration(s) * s->lsize + 1);
+    finalize(s, res, trace_host, cap);
+    return;
+  }
   cudaEvent_t ev[2];
   L1G_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
   L1G_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));

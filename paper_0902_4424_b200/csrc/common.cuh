@@ -213,6 +213,25 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 }  // namespace l1g
 
+// Debug timeline (L1G_TIMELINE builds only; tools/prof_solve.py --timeline): per iteration k
+// and kernel, the earliest CTA entry and the earliest return from griddepcontrol.wait, by
+// atomicMin of %globaltimer into a table of the kernel's translation unit.
+#ifdef L1G_TIMELINE
+#define L1G_TL_ENTRY const unsigned long long tl_entry__ = ::l1g::globaltimer();
+#define L1G_TL_WAITED(cond, tab, kid, k)                                                 \
+  if ((cond) && threadIdx.x == 0) {                                                      \
+    atomicMin(&(tab)[((k) & 255) * 16 + 2 * (kid)], tl_entry__);                         \
+    atomicMin(&(tab)[((k) & 255) * 16 + 2 * (kid) + 1],                                  \
+              (unsigned long long)::l1g::globaltimer());                                 \
+  }
+#define L1G_TL_STAMP(cond, tab, slot, k) \
+  if (cond) (tab)[((k) & 255) * 16 + (slot)] = (unsigned long long)::l1g::globaltimer();
+#else
+#define L1G_TL_ENTRY
+#define L1G_TL_WAITED(cond, tab, kid, k)
+#define L1G_TL_STAMP(cond, tab, slot, k)
+#endif
+
 #define L1G_CUDA(call)                                                                  \
   do {                                                                                  \
     cudaError_t e__ = (call);                                                           \

@@ -22,6 +22,10 @@
 
 namespace l1g {
 
+#ifdef L1G_TIMELINE
+__device__ unsigned long long g_tl_gemv[256 * 16];
+#endif
+
 constexpr int STAGES = 3;
 constexpr int TILES_PER_STAGE = 4;
 constexpr int DPAD = 16;  // padding of the d slice (doubles), covers d_pos<4>(31)
@@ -285,7 +289,9 @@ __device__ __forceinline__ double fin_join_w(const double (*sv)[32], int wpg, in
 }
 
 __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a0) {
+  L1G_TL_ENTRY
   pdl_wait_and_trigger();
+  L1G_TL_WAITED(a0.mode == FWD_ITER && blockIdx.y == 0, g_tl_gemv, 2, a0.st->k)
   FwdArgs a = batch_view(a0, blockIdx.y);
   if (blockIdx.y && a.vout) a.vout += blockIdx.y * a0.bs.bn;
   const int64_t on = blockIdx.y * a0.bs.bn;
@@ -350,6 +356,7 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a0) {
   if (threadIdx.x == 0) s_last = atomicAdd(a.cnt_all, 1u) == gridDim.x - 1u;
   __syncthreads();
   if (!s_last) return;
+  L1G_TL_STAMP(a.mode == FWD_ITER && blockIdx.y == 0 && threadIdx.x == 0, g_tl_gemv, 12, a.st->k)
   __threadfence();
   unsigned long long sw[DS_PER_LANE];
   if (warp == 0) state_prefetch(a.st, lane, sw);  // in flight with the group sums
@@ -364,10 +371,13 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a0) {
   *a.cnt_all = 0;
   if (a.task_ctr) *a.task_ctr = 0;
   fwd_tail(a.st, s, a.mode, A, Bv);
+  L1G_TL_STAMP(a.mode == FWD_ITER && blockIdx.y == 0, g_tl_gemv, 13, s.k)
 }
 
 __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
+  L1G_TL_ENTRY
   pdl_wait_and_trigger();
+  L1G_TL_WAITED(a0.mode == ADJ_ITER && blockIdx.y == 0, g_tl_gemv, 4, a0.st->k)
   AdjArgs a = batch_view(a0, blockIdx.y);
   if (blockIdx.y && a.vout) a.vout += blockIdx.y * a0.bs.bp;
   const int64_t ofp = blockIdx.y * a0.bs.bp;
@@ -445,6 +455,7 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
   if (threadIdx.x == 0) s_last = atomicAdd(a.cnt_all, 1u) == gridDim.x - 1u;
   __syncthreads();
   if (!s_last) return;
+  L1G_TL_STAMP(blockIdx.y == 0 && threadIdx.x == 0, g_tl_gemv, 10, st->k)
   __threadfence();
   unsigned long long sw[DS_PER_LANE];
   if (warp == 0) state_prefetch(st, lane, sw);  // in flight with the group sums
@@ -459,6 +470,7 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
   if (lane != 0) return;
   *a.cnt_all = 0;
   adj_tail(st, s, SZ, SS, ZZ);
+  L1G_TL_STAMP(blockIdx.y == 0, g_tl_gemv, 11, s.k)
 }
 
 // ============================================================================ forward
@@ -558,11 +570,9 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdA
 // ============================================================================ adjoint
 template <int SPLIT>
 __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) adj_kernel(const AdjArgs a) {
-  pdl_wait_and_trigger();
   constexpr int NCONS = 4 * SPLIT;
   constexpr int NQ = 32 / SPLIT;  // column pairs per warp
   constexpr int RPL = 32 / SPLIT; // rows per lane group
-  if (a.mode != ADJ_APPLY && a.st->status != RUNNING) return;
   extern __shared__ __align__(128) unsigned char smem[];
   double* sbase = reinterpret_cast<double*>(smem);
   double* vslot = sbase + (size_t)STAGES * ADJ_STAGE_DBL;         // [2][2][MAX_TR] r, kd
@@ -585,6 +595,28 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) adj_kernel(const AdjA
   }
   __syncthreads();
   const int ntasks = a.ncg * a.nrr;
+  // K is immutable: the first ring stages of this CTA's first task are requested before
+  // waiting for the preceding grid (PDL), so the ring fill overlaps the previous kernel.
+  L1G_TL_ENTRY
+  int npre = 0;
+  if (threadIdx.x == 0 && (int)blockIdx.x < ntasks) {
+    const int t = blockIdx.x;
+    const int cg = t / a.nrr, rr = t - cg * a.nrr;
+    const int64_t rb0 = (int64_t)rr * a.blocks;
+    const int nb = (int)(a.nrb - rb0 < (int64_t)a.blocks ? a.nrb - rb0 : (int64_t)a.blocks);
+    npre = nb < STAGES ? nb : STAGES;
+    for (int s = 0; s < npre; ++s) {
+      mbar_arrive_expect_tx(&full[s], TILES_PER_STAGE * TILE_BYTES);
+      bulk_g2s(sbase + (size_t)s * ADJ_STAGE_DBL, a.K + tile_offset(rb0 + s, 4 * (int64_t)cg, a.ncb),
+               TILES_PER_STAGE * TILE_BYTES, &full[s]);
+    }
+  }
+  pdl_wait_and_trigger();
+  L1G_TL_WAITED(a.mode == ADJ_ITER, g_tl_gemv, 3, a.st->k)
+  if (a.mode != ADJ_APPLY && a.st->status != RUNNING) {
+    for (int s = 0; s < npre; ++s) mbar_wait(&full[s], 0);  // no copy outlives the CTA
+    return;
+  }
   const int64_t tr = (int64_t)a.blocks * TR;
   const int cur = (a.mode == ADJ_APPLY) ? 0 : a.st->cur;
   const double* rin = (a.mode == ADJ_APPLY) ? a.vin : a.vb.r[cur];
@@ -606,11 +638,13 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) adj_kernel(const AdjA
         bulk_g2s(vs, rin + row0, vbytes, &vfull[j & 1]);
         if (a.mode == ADJ_ITER) bulk_g2s(vs + MAX_TR, a.vb.kd + row0, vbytes, &vfull[j & 1]);
         for (int s = 0; s < nb; ++s) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          mbar_arrive_expect_tx(&full[stage], TILES_PER_STAGE * TILE_BYTES);
-          bulk_g2s(sbase + (size_t)stage * ADJ_STAGE_DBL,
-                   a.K + tile_offset(rb0 + s, 4 * (int64_t)cg, a.ncb),
-                   TILES_PER_STAGE * TILE_BYTES, &full[stage]);
+          if (j > 0 || s >= npre) {  // (the first npre stages were issued before the wait)
+            mbar_wait(&empty[stage], phase ^ 1u);
+            mbar_arrive_expect_tx(&full[stage], TILES_PER_STAGE * TILE_BYTES);
+            bulk_g2s(sbase + (size_t)stage * ADJ_STAGE_DBL,
+                     a.K + tile_offset(rb0 + s, 4 * (int64_t)cg, a.ncb),
+                     TILES_PER_STAGE * TILE_BYTES, &full[stage]);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1u;
@@ -724,7 +758,9 @@ static size_t sp_smem() {
 }
 
 __global__ void __launch_bounds__(32 * (SP_NCW + 1), 1) fwd_sparse_kernel(const FwdArgs a) {
+  L1G_TL_ENTRY
   pdl_wait_and_trigger();
+  L1G_TL_WAITED(true, g_tl_gemv, 1, a.st->k)
   if (a.st->status != RUNNING) return;
   extern __shared__ __align__(128) unsigned char smem[];
   SpEnt* ent = reinterpret_cast<SpEnt*>(smem);  // [2][SP_W]
@@ -1128,3 +1164,14 @@ void launch_adj_combine(const Op& op, const Workspace& ws, int mode, const doubl
 }
 
 }  // namespace l1g
+
+#ifdef L1G_TIMELINE
+extern "C" int l1g_debug_timeline_gemv(unsigned long long* out4096, int reset) {
+  if (reset) {
+    static unsigned long long ones[256 * 16];
+    for (auto& v : ones) v = ~0ull;
+    return (int)cudaMemcpyToSymbol(l1g::g_tl_gemv, ones, sizeof(ones));
+  }
+  return (int)cudaMemcpyFromSymbol(out4096, l1g::g_tl_gemv, sizeof(unsigned long long) * 256 * 16);
+}
+#endif

@@ -208,9 +208,15 @@ __device__ __forceinline__ double soft(double v, double th) {
 }
 
 // ---------------------------------------------------------------- the kernel
+#ifdef L1G_TIMELINE
+__device__ unsigned long long g_tl_proj[256 * 16];
+#endif
+
 template <int M>
 __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
+  L1G_TL_ENTRY
   pdl_wait_and_trigger();
+  L1G_TL_WAITED(a.mode == PROJ_ITER && blockIdx.x == 0, g_tl_proj, 0, a.st->k)
   cg::cluster_group cl = cg::this_cluster();
   const unsigned rank = cl.block_rank();
   const int cs = a.cs;
@@ -823,6 +829,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   }
   if (prof)
     for (int i = 0; i < 24; ++i) st->prof[i] = sst.prof[i];
+  L1G_TL_STAMP(a.mode == PROJ_ITER && blockIdx.x == 0 && tid == 0, g_tl_proj, 14, sst.k)
   cl.sync();
 }
 
@@ -940,5 +947,16 @@ extern "C" int l1g_debug_prefix_trace(long long* trace192, long long* stamps520)
   cudaMemcpyFromSymbol(trace192, g_ptrace, sizeof(long long) * 192);
   cudaMemcpyFromSymbol(stamps520, g_pstamp, sizeof(long long) * 65 * 8);
   return 0;
+}
+#endif
+
+#ifdef L1G_TIMELINE
+extern "C" int l1g_debug_timeline_proj(unsigned long long* out4096, int reset) {
+  if (reset) {
+    static unsigned long long ones[256 * 16];
+    for (auto& v : ones) v = ~0ull;
+    return (int)cudaMemcpyToSymbol(l1g::g_tl_proj, ones, sizeof(ones));
+  }
+  return (int)cudaMemcpyFromSymbol(out4096, l1g::g_tl_proj, sizeof(unsigned long long) * 256 * 16);
 }
 #endif

@@ -12,11 +12,57 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+if "--timeline" in sys.argv:  # the L1G_TIMELINE build (paper_0902_4424_b200.build.build_variant)
+    os.environ["L1G_LIB_PATH"] = os.path.join(ROOT, "paper_0902_4424_b200", "libl1g_tl.so")
+
 import numpy as np  # noqa: E402
 
 import paper_0902_4424_b200 as l1  # noqa: E402
 from paper_0902_4424_b200 import _lib as L  # noqa: E402
 from paper_0902_4424_b200 import harness as H  # noqa: E402
+
+
+def timeline(lib, iters):
+    """Per kernel: mean in-graph phase (start after griddepcontrol.wait to the next kernel's),
+    and how early its first CTA entered before the wait released."""
+    g, pj = (C.c_ulonglong * 4096)(), (C.c_ulonglong * 4096)()
+    lib.l1g_debug_timeline_gemv(g, 0)
+    lib.l1g_debug_timeline_proj(pj, 0)
+    t = np.minimum(np.frombuffer(g, dtype=np.uint64), np.frombuffer(pj, dtype=np.uint64))
+    t = t.reshape(256, 16).astype(np.float64)
+    names = ["proj", "fwd_sparse", "fwd_finish", "adj", "adj_finish"]
+    ks = [k for k in range(5, min(iters, 256) - 1) if np.all(t[k, :10] < 1.8e19) and t[k + 1, 1] < 1.8e19]
+    if not ks:
+        print("timeline: no complete iterations")
+        return
+    ph, lead = np.zeros(5), np.zeros(5)
+    for k in ks:
+        w = [t[k, 2 * i + 1] for i in range(5)] + [t[k + 1, 1]]
+        for i in range(5):
+            ph[i] += w[i + 1] - w[i]
+            lead[i] += t[k, 2 * i + 1] - t[k, 2 * i]
+    ph /= len(ks)
+    lead /= len(ks)
+    sub = {}
+    for name, a, b in [("adj_finish tail start", 9, 10), ("adj_finish tail", 10, 11),
+                       ("adj_tail -> next proj", 11, 17), ("fwd_finish tail start", 5, 12),
+                       ("fwd_finish tail", 12, 13), ("fwd_tail -> adj", 13, 7),
+                       ("proj body", 1, 14), ("proj end -> fwd_sparse", 14, 3)]:
+        vals = []
+        for k in ks:
+            ta = t[k, a] if a < 16 else t[k + 1, a - 16]
+            tb = t[k, b] if b < 16 else t[k + 1, b - 16]
+            if ta < 1.8e19 and tb < 1.8e19 and tb > 0 and ta > 0:
+                vals.append(tb - ta)
+        if vals:
+            sub[name] = np.median(vals) / 1e3
+            if name == "adj_tail -> next proj":
+                print("adj_tail -> next proj per iteration (us):",
+                      " ".join(f"{v/1e3:.1f}" for v in vals[:24]))
+    print("timeline details (median us): " + "  ".join(f"{k} {v:.2f}" for k, v in sub.items()))
+    print(f"timeline over {len(ks)} iterations (us): " + "  ".join(
+        f"{n} {p/1e3:.2f} (entered {l/1e3:.2f} early)" for n, p, l in zip(names, ph, lead)) +
+        f"  | iteration {ph.sum()/1e3:.2f}")
 
 
 def main():
@@ -27,6 +73,8 @@ def main():
     ap.add_argument("--profile", action="store_true", help="print projection phase profile")
     ap.add_argument("--timing", action="store_true", help="per-kernel CUDA-event timing")
     ap.add_argument("--trace", action="store_true", help="print per-iteration support sizes")
+    ap.add_argument("--timeline", action="store_true",
+                    help="in-graph kernel start times per iteration (libl1g_tl.so)")
     a = ap.parse_args()
     spec = H.CONFIGS[a.config]
     fx = os.path.join(ROOT, "tests", "golden", "sigma_hat.json")
@@ -43,6 +91,9 @@ def main():
     if a.timing:
         L.check(lib.l1g_solver_set_timing(h, 1))
     for s in range(a.solves):
+        if a.timeline:
+            lib.l1g_debug_timeline_gemv(None, 1)
+            lib.l1g_debug_timeline_proj(None, 1)
         t = time.perf_counter()
         L.check(lib.l1g_solver_init(h, None))
         cap = a.iters if a.trace else 0
@@ -56,6 +107,8 @@ def main():
         sup = [recs[i].support for i in range(min(res.iterations, a.iters))]
         print("support per iteration:", sup)
         print("alpha per iteration:", [f"{recs[i].alpha:.3g}" for i in range(min(res.iterations, a.iters))])
+    if a.timeline:
+        timeline(lib, res.iterations)
     if a.timing:
         tp, tf, ta, ti, tl = (C.c_double(), C.c_double(), C.c_double(), C.c_int64(),
                               C.c_int64())
