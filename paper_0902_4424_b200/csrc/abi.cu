@@ -95,12 +95,13 @@ void free_ws(Workspace& ws) {
   ws = Workspace{};
 }
 
-// loop condition of the run graph (build_loop_graph): another body while the run is live
-__global__ void loop_cond_kernel(const DevState* st, cudaGraphConditionalHandle h) {
-  cudaGraphSetConditional(h, st->status == RUNNING ? 1u : 0u);
+// loop condition of the run graphs (make_while_graph): another body while the run is live
+// (single run: its status; batched runs: the live-problem counter)
+__global__ void loop_cond_kernel(const DevState* st, const int* nrun, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, (nrun ? *nrun > 0 : st->status == RUNNING) ? 1u : 0u);
 }
-void loop_cond(const DevState* st, cudaGraphConditionalHandle h, cudaStream_t s) {
-  loop_cond_kernel<<<1, 1, 0, s>>>(st, h);
+void loop_cond(const DevState* st, const int* nrun, cudaGraphConditionalHandle h, cudaStream_t s) {
+  loop_cond_kernel<<<1, 1, 0, s>>>(st, nrun, h);
   L1G_CUDA(cudaGetLastError());
 }
 
@@ -480,17 +481,68 @@ void build_graphs(l1g_solver* s) {
   }
 }
 
-// One graph for the whole run: WHILE (status == RUNNING) { gsize iterations }.  The loop
-// condition is set on the device after every body, so the host launches once and waits; no
-// graph boundary (a host round trip, ~15-20 us) sits between chunks of iterations.  Returns
-// false (and leaves the chunked graphs in charge) if the driver rejects the construction.
+// A graph WHILE (condition) { body }: `body` enqueues the loop body on `st`, `cond` enqueues
+// the kernel that sets the condition for the next round.  The host launches it once and
+// waits; no graph boundary (a host round trip, ~15-20 us) sits between chunks of iterations.
+// Returns nullptr (after cleaning up) if the driver rejects the construction, so callers keep
+// their chunked graphs.
+template <class Body, class Cond>
+cudaGraphExec_t make_while_graph(cudaStream_t st, const Body& body, const Cond& cond) {
+  {
+    const char* e = getenv("L1G_LOOP_GRAPH");
+    if (e && std::strcmp(e, "0") == 0) return nullptr;
+    // under a profiler (ncu / nsys injection environment) -- ncu cannot profile kernel
+    // nodes of graphs with conditional nodes, so profiled runs keep the chunked graphs
+    const bool profiled = getenv("CUDA_INJECTION64_PATH") || getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") ||
+                          getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR");
+    if (profiled && !(e && std::strcmp(e, "1") == 0)) return nullptr;
+  }
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  bool capturing = false;
+  auto fail = [&]() -> cudaGraphExec_t {
+    if (capturing) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(st, &junk);
+      if (junk) cudaGraphDestroy(junk);
+    }
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return nullptr;
+  };
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return fail();
+  cudaGraphConditionalHandle h;
+  if (cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault) != cudaSuccess)
+    return fail();
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &cp) != cudaSuccess) return fail();
+  if (cudaStreamBeginCaptureToGraph(st, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                    cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return fail();
+  capturing = true;
+  try {
+    body();
+    cond(h);
+  } catch (const CudaError&) {
+    return fail();
+  }
+  cudaGraph_t body_out = nullptr;
+  capturing = false;
+  if (cudaStreamEndCapture(st, &body_out) != cudaSuccess) return fail();
+  if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) return fail();
+  cudaGraphDestroy(g);
+  return ex;
+}
+
+// the whole run as one launch: WHILE (status == RUNNING) { lsize iterations }
 bool build_loop_graph(l1g_solver* s) {
   if (s->gloop || s->gloop_tried) return s->gloop != nullptr;
   s->gloop_tried = true;
-  {
-    const char* e = getenv("L1G_LOOP_GRAPH");
-    if (e && std::strcmp(e, "0") == 0) return false;
-  }
   {
     const GemvPlan& pl = s->op->plan;
     const double bytes = 2.0 * (double)pl.n_pad * (double)pl.p_pad * 8.0 * members(s).size();
@@ -499,52 +551,10 @@ bool build_loop_graph(l1g_solver* s) {
     const double target = e ? atof(e) : 8000.0;
     s->lsize = (int)std::max(1.0, std::min(64.0, target / est_us));
   }
-  cudaGraph_t g = nullptr;
-  cudaGraphExec_t ex = nullptr;
-  bool capturing = false;
-  auto fail = [&](cudaError_t) {
-    if (capturing) {
-      cudaGraph_t junk = nullptr;
-      cudaStreamEndCapture(s->stream, &junk);
-      if (junk) cudaGraphDestroy(junk);
-    }
-    if (g) cudaGraphDestroy(g);
-    cudaGetLastError();
-    return false;
-  };
-  cudaError_t e = cudaGraphCreate(&g, 0);
-  if (e != cudaSuccess) return fail(e);
-  cudaGraphConditionalHandle h;
-  e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
-  if (e != cudaSuccess) return fail(e);
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  cudaGraphNode_t node;
-  e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
-  if (e != cudaSuccess) return fail(e);
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  e = cudaStreamBeginCaptureToGraph(s->stream, body, nullptr, nullptr, 0,
-                                    cudaStreamCaptureModeThreadLocal);
-  if (e != cudaSuccess) return fail(e);
-  capturing = true;
-  try {
-    for (int i = 0; i < s->lsize; ++i) enqueue_iteration(s);
-    loop_cond(s->st, h, s->stream);
-  } catch (const CudaError&) {
-    return fail(cudaErrorUnknown);
-  }
-  cudaGraph_t body_out = nullptr;
-  capturing = false;
-  e = cudaStreamEndCapture(s->stream, &body_out);
-  if (e != cudaSuccess) return fail(e);
-  e = cudaGraphInstantiate(&ex, g, 0);
-  if (e != cudaSuccess) return fail(e);
-  cudaGraphDestroy(g);
-  s->gloop = ex;
-  return true;
+  s->gloop = make_while_graph(
+      s->stream, [&] { for (int i = 0; i < s->lsize; ++i) enqueue_iteration(s); },
+      [&](cudaGraphConditionalHandle h) { loop_cond(s->st, nullptr, h, s->stream); });
+  return s->gloop != nullptr;
 }
 
 void accumulate_timing(l1g_solver* s, int gi, int64_t real_iters) {
@@ -774,6 +784,8 @@ struct l1g_batch {
   int* nrun = nullptr;
   int* nrun_host = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  cudaGraphExec_t gloop = nullptr;  // WHILE (live problems) { gsize lockstep iterations }
+  bool gloop_tried = false;
   int gsize = 0;
   int64_t launches = 0;
   bool inited = false;
@@ -786,6 +798,7 @@ void batch_free(l1g_batch* b) {
   if (!b) return;
   cudaSetDevice(b->op->c->device);
   if (b->gexec) cudaGraphExecDestroy(b->gexec);
+  if (b->gloop) cudaGraphExecDestroy(b->gloop);
   for (int i = 0; i < 2; ++i) {
     dfree(b->vb.x[i]);
     dfree(b->vb.g[i]);
@@ -950,9 +963,23 @@ void batch_run(l1g_batch* b, const l1g_stop_rule& stop, l1g_result* res) {
     L1G_CUDA(cudaGraphInstantiate(&b->gexec, g, 0));
     cudaGraphDestroy(g);
   }
+  if (!b->gloop_tried) {
+    b->gloop_tried = true;
+    b->gloop = make_while_graph(
+        s, [&] { for (int i = 0; i < b->gsize; ++i) batch_enqueue_iteration(b); },
+        [&](cudaGraphConditionalHandle h) { loop_cond(nullptr, b->nrun, h, s); });
+  }
   const int64_t cap = stop.max_iterations > 0 ? stop.max_iterations / b->gsize + 3 : INT64_MAX;
   volatile int* flag = b->nrun_host;
-  for (int64_t launched = 0;;) {
+  if (b->gloop) {
+    int64_t k0 = 0, k1 = 0;
+    L1G_CUDA(cudaMemcpyAsync(&k0, &b->st->k, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    L1G_CUDA(cudaGraphLaunch(b->gloop, s));
+    L1G_CUDA(cudaMemcpyAsync(&k1, &b->st->k, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    L1G_CUDA(cudaStreamSynchronize(s));
+    b->launches += ((k1 - k0) / b->gsize + 1) * (6LL * b->gsize + 1);
+  }
+  for (int64_t launched = 0; !b->gloop;) {
     L1G_CUDA(cudaGraphLaunch(b->gexec, s));
     b->launches += 6LL * b->gsize;
     L1G_CUDA(cudaMemcpyAsync((void*)flag, b->nrun, sizeof(int), cudaMemcpyDeviceToHost, s));
