@@ -17,4 +17,7 @@ ncu --set full --import-source on --clock-control none -k regex:"bfwd|badj|proj_
     -o gpurun_out/full_c5 -f python tools/prof_batch.py --iters 5 --solves 1 > gpurun_out/ncu_full_c5.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_c5.csv \
     python tools/prof_batch.py --iters 20 --solves 1 > gpurun_out/ncu_launch_c5.log 2>&1
+# in-graph kernel timeline (debug build with %globaltimer stamps, not a profiler)
+python tools/prof_solve.py --config C2 --iters 80 --solves 2 --timeline > gpurun_out/timeline_c2.txt 2>&1
+python tools/prof_solve.py --config C2 --iters 80 --solves 2 --profile > gpurun_out/proj_phases_c2.txt 2>&1
 ls -la gpurun_out
