@@ -41,6 +41,9 @@ def timeline(lib, iters):
         for i in range(5):
             ph[i] += w[i + 1] - w[i]
             lead[i] += t[k, 2 * i + 1] - t[k, 2 * i]
+    first = [k for k in range(0, min(iters, 256) - 1) if np.all(t[k, :10] < 1.8e19) and t[k + 1, 1] < 1.8e19][:12]
+    print("proj phase of the first iterations (us):",
+          " ".join(f"{(t[k, 3] - t[k, 1]) / 1e3:.0f}" for k in first))
     ph /= len(ks)
     lead /= len(ks)
     sub = {}
