@@ -76,6 +76,7 @@ struct ProjShared {
 // ---------------------------------------------------------------- distributed sort state
 constexpr int NB = 256;  // key-bit bins of the cluster bucket sort
 constexpr int RANK_MAXBIN = 256;  // largest bin the rank sort takes (else bitonic sorts)
+constexpr int SMALL_RANK = 256;   // single-CTA path: rank sort up to this many candidates
 struct SortShared {
   int hist[NB];    // this CTA's candidates per bin
   int gcnt[NB];    // cluster-wide candidates per bin
@@ -675,9 +676,25 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         count(11, (double)total);
         if (rank == 0) {
           double* c = in_smem ? dyn : gcand;
-          for (int64_t i = total + tid; i < n2; i += PT) c[i] = 0.0;
-          __syncthreads();
-          bitonic_desc(c, (int)n2);
+          if (total <= SMALL_RANK) {
+            // few candidates: each one's place is the number of larger ones (equal ones by
+            // position), one thread per candidate, every read a shared-memory broadcast
+            double m = 0.0;
+            int r = 0;
+            if (tid < total) {
+              m = c[tid];
+              for (int j = 0; j < (int)total; ++j) {
+                const double y = c[j];
+                r += (y > m) | ((y == m) & (j < tid));
+              }
+            }
+            __syncthreads();
+            if (tid < total) c[r] = m;
+          } else {
+            for (int64_t i = total + tid; i < n2; i += PT) c[i] = 0.0;
+            __syncthreads();
+            bitonic_desc(c, (int)n2);
+          }
           __syncthreads();
           if (tid == 0 && next >= 0.0) c[total] = next;
           __syncthreads();
