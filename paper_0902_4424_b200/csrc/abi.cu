@@ -493,7 +493,8 @@ cudaGraphExec_t make_while_graph(cudaStream_t st, const Body& body, const Cond& 
     if (e && std::strcmp(e, "0") == 0) return nullptr;
     // under a profiler (ncu / nsys injection environment) -- ncu cannot profile kernel
     // nodes of graphs with conditional nodes, so profiled runs keep the chunked graphs
-    const bool profiled = getenv("CUDA_INJECTION64_PATH") || getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") ||
+    const bool profiled = getenv("CUDA_INJECTION64_PATH") ||
+                          getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") ||
                           getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR");
     if (profiled && !(e && std::strcmp(e, "1") == 0)) return nullptr;
   }
@@ -528,7 +529,7 @@ cudaGraphExec_t make_while_graph(cudaStream_t st, const Body& body, const Cond& 
   try {
     body();
     cond(h);
-  } catch (const CudaError&) {
+  } catch (...) {  // the chunked graphs enqueue the same work and report the error
     return fail();
   }
   cudaGraph_t body_out = nullptr;
