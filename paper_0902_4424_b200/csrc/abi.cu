@@ -376,7 +376,10 @@ void solver_init(l1g_solver* s, const double* x0_host) {
     state_start(q->st, s->stream);
   }
   if (!s->split()) {
-    launch_fwd(*s->op, s->ws, FWD_INIT, s->vb.x[0], nullptr, &s->vb, s->st, s->stream);
+    if (x0_host)
+      launch_fwd(*s->op, s->ws, FWD_INIT, s->vb.x[0], nullptr, &s->vb, s->st, s->stream);
+    else
+      launch_fwd_init_zero(*s->op, s->ws, &s->vb, s->st, s->stream);
     launch_adj(*s->op, s->ws, ADJ_INIT, nullptr, nullptr, &s->vb, s->st, s->stream);
   } else {
     for (l1g_solver* q : m)
@@ -394,7 +397,9 @@ void solver_init(l1g_solver* s, const double* x0_host) {
   for (l1g_solver* q : m)
     launch_proj(q->pp, PROJ_ALPHA0, q->p, q->p_pad, q->vb.x[0], q->vb.g[0], nullptr, q->pscr,
                 q->st, &q->vb, s->stream);
-  s->launches += (x0_host ? 7 : 6) * (int64_t)m.size() + (s->split() ? 2 * (int64_t)m.size() : 0);
+  // (x0 = 0 unsharded: the forward pass over K is skipped, launch_fwd_init_zero)
+  s->launches += (x0_host ? 7 : (s->split() ? 6 : 5)) * (int64_t)m.size() +
+                 (s->split() ? 2 * (int64_t)m.size() : 0);
   s->inited = true;
 }
 

@@ -166,6 +166,8 @@ void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* par
 GemvPlan make_plan(int64_t n, int64_t p, int sm_count);
 void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
                 DevState* st, cudaStream_t s, bool sparse = false);
+void launch_fwd_init_zero(const Op& op, const Workspace& ws, const VecBufs* vb, DevState* st,
+                          cudaStream_t s);
 void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
                 DevState* st, cudaStream_t s);
 // column-sharded runs: the shard's tree values (n_pad / p_pad of the shard) and the

@@ -1120,6 +1120,18 @@ void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, 
   fin_launch(a, s);
 }
 
+// gp_init from x0 = 0 (gpss.cpp:126-129): K x0 is exactly zero (each product is +-0 and so
+// is every pairwise sum; r = +-0 - y = -y either way), so the forward pass over K is skipped
+// and the finish runs on one zero partial per row -- the same r, f and state as the full
+// product.  The matvec is still counted by the caller (test_gpss.cpp:366-375).
+void launch_fwd_init_zero(const Op& op, const Workspace& ws, const VecBufs* vb, DevState* st,
+                          cudaStream_t s) {
+  FwdArgs a = fwd_args(op, ws, FWD_INIT, nullptr, nullptr, vb, st);
+  a.ncr = 1;
+  L1G_CUDA(cudaMemsetAsync(ws.fwd_part, 0, (size_t)op.plan.n_pad * sizeof(double), s));
+  fin_launch(a, s);
+}
+
 void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
                 const VecBufs* vb, DevState* st, cudaStream_t s) {
   const AdjArgs a = adj_args(op, ws, mode, vin, vout, vb, st);
