@@ -902,8 +902,15 @@ void batch_products(l1g_batch* b, int fmode, const double* D, int amode, const d
   if (proj_first)
     launch_proj(b->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, b->pscr, b->st,
                 &b->vb, s, b->B, b->scr_stride);
-  launch_bfwd(*b->op, b->bp, D, b->part, s);
-  launch_bfin(bfin_args(b, fmode, false), false, pl.n_pad, s);
+  if (D) {
+    launch_bfwd(*b->op, b->bp, D, b->part, s);
+    launch_bfin(bfin_args(b, fmode, false), false, pl.n_pad, s);
+  } else {  // gp_init from X0 = 0: K X0 is exactly zero (see launch_fwd_init_zero)
+    BFinArgs fa = bfin_args(b, fmode, false);
+    fa.splits = 1;
+    L1G_CUDA(cudaMemsetAsync(b->part, 0, (size_t)b->bp.Bp * pl.n_pad * sizeof(double), s));
+    launch_bfin(fa, false, pl.n_pad, s);
+  }
   if (rupdate) launch_brupdate(bfin_args(b, fmode, false), b->rn, s);
   launch_badj(*b->op, b->bp, R, b->part, s);
   launch_bfin(bfin_args(b, amode, true), true, pl.p_pad, s);
@@ -934,10 +941,10 @@ void batch_init(l1g_batch* b, const double* X0) {
   }
   L1G_CUDA(cudaMemcpyAsync(b->st, hs.data(), sizeof(DevState) * b->B, cudaMemcpyHostToDevice, s));
   for (int i = 0; i < b->B; ++i) state_start(b->st + i, s);
-  batch_products(b, FWD_INIT, b->vb.x[0], ADJ_INIT, b->vb.r[0], false, false);
+  batch_products(b, FWD_INIT, X0 ? b->vb.x[0] : nullptr, ADJ_INIT, b->vb.r[0], false, false);
   launch_proj(b->pp, PROJ_ALPHA0, pl.p, pl.p_pad, b->vb.x[0], b->vb.g[0], nullptr, b->pscr, b->st,
               &b->vb, s, b->B, b->scr_stride);
-  b->launches += 5 + b->B;
+  b->launches += (X0 ? 5 : 4) + b->B;
   b->inited = true;
 }
 
