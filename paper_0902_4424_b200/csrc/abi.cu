@@ -549,6 +549,9 @@ cudaGraphExec_t make_while_graph(cudaStream_t st, const Body& body, const Cond& 
 bool build_loop_graph(l1g_solver* s) {
   if (s->gloop || s->gloop_tried) return s->gloop != nullptr;
   s->gloop_tried = true;
+  // NCCL-sharded runs keep the chunked graphs: NCCL collectives inside conditional-node
+  // bodies are not a configuration multi-rank runs have been checked with
+  if (s->comm) return false;
   {
     const GemvPlan& pl = s->op->plan;
     const double bytes = 2.0 * (double)pl.n_pad * (double)pl.p_pad * 8.0 * members(s).size();
