@@ -2,7 +2,7 @@
 # ncu evidence for profiles/ (run on the GPU box after the same commands exited 0 without ncu).
 #   cold launch lists (recipe: gpu__time_duration.sum, --clock-control none, caches flushed),
 #   warm launch lists (--cache-control none: closer to the in-graph durations), and one
-#   --set full capture per hot kernel.
+#   --set full capture per hot kernel.  Then, here: python tools/write_profiles.py
 set -x
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_c2.csv \
