@@ -154,3 +154,32 @@ def test_budgets_and_objective_tol():
                                                         stop.objective_tol))
         assert sol.iterations == ro["iterations"] and int(sol.reason) == ro["reason"]
         assert sol.matvecs.count == ro["matvecs"] and np.array_equal(sol.x, xo)
+
+
+@pytest.mark.parametrize("spec,iters,kind", [(PB.C2_MINI, 150, "feasible"), (PB.RAGGED, 120, "feasible"),
+                                             (PB.C2_MINI, 150, "zeros")],
+                         ids=lambda v: getattr(v, "name", str(v)))
+def test_trajectory_from_x0(spec, iters, kind):
+    """gp_init from a given x0 (gpss.cpp:117-134): a feasible nonzero start, and an explicit
+    all-zero x0, which takes the full forward pass over K where x0 = None skips it
+    (launch_fwd_init_zero) -- both bit-identical to the oracle."""
+    P = O.build_problem(spec)
+    rng = np.random.default_rng(11)
+    if kind == "zeros":
+        x0 = np.zeros(spec.p)
+    else:
+        x0 = O.project_l1(rng.normal(size=spec.p), 0.5 * P["rho"])[0]
+    xo, ro, reco, _ = O.gpss_solve(P["K"], P["y"], P["rho"], O.GpConfig(),
+                                   O.StopRule(iters, 0, 0, 0.0), x0=x0)
+    op = l1.DenseOperator(P["K"])
+    trace = []
+    sol = l1.gpss_solve(l1.Objective(op, P["y"]), l1.L1Ball(P["rho"]), l1.GpConfig(),
+                        l1.StopRule(max_iterations=iters, stationarity_tol=0.0), x0=x0,
+                        trace=trace)
+    assert sol.iterations == ro["iterations"]
+    assert sol.matvecs.count == ro["matvecs"]
+    assert np.array_equal(sol.x, xo), np.abs(sol.x - xo).max()
+    assert sol.objective == ro["objective"]
+    for a, b in zip(trace, reco):
+        for f in FIELDS:
+            assert same(getattr(a, f), b[f]), (b["k"], f, getattr(a, f), b[f])
