@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
   double (*tsv)[FIN_W][32] = reinterpret_cast<double (*)[FIN_W][32]>(&sv[0][0][0]);
   double sums[3];
   cta_tree_arrays<3>(a.grpsum, ngrp, 3, tsv, sums);
+  L1G_TL_STAMP(blockIdx.y == 0 && threadIdx.x == 0, g_tl_gemv, 15, st->k)
   if (warp != 0) return;
   const double SZ = sums[0], SS = sums[1], ZZ = sums[2];
   __shared__ DevState s;

@@ -47,7 +47,8 @@ def timeline(lib, iters):
     ph /= len(ks)
     lead /= len(ks)
     sub = {}
-    for name, a, b in [("adj_finish tail start", 9, 10), ("adj_finish tail", 10, 11),
+    for name, a, b in [("adj_finish tail start", 9, 10), ("adj_finish tail tree", 10, 15),
+                       ("adj_finish tail scalar", 15, 11), ("adj_finish tail", 10, 11),
                        ("adj_tail -> next proj", 11, 17), ("fwd_finish tail start", 5, 12),
                        ("fwd_finish tail", 12, 13), ("fwd_tail -> adj", 13, 7),
                        ("proj body", 1, 14), ("proj end -> fwd_sparse", 14, 3)]:
