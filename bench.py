@@ -316,12 +316,15 @@ def run_batch(args, world, rank, local, pg):
     L.check(lib.l1g_batch_get_x(h, L.ptr(X_dev)))
     lib.l1g_batch_destroy(h)
 
-    # end to end: l1g_gpss_solve_batched with host Y / rho in and X / results out
-    X = np.empty((B, p))
+    # end to end: l1g_gpss_solve_batched with host Y / rho in and X / results out, the host
+    # buffers pinned (page-locked) as the contract asks
+    Yh = torch.empty((B, n), dtype=torch.float64, pin_memory=True).numpy()
+    Yh[:] = Y
+    X = torch.empty((B, p), dtype=torch.float64, pin_memory=True).numpy()
     res2 = (L.ResultC * B)()
 
     def e2e_once():
-        L.check(lib.l1g_gpss_solve_batched(P["op"].h, B, L.ptr(Y), L.ptr(rho), C.byref(cfg),
+        L.check(lib.l1g_gpss_solve_batched(P["op"].h, B, L.ptr(Yh), L.ptr(rho), C.byref(cfg),
                                            C.byref(stop), L.ptr(X), res2), "solve_batched")
         return max(res2[i].iterations for i in range(B))
 
