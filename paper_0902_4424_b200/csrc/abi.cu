@@ -17,6 +17,7 @@
 #include "comm.h"
 #include "common.cuh"
 #include "engine.h"
+#include "scalar.cuh"
 #include "vec.h"
 
 using namespace l1g;
@@ -96,9 +97,16 @@ void free_ws(Workspace& ws) {
 }
 
 // loop condition of the run graphs (make_while_graph): another body while the run is live
-// (single run: its status; batched runs: the live-problem counter)
+// (single run: its status; batched runs: the live-problem counter).  A run already past its
+// budget (which the projection's loop-top checks stop exactly) ends the loop regardless, so a
+// fault in the device state cannot keep the graph running; the host then reports the run
+// as not stopped.
 __global__ void loop_cond_kernel(const DevState* st, const int* nrun, cudaGraphConditionalHandle h) {
-  cudaGraphSetConditional(h, (nrun ? *nrun > 0 : st->status == RUNNING) ? 1u : 0u);
+  bool live = nrun ? *nrun > 0 : st->status == RUNNING;
+  if (st->max_iterations > 0 && st->k > st->max_iterations + 1) live = false;
+  if (st->max_matvecs > 0 && st->matvecs > st->max_matvecs + 4) live = false;
+  if (st->max_seconds > 0.0 && elapsed_s(st) > st->max_seconds + 1.0) live = false;
+  cudaGraphSetConditional(h, live ? 1u : 0u);
 }
 void loop_cond(const DevState* st, const int* nrun, cudaGraphConditionalHandle h, cudaStream_t s) {
   loop_cond_kernel<<<1, 1, 0, s>>>(st, nrun, h);
@@ -983,7 +991,7 @@ void batch_run(l1g_batch* b, const l1g_stop_rule& stop, l1g_result* res) {
     b->gloop_tried = true;
     b->gloop = make_while_graph(
         s, [&] { for (int i = 0; i < b->gsize; ++i) batch_enqueue_iteration(b); },
-        [&](cudaGraphConditionalHandle h) { loop_cond(nullptr, b->nrun, h, s); });
+        [&](cudaGraphConditionalHandle h) { loop_cond(b->st, b->nrun, h, s); });
   }
   const int64_t cap = stop.max_iterations > 0 ? stop.max_iterations / b->gsize + 3 : INT64_MAX;
   volatile int* flag = b->nrun_host;
