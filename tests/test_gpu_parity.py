@@ -183,3 +183,31 @@ def test_trajectory_from_x0(spec, iters, kind):
     for a, b in zip(trace, reco):
         for f in FIELDS:
             assert same(getattr(a, f), b[f]), (b["k"], f, getattr(a, f), b[f])
+
+
+@pytest.mark.parametrize("params", [
+    dict(beta=1e-2, theta=0.3, memory=4, alpha_min=1e-6, alpha_max=1e3, tau1=0.9,
+         alpha2_memory=5),
+    dict(beta=0.25, theta=0.7, memory=2, alpha_min=1e-3, alpha_max=50.0, tau1=0.1,
+         alpha2_memory=1),
+], ids=["nonmonotone_wide_tau", "tight_alpha_clamps"])
+def test_trajectory_config_variants(params):
+    """Every GpConfig field (gpss.hpp:14-24) reaches the device steplength, clamps, history
+    and backtracking rule: non-default configurations stay bit-identical to the oracle."""
+    spec = PB.C2_MINI
+    P = O.build_problem(spec)
+    iters = 150
+    xo, ro, reco, _ = O.gpss_solve(P["K"], P["y"], P["rho"], O.GpConfig(**params),
+                                   O.StopRule(iters, 0, 0, 0.0))
+    op = l1.DenseOperator(P["K"])
+    trace = []
+    sol = l1.gpss_solve(l1.Objective(op, P["y"]), l1.L1Ball(P["rho"]), l1.GpConfig(**params),
+                        l1.StopRule(max_iterations=iters, stationarity_tol=0.0), trace=trace)
+    assert sol.iterations == ro["iterations"]
+    assert int(sol.reason) == ro["reason"]
+    assert np.array_equal(sol.x, xo), np.abs(sol.x - xo).max()
+    assert sol.objective == ro["objective"]
+    assert list(sol.f_history) == ro["f_history"]
+    for a, b in zip(trace, reco):
+        for f in FIELDS:
+            assert same(getattr(a, f), b[f]), (b["k"], f, getattr(a, f), b[f])
