@@ -211,3 +211,25 @@ def test_trajectory_config_variants(params):
     for a, b in zip(trace, reco):
         for f in FIELDS:
             assert same(getattr(a, f), b[f]), (b["k"], f, getattr(a, f), b[f])
+
+
+def test_max_seconds_stop():
+    """The wall-clock budget (gpss.cpp:242-245) is checked on the device (%globaltimer) at the
+    top of every iteration, inside the one-launch run graph: the run stops with MaxSeconds
+    and its iterate is the oracle's after the same number of iterations."""
+    spec = PB.C3_MINI
+    P = O.build_problem(spec)
+    op = l1.DenseOperator(P["K"])
+    obj, ball = l1.Objective(op, P["y"]), l1.L1Ball(P["rho"])
+    # (the clock starts with gp_init, as gpss.cpp:224 does: a first solve also pays for
+    # building the run graph, so the budget is applied to the second one)
+    l1.gpss_solve(obj, ball, l1.GpConfig(), l1.StopRule(max_iterations=5, stationarity_tol=0.0))
+    sol = l1.gpss_solve(obj, ball, l1.GpConfig(),
+                        l1.StopRule(max_iterations=0, max_seconds=3e-3, stationarity_tol=0.0))
+    assert sol.reason == l1.StopReason.MaxSeconds, sol.reason
+    assert sol.iterations >= 1
+    xo, ro, _, _ = O.gpss_solve(P["K"], P["y"], P["rho"], O.GpConfig(),
+                                O.StopRule(sol.iterations, 0, 0, 0.0))
+    assert ro["iterations"] == sol.iterations
+    assert np.array_equal(sol.x, xo)
+    assert sol.objective == ro["objective"]
