@@ -15,11 +15,14 @@ from tests.test_gpu_parity import FIELDS, same
 
 pytestmark = pytest.mark.gpu
 
-MODES = [{"L1G_LOOP_GRAPH": "0"}, {}, {"L1G_LOOP_US": "1"}]
+# chunked graphs; the WHILE loop; one iteration per loop body; a profiler's injection
+# environment (ncu sets NV_COMPUTE_PROFILER_PERFWORKS_DIR): chunked graphs again
+MODES = [{"L1G_LOOP_GRAPH": "0"}, {}, {"L1G_LOOP_US": "1"},
+         {"NV_COMPUTE_PROFILER_PERFWORKS_DIR": "/nonexistent"}]
 
 
 def _set_mode(monkeypatch, env):
-    for k in ("L1G_LOOP_GRAPH", "L1G_LOOP_US"):
+    for k in ("L1G_LOOP_GRAPH", "L1G_LOOP_US", "NV_COMPUTE_PROFILER_PERFWORKS_DIR"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
