@@ -233,3 +233,34 @@ def test_max_seconds_stop():
     assert ro["iterations"] == sol.iterations
     assert np.array_equal(sol.x, xo)
     assert sol.objective == ro["objective"]
+
+
+@pytest.mark.parametrize("scale", ["tiny", "subnormal", "huge", "wide", "outlier"])
+def test_projection_extreme_magnitudes(scale):
+    """Edge magnitudes through the exact sort-and-scan: sums near the bottom of the normal
+    range (the prefix's plain-step path), subnormal entries, sums near the overflow limit,
+    vectors spanning hundreds of binades (many epochs) and one dominant entry."""
+    rng = np.random.default_rng(["tiny", "subnormal", "huge", "wide", "outlier"].index(scale) + 90)
+    for rep in range(12):
+        p = int(rng.integers(2, 6000)) if rep % 3 else int(rng.integers(2, 300))
+        z = rng.normal(size=p)
+        if scale == "tiny":
+            x = z * 1e-300
+        elif scale == "subnormal":
+            x = z * 1e-300
+            x[::3] = rng.choice([5e-324, -1e-320, 2.5e-315], size=x[::3].size)
+        elif scale == "huge":
+            x = z * 1e300 / max(p, 1)
+        elif scale == "wide":
+            x = z * 10.0 ** rng.uniform(-200, 200, size=p)
+        else:
+            x = z * 1e-3
+            x[int(rng.integers(0, p))] = 1e6
+        for frac in (0.95, 0.5, 0.05):
+            rho = frac * float(np.abs(x).sum())
+            if not np.isfinite(rho):
+                continue
+            u, th, sup = O.project_l1(x, rho)
+            pr = l1.project_l1_ball_with_threshold(x, l1.L1Ball(rho))
+            assert pr.threshold == th and pr.support == sup, (scale, rep, frac)
+            assert np.array_equal(pr.point, u), (scale, rep, frac)
