@@ -264,3 +264,23 @@ def test_projection_extreme_magnitudes(scale):
             pr = l1.project_l1_ball_with_threshold(x, l1.L1Ball(rho))
             assert pr.threshold == th and pr.support == sup, (scale, rep, frac)
             assert np.array_equal(pr.point, u), (scale, rep, frac)
+
+
+def test_operator_extreme_magnitudes():
+    """K x and K^T r bit for bit when the products are subnormal (fp64 on the device keeps
+    denormals; every product and sum is one IEEE operation on both sides), near the overflow
+    limit, and spread over many binades."""
+    rng = np.random.default_rng(21)
+    for (n, p) in [(77, 301), (256, 1024), (129, 2100)]:
+        base = rng.normal(size=(n, p))
+        for kscale, vscale in [(1e-160, 1e-160), (1e-300, 1.0), (1e150, 1e150 / 4096),
+                               (None, None)]:
+            if kscale is None:
+                K = base * 10.0 ** rng.uniform(-100, 100, size=(n, p))
+                x, r = rng.normal(size=p) * 1e-50, rng.normal(size=n) * 1e50
+            else:
+                K = base * kscale
+                x, r = rng.normal(size=p) * vscale, rng.normal(size=n) * vscale
+            op = l1.DenseOperator(K)
+            assert np.array_equal(op.apply(x), O.apply(K, x)), (n, p, kscale)
+            assert np.array_equal(op.apply_adjoint(r), O.apply_adjoint(K, r)), (n, p, kscale)
