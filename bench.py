@@ -2,11 +2,15 @@
 """Benchmark of the GPSS iteration loop (BASELINE.json metric: projected-gradient
 iterations/s and achieved HBM GB/s of K streamed vs peak).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl b200|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl b200|reference]
 
-A step is one gpss_solve of the config (C2: 8192x32768, 300 iterations, x0 = 0) with K
-resident in HBM.  K (2 GiB) is larger than L2, so no flush is needed between steps.
-With N > 1 (torchrun) the same problem is column-sharded over the N GPUs (strong scaling).
+A step is one gpss_solve of the config with K resident in HBM.  The default workload is C4
+(BASELINE.json configs[3]: 32768x262144 Gaussian, 68.7 GB, 200 iterations, x0 = 0) at every
+N, the config the north star's multi-GPU target names; it fits one 180 GB B200, so the N=1
+line of the scaling run is the same workload (--config C1/C2/C3/C5 select the others).  K
+is larger than L2, so no flush is needed between steps.  With N > 1 the problem is
+column-sharded over the N GPUs (strong scaling); `--gpus N` launches the N ranks itself
+(torch.distributed.run) when it is not already running under a launcher.
 `value` = iterations / device time (CUDA events on the solver stream, max over ranks);
 `e2e` = the same metric through the C-ABI call l1g_gpss_solve with host y and x buffers
 (copies inside the timed region).  Prints one JSON line on rank 0.
@@ -98,6 +102,28 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+def spawn_if_needed(args):
+    """`--gpus N` with no launcher around us: re-run this command under torch.distributed.run
+    with N ranks (127.0.0.1 rendezvous) and exit with its code.  Under a launcher the world
+    size must equal N."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+            sys.exit(2)
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -131,57 +157,121 @@ def barrier(pg):
 
 
 # ------------------------------------------------------------------ CPU baseline (oracle)
-def ref_time(K, y, rho, iters, threads=None):
-    """Time the reference's own gpss_solve (oracle/_ref fast build: reference sources +
-    Eigen stand-in with OpenMP GEMVs) for `iters` iterations from x0 = 0."""
-    from oracle import oracle as O
-    from oracle import ref as R
-    kind = "fast" if R.available("fast") else None
-    if threads:
-        os.environ["OMP_NUM_THREADS"] = str(threads)
-    if kind is None:
+def host_ram_gb():
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable:"):
+                return int(ln.split()[1]) / 2**20
+    except Exception:
+        pass
+    return 0.0
+
+
+def omp_threads(n):
+    """Thread count of the OpenMP runtime the oracle and oracle/_ref share (libgomp)."""
+    import ctypes as C
+    try:
+        C.CDLL("libgomp.so.1").omp_set_num_threads(int(n))
+    except OSError:
+        pass
+
+
+class CpuRef:
+    """The reference's CPU path on this host.  kind "reference": the reference's own
+    gpss.cpp/prox.cpp/linear_operator.cpp (oracle/_ref/libref_fast.so: Eigen stand-in with
+    OpenMP GEMVs over outputs and sequential sums); it keeps its own column-major copy of K.
+    kind "port": the oracle's restatement in LITERAL mode on the row-major K in place -- the
+    same arithmetic (bit-identical records and iterates on every config of
+    profiles/r02_divergence.json), used when the host cannot hold the second copy (C4)."""
+
+    def __init__(self, K, kind):
+        from oracle import ref as R
+        self.K, self.kind = K, kind
+        self.op = R.RefOperator(K, "fast") if kind == "reference" else None
+
+    def solve(self, y, rho, iters, threads=None):
+        from oracle import oracle as O
+        omp_threads(threads or (os.cpu_count() or 1))
+        stop = O.StopRule(iters, 0, 0, 0.0)
         t0 = time.perf_counter()
-        _, res, _, _ = O.gpss_solve(K, y, rho, O.GpConfig(), O.StopRule(iters, 0, 0, 0.0),
-                                    trace=False)
-        return time.perf_counter() - t0, res["iterations"], "port", 1
-    op = R.RefOperator(K, kind)
-    t0 = time.perf_counter()
-    _, res, _ = op.gpss_solve(y, rho, O.GpConfig(), O.StopRule(iters, 0, 0, 0.0), trace=False)
-    dt = time.perf_counter() - t0
-    return dt, res["iterations"], "reference", int(os.environ.get("OMP_NUM_THREADS",
-                                                                   os.cpu_count() or 1))
+        if self.op is not None:
+            _, res, _ = self.op.gpss_solve(y, rho, O.GpConfig(), stop, trace=False)
+        else:
+            with O.mode(O.LITERAL):
+                _, res, _, _ = O.gpss_solve(self.K, y, rho, O.GpConfig(), stop, trace=False)
+        dt = time.perf_counter() - t0
+        omp_threads(os.cpu_count() or 1)
+        return dt, res["iterations"]
+
+
+def cpu_ref_for(K):
+    """The reference's own sources when the host can hold their column-major copy of K next
+    to ours, else the literal-mode port on K in place."""
+    from oracle import ref as R
+    gb = K.nbytes / 2**30
+    if R.available("fast") and host_ram_gb() > 1.2 * gb + 4:
+        return CpuRef(K, "reference")
+    return CpuRef(K, "port")
+
+
+def host_fits(cfgname):
+    """None when the host can hold the config's K, else the reason."""
+    from tests import problems as PB
+    if cfgname == "C5":
+        return None
+    spec = getattr(PB, cfgname)
+    need = spec.n * spec.p * 8 / 2**30 * 1.1 + 4
+    have = host_ram_gb()
+    if have < need:
+        return (f"host RAM: {cfgname} needs ~{need:.0f} GiB for K on the host, "
+                f"{have:.0f} GiB available")
+    return None
+
+
+def cpu_sample(cref, y, rho, target_s, cap, threads=None):
+    """A bounded sample: enough iterations for ~target_s of CPU work (>= 1)."""
+    dt1, it1 = cref.solve(y, rho, 1, threads)
+    per = max(1, min(cap, int(target_s * max(it1, 1) / max(dt1, 1e-4))))
+    if per == 1:
+        return dt1, it1, 1
+    dt, itn = cref.solve(y, rho, per, threads)
+    return dt, itn, per
+
+
+def cpu_leg(K, y, rho, label, per_unit=1):
+    """cpu_baseline of the b200 arm: the reference CPU path on a bounded sample of the same
+    workload, with all host threads and (the reference's own setting) with one thread."""
+    cref = cpu_ref_for(K)
+    cores = os.cpu_count() or 1
+    dt, itn, _ = cpu_sample(cref, y, rho, 12.0, 400)
+    dt1, itn1, _ = cpu_sample(cref, y, rho, 8.0, 400, threads=1)
+    src = ("reference sources via oracle/_ref/libref_fast.so, OpenMP GEMVs"
+           if cref.kind == "reference" else
+           "oracle LITERAL mode (bit-identical to the reference sources), OpenMP GEMVs")
+    return {"value": itn / dt / per_unit, "unit": UNIT, "cores": cores, "kind": cref.kind,
+            "sample": f"{itn} GPSS iterations (incl. gp_init) of {label} from x0=0, {src}, "
+                      f"{cores} threads" + (f", scaled to lockstep iterations (/{per_unit})"
+                                            if per_unit > 1 else ""),
+            "single_thread": {"value": itn1 / dt1 / per_unit, "cores": 1,
+                              "sample": f"{itn1} iterations, 1 thread: the reference's own "
+                                        "build has no OpenMP and Eigen's GEMV is "
+                                        "single-threaded"}}
 
 
 def host_problem(spec_name):
-    """C2-shaped problem built on the host with the oracle generators (no GPU code)."""
-    from concurrent.futures import ThreadPoolExecutor
+    """The config's problem built on the host with the oracle generators and canonical
+    reductions (bit-identical to the device build: tests/test_gpu_fullsize_parity.py)."""
+    import copy
 
     from oracle import oracle as O
     from tests import problems as PB
-    spec = getattr(PB, spec_name)
-    n, p = spec.n, spec.p
-    K = np.empty((n, p))
-    rows = max(1, (1 << 24) // p)
-
-    def fill(r0):
-        r1 = min(n, r0 + rows)
-        seg = K[r0:r1].reshape(-1)
-        seg[:] = O.fill_normal(spec.seed, 0, r0 * p, (r1 - r0) * p)
-
-    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
-        list(ex.map(fill, range(0, n, rows)))
-    sigma = sigma_fixture(spec_name)
-    if sigma is None:  # short power iteration as a stand-in scale (timing only)
-        sigma, _ = O.spectral_norm(K, 8, 1e-8)
-    K *= 0.9 / sigma
-    x_true = np.zeros(p)
-    sup = O.sample_support(spec.seed, 1, p, spec.nnz)
-    x_true[sup] = O.x_true_values(spec, spec.nnz)
-    clean = K @ x_true
-    e = O.fill_normal(spec.seed, 2, 0, n)
-    sig = spec.noise * math.sqrt(float(clean @ clean)) / math.sqrt(n)
-    y = clean + sig * e
-    return K, y, float(np.abs(x_true).sum())
+    spec = copy.copy(getattr(PB, spec_name))
+    if spec.kind == "gaussian":
+        spec.sigma_hat = sigma_fixture(spec_name)
+        if spec.sigma_hat is None:  # short power iteration as a stand-in scale (timing only)
+            spec.power_iters = 8
+    P = O.build_problem(spec)
+    return P["K"], P["y"], float(P["rho"])
 
 
 def host_batch_problem0():
@@ -205,40 +295,52 @@ def host_batch_problem0():
 
 
 def run_reference(args, world, rank, pg):
-    """--impl reference: the reference CPU path on this box's host cores."""
+    """--impl reference: the reference CPU path on this box's host cores (all threads)."""
     if rank != 0:
         return
     cfgname = args.config
     scale = 1
+    why = host_fits(cfgname)
+    if why is not None:
+        print(json.dumps({"impl": "reference", "unavailable": why}), flush=True)
+        return
+    t_setup = time.perf_counter()
     if cfgname == "C5":  # problems are solved one by one there: lockstep unit = B problems
         K, y, rho, scale = host_batch_problem0()
     else:
         K, y, rho = host_problem(cfgname)
-    from oracle import ref as R
+    cref = cpu_ref_for(K)
+    setup_s = time.perf_counter() - t_setup
     n, p = K.shape
-    # bounded sample per step: enough iterations for ~5 s of CPU work
-    dt1, it1, kind, cores = ref_time(K, y, rho, 2)
-    per_step = max(1, min(args.ref_iters or 1000, int(5.0 * max(it1, 1) / max(dt1, 1e-3))))
+    cores = os.cpu_count() or 1
+    # bounded sample per step, sized so all warmup + timed steps take ~2-3 minutes
+    dt1, it1 = cref.solve(y, rho, 1)
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    per_step = max(1, min(args.ref_iters or 1000, int(budget * max(it1, 1) / max(dt1, 1e-3))))
     for _ in range(args.warmup):
-        ref_time(K, y, rho, per_step)
+        cref.solve(y, rho, per_step)
     times, total_it = [], 0
     for _ in range(args.steps):
-        dt, itn, kind, cores = ref_time(K, y, rho, per_step)
+        dt, itn = cref.solve(y, rho, per_step)
         times.append(dt)
         total_it += itn
     total_t = sum(times)
     v = total_it / total_t / scale
+    src = ("reference gpss.cpp/prox.cpp/linear_operator.cpp via oracle/_ref/libref_fast.so "
+           "(Eigen stand-in: OpenMP GEMVs over outputs, sequential sums)"
+           if cref.kind == "reference" else
+           "oracle restatement in LITERAL mode (the reference's arithmetic, bit-identical to "
+           "oracle/_ref/libref_fast.so; K row-major in place)")
     sample = (f"{per_step} GPSS iterations per step of {cfgname} ({n}x{p}) from x0=0, "
               + (f"problem 0 of {scale} solved alone, scaled to lockstep iterations (/{scale}), "
-                 if scale > 1 else "") +
-              f"reference gpss.cpp/prox.cpp/linear_operator.cpp via oracle/_ref "
-              f"({'OpenMP Eigen stand-in' if kind == 'reference' else 'C port'})")
+                 if scale > 1 else "") + src + f", {cores} threads")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Philox Gaussian, oracle generator on the host)",
-            "config": {"workload": cfgname, "n": n, "p": p, "iterations_per_step": per_step},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+            "config": {"workload": cfgname, "n": n, "p": p, "iterations_per_step": per_step,
+                       "setup_s": round(setup_s, 1)},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": cref.kind,
                              "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gbs_K": v * 2 * n * p * 8 / 1e9}
@@ -357,12 +459,7 @@ def run_batch(args, world, rank, local, pg):
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
             K = P["op"].matrix()
-            per = 20
-            dt, itn, kind, cores = ref_time(K, Y[0], float(rho[0]), per)
-            cpu = {"value": itn / dt / B, "unit": UNIT, "cores": cores, "kind": kind,
-                   "sample": f"{itn} GPSS iterations of problem 0 of C5 solved alone "
-                             f"(reference sources), scaled to lockstep iterations of {B} "
-                             f"problems (/{B})"}
+            cpu = cpu_leg(K, Y[0], float(rho[0]), f"problem 0 of C5 solved alone", per_unit=B)
             del K
         except Exception as ex:
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
@@ -553,33 +650,37 @@ def run_b200(args, world, rank, local, pg):
                     "GBps_incl_finish": sp_cols * n * 8.0 / (avg["fwd"] / 1e3) / 1e9},
                 "share_of_iteration": {k: round(v / sum(avg.values()), 4)
                                        for k, v in avg.items()},
-                "iteration_GBps_2npx8": 2 * k_bytes * done_iters / (dev_ms / 1e3) / 1e9}
+                # K bytes the iteration actually reads (adjoint: all of K; forward: the
+                # support columns of d), per second of the timed solves
+                "iteration_GBps_K_read": None if sp_cols is None else
+                (k_bytes + sp_cols * n * 8.0) * done_iters / (dev_ms / 1e3) / 1e9,
+                "iteration_frac_K_read": None if sp_cols is None else
+                (k_bytes + sp_cols * n * 8.0) * done_iters / (dev_ms / 1e3) / 1e9 / hbm,
+                "nominal_iteration_GBps_2npx8": 2 * k_bytes * done_iters / (dev_ms / 1e3) / 1e9}
 
     # ---- CPU baseline on rank 0 at N=1 (bounded sample of the same workload)
     cpu = None
-    if world == 1 and rank == 0 and not args.no_cpu_baseline and args.config in ("C1", "C2",
-                                                                                   "C3"):
-        try:
-            K = op.matrix()  # the same bits the oracle generator produces (tests pin this)
-            it_cpu = 2 if n * p > 1e8 else 20
-            dt, itn, kind, cores = ref_time(K, y, rho, it_cpu)
-            per = max(1, min(400, int(12.0 * max(itn, 1) / max(dt, 1e-4))))
-            dt, itn, kind, cores = ref_time(K, y, rho, per)
-            cpu = {"value": itn / dt, "unit": UNIT, "cores": cores, "kind": kind,
-                   "sample": f"{itn} GPSS iterations (incl. gp_init) of {args.config} from x0=0 "
-                             f"({'reference sources, OpenMP Eigen stand-in' if kind == 'reference' else 'C port, 1 thread'})"}
-            del K
-        except Exception as ex:  # reported, never fatal
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        why = host_fits(args.config)
+        if why is not None:
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"failed: {ex}"}
+                   "sample": f"skipped: {why}"}
+        else:
+            try:
+                Kh, yh, rhoh = host_problem(args.config)  # same bits as the device build
+                cpu = cpu_leg(Kh, yh, rhoh, args.config)
+                del Kh
+            except Exception as ex:  # reported, never fatal
+                cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                       "sample": f"failed: {ex}"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded Philox Gaussian K scaled to ||K||_2=0.9, generated "
-                        "on device; BASELINE.json configs[1])",
+                "data": "synthetic (seeded Philox streams, generated on device; BASELINE.json "
+                        f"configs[{int(args.config[1]) - 1}])",
                 "config": {"workload": f"{args.config}: {spec.kind} {n}x{p}, nnz {spec.nnz}, "
                                        f"{iters} iterations, x0=0, stationarity_tol=0",
                            "n": n, "p": p, "iterations_per_step": done_iters / args.steps,
@@ -609,7 +710,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--iters", type=int, default=0)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -618,6 +719,7 @@ def main():
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the NCCL-sharded solver path even on one GPU (a 1-rank communicator)")
     args = ap.parse_args()
+    spawn_if_needed(args)
     world, rank, local, pg = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank, pg)

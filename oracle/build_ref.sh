@@ -14,6 +14,7 @@ mkdir -p "$OUT"
 SRCS="$REF/src/gpss.cpp $REF/src/prox.cpp $REF/src/linear_operator.cpp $REF/src/objective.cpp $REF/src/psd.cpp $REF/src/shrinkage.cpp $REF/src/problem_io.cpp $HERE/ref_capi.cpp"
 CXX="${L1_REF_CXX:-/usr/bin/g++}"
 COMMON="-std=c++20 -fPIC -shared -ffp-contract=off -fno-fast-math -I$HERE/eigen_shim -I$REF/include"
-$CXX -O2 $COMMON -o "$OUT/libref_canon.so" $SRCS
+# OpenMP splits GEMV outputs over threads only: the canonical values do not depend on it
+$CXX -O2 -fopenmp $COMMON -o "$OUT/libref_canon.so" $SRCS
 $CXX -O3 -fopenmp -DL1SHIM_FAST $COMMON -o "$OUT/libref_fast.so" $SRCS
 echo "built $OUT/libref_canon.so $OUT/libref_fast.so"

@@ -2,7 +2,7 @@
  * l1oracle.c -- CPU restatement of the reference GPSS path (TEST INFRASTRUCTURE ONLY).
  *
  * See l1oracle.h for scope and the reduction-order contract.  Build with
- *   gcc -O2 -ffp-contract=off -fno-fast-math  (no -march: the reference's Release build
+ *   gcc -O2 -fopenmp -ffp-contract=off -fno-fast-math  (no -march: the reference's Release build
  *   targets baseline x86-64, which has no FMA, so every a*b+c rounds twice)
  * Every function cites the reference lines it follows (paths relative to
  * /root/reference/proj/core).
@@ -112,54 +112,76 @@ double orc_linf(const double* a, int64_t m) {
  * K is row-major n x p here; the reference stores Eigen column-major, which changes no
  * value because the reduction order is fixed by the mode, not by the storage.
  * ---------------------------------------------------------------------------------- */
+/* OpenMP (when built with -fopenmp) splits the OUTPUTS across threads only: each output's
+ * reduction runs in one thread in the order of the active mode, so the values do not depend
+ * on the thread count (order-preserving; the full-size parity tests rely on this). */
 void orc_apply(const double* K, int64_t n, int64_t p, const double* x, double* out) {
+#pragma omp parallel for schedule(static) if (n * p > (1 << 18))
   for (int64_t i = 0; i < n; ++i) out[i] = orc_dot(K + i * p, x, p);
 }
 
-void orc_apply_adjoint(const double* K, int64_t n, int64_t p, const double* r, double* out) {
+/* one block of columns [j0, j1) of K^T r; the carry pattern depends only on i */
+static void adjoint_block(const double* K, int64_t n, int64_t p, const double* r, int64_t j0,
+                          int64_t j1, double* out, double* lvl, double* cur, int levels) {
+  const int64_t w = j1 - j0;
   if (g_mode == ORC_LITERAL) {
-    for (int64_t j = 0; j < p; ++j) out[j] = 0.0;
+    for (int64_t j = 0; j < w; ++j) out[j0 + j] = 0.0;
     for (int64_t i = 0; i < n; ++i) {
-      const double* row = K + i * p;
+      const double* row = K + i * p + j0;
       const double ri = r[i];
-      for (int64_t j = 0; j < p; ++j) out[j] += row[j] * ri;
+      for (int64_t j = 0; j < w; ++j) out[j0 + j] += row[j] * ri;
     }
     return;
   }
-  /* per-column pairwise trees over i; the carry pattern depends only on i */
-  int levels = 1;
-  while (((int64_t)1 << (levels - 1)) < n) ++levels;
-  double* lvl = (double*)malloc(sizeof(double) * (size_t)levels * (size_t)(p > 0 ? p : 1));
-  double* cur = (double*)malloc(sizeof(double) * (size_t)(p > 0 ? p : 1));
+  (void)levels;
   for (int64_t i = 0; i < n; ++i) {
-    const double* row = K + i * p;
+    const double* row = K + i * p + j0;
     const double ri = r[i];
-    for (int64_t j = 0; j < p; ++j) cur[j] = row[j] * ri;
+    for (int64_t j = 0; j < w; ++j) cur[j] = row[j] * ri;
     uint64_t c = (uint64_t)i;
     int l = 0;
     while (c & 1u) {
-      const double* lv = lvl + (size_t)l * (size_t)p;
-      for (int64_t j = 0; j < p; ++j) cur[j] = lv[j] + cur[j];
+      const double* lv = lvl + (size_t)l * (size_t)w;
+      for (int64_t j = 0; j < w; ++j) cur[j] = lv[j] + cur[j];
       c >>= 1;
       ++l;
     }
-    memcpy(lvl + (size_t)l * (size_t)p, cur, sizeof(double) * (size_t)p);
+    memcpy(lvl + (size_t)l * (size_t)w, cur, sizeof(double) * (size_t)w);
   }
-  for (int64_t j = 0; j < p; ++j) out[j] = 0.0;
+  for (int64_t j = 0; j < w; ++j) out[j0 + j] = 0.0;
   uint64_t m = (uint64_t)n;
   int have = 0;
   for (int l = 0; m; ++l, m >>= 1) {
     if (m & 1u) {
-      const double* lv = lvl + (size_t)l * (size_t)p;
+      const double* lv = lvl + (size_t)l * (size_t)w;
       if (have)
-        for (int64_t j = 0; j < p; ++j) out[j] = lv[j] + out[j];
+        for (int64_t j = 0; j < w; ++j) out[j0 + j] = lv[j] + out[j0 + j];
       else
-        memcpy(out, lv, sizeof(double) * (size_t)p);
+        memcpy(out + j0, lv, sizeof(double) * (size_t)w);
       have = 1;
     }
   }
-  free(lvl);
-  free(cur);
+}
+
+/* per-column reductions over i (pairwise trees, or sequential in LITERAL mode), column
+ * blocks split across threads */
+void orc_apply_adjoint(const double* K, int64_t n, int64_t p, const double* r, double* out) {
+  int levels = 1;
+  while (((int64_t)1 << (levels - 1)) < n) ++levels;
+  const int64_t bw = 512;
+  const int64_t nb = (p + bw - 1) / bw;
+#pragma omp parallel if (n * p > (1 << 18))
+  {
+    double* lvl = (double*)malloc(sizeof(double) * (size_t)levels * (size_t)bw);
+    double* cur = (double*)malloc(sizeof(double) * (size_t)bw);
+#pragma omp for schedule(static)
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t j0 = b * bw, j1 = j0 + bw < p ? j0 + bw : p;
+      adjoint_block(K, n, p, r, j0, j1, out, lvl, cur, levels);
+    }
+    free(lvl);
+    free(cur);
+  }
 }
 
 /* linear_operator.cpp:43-60 */
@@ -757,19 +779,23 @@ double orc_normal(uint64_t seed, uint32_t stream, uint64_t index) {
 
 void orc_fill_normal(uint64_t seed, uint32_t stream, uint64_t first, int64_t count,
                      double* out) {
+#pragma omp parallel for schedule(static) if (count > (1 << 16))
   for (int64_t t = 0; t < count; ++t) out[t] = orc_normal(seed, stream, first + (uint64_t)t);
 }
 
 /* entry (i, j) is normal number i*p + j of stream 0 */
 void orc_gaussian_matrix(uint64_t seed, int64_t n, int64_t p, double* K) {
   const uint64_t total = (uint64_t)n * (uint64_t)p;
-  uint64_t e = 0;
-  for (; e + 1 < total; e += 2) normal_pair(seed, 0u, e >> 1, &K[e], &K[e + 1]);
-  if (e < total) K[e] = orc_normal(seed, 0u, e);
+  const int64_t pairs = (int64_t)(total / 2);
+#pragma omp parallel for schedule(static) if (pairs > (1 << 16))
+  for (int64_t q = 0; q < pairs; ++q)
+    normal_pair(seed, 0u, (uint64_t)q, &K[2 * q], &K[2 * q + 1]);
+  if (total & 1u) K[total - 1] = orc_normal(seed, 0u, total - 1);
 }
 
 /* square Toeplitz blur: K[i][j] = taps[i - j + radius] for |i - j| <= radius, else 0 */
 void orc_blur_matrix(int64_t n, const double* taps, int radius, double* K) {
+#pragma omp parallel for schedule(static) if (n > 1024)
   for (int64_t i = 0; i < n; ++i)
     for (int64_t j = 0; j < n; ++j) {
       const int64_t o = i - j;
@@ -778,6 +804,7 @@ void orc_blur_matrix(int64_t n, const double* taps, int radius, double* K) {
 }
 
 void orc_scale(double* a, int64_t m, double c) {
+#pragma omp parallel for schedule(static) if (m > (1 << 20))
   for (int64_t i = 0; i < m; ++i) a[i] = a[i] * c;
 }
 

@@ -7,6 +7,7 @@
 // reductions, parity) and oracle/_ref/libref_fast.so (OpenMP GEMVs, CPU timing baseline).
 // Structs are layout-compatible with oracle/l1oracle.h.
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -23,8 +24,12 @@ using namespace l1solve;
 namespace {
 Matrix from_row_major(const double* K, long n, long p) {
   Matrix m(n, p);
-  for (long i = 0; i < n; ++i)
-    for (long j = 0; j < p; ++j) m(i, j) = K[i * p + j];
+  // blocked transpose into the column-major storage (OpenMP builds split the column tiles)
+#pragma omp parallel for schedule(static) if (n * p > (1L << 20))
+  for (long j0 = 0; j0 < p; j0 += 64)
+    for (long i0 = 0; i0 < n; i0 += 64)
+      for (long j = j0; j < std::min(j0 + 64, p); ++j)
+        for (long i = i0; i < std::min(i0 + 64, n); ++i) m(i, j) = K[i * p + j];
   return m;
 }
 Vector vec(const double* x, long m) {
