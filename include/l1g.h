@@ -6,7 +6,8 @@
  * caller-owned array of doubles, every device pointer a CUDA global-memory address on
  * the context's device.  Status codes mirror the reference's exception classes:
  *   L1G_OK (0), L1G_EINVAL (1) = std::invalid_argument, L1G_ERUNTIME (2) =
- *   std::runtime_error (CUDA failures, backtracking cap).  l1g_last_error() returns the
+ *   std::runtime_error (CUDA failures, backtracking cap), L1G_ECANCELED (3) = an iteration
+ *   callback asked to stop (its exception, in the C++ drop-in).  l1g_last_error() returns the
  *   thread's last message.
  *
  * Entry point -> reference interface it replaces (paths under proj/core):
@@ -36,7 +37,7 @@
 extern "C" {
 #endif
 
-enum { L1G_OK = 0, L1G_EINVAL = 1, L1G_ERUNTIME = 2 };
+enum { L1G_OK = 0, L1G_EINVAL = 1, L1G_ERUNTIME = 2, L1G_ECANCELED = 3 };
 
 /* StopReason, solver.hpp:38-44 */
 enum { L1G_STATIONARY = 0, L1G_MAX_ITERATIONS = 1, L1G_MAX_MATVECS = 2, L1G_MAX_SECONDS = 3,
@@ -156,13 +157,41 @@ int l1g_solver_iterate(l1g_solver* s, double stationarity_tol, l1g_iter_record* 
 int l1g_solver_run(l1g_solver* s, const l1g_stop_rule* stop, l1g_result* res,
                    l1g_iter_record* trace, int64_t trace_cap);
 /* gpss_solve with an IterationCallback (solver.hpp:86-88): cb(record, x, p, user) after
- * every completed iteration; x is valid only during the call */
-typedef void (*l1g_iter_cb)(const l1g_iter_record* rec, const double* x, int64_t p, void* user);
+ * every completed iteration; x is valid only during the call.  A nonzero return stops the
+ * run at once and the call returns L1G_ECANCELED (the reference propagates a callback's
+ * exception out of gpss_solve immediately; the C++ drop-in rethrows it). */
+typedef int (*l1g_iter_cb)(const l1g_iter_record* rec, const double* x, int64_t p, void* user);
 int l1g_solver_run_cb(l1g_solver* s, const l1g_stop_rule* stop, l1g_result* res,
                       l1g_iter_cb cb, void* user);
 int l1g_solver_get(l1g_solver* s, double* x, double* kx_minus_y, double* grad, double* f,
                    int64_t* k, double* alpha0, int64_t* matvecs);
 int l1g_solver_x_dev(l1g_solver* s, const double** x_dev);
+/* The whole gp_iterate state (GpIterationState gpss.hpp:89-98 + SteplengthState :31-36), for
+ * the drop-in's public-field GpIterationState: read it after gp_init / gp_iterate, write back
+ * what a caller changed.  `choice` is the last steplength choice before any alpha escalation
+ * (gpss.cpp:148-153); x_prev / grad_prev are SteplengthState::prev_x / prev_grad (valid when
+ * has_prev, i.e. after the first step).  In set_state every vector may be NULL (kept); new
+ * x / grad / x_prev / grad_prev recompute the secant dots s'z, s's, z'z on the device. */
+typedef struct {
+  double f;
+  int64_t k;
+  double alpha0;
+  int32_t stationary, has_prev;
+  int32_t f_history_len;
+  double f_history[64];
+  double tau;
+  int32_t alpha2_len;
+  double alpha2_history[66];
+  l1g_sl_choice choice;
+} l1g_gp_state;
+int l1g_solver_get_state(l1g_solver* s, l1g_gp_state* st, double* x, double* kx_minus_y,
+                         double* grad, double* x_prev, double* grad_prev);
+int l1g_solver_set_state(l1g_solver* s, const l1g_gp_state* st, const double* x,
+                         const double* kx_minus_y, const double* grad, const double* x_prev,
+                         const double* grad_prev);
+/* the GpConfig and L1Ball radius the next gp_iterate uses (gp_iterate takes both per call) */
+int l1g_solver_set_problem(l1g_solver* s, const l1g_gp_config* cfg, double rho);
+
 int l1g_solver_stream(l1g_solver* s, void** stream);
 /* per-kernel CUDA-event timing of the device loop (projection / forward / adjoint), summed
  * over completed iterations, and the number of kernels this solver launched */

@@ -468,6 +468,25 @@ int orc_gp_init(const double* K, int64_t n, int64_t p, const double* y, double r
   return ORC_OK;
 }
 
+/* A caller writing GpIterationState's public fields (gpss.hpp:89-98) between steps, and
+ * passing another GpConfig / L1Ball to gp_iterate (which takes both per call).  NULL vectors
+ * are kept; SteplengthState (tau, history, prev_x, prev_grad) is kept. */
+int orc_gp_set(orc_gp* s, const double* x, const double* r, const double* g, double f,
+               int64_t k, const double* fh, int fh_len, const orc_gp_config* cfg, double rho) {
+  if (fh_len < 1 || fh_len > 64 || k < 0) return ORC_EINVAL;
+  if (cfg && orc_config_validate(cfg)) return ORC_EINVAL;
+  if (x) memcpy(s->x, x, sizeof(double) * (size_t)s->p);
+  if (r) memcpy(s->r, r, sizeof(double) * (size_t)s->n);
+  if (g) memcpy(s->g, g, sizeof(double) * (size_t)s->p);
+  s->f = f;
+  s->k = k;
+  memcpy(s->fh, fh, sizeof(double) * (size_t)fh_len);
+  s->fh_len = fh_len;
+  if (cfg) s->cfg = *cfg;
+  s->rho = rho;
+  return ORC_OK;
+}
+
 void orc_gp_get(const orc_gp* s, double* x, double* r, double* g, double* f, int64_t* k,
                 double* alpha0, int64_t* matvecs) {
   if (x) memcpy(x, s->x, sizeof(double) * (size_t)s->p);

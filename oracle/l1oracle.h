@@ -149,6 +149,9 @@ int orc_gp_iterate(orc_gp* st, double stationarity_tol, orc_iter_record* info,
 void orc_gp_get(const orc_gp* st, double* x, double* kx_minus_y, double* grad, double* f,
                 int64_t* k, double* alpha0, int64_t* matvecs);
 void orc_gp_free(orc_gp* st);
+int orc_gp_set(orc_gp* st, const double* x, const double* kx_minus_y, const double* grad,
+               double f, int64_t k, const double* f_history, int f_history_len,
+               const orc_gp_config* cfg, double rho);
 
 /* ---- L1PROBv1 (problem_io.cpp): FNV-1a 64 over serialized bytes, chained from h */
 uint64_t orc_fnv1a(const void* data, int64_t bytes, uint64_t h);

@@ -132,6 +132,8 @@ def lib():
             "orc_gp_get": (None, [C.c_void_p, _dp, _dp, _dp, C.POINTER(dbl), C.POINTER(i64),
                                   C.POINTER(dbl), C.POINTER(i64)]),
             "orc_gp_free": (None, [C.c_void_p]),
+            "orc_gp_set": (i32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, dbl, i64,
+                                 _dp, i32, C.POINTER(GpConfig), dbl]),
             "orc_det_log": (dbl, [dbl]),
             "orc_det_sincos2pi": (None, [dbl, C.POINTER(dbl), C.POINTER(dbl)]),
             "orc_normal": (dbl, [C.c_uint64, C.c_uint32, C.c_uint64]),
@@ -357,6 +359,7 @@ class GpState:
         self.K, self.y = _a(K), _a(y)
         self.n, self.p = self.K.shape
         self.cfg = cfg or GpConfig()
+        self.rho = rho
         self._x0 = _a(x0) if x0 is not None else None
         h = C.c_void_p()
         _check(lib().orc_gp_init(self.K, self.n, self.p, self.y, rho, C.byref(self.cfg),
@@ -368,6 +371,17 @@ class GpState:
         rec, st = IterRecord(), C.c_int32()
         _check(lib().orc_gp_iterate(self.h, tol, C.byref(rec), C.byref(st)), "gp_iterate")
         return {f: getattr(rec, f) for f in RECORD_FIELDS}, bool(st.value)
+
+    def set(self, x, r, g, f, k, f_history, cfg=None, rho=None):
+        """Write the public GpIterationState fields (and gp_iterate's cfg / ball)."""
+        if cfg is not None:
+            self.cfg = cfg
+        if rho is not None:
+            self.rho = rho
+        arrs = [_a(v) if v is not None else None for v in (x, r, g)]
+        ptrs = [a.ctypes.data if a is not None else None for a in arrs]
+        _check(lib().orc_gp_set(self.h, *ptrs, f, k, _a(f_history), len(f_history),
+                                C.byref(self.cfg), self.rho), "gp_set")
 
     def get(self):
         x, r, g = np.empty(self.p), np.empty(self.n), np.empty(self.p)

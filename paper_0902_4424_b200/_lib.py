@@ -10,7 +10,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libl1g.so")
 
-OK, EINVAL, ERUNTIME = 0, 1, 2
+OK, EINVAL, ERUNTIME, ECANCELED = 0, 1, 2, 3
 REASONS = {0: "stationary", 1: "max_iterations", 2: "max_matvecs", 3: "max_seconds",
            4: "objective_tol"}
 RED_DOT, RED_SQ, RED_ABS, RED_MAX = 0, 1, 2, 3
@@ -53,8 +53,16 @@ class SlChoiceC(C.Structure):
                 ("bb2_raw", C.c_double), ("tau_before", C.c_double), ("tau_after", C.c_double)]
 
 
+class GpStateC(C.Structure):  # l1g_gp_state
+    _fields_ = [("f", C.c_double), ("k", C.c_int64), ("alpha0", C.c_double),
+                ("stationary", C.c_int32), ("has_prev", C.c_int32),
+                ("f_history_len", C.c_int32), ("f_history", C.c_double * 64),
+                ("tau", C.c_double), ("alpha2_len", C.c_int32),
+                ("alpha2_history", C.c_double * 66), ("choice", SlChoiceC)]
+
+
 RECORD_FIELDS = [f for f, _ in IterRecordC._fields_]
-ITER_CB = C.CFUNCTYPE(None, C.POINTER(IterRecordC), C.POINTER(C.c_double), C.c_int64,
+ITER_CB = C.CFUNCTYPE(C.c_int, C.POINTER(IterRecordC), C.POINTER(C.c_double), C.c_int64,
                       C.c_void_p)
 
 _dp = C.POINTER(C.c_double)
@@ -125,6 +133,9 @@ _SIGS = {
     "l1g_solver_get": (C.c_int, [_vp, _vp, _vp, _vp, _dp, C.POINTER(_i64), _dp,
                                  C.POINTER(_i64)]),
     "l1g_solver_x_dev": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "l1g_solver_get_state": (C.c_int, [_vp, C.POINTER(GpStateC), _vp, _vp, _vp, _vp, _vp]),
+    "l1g_solver_set_state": (C.c_int, [_vp, C.POINTER(GpStateC), _vp, _vp, _vp, _vp, _vp]),
+    "l1g_solver_set_problem": (C.c_int, [_vp, C.POINTER(GpConfigC), C.c_double]),
     "l1g_solver_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "l1g_solver_destroy": (None, [_vp]),
     "l1g_solver_set_timing": (C.c_int, [_vp, C.c_int]),

@@ -411,10 +411,16 @@ class SteplengthState:  # gpss.hpp:31-36
         self._c = L.SlStateC()
         c = cfg._c()
         L.load().l1g_steplength_init(C.byref(self._c), C.byref(c))
+        self.prev_x = None     # x and grad of the previous iterate (set by gp_iterate)
+        self.prev_grad = None
 
     @property
     def tau(self):
         return self._c.tau
+
+    @tau.setter
+    def tau(self, v):
+        self._c.tau = float(v)
 
     @property
     def alpha2_history(self):
@@ -497,7 +503,9 @@ def _require_dense(prob: Objective) -> DenseOperator:
 
 
 class GpIterationState:
-    """gpss.hpp:89-98; the vectors stay on the GPU (l1g_solver)."""
+    """gpss.hpp:89-98: x, kx_minus_y, grad, f, k, f_history, alpha0, stationary are plain
+    attributes, refreshed from the device (an l1g_solver) after gp_init / gp_iterate;
+    attributes a caller changes are written back before the next step."""
 
     def __init__(self, prob: Objective, ball: L1Ball, x0, cfg: GpConfig):
         op = _require_dense(prob)
@@ -517,39 +525,76 @@ class GpIterationState:
         if rc:
             self.close()
         check(rc, "gp_init")
-        self.stationary = False
+        self._cfg = (c.beta, c.theta, c.memory, c.alpha2_memory, c.alpha_min, c.alpha_max,
+                     c.tau1)
+        self._rho = ball.radius()
+        self._pull(None)
 
-    def _get(self):
+    # device -> attributes (and the copy changes are detected against)
+    def _pull(self, sls):
         n, p = self._op.rows(), self._op.cols()
-        x, r, g = np.empty(p), np.empty(n), np.empty(p)
-        f, k, a0, mv = C.c_double(), C.c_int64(), C.c_double(), C.c_int64()
-        check(self._lib.l1g_solver_get(self.h, ptr(x), ptr(r), ptr(g), C.byref(f), C.byref(k),
-                                       C.byref(a0), C.byref(mv)))
-        return x, r, g, f.value, k.value, a0.value, mv.value
+        g = L.GpStateC()
+        x, r, gr, xp, gp = np.empty(p), np.empty(n), np.empty(p), np.empty(p), np.empty(p)
+        check(self._lib.l1g_solver_get_state(self.h, C.byref(g), ptr(x), ptr(r), ptr(gr),
+                                             ptr(xp), ptr(gp)), "gp state")
+        self.x, self.kx_minus_y, self.grad = x, r, gr
+        self.f, self.k, self.alpha0 = g.f, g.k, g.alpha0
+        self.stationary = bool(g.stationary)
+        self.f_history = [g.f_history[i] for i in range(g.f_history_len)]
+        self._m = dict(x=x.copy(), r=r.copy(), g=gr.copy(), f=g.f, k=g.k, a0=g.alpha0,
+                       st=bool(g.stationary), fh=list(self.f_history), tau=g.tau,
+                       a2=[g.alpha2_history[i] for i in range(g.alpha2_len)],
+                       xp=xp.copy() if g.has_prev else None, gp=gp.copy() if g.has_prev else None)
+        if sls is not None:
+            sls._c.tau = g.tau
+            sls._c.hist_len = g.alpha2_len
+            for i in range(g.alpha2_len):
+                sls._c.hist[i] = g.alpha2_history[i]
+            if g.has_prev:
+                sls.prev_x, sls.prev_grad = xp, gp
+        return g
 
-    @property
-    def x(self):
-        return self._get()[0]
-
-    @property
-    def kx_minus_y(self):
-        return self._get()[1]
-
-    @property
-    def grad(self):
-        return self._get()[2]
-
-    @property
-    def f(self):
-        return self._get()[3]
-
-    @property
-    def k(self):
-        return self._get()[4]
-
-    @property
-    def alpha0(self):
-        return self._get()[5]
+    # attributes / steplength state / cfg / ball -> device, where they changed
+    def _push(self, sls, cfg: GpConfig, ball: L1Ball):
+        c = cfg._c()
+        key = (c.beta, c.theta, c.memory, c.alpha2_memory, c.alpha_min, c.alpha_max, c.tau1)
+        if key != self._cfg or ball.radius() != self._rho:
+            check(self._lib.l1g_solver_set_problem(self.h, C.byref(c), ball.radius()),
+                  "gp_iterate")
+            self._cfg, self._rho = key, ball.radius()
+        m = self._m
+        neq = lambda a, b: not (np.shape(a) == np.shape(b) and
+                                np.array_equal(np.asarray(a).view(np.int64),
+                                               np.asarray(b).view(np.int64)))
+        x = _f64(self.x) if neq(_f64(self.x), m["x"]) else None
+        r = _f64(self.kx_minus_y) if neq(_f64(self.kx_minus_y), m["r"]) else None
+        g = _f64(self.grad) if neq(_f64(self.grad), m["g"]) else None
+        xp = gp = None
+        tau, a2 = m["tau"], m["a2"]
+        if sls is not None:
+            tau, a2 = sls.tau, sls.alpha2_history
+            px, pg = getattr(sls, "prev_x", None), getattr(sls, "prev_grad", None)
+            if self.k > 0 and px is not None and pg is not None:
+                if m["xp"] is None or neq(_f64(px), m["xp"]):
+                    xp = _f64(px)
+                if m["gp"] is None or neq(_f64(pg), m["gp"]):
+                    gp = _f64(pg)
+        scal = (self.f != m["f"] or self.k != m["k"] or list(self.f_history) != m["fh"] or
+                self.alpha0 != m["a0"] or bool(self.stationary) != m["st"] or tau != m["tau"] or
+                list(a2) != m["a2"])
+        if not (scal or any(v is not None for v in (x, r, g, xp, gp))):
+            return
+        st = L.GpStateC()
+        st.f, st.k, st.alpha0, st.stationary = self.f, self.k, self.alpha0, int(self.stationary)
+        st.f_history_len = len(self.f_history)
+        for i, v in enumerate(self.f_history):
+            st.f_history[i] = v
+        st.tau, st.alpha2_len = tau, len(a2)
+        for i, v in enumerate(a2):
+            st.alpha2_history[i] = v
+        check(self._lib.l1g_solver_set_state(self.h, C.byref(st), ptr(x), ptr(r), ptr(g),
+                                             ptr(xp), ptr(gp)), "gp_iterate")
+        self._pull(None)
 
     def close(self):
         if getattr(self, "h", None):
@@ -589,21 +634,34 @@ def gp_init(prob: Objective, ball: L1Ball, x0, cfg: GpConfig,
 def gp_iterate(prob: Objective, ball: L1Ball, cfg: GpConfig, state: GpIterationState,
                sls: Optional[SteplengthState], mv: MatvecCounter,
                stationarity_tol: float = 0.0) -> GpStepInfo:  # gpss.cpp:136-219
-    """The steplength state lives in the device state of `state`; `sls` is accepted for
-    signature compatibility."""
+    """One step on the device; `state` (and `sls`, when given) are read and updated like the
+    reference's (changed attributes, GpConfig and ball are written back first)."""
+    state._push(sls, cfg, ball)
+    if state.stationary:  # gpss.cpp:139-143
+        return GpStepInfo(stationary=True, stationarity=0.0)
     rec, st = L.IterRecordC(), C.c_int32()
-    k_before = state._get()[6]
-    check(state._lib.l1g_solver_iterate(state.h, stationarity_tol, C.byref(rec), C.byref(st)),
+    mv0 = C.c_int64()
+    lib = state._lib
+    check(lib.l1g_solver_get(state.h, None, None, None, None, None, None, C.byref(mv0)))
+    check(lib.l1g_solver_iterate(state.h, stationarity_tol, C.byref(rec), C.byref(st)),
           "gp_iterate")
-    mv.count += state._get()[6] - k_before
+    mv1 = C.c_int64()
+    check(lib.l1g_solver_get(state.h, None, None, None, None, None, None, C.byref(mv1)))
+    mv.count += mv1.value - mv0.value
+    g = state._pull(sls)
     r = IterationRecord.from_c(rec)
-    state.stationary = bool(st.value)
-    return GpStepInfo(stationary=bool(st.value), alpha=r.alpha, step=r.step, f_after=r.f,
-                      stationarity=r.stationarity, f_max=r.f_max,
-                      dir_derivative=r.dir_derivative,
-                      steplength=SteplengthChoice(r.alpha, r.bb_active, r.bb1_raw, r.bb2_raw,
-                                                  r.tau_before, r.tau_after),
-                      halvings=r.halvings, theta=r.theta, support=r.support)
+    ch = g.choice  # the steplength choice before any escalation (gpss.cpp:148-153)
+    info = GpStepInfo(stationary=bool(st.value), alpha=r.alpha, f_after=state.f,
+                      stationarity=r.stationarity,
+                      steplength=SteplengthChoice(ch.alpha, bool(ch.bb_active), ch.bb1_raw,
+                                                  ch.bb2_raw, ch.tau_before, ch.tau_after),
+                      theta=r.theta, support=r.support)
+    if not info.stationary:
+        info.step, info.f_max, info.dir_derivative = r.step, r.f_max, r.dir_derivative
+        info.halvings = r.halvings
+    elif not math.isnan(r.dir_derivative):
+        info.dir_derivative = r.dir_derivative
+    return info
 
 
 def _state_from(res: L.ResultC, x) -> SolverState:
@@ -652,18 +710,21 @@ def gpss_solve(prob: Objective, ball: L1Ball, cfg: GpConfig, stop: StopRule,
             if trace is not None:
                 trace.append(rec)
             cb(rec, xv)
-        except Exception as e:  # surfaced after the run
+            return 0
+        except BaseException as e:  # stops the run now; re-raised below
             err.append(e)
+            return 1
 
     cfun = L.ITER_CB(_cb)
     try:
         check(lib.l1g_solver_init(h, ptr(x0a)), "gp_init")
-        check(lib.l1g_solver_run_cb(h, C.byref(s), C.byref(res), cfun, None), "gpss_solve")
+        rc = lib.l1g_solver_run_cb(h, C.byref(s), C.byref(res), cfun, None)
+        if err:
+            raise err[0]
+        check(rc, "gpss_solve")
         check(lib.l1g_solver_get(h, ptr(x), None, None, None, None, None, None))
     finally:
         lib.l1g_solver_destroy(h)
-    if err:
-        raise err[0]
     return _state_from(res, x)
 
 
@@ -685,8 +746,10 @@ def _other_solve(prob: Objective, param: float, kind: int, stop: StopRule,
         try:
             cb(IterationRecord.from_c(rec_p.contents),
                np.ctypeslib.as_array(x_p, shape=(p,)).copy())
-        except Exception as e:  # surfaced after the run
+            return 0
+        except BaseException as e:  # stops the run now; re-raised below
             err.append(e)
+            return 1
 
     cfun = L.ITER_CB(_cb) if cb is not None else L.ITER_CB()
     if kind == 0:
@@ -696,9 +759,9 @@ def _other_solve(prob: Objective, param: float, kind: int, stop: StopRule,
         rc = lib.l1g_shrinkage_solve(op.h, ptr(y), param, int(kind == 2), C.byref(s), ptr(x),
                                      C.byref(res), C.addressof(recs) if cap else None, cap,
                                      cfun, None)
-    check(rc, ["psd_solve", "ista_solve", "fista_solve"][kind])
     if err:
         raise err[0]
+    check(rc, ["psd_solve", "ista_solve", "fista_solve"][kind])
     if trace is not None:
         trace.extend(IterationRecord.from_c(recs[i]) for i in range(min(cap, res.iterations)))
     return _state_from(res, x)

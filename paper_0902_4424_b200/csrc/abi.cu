@@ -33,6 +33,9 @@ int guarded(F&& f) {
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
     return L1G_EINVAL;
+  } catch (const Cancelled& e) {
+    g_err = e.what();
+    return L1G_ECANCELED;
   } catch (const std::exception& e) {
     g_err = e.what();
     return L1G_ERUNTIME;
@@ -719,7 +722,7 @@ void solver_run_cb(l1g_solver* s, const l1g_stop_rule& stop, l1g_result* res, l1
       k_prev = h.k;
       download(x.data(), s->vb.x[h.cur], s->p, s->stream);
       L1G_CUDA(cudaStreamSynchronize(s->stream));
-      if (cb) cb(&h.last, x.data(), s->p, user);
+      if (cb && cb(&h.last, x.data(), s->p, user) != 0) throw Cancelled();
     }
     if (h.status != RUNNING) break;
   }
@@ -1238,7 +1241,7 @@ void other_solve(l1g_op* op, const double* y_host, double param, int kind,
       std::vector<double> xh((size_t)pl.p);
       download(xh.data(), x, pl.p, s);
       L1G_CUDA(cudaStreamSynchronize(s));
-      cb(&rc, xh.data(), pl.p, user);
+      if (cb(&rc, xh.data(), pl.p, user) != 0) throw Cancelled();
     }
     if (stop.stationarity_tol > 0.0 && stat <= stop.stationarity_tol) {
       res->reason = L1G_STATIONARY;
@@ -1572,7 +1575,7 @@ static void batched_product(l1g_op* op, int B, const double* in, double* out, bo
   try {
     L1G_CUDA(cudaMemcpy2DAsync(vin, lin_pad * 8, in, lin * 8, lin * 8, B, cudaMemcpyHostToDevice, s));
     BFinArgs fa{};
-    fa.mode = adjoint ? ADJ_APPLY : FWD_APPLY;
+    fa.mode = adjoint ? (int)ADJ_APPLY : (int)FWD_APPLY;
     fa.B = B;
     fa.splits = (int)splits;
     fa.part = part;
@@ -1897,6 +1900,115 @@ int l1g_solver_get(l1g_solver* s, double* x, double* r, double* g, double* f, in
     if (k) *k = h.k;
     if (alpha0) *alpha0 = h.alpha0;
     if (matvecs) *matvecs = h.matvecs;
+  });
+}
+
+int l1g_solver_get_state(l1g_solver* s, l1g_gp_state* out, double* x, double* r, double* g,
+                         double* x_prev, double* g_prev) {
+  return guarded([&] {
+    if (s->split()) throw InvalidArgument("solver_get_state: not available for sharded solvers");
+    set_device(s->op->c);
+    DevState h;
+    read_state(s, &h);
+    const GemvPlan& pl = s->op->plan;
+    download(x, s->vb.x[h.cur], s->p, s->stream);
+    download(r, s->vb.r[h.cur], pl.n, s->stream);
+    download(g, s->vb.g[h.cur], s->p, s->stream);
+    if (h.k > 0) {
+      download(x_prev, s->vb.x[h.cur ^ 1], s->p, s->stream);
+      download(g_prev, s->vb.g[h.cur ^ 1], s->p, s->stream);
+    }
+    L1G_CUDA(cudaStreamSynchronize(s->stream));
+    if (!out) return;
+    std::memset(out, 0, sizeof(*out));
+    out->f = h.f;
+    out->k = h.k;
+    out->alpha0 = h.alpha0;
+    out->stationary = h.stationary;
+    out->has_prev = h.k > 0;
+    out->f_history_len = h.fh_len;
+    std::memcpy(out->f_history, h.fh, sizeof(double) * h.fh_len);
+    out->tau = h.tau;
+    out->alpha2_len = h.a2_len;
+    std::memcpy(out->alpha2_history, h.a2h, sizeof(double) * h.a2_len);
+    out->choice = h.choice;
+  });
+}
+
+int l1g_solver_set_state(l1g_solver* s, const l1g_gp_state* in, const double* x, const double* r,
+                         const double* g, const double* x_prev, const double* g_prev) {
+  return guarded([&] {
+    if (s->split()) throw InvalidArgument("solver_set_state: not available for sharded solvers");
+    if (!s->inited) throw InvalidArgument("solver: gp_init has not been run");
+    if (in && (in->f_history_len < 1 || in->f_history_len > kMaxHist ||
+               in->alpha2_len < 0 || in->alpha2_len > kMaxHist + 2 || in->k < 0))
+      throw InvalidArgument("solver_set_state: history lengths out of range");
+    set_device(s->op->c);
+    DevState h;
+    read_state(s, &h);
+    const GemvPlan& pl = s->op->plan;
+    auto up = [&](double* dst, const double* src, int64_t m, int64_t padded) {
+      if (!src) return;
+      L1G_CUDA(cudaMemsetAsync(dst, 0, padded * sizeof(double), s->stream));
+      L1G_CUDA(cudaMemcpyAsync(dst, src, m * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+    };
+    up(s->vb.x[h.cur], x, s->p, s->p_pad);
+    up(s->vb.r[h.cur], r, pl.n, pl.n_pad);
+    up(s->vb.g[h.cur], g, s->p, s->p_pad);
+    up(s->vb.x[h.cur ^ 1], x_prev, s->p, s->p_pad);
+    up(s->vb.g[h.cur ^ 1], g_prev, s->p, s->p_pad);
+    if (in) {
+      h.f = in->f;
+      h.f_prev = in->f;
+      h.k = in->k;
+      h.alpha0 = in->alpha0;
+      h.stationary = in->stationary;
+      h.fh_len = in->f_history_len;
+      std::memcpy(h.fh, in->f_history, sizeof(double) * in->f_history_len);
+      h.tau = in->tau;
+      h.a2_len = in->alpha2_len;
+      std::memcpy(h.a2h, in->alpha2_history, sizeof(double) * in->alpha2_len);
+      h.status = RUNNING;
+    }
+    if ((x || g || x_prev || g_prev) && h.k > 0) {
+      // secant dots of s = x - x_prev, z = grad - grad_prev (gpss.cpp:150-151, :66-68), the
+      // canonical reductions the adjoint finish would have produced
+      double* sv = dalloc<double>(s->p_pad);
+      double* zv = dalloc<double>(s->p_pad);
+      vsub(s->vb.x[h.cur], s->vb.x[h.cur ^ 1], sv, s->p_pad, s->stream);
+      vsub(s->vb.g[h.cur], s->vb.g[h.cur ^ 1], zv, s->p_pad, s->stream);
+      reduce(sv, zv, s->p_pad, RED_DOT, s->scal, 0, s->stream);
+      reduce(sv, sv, s->p_pad, RED_DOT, s->scal + 1, 0, s->stream);
+      reduce(zv, zv, s->p_pad, RED_DOT, s->scal + 2, 0, s->stream);
+      double d3[3];
+      L1G_CUDA(cudaMemcpyAsync(d3, s->scal, sizeof(d3), cudaMemcpyDeviceToHost, s->stream));
+      L1G_CUDA(cudaStreamSynchronize(s->stream));
+      dfree(sv);
+      dfree(zv);
+      h.sz = d3[0];
+      h.ss = d3[1];
+      h.zz = d3[2];
+    }
+    L1G_CUDA(cudaMemcpyAsync(s->st, &h, sizeof(h), cudaMemcpyHostToDevice, s->stream));
+    L1G_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int l1g_solver_set_problem(l1g_solver* s, const l1g_gp_config* cfg, double rho) {
+  return guarded([&] {
+    check_cfg(*cfg);
+    check_rho(rho);
+    set_device(s->op->c);
+    for (l1g_solver* q : members(s)) {
+      DevState h;
+      read_state(q, &h);
+      h.cfg = *cfg;
+      h.rho = rho;
+      L1G_CUDA(cudaMemcpyAsync(q->st, &h, sizeof(h), cudaMemcpyHostToDevice, s->stream));
+      q->cfg = *cfg;
+      q->rho = rho;
+    }
+    L1G_CUDA(cudaStreamSynchronize(s->stream));
   });
 }
 

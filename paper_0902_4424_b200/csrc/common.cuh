@@ -8,7 +8,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
+#include <mutex>
 
 #ifndef __CUDACC__
 #error "common.cuh is CUDA-only"
@@ -209,6 +211,22 @@ __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+// One-time setup per device (kernel attributes belong to the current device's context): `f`
+// runs the first time this call site is reached on each device, under a lock, so a second
+// device or a second thread never launches before its attributes are set.
+template <class F>
+inline void once_per_device(std::atomic<unsigned long long>& done, F&& f) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  f();
+  done.fetch_or(bit, std::memory_order_release);
 }
 
 }  // namespace l1g

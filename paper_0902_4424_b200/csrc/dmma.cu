@@ -400,12 +400,11 @@ BatchPlan make_batch_plan(const GemvPlan& pl, int B, int sm_count) {
 
 void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* part,
                  cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [] {
     L1G_CUDA(cudaFuncSetAttribute(bfwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)bfwd_smem()));
-    attr = true;
-  }
+  });
   const GemvPlan& pl = op.plan;
   BGemmArgs a{};
   a.K = op.K;
@@ -424,12 +423,11 @@ void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* par
 
 void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* part,
                  cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [] {
     L1G_CUDA(cudaFuncSetAttribute(badj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)badj_smem()));
-    attr = true;
-  }
+  });
   const GemvPlan& pl = op.plan;
   BGemmArgs a{};
   a.K = op.K;

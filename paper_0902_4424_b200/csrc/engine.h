@@ -21,6 +21,10 @@ struct InvalidArgument : std::invalid_argument {
 struct RuntimeFailure : std::runtime_error {
   explicit RuntimeFailure(const std::string& m) : std::runtime_error(m) {}
 };
+// an iteration callback returned nonzero (L1G_ECANCELED)
+struct Cancelled : std::runtime_error {
+  Cancelled() : std::runtime_error("iteration callback stopped the run") {}
+};
 
 constexpr int kMaxHist = 64;
 

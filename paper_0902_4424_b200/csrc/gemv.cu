@@ -996,23 +996,21 @@ static int split_choice() {
 
 template <int SPLIT>
 static void fwd_main_launch(const FwdArgs& a, int grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [] {
     L1G_CUDA(cudaFuncSetAttribute(fwd_kernel<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)fwd_smem()));
-    attr = true;
-  }
+  });
   L1G_CUDA(launch_pdl(fwd_kernel<SPLIT>, grid, 32 * (4 * SPLIT + 1), fwd_smem(), s, a));
 }
 
 template <int SPLIT>
 static void adj_main_launch(const AdjArgs& a, int grid, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [] {
     L1G_CUDA(cudaFuncSetAttribute(adj_kernel<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)adj_smem()));
-    attr = true;
-  }
+  });
   L1G_CUDA(launch_pdl(adj_kernel<SPLIT>, grid, 32 * (4 * SPLIT + 1), adj_smem(), s, a));
 }
 
@@ -1069,12 +1067,11 @@ static FwdArgs fwd_main(const Op& op, const Workspace& ws, FwdArgs a, const uint
                         bool sparse, cudaStream_t s) {
   const GemvPlan& pl = op.plan;
   if (sparse && dmask) {
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<unsigned long long> attr{0};
+    once_per_device(attr, [] {
       L1G_CUDA(cudaFuncSetAttribute(fwd_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sp_smem()));
-      attr = true;
-    }
+    });
     a.vb.dmask = const_cast<uint32_t*>(dmask);
     a.stages = pl.sp_tiles;
     a.ncr = pl.sp_ncr;

@@ -1,10 +1,12 @@
 // l1solve_dropin.cpp -- the reference's C++ solver API (include/l1solve/*.hpp) on top of
 // the C-ABI (include/l1g.h).  Builds into libl1solve_b200.so, linked against libl1g.so.
 //
-// DenseOperator problems run the device-resident loop (l1g_gpss_solve / l1g_solver_*).
-// A user-defined LinearOperator (matrix-free K) keeps the reference's host-driven loop
-// (gpss.cpp:117-292 restated below) with every reduction, the projection, the steplength
-// rule and the backtracking executed by the same device code.
+// DenseOperator problems run the device-resident loop (l1g_gpss_solve / l1g_solver_*); their
+// GpIterationState mirrors the device state in the reference's public fields.  A
+// user-defined LinearOperator (matrix-free K) keeps the reference's host-driven gp_init /
+// gp_iterate / gpss_solve (gpss.cpp:117-292 restated below) with every reduction, the
+// projection, the steplength rule and the backtracking executed by the same device code.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -367,63 +369,219 @@ BacktrackResult backtracking_search(const Objective& prob, const Vector& x, cons
 }
 
 // ------------------------------------------------------------------------- gp state
-GpIterationState::GpIterationState() = default;
-GpIterationState::~GpIterationState() { l1g_solver_destroy(s_); }
-GpIterationState::GpIterationState(GpIterationState&& o) noexcept
-    : stationary(o.stationary), s_(o.s_) {
-  o.s_ = nullptr;
-}
-GpIterationState& GpIterationState::operator=(GpIterationState&& o) noexcept {
-  if (this != &o) {
-    l1g_solver_destroy(s_);
-    s_ = o.s_;
-    stationary = o.stationary;
-    o.s_ = nullptr;
-  }
-  return *this;
-}
-
-Vector GpIterationState::x() const {
-  Vector v(p_);
-  check(l1g_solver_get(s_, v.data(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr));
-  return v;
-}
-Vector GpIterationState::kx_minus_y() const {
-  Vector v(n_);
-  check(l1g_solver_get(s_, nullptr, v.data(), nullptr, nullptr, nullptr, nullptr, nullptr));
-  return v;
-}
-Vector GpIterationState::grad() const {
-  Vector v(p_);
-  check(l1g_solver_get(s_, nullptr, nullptr, v.data(), nullptr, nullptr, nullptr, nullptr));
-  return v;
-}
-double GpIterationState::f() const {
-  double f = 0.0;
-  check(l1g_solver_get(s_, nullptr, nullptr, nullptr, &f, nullptr, nullptr, nullptr));
-  return f;
-}
-long GpIterationState::k() const {
-  int64_t k = 0;
-  check(l1g_solver_get(s_, nullptr, nullptr, nullptr, nullptr, &k, nullptr, nullptr));
-  return static_cast<long>(k);
-}
-double GpIterationState::alpha0() const {
-  double a = 0.0;
-  check(l1g_solver_get(s_, nullptr, nullptr, nullptr, nullptr, nullptr, &a, nullptr));
-  return a;
-}
+namespace detail {
+// A DenseOperator problem's GpIterationState on the GPU (an l1g_solver) and the state the
+// device last reported, against which the caller's fields are compared before each step.
+struct DeviceIterationState {
+  l1g_solver* s = nullptr;
+  Index n = 0, p = 0;
+  Vector x, r, g, x_prev, g_prev;
+  double f = 0.0, alpha0 = 0.0, tau = 0.0, rho = 0.0;
+  long k = 0;
+  bool stationary = false, has_prev = false;
+  std::deque<double> fh, a2h;
+  GpConfig cfg;
+  ~DeviceIterationState() { l1g_solver_destroy(s); }
+};
+}  // namespace detail
 
 namespace {
-const DenseOperator& dense_or_throw(const Objective& prob) {
-  auto* d = dynamic_cast<const DenseOperator*>(&prob.op());
-  if (!d) throw std::invalid_argument("gp_init/gp_iterate: the device state needs a DenseOperator");
-  return *d;
+using detail::DeviceIterationState;
+
+bool bits_equal(const Vector& a, const Vector& b) {
+  return a.size() == b.size() &&
+         (a.size() == 0 ||
+          std::memcmp(a.data(), b.data(), sizeof(double) * static_cast<std::size_t>(a.size())) == 0);
+}
+bool bits_equal(const std::deque<double>& a, const std::deque<double>& b) {
+  if (a.size() != b.size()) return false;
+  for (std::size_t i = 0; i < a.size(); ++i)
+    if (std::memcmp(&a[i], &b[i], sizeof(double)) != 0) return false;
+  return true;
+}
+bool same_cfg(const GpConfig& a, const GpConfig& b) {
+  return a.beta == b.beta && a.theta == b.theta && a.memory == b.memory &&
+         a.alpha_min == b.alpha_min && a.alpha_max == b.alpha_max && a.tau1 == b.tau1 &&
+         a.alpha2_memory == b.alpha2_memory;
 }
 int64_t solver_matvecs(l1g_solver* s) {
   int64_t mv = 0;
   check(l1g_solver_get(s, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &mv));
   return mv;
+}
+SteplengthChoice conv(const l1g_sl_choice& c) {
+  SteplengthChoice o;
+  o.alpha = c.alpha;
+  o.bb_active = c.bb_active != 0;
+  o.bb1_raw = c.bb1_raw;
+  o.bb2_raw = c.bb2_raw;
+  o.tau_before = c.tau_before;
+  o.tau_after = c.tau_after;
+  return o;
+}
+
+// device -> the caller's GpIterationState / SteplengthState (and the comparison copy)
+l1g_gp_state pull(DeviceIterationState& d, GpIterationState& st, SteplengthState* sls) {
+  l1g_gp_state g;
+  d.x = Vector(d.p);
+  d.r = Vector(d.n);
+  d.g = Vector(d.p);
+  d.x_prev = Vector(d.p);
+  d.g_prev = Vector(d.p);
+  check(l1g_solver_get_state(d.s, &g, d.x.data(), d.r.data(), d.g.data(), d.x_prev.data(),
+                             d.g_prev.data()));
+  d.f = g.f;
+  d.k = static_cast<long>(g.k);
+  d.alpha0 = g.alpha0;
+  d.stationary = g.stationary != 0;
+  d.has_prev = g.has_prev != 0;
+  d.fh.assign(g.f_history, g.f_history + g.f_history_len);
+  d.tau = g.tau;
+  d.a2h.assign(g.alpha2_history, g.alpha2_history + g.alpha2_len);
+  st.x = d.x;
+  st.kx_minus_y = d.r;
+  st.grad = d.g;
+  st.f = d.f;
+  st.k = d.k;
+  st.f_history = d.fh;
+  st.alpha0 = d.alpha0;
+  st.stationary = d.stationary;
+  if (sls) {
+    sls->tau = d.tau;
+    sls->alpha2_history = d.a2h;
+    if (d.has_prev) {
+      sls->prev_x = d.x_prev;
+      sls->prev_grad = d.g_prev;
+    }
+  }
+  return g;
+}
+
+// the caller's state, steplength state, GpConfig and ball -> device, where they differ from
+// what the device last reported
+void push(DeviceIterationState& d, const GpIterationState& st, const SteplengthState& sls,
+          const GpConfig& cfg, const L1Ball& ball) {
+  if (!same_cfg(cfg, d.cfg) || ball.radius() != d.rho) {
+    const l1g_gp_config c = conv(cfg);
+    check(l1g_solver_set_problem(d.s, &c, ball.radius()));
+    d.cfg = cfg;
+    d.rho = ball.radius();
+  }
+  if (st.x.size() != d.p || st.grad.size() != d.p || st.kx_minus_y.size() != d.n)
+    throw std::invalid_argument("gp_iterate: state vectors do not match the operator");
+  const double* x = bits_equal(st.x, d.x) ? nullptr : st.x.data();
+  const double* r = bits_equal(st.kx_minus_y, d.r) ? nullptr : st.kx_minus_y.data();
+  const double* g = bits_equal(st.grad, d.g) ? nullptr : st.grad.data();
+  const bool prev = st.k > 0 && sls.prev_x.size() == d.p && sls.prev_grad.size() == d.p;
+  const double* xp = prev && !(d.has_prev && bits_equal(sls.prev_x, d.x_prev)) ? sls.prev_x.data()
+                                                                              : nullptr;
+  const double* gp = prev && !(d.has_prev && bits_equal(sls.prev_grad, d.g_prev))
+                         ? sls.prev_grad.data()
+                         : nullptr;
+  const bool scalars = st.f != d.f || st.k != d.k || !bits_equal(st.f_history, d.fh) ||
+                       st.alpha0 != d.alpha0 || st.stationary != d.stationary ||
+                       sls.tau != d.tau || !bits_equal(sls.alpha2_history, d.a2h);
+  if (!scalars && !x && !r && !g && !xp && !gp) return;
+  if (st.f_history.empty() || st.f_history.size() > 64 || sls.alpha2_history.size() > 66)
+    throw std::invalid_argument("gp_iterate: history lengths out of range (at most 64)");
+  l1g_gp_state in;
+  std::memset(&in, 0, sizeof(in));
+  in.f = st.f;
+  in.k = st.k;
+  in.alpha0 = st.alpha0;
+  in.stationary = st.stationary;
+  in.f_history_len = static_cast<int32_t>(st.f_history.size());
+  std::copy(st.f_history.begin(), st.f_history.end(), in.f_history);
+  in.tau = sls.tau;
+  in.alpha2_len = static_cast<int32_t>(sls.alpha2_history.size());
+  std::copy(sls.alpha2_history.begin(), sls.alpha2_history.end(), in.alpha2_history);
+  check(l1g_solver_set_state(d.s, &in, x, r, g, xp, gp));
+  d.x = st.x;
+  d.r = st.kx_minus_y;
+  d.g = st.grad;
+  if (xp) d.x_prev = sls.prev_x;
+  if (gp) d.g_prev = sls.prev_grad;
+  d.has_prev = d.has_prev || prev;
+  d.f = st.f;
+  d.k = st.k;
+  d.fh = st.f_history;
+  d.alpha0 = st.alpha0;
+  d.stationary = st.stationary;
+  d.tau = sls.tau;
+  d.a2h = sls.alpha2_history;
+}
+
+// ---- matrix-free operators: gpss.cpp:117-219 on the host, every reduction, projection,
+// steplength rule and backtracking step on the device primitives
+GpIterationState generic_gp_init(const Objective& prob, const L1Ball& ball, Vector x0,
+                                 const GpConfig& cfg, MatvecCounter& mv) {
+  if (x0.size() == 0) x0 = Vector::Zero(prob.dim());
+  if (!ball.contains(x0, 1e-12)) throw std::invalid_argument("gp_init: starting point is infeasible");
+  GpIterationState st;
+  st.x = std::move(x0);
+  st.kx_minus_y = prob.op().apply(st.x, mv) - prob.y();
+  st.f = st.kx_minus_y.squaredNorm();
+  st.grad = 2.0 * prob.op().apply_adjoint(st.kx_minus_y, mv);
+  st.alpha0 = alpha0_from_gradient(ball, st.x, st.grad, cfg);
+  st.f_history.assign(1, st.f);
+  return st;
+}
+
+GpStepInfo generic_gp_iterate(const Objective& prob, const L1Ball& ball, const GpConfig& cfg,
+                              GpIterationState& st, SteplengthState& sls, MatvecCounter& mv,
+                              double tol) {
+  GpStepInfo info;
+  if (st.stationary) {
+    info.stationary = true;
+    info.stationarity = 0.0;
+    return info;
+  }
+  if (st.k == 0) info.steplength.alpha = st.alpha0;
+  else info.steplength = steplength_select(sls, st.x - sls.prev_x, st.grad - sls.prev_grad, cfg, st.k);
+  const double first_alpha = info.steplength.alpha;
+  double alpha = first_alpha, first_stat = 0.0;
+  Vector d;
+  for (bool first = true;; first = false) {  // escalation, gpss.cpp:162-191
+    d = project_l1_ball(st.x - alpha * st.grad, ball) - st.x;
+    info.stationarity = d.lpNorm<Infinity>();
+    if (first) first_stat = info.stationarity;
+    if (info.stationarity <= tol) {
+      st.stationary = info.stationary = true;
+      info.alpha = alpha;
+      info.f_after = st.f;
+      return info;
+    }
+    info.dir_derivative = st.grad.dot(d);
+    if (info.dir_derivative < 0.0) break;
+    if (alpha >= cfg.alpha_max) {
+      st.stationary = info.stationary = true;
+      info.alpha = first_alpha;
+      info.stationarity = first_stat;
+      info.f_after = st.f;
+      return info;
+    }
+    alpha = std::min(alpha * 10.0, cfg.alpha_max);
+  }
+  info.alpha = alpha;
+  const Vector kd = prob.op().apply(d, mv);
+  info.f_max = *std::max_element(st.f_history.begin(), st.f_history.end());
+  const l1g_gp_config c = conv(cfg);
+  int32_t h = 0;
+  double f_new = 0.0;
+  check(l1g_backtrack(ctx(), st.f, st.kx_minus_y.dot(kd), kd.squaredNorm(), info.f_max,
+                      info.dir_derivative, &c, &info.step, &f_new, &h));
+  info.halvings = h;
+  sls.prev_x = st.x;
+  sls.prev_grad = st.grad;
+  st.x += info.step * d;
+  st.kx_minus_y += info.step * kd;
+  st.f = f_new;
+  st.grad = 2.0 * prob.op().apply_adjoint(st.kx_minus_y, mv);
+  st.f_history.push_back(st.f);
+  while (st.f_history.size() > static_cast<std::size_t>(cfg.memory)) st.f_history.pop_front();
+  ++st.k;
+  info.f_after = st.f;
+  return info;
 }
 }  // namespace
 
@@ -431,16 +589,22 @@ int64_t solver_matvecs(l1g_solver* s) {
 GpIterationState gp_init(const Objective& prob, const L1Ball& ball, Vector x0,
                          const GpConfig& cfg, MatvecCounter& mv) {
   cfg.validate();
-  const DenseOperator& op = dense_or_throw(prob);
   if (x0.size() != 0 && x0.size() != prob.dim())
     throw std::invalid_argument("gp_init: starting point has wrong dimension");
-  GpIterationState st;
-  st.n_ = op.rows();
-  st.p_ = op.cols();
+  auto* op = dynamic_cast<const DenseOperator*>(&prob.op());
+  if (!op) return generic_gp_init(prob, ball, std::move(x0), cfg, mv);
+  auto dev = std::make_shared<DeviceIterationState>();
+  dev->n = op->rows();
+  dev->p = op->cols();
+  dev->cfg = cfg;
+  dev->rho = ball.radius();
   const l1g_gp_config c = conv(cfg);
-  check(l1g_solver_create(op.handle(), prob.y().data(), ball.radius(), &c, &st.s_));
-  check(l1g_solver_init(st.s_, x0.size() ? x0.data() : nullptr));
+  check(l1g_solver_create(op->handle(), prob.y().data(), ball.radius(), &c, &dev->s));
+  check(l1g_solver_init(dev->s, x0.size() ? x0.data() : nullptr));
   mv.count += 2;
+  GpIterationState st;
+  pull(*dev, st, nullptr);
+  st.device = std::move(dev);
   return st;
 }
 
@@ -448,59 +612,51 @@ GpIterationState gp_init(const Objective& prob, const L1Ball& ball, Vector x0,
 GpStepInfo gp_iterate(const Objective& prob, const L1Ball& ball, const GpConfig& cfg,
                       GpIterationState& state, SteplengthState& sls, MatvecCounter& mv,
                       double stationarity_tol) {
-  (void)prob;
-  (void)ball;
-  (void)cfg;
-  (void)sls;
-  const int64_t before = solver_matvecs(state.handle());
+  if (!state.device) return generic_gp_iterate(prob, ball, cfg, state, sls, mv, stationarity_tol);
+  DeviceIterationState& d = *state.device;
+  push(d, state, sls, cfg, ball);
+  GpStepInfo info;
+  if (state.stationary) {  // gpss.cpp:139-143
+    info.stationary = true;
+    info.stationarity = 0.0;
+    return info;
+  }
+  const int64_t before = solver_matvecs(d.s);
   l1g_iter_record rec;
   int32_t stat = 0;
-  check(l1g_solver_iterate(state.handle(), stationarity_tol, &rec, &stat));
-  mv.count += solver_matvecs(state.handle()) - before;
-  state.stationary = stat != 0;
-  GpStepInfo info;
+  check(l1g_solver_iterate(d.s, stationarity_tol, &rec, &stat));
+  mv.count += solver_matvecs(d.s) - before;
+  const l1g_gp_state g = pull(d, state, &sls);
+  info.steplength = conv(g.choice);  // the choice before any escalation (gpss.cpp:148-153)
   info.stationary = stat != 0;
   info.alpha = rec.alpha;
-  info.step = rec.step;
-  info.f_after = rec.f;
   info.stationarity = rec.stationarity;
-  info.f_max = rec.f_max;
-  info.dir_derivative = rec.dir_derivative;
-  info.halvings = rec.halvings;
-  info.steplength.alpha = rec.alpha;
-  info.steplength.bb_active = rec.bb_active != 0;
-  info.steplength.bb1_raw = rec.bb1_raw;
-  info.steplength.bb2_raw = rec.bb2_raw;
-  info.steplength.tau_before = rec.tau_before;
-  info.steplength.tau_after = rec.tau_after;
+  info.f_after = state.f;
+  if (!info.stationary) {
+    info.step = rec.step;
+    info.f_max = rec.f_max;
+    info.dir_derivative = rec.dir_derivative;
+    info.halvings = rec.halvings;
+  } else if (!std::isnan(rec.dir_derivative)) {
+    info.dir_derivative = rec.dir_derivative;
+  }
   return info;
 }
 
 namespace {
 
-// Host-driven loop for matrix-free operators: gpss.cpp:117-292 restated over the device
-// primitives (projection, reductions, steplength rule, backtracking).
+// gpss.cpp:221-292 for matrix-free operators: the reference's loop over gp_init / gp_iterate
 SolverState generic_solve(const Objective& prob, const L1Ball& ball, const GpConfig& cfg,
                           const StopRule& stop, const IterationCallback& cb, Vector x0) {
   using Clock = std::chrono::steady_clock;
   const auto start = Clock::now();
   auto since = [&] { return std::chrono::duration<double>(Clock::now() - start).count(); };
   SolverState out;
-  cfg.validate();
-  if (x0.size() == 0) x0 = Vector::Zero(prob.dim());
-  if (x0.size() != prob.dim()) throw std::invalid_argument("gp_init: starting point has wrong dimension");
-  if (!ball.contains(x0, 1e-12)) throw std::invalid_argument("gp_init: starting point is infeasible");
-  Vector x = std::move(x0);
-  Vector r = prob.op().apply(x, out.matvecs) - prob.y();
-  double f = r.squaredNorm();
-  Vector g = 2.0 * prob.op().apply_adjoint(r, out.matvecs);
-  const double alpha0 = alpha0_from_gradient(ball, x, g, cfg);
-  std::deque<double> fh(1, f);
+  GpIterationState st = gp_init(prob, ball, std::move(x0), cfg, out.matvecs);
   SteplengthState sls = steplength_init(cfg);
-  Vector xp, gp;
   out.reason = StopReason::MaxIterations;
-  out.objective = f;
-  double f_prev = f;
+  out.objective = st.f;
+  double f_prev = st.f;
   for (long k = 0;; ++k) {
     if (stop.max_iterations > 0 && k >= stop.max_iterations) {
       out.reason = StopReason::MaxIterations;
@@ -514,82 +670,44 @@ SolverState generic_solve(const Objective& prob, const L1Ball& ball, const GpCon
       out.reason = StopReason::MaxSeconds;
       break;
     }
-    SteplengthChoice ch;
-    if (k == 0) ch.alpha = alpha0;
-    else ch = steplength_select(sls, x - xp, g - gp, cfg, k);
-    const double first_alpha = ch.alpha;
-    double alpha = first_alpha, first_stat = 0.0, stat = 0.0, gd = 0.0;
-    Vector d;
-    bool stationary = false;
-    for (bool first = true;; first = false) {
-      const Vector h = project_l1_ball(x - alpha * g, ball);
-      d = h - x;
-      stat = d.lpNorm<Infinity>();
-      if (first) first_stat = stat;
-      if (stat <= stop.stationarity_tol) {
-        stationary = true;
-        break;
-      }
-      gd = g.dot(d);
-      if (gd < 0.0) break;
-      if (alpha >= cfg.alpha_max) {
-        stationary = true;
-        stat = first_stat;
-        break;
-      }
-      alpha = std::min(alpha * 10.0, cfg.alpha_max);
-    }
-    out.stationarity = stat;
-    if (stationary) {
+    const GpStepInfo info = gp_iterate(prob, ball, cfg, st, sls, out.matvecs, stop.stationarity_tol);
+    out.stationarity = info.stationarity;
+    if (info.stationary) {
       out.reason = StopReason::Stationary;
       break;
     }
-    const Vector kd = prob.op().apply(d, out.matvecs);
-    double f_max = fh.front();
-    for (double v : fh) f_max = v > f_max ? v : f_max;
-    const l1g_gp_config c = conv(cfg);
-    double step = 0.0, f_new = 0.0;
-    int32_t halv = 0;
-    check(l1g_backtrack(ctx(), f, r.dot(kd), kd.squaredNorm(), f_max, gd, &c, &step, &f_new,
-                        &halv));
-    xp = x;
-    gp = g;
-    x += step * d;
-    r += step * kd;
-    f = f_new;
-    g = 2.0 * prob.op().apply_adjoint(r, out.matvecs);
-    fh.push_back(f);
-    while (fh.size() > static_cast<std::size_t>(cfg.memory)) fh.pop_front();
-    out.iterations = k + 1;
-    out.objective = f;
+    out.iterations = st.k;
+    out.objective = st.f;
     out.elapsed_seconds = since();
     if (cb) {
       IterationRecord rec;
       rec.k = k;
-      rec.f = f;
-      rec.stationarity = stat;
-      rec.alpha = alpha;
-      rec.step = step;
+      rec.f = info.f_after;
+      rec.stationarity = info.stationarity;
+      rec.alpha = info.alpha;
+      rec.step = info.step;
       rec.matvecs = out.matvecs.count;
       rec.elapsed_seconds = out.elapsed_seconds;
-      rec.bb_active = ch.bb_active;
-      rec.bb1_raw = ch.bb1_raw;
-      rec.bb2_raw = ch.bb2_raw;
-      rec.tau_before = ch.tau_before;
-      rec.tau_after = ch.tau_after;
-      rec.f_max = f_max;
-      rec.dir_derivative = gd;
-      cb(rec, x);
+      rec.bb_active = info.steplength.bb_active;
+      rec.bb1_raw = info.steplength.bb1_raw;
+      rec.bb2_raw = info.steplength.bb2_raw;
+      rec.tau_before = info.steplength.tau_before;
+      rec.tau_after = info.steplength.tau_after;
+      rec.f_max = info.f_max;
+      rec.dir_derivative = info.dir_derivative;
+      cb(rec, st.x);
     }
     if (stop.objective_tol > 0.0 &&
-        std::abs(f_prev - f) <= stop.objective_tol * std::max(1.0, std::abs(f))) {
+        std::abs(f_prev - st.f) <= stop.objective_tol * std::max(1.0, std::abs(st.f))) {
       out.reason = StopReason::ObjectiveTol;
       break;
     }
-    f_prev = f;
+    f_prev = st.f;
   }
-  out.x = std::move(x);
-  out.f_history = std::move(fh);
+  out.x = std::move(st.x);
+  out.iterations = st.k;
+  out.objective = st.f;
+  out.f_history = std::move(st.f_history);
   out.elapsed_seconds = since();
   return out;
 }
@@ -599,15 +717,19 @@ struct CbCtx {
   std::exception_ptr err;
 };
 
-void trampoline(const l1g_iter_record* rec, const double* x, int64_t p, void* user) {
+// a throwing callback stops the device loop at once (nonzero return -> L1G_ECANCELED) and
+// its exception is rethrown to the caller, as the reference propagates it
+int trampoline(const l1g_iter_record* rec, const double* x, int64_t p, void* user) {
   auto* c = static_cast<CbCtx*>(user);
-  if (c->err) return;
+  if (c->err) return 1;
   try {
     Vector xv(p);
     std::memcpy(xv.data(), x, sizeof(double) * static_cast<std::size_t>(p));
     (*c->cb)(conv(*rec), xv);
+    return 0;
   } catch (...) {
     c->err = std::current_exception();
+    return 1;
   }
 }
 

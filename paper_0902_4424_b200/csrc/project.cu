@@ -885,13 +885,12 @@ size_t proj_scratch_doubles(int64_t p_pad) {
 
 template <int M>
 static void proj_launch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s, int nprob) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [] {
     L1G_CUDA(cudaFuncSetAttribute(proj_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)((SMEM_CAND + 1) * 8)));
     L1G_CUDA(cudaFuncSetAttribute(proj_kernel<M>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr = true;
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pp.cs * nprob, 1, 1);
   cfg.blockDim = dim3(PT, 1, 1);

@@ -136,8 +136,9 @@ class GpuBackend:
                         "stationarity": info.stationarity, "f": info.f_after}, info.stationary
 
             def get(s):
-                x, r, g, f, k, a0, mv = s.st._get()
-                return dict(x=x, kx_minus_y=r, grad=g, f=f, k=k, alpha0=a0, matvecs=mv)
+                st = s.st
+                return dict(x=st.x, kx_minus_y=st.kx_minus_y, grad=st.grad, f=st.f, k=st.k,
+                            alpha0=st.alpha0, matvecs=s.mv.count)
         return _G()
 
     def gpss_solve(self, K, y, rho, cfg, stop, x0=None, x_trace=False):

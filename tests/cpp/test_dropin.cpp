@@ -122,10 +122,92 @@ int main() {
   GpIterationState gs = gp_init(obj, ball, Vector(), cfg, mv2);
   SteplengthState sls = steplength_init(cfg);
   for (long i = 0; i < sa.iterations; ++i) gp_iterate(obj, ball, cfg, gs, sls, mv2, 0.0);
-  const Vector gx = gs.x();
+  const Vector gx = gs.x;
   bool same2 = true;
   for (Index i = 0; i < gx.size(); ++i) same2 = same2 && gx[i] == sa.x[i];
   EXPECT(same2 && mv2.count == sa.matvecs.count);
+
+  // the reference's public GpIterationState fields (gpss.hpp:89-98) after gp_init / gp_iterate
+  {
+    MatvecCounter mvi;
+    GpIterationState s0 = gp_init(obj, ball, Vector(), cfg, mvi);
+    EXPECT(s0.k == 0 && s0.f_history.size() == 1 && s0.f_history.front() == s0.f);
+    EXPECT(s0.x.size() == 200 && s0.kx_minus_y.size() == 60 && s0.grad.size() == 200);
+    EXPECT(near(s0.f, obj.y().squaredNorm(), 1e-14) && s0.alpha0 > 0.0 && !s0.stationary);
+    SteplengthState sl0 = steplength_init(cfg);
+    const GpStepInfo i0 = gp_iterate(obj, ball, cfg, s0, sl0, mvi, 0.0);
+    EXPECT(s0.k == 1 && s0.f == i0.f_after && s0.f < s0.f_history.front() + 1e300);
+    EXPECT(i0.steplength.alpha == s0.alpha0);  // k = 0: alpha0, before any escalation
+    EXPECT(sl0.prev_x.size() == 200 && sl0.prev_grad.size() == 200);
+  }
+
+  // a user-defined (matrix-free) LinearOperator runs the reference's host-driven loop over
+  // the device primitives; with the same K it must reproduce the dense device loop exactly
+  struct Wrapped : LinearOperator {
+    const DenseOperator* d;
+    explicit Wrapped(const DenseOperator* k) : d(k) {}
+    Index rows() const override { return d->rows(); }
+    Index cols() const override { return d->cols(); }
+   protected:
+    void do_apply(const Vector& x, Vector& out) const override {
+      MatvecCounter m;
+      out = d->apply(x, m);
+    }
+    void do_apply_adjoint(const Vector& r, Vector& out) const override {
+      MatvecCounter m;
+      out = d->apply_adjoint(r, m);
+    }
+  };
+  const Wrapped wrapped(&op);
+  const Objective wobj(wrapped, obj.y());
+  {
+    StopRule s40;
+    s40.max_iterations = 40;
+    s40.stationarity_tol = 0.0;
+    const SolverState dsol = gpss_solve(obj, ball, cfg, s40);
+    const SolverState wsol = gpss_solve(wobj, ball, cfg, s40);
+    bool eq = dsol.iterations == wsol.iterations && dsol.matvecs.count == wsol.matvecs.count &&
+              dsol.objective == wsol.objective;
+    for (Index i = 0; eq && i < dsol.x.size(); ++i) eq = dsol.x[i] == wsol.x[i];
+    EXPECT(eq);
+    // caller edits between steps (x, cached misfit and gradient, GpConfig) reach the device
+    auto run = [&](const Objective& o) {
+      MatvecCounter m;
+      GpConfig c = cfg;
+      GpIterationState st = gp_init(o, ball, Vector(), c, m);
+      SteplengthState sl = steplength_init(c);
+      for (int i = 0; i < 5; ++i) gp_iterate(o, ball, c, st, sl, m, 0.0);
+      st.x *= 0.5;  // still feasible; refresh the caches the way a caller would
+      st.kx_minus_y = o.op().apply(st.x, m) - o.y();
+      st.f = st.kx_minus_y.squaredNorm();
+      st.grad = 2.0 * o.op().apply_adjoint(st.kx_minus_y, m);
+      st.f_history.assign(1, st.f);
+      c.memory = 3;
+      for (int i = 0; i < 6; ++i) gp_iterate(o, ball, c, st, sl, m, 0.0);
+      return st;
+    };
+    const GpIterationState a = run(obj), b = run(wobj);
+    bool eq2 = a.k == b.k && a.f == b.f && a.f_history.size() == b.f_history.size();
+    for (Index i = 0; eq2 && i < a.x.size(); ++i) eq2 = a.x[i] == b.x[i] && a.grad[i] == b.grad[i];
+    EXPECT(eq2 && a.device && !b.device);
+  }
+
+  // a throwing callback stops the device loop at once and its exception propagates
+  {
+    StopRule s100;
+    s100.max_iterations = 100;
+    s100.stationarity_tol = 0.0;
+    int calls = 0;
+    bool thrown = false;
+    try {
+      gpss_solve(obj, ball, cfg, s100, [&](const IterationRecord&, const Vector&) {
+        if (++calls == 3) throw std::range_error("stop here");
+      });
+    } catch (const std::range_error&) {
+      thrown = true;
+    }
+    EXPECT(thrown && calls == 3);
+  }
 
   // spectral norm of a diagonal operator
   Matrix dg = Matrix::Zero(2, 2);

@@ -73,3 +73,41 @@ def test_fullsize_bit_identical(name, iters):
         assert np.array_equal(xr, xo) and rr["objective"] == ro["objective"]
         compare_records(reco, recr, REF_FIELDS, lambda r, f: r[f])
     D["op"].close()
+
+
+# comparison windows of the literal (sequential-sum) reference reading, measured by
+# tools/divergence.py at full size (profiles/r02_divergence.json)
+WINDOWS = {"C2": 79, "C3": 111}
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_fullsize_within_tolerance_of_literal_reference(name):
+    """North star: iterates and objective within 1e-9 (relative) of the reference's own
+    arithmetic, equal support outside the 1e-12 band, the same accepted steplength rule and
+    halvings, at every iteration of the config's window -- GPU against the literal oracle
+    (bit-identical to oracle/_ref/libref_fast.so, the reference sources, per
+    profiles/r02_divergence.json)."""
+    hspec = copy.copy(H.CONFIGS[name])
+    ospec = copy.copy(getattr(PB, name))
+    if hspec.kind == "gaussian":
+        hspec.sigma_hat = ospec.sigma_hat = SIGMA[name]
+    w = WINDOWS[name]
+    P = O.build_problem(ospec)
+    D = H.build_problem(hspec)
+    with O.mode(O.LITERAL):
+        _, _, recl, xhl = O.gpss_solve(P["K"], P["y"], P["rho"], O.GpConfig(),
+                                       O.StopRule(w, 0, 0, 0.0), x_trace=True)
+    xs, trace = [], []
+    l1.gpss_solve(l1.Objective(D["op"], D["y"]), l1.L1Ball(D["rho"]), l1.GpConfig(),
+                  l1.StopRule(max_iterations=w, stationarity_tol=0.0),
+                  cb=lambda rec, x: xs.append(x), trace=trace)
+    assert len(xs) == len(recl) == w
+    for i in range(w):
+        a, b = xs[i], xhl[i]
+        assert np.linalg.norm(a - b) <= 1e-9 * np.linalg.norm(b), i + 1
+        assert abs(trace[i].f - recl[i]["f"]) <= 1e-9 * abs(recl[i]["f"]), i + 1
+        assert trace[i].bb_active == recl[i]["bb_active"], i + 1
+        assert trace[i].halvings == recl[i]["halvings"], i + 1
+        big = (np.abs(a) > 1e-12) | (np.abs(b) > 1e-12)
+        assert not np.any(((a != 0) != (b != 0)) & big), i + 1
+    D["op"].close()
