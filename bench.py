@@ -583,7 +583,7 @@ def run_b200(args, world, rank, local, pg):
         xk, xg = C.c_double(), C.c_double()
         L.check(lib.l1g_solver_time_exchange(h, 20, C.byref(xk), C.byref(xg)), "time_exchange")
         nccl = {"allgather_Kd_ms": round(max_over_ranks(pg, xk.value), 5),
-                "allgather_KTr_ms": round(max_over_ranks(pg, xg.value), 5),
+                "allgather_xg_packet_ms": round(max_over_ranks(pg, xg.value), 5),
                 "share_of_iteration": round((xk.value + xg.value) /
                                             (dev_ms / max(done_iters, 1)), 4)}
     prof = (C.c_double * 24)()
@@ -686,8 +686,9 @@ def run_b200(args, world, rank, local, pg):
                            "n": n, "p": p, "iterations_per_step": done_iters / args.steps,
                            "stop_reason": reason, "rho": rho, "sigma_hat": P["sigma_hat"],
                            "l2": "inputs larger than L2 (K = %.2f GiB)" % (k_bytes / 2**30),
-                           "parallelism": (f"column-sharded over {world} GPUs (NCCL "
-                                           "allgather of K d / K^T r shard values)")
+                           "parallelism": (f"column-sharded over {world} GPUs (rank-owned x, g "
+                                           "slices; NCCL allgathers of the K d shard values "
+                                           "and of the [x | g | dots] packets)")
                            if sharded else "single",
                            "setup_s": round(setup_s, 3)},
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 8,

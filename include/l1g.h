@@ -223,9 +223,11 @@ int l1g_shrinkage_solve(l1g_op* op, const double* y, double lambda, int accelera
 
 /* ---- column-sharded runs (no reference counterpart: the reference is
  * single-threaded).  Shard r of R holds columns [r*p/R, (r+1)*p/R) of K as its own l1g_op
- * (p/R a multiple of 256); x, g and d are replicated, and each iteration exchanges the
- * shard tree values of K d (n doubles per shard) and of K^T r (p/R doubles per shard).
- * With p/R a power of two the result is bit-identical to the unsharded solve.
+ * (p/R a multiple of 256) and owns that slice of x and g.  Each iteration exchanges the shard
+ * tree values of K d (n doubles per shard) and, after the adjoint, the shard's packet: its new
+ * x and g slices and its subtree values of s'z, s's, z'z with its clock (2 p/R + 8 doubles);
+ * the projection runs on the gathered x, g and joins the dots over the ranks.  With p/R a
+ * power of two the result is bit-identical to the unsharded solve.
  *   l1g_solver_create_group: R shards in this process on one device, run in lockstep
  *     (exchange = device copies); the other l1g_solver_* calls take the returned leader.
  *   l1g_comm_*: an NCCL communicator, one shard per process (rank r owns shard r). */
@@ -234,10 +236,17 @@ int l1g_solver_create_group(l1g_op* const* ops, int nshards, const double* y, do
                             const l1g_gp_config* cfg, l1g_solver** out);
 int l1g_comm_unique_id(void* id128);
 int l1g_comm_create(l1g_ctx* ctx, int rank, int nranks, const void* id128, l1g_comm** out);
+/* a communicator whose transport is the caller's own host allgather (no NCCL): every
+ * exchange is staged through pinned host memory and `fn` runs as a host node of the
+ * iteration graph -- e.g. gloo between processes sharing one GPU in tests.  fn must fill
+ * recv[r * count + i] with rank r's send[i] and return 0. */
+typedef int (*l1g_allgather_fn)(const double* send, double* recv, int64_t count, void* user);
+int l1g_comm_create_host(l1g_ctx* ctx, int rank, int nranks, l1g_allgather_fn fn, void* user,
+                         l1g_comm** out);
 void l1g_comm_destroy(l1g_comm* comm);
 int l1g_solver_create_sharded(l1g_op* op, l1g_comm* comm, const double* y, double rho,
                               const l1g_gp_config* cfg, l1g_solver** out);
-/* average duration of the two per-iteration exchanges (K d values, K^T r values) over `reps`
+/* average duration of the two per-iteration exchanges (K d values; [x | g | dots] packets) over `reps`
  * standalone launches on the solver stream (NCCL time, reported next to the solve) */
 int l1g_solver_time_exchange(l1g_solver* s, int reps, double* kd_ms, double* g_ms);
 /* ---- batched right-hand sides (BASELINE C5): B

@@ -65,6 +65,8 @@ RECORD_FIELDS = [f for f, _ in IterRecordC._fields_]
 ITER_CB = C.CFUNCTYPE(C.c_int, C.POINTER(IterRecordC), C.POINTER(C.c_double), C.c_int64,
                       C.c_void_p)
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64,
+                           C.c_void_p)
 _dp = C.POINTER(C.c_double)
 _vp = C.c_void_p
 _i64 = C.c_int64
@@ -109,6 +111,8 @@ _SIGS = {
     "l1g_comm_unique_id": (C.c_int, [_vp]),
     "l1g_comm_create": (C.c_int, [_vp, C.c_int, C.c_int, _vp, C.POINTER(_vp)]),
     "l1g_comm_destroy": (None, [_vp]),
+    "l1g_comm_create_host": (C.c_int, [_vp, C.c_int, C.c_int, ALLGATHER_FN, _vp,
+                                       C.POINTER(_vp)]),
     "l1g_solver_create_sharded": (C.c_int, [_vp, _vp, _vp, C.c_double, C.POINTER(GpConfigC),
                                             C.POINTER(_vp)]),
     "l1g_batch_create": (C.c_int, [_vp, C.c_int, _vp, _vp, C.POINTER(GpConfigC), C.POINTER(_vp)]),

@@ -177,15 +177,33 @@ struct l1g_solver {
   l1g_op* op = nullptr;  // this shard's columns of K (all of K when unsharded)
   cudaStream_t stream = nullptr;
   bool own_stream = true;
-  // vectors span all p columns of the problem; the shard holds K[:, col0 : col0 + op->p]
+  // p / p_pad: all columns of the problem; the shard holds K[:, col0 : col0 + op->p]
   int64_t p = 0, p_pad = 0, col0 = 0;
-  // column sharding: an NCCL communicator (one shard per process)
-  // or in-process shards on one device run in lockstep by the leader (group[0] == this)
+  // column sharding: an NCCL communicator (one shard per process) or
+  // in-process shards on one device run in lockstep by the leader (group[0] == this).  A
+  // shard owns its slice of x and g (vb: op->p columns); the adjoint finish writes the new
+  // slices and its subtree values of the secant dots into `pack`, whose allgather gives every
+  // rank the full x, g (vbp: the projection's view) and the ranks' scalars (scal_all).
   int nranks = 1;
   l1g_comm* comm = nullptr;
   std::vector<l1g_solver*> group;
-  double *kd_send = nullptr, *kd_recv = nullptr, *g_send = nullptr, *g_recv = nullptr;
-  bool split() const { return comm != nullptr || group.size() > 1; }
+  double *kd_send = nullptr, *kd_recv = nullptr;
+  double *pack = nullptr, *x_full = nullptr, *g_full = nullptr, *scal_all = nullptr;
+  double* d_full = nullptr;
+  uint32_t* dmask_full = nullptr;
+  VecBufs vbp{};
+  // host transport: pinned staging buffers and the host-node arguments of the two exchanges
+  struct HostXchg {
+    Comm* comm;
+    const double* send;
+    double* recv;
+    int64_t count;
+    int rc;
+  };
+  double *h_send = nullptr, *h_recv = nullptr;
+  HostXchg hx[2]{};
+  // sharded layout (an NCCL / host communicator or an in-process group, even of one shard)
+  bool split() const { return d_full != nullptr; }
   Workspace ws;
   VecBufs vb{};
   double* y = nullptr;
@@ -246,8 +264,12 @@ void solver_free(l1g_solver* s) {
   s->group.clear();
   dfree(s->kd_send);
   dfree(s->kd_recv);
-  dfree(s->g_send);
-  dfree(s->g_recv);
+  if (s->h_send) cudaFreeHost(s->h_send);
+  if (s->h_recv) cudaFreeHost(s->h_recv);
+  dfree(s->pack);
+  dfree(s->x_full);
+  dfree(s->g_full);
+  dfree(s->scal_all);
   for (auto& g : s->gexec)
     if (g) cudaGraphExecDestroy(g);
   if (s->gloop) cudaGraphExecDestroy(s->gloop);
@@ -258,9 +280,14 @@ void solver_free(l1g_solver* s) {
     dfree(s->vb.g[i]);
     dfree(s->vb.r[i]);
   }
-  dfree(s->vb.d);
+  if (s->d_full) {
+    dfree(s->d_full);
+    dfree(s->dmask_full);
+  } else {
+    dfree(s->vb.d);
+    dfree(s->vb.dmask);
+  }
   dfree(s->vb.kd);
-  dfree(s->vb.dmask);
   dfree(s->y);
   dfree(s->st);
   dfree(s->pscr);
@@ -294,15 +321,34 @@ l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho, int nra
     } else {
       L1G_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     }
-    alloc_ws(s->ws, pl, s->p_pad);
-    for (int i = 0; i < 2; ++i) {
-      s->vb.x[i] = dalloc<double>(s->p_pad);
-      s->vb.g[i] = dalloc<double>(s->p_pad);
+    alloc_ws(s->ws, pl);
+    for (int i = 0; i < 2; ++i) {  // this shard's columns (all of them when unsharded)
+      s->vb.x[i] = dalloc<double>(pl.p_pad);
+      s->vb.g[i] = dalloc<double>(pl.p_pad);
       s->vb.r[i] = dalloc<double>(pl.n_pad);
     }
-    s->vb.d = dalloc<double>(s->p_pad);
     s->vb.kd = dalloc<double>(pl.n_pad);
-    s->vb.dmask = dalloc<uint32_t>((size_t)s->p_pad / 32 + 2);
+    if (nranks > 1 || sharded) {
+      if (col0 % 64) throw InvalidArgument("sharded solver: shard offsets must be multiples of 64");
+      // d and its support bitmap over all columns (the projection writes them); the shard's
+      // slices feed its forward product and its x update
+      s->d_full = dalloc<double>(s->p_pad);
+      s->dmask_full = dalloc<uint32_t>((size_t)s->p_pad / 32 + 2);
+      s->vb.d = s->d_full + col0;
+      s->vb.dmask = s->dmask_full + col0 / 32;
+      s->x_full = dalloc<double>(s->p_pad);
+      s->g_full = dalloc<double>(s->p_pad);
+      s->pack = dalloc<double>((size_t)2 * pl.p_pad + SHARD_SCAL);
+      s->scal_all = dalloc<double>((size_t)nranks * SHARD_SCAL);
+      s->vbp = s->vb;
+      s->vbp.x[0] = s->vbp.x[1] = s->x_full;
+      s->vbp.g[0] = s->vbp.g[1] = s->g_full;
+      s->vbp.d = s->d_full;
+      s->vbp.dmask = s->dmask_full;
+    } else {
+      s->vb.d = dalloc<double>(pl.p_pad);
+      s->vb.dmask = dalloc<uint32_t>((size_t)pl.p_pad / 32 + 2);
+    }
     {
       const char* e = getenv("L1G_FWD");
       s->fwd_sparse = !(e && std::strcmp(e, "dense") == 0);
@@ -315,8 +361,6 @@ l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho, int nra
     if (nranks > 1 || sharded) {
       s->kd_send = dalloc<double>(pl.n_pad);
       s->kd_recv = dalloc<double>((size_t)pl.n_pad * nranks);
-      s->g_send = dalloc<double>(pl.p_pad);
-      s->g_recv = dalloc<double>((size_t)pl.p_pad * nranks);
     }
     s->scal = dalloc<double>(16);
     L1G_CUDA(cudaHostAlloc(&s->status_host, 256, cudaHostAllocDefault));
@@ -341,27 +385,77 @@ std::vector<l1g_solver*> members(l1g_solver* s) {
   return s->group;
 }
 
-// allgather of the shard vectors `which` (0: K d tree values, n_pad each; 1: K^T r tree
-// values, the shard's p each) into every member's receive buffer
+// the two allgathers of a sharded iteration: which = 0, the shards' tree values of K d (n_pad
+// each) into kd_recv; which = 1, the shards' packets [x | g | scalars] into the full x, g and
+// the ranks' scalars of every member
+void host_exchange_node(void* arg) {  // a host node of the iteration graph
+  auto* x = static_cast<l1g_solver::HostXchg*>(arg);
+  x->rc = x->comm->host_fn(x->send, x->recv, x->count, x->comm->host_user);
+  if (x->rc != 0) std::fprintf(stderr, "l1g: host allgather failed (%d)\n", x->rc);
+}
+
 void exchange(l1g_solver* s, int which) {
   const GemvPlan& pl = s->op->plan;
-  const size_t cnt = which == 0 ? (size_t)pl.n_pad : (size_t)pl.p_pad;
+  const size_t pr = (size_t)pl.p_pad;
+  if (s->comm && s->comm->impl->host()) {
+    // pinned staging: device -> host, the caller's allgather as a host node, host -> device
+    Comm* c = s->comm->impl;
+    const int R = c->nranks;
+    const size_t cnt = which == 0 ? (size_t)pl.n_pad : 2 * pr + SHARD_SCAL;
+    if (!s->h_send) {
+      const size_t mx = std::max((size_t)pl.n_pad, 2 * pr + SHARD_SCAL);
+      L1G_CUDA(cudaHostAlloc(&s->h_send, mx * sizeof(double), cudaHostAllocDefault));
+      L1G_CUDA(cudaHostAlloc(&s->h_recv, mx * R * sizeof(double), cudaHostAllocDefault));
+    }
+    l1g_solver::HostXchg& hx = s->hx[which];
+    hx = {c, s->h_send, s->h_recv, (int64_t)cnt, 0};
+    L1G_CUDA(cudaMemcpyAsync(s->h_send, which == 0 ? s->kd_send : s->pack, cnt * sizeof(double),
+                             cudaMemcpyDeviceToHost, s->stream));
+    L1G_CUDA(cudaLaunchHostFunc(s->stream, host_exchange_node, &hx));
+    if (which == 0) {
+      L1G_CUDA(cudaMemcpyAsync(s->kd_recv, s->h_recv, cnt * R * sizeof(double),
+                               cudaMemcpyHostToDevice, s->stream));
+      return;
+    }
+    // [R][x | g | scalars] -> x_full, g_full, scal_all
+    L1G_CUDA(cudaMemcpy2DAsync(s->x_full, pr * 8, s->h_recv, cnt * 8, pr * 8, R,
+                               cudaMemcpyHostToDevice, s->stream));
+    L1G_CUDA(cudaMemcpy2DAsync(s->g_full, pr * 8, s->h_recv + pr, cnt * 8, pr * 8, R,
+                               cudaMemcpyHostToDevice, s->stream));
+    L1G_CUDA(cudaMemcpy2DAsync(s->scal_all, SHARD_SCAL * 8, s->h_recv + 2 * pr, cnt * 8,
+                               SHARD_SCAL * 8, R, cudaMemcpyHostToDevice, s->stream));
+    return;
+  }
   if (s->comm) {
-    comm_allgather(s->comm->impl, which == 0 ? s->kd_send : s->g_send,
-                   which == 0 ? s->kd_recv : s->g_recv, cnt, s->stream);
+    if (which == 0) {
+      comm_allgather(s->comm->impl, s->kd_send, s->kd_recv, (size_t)pl.n_pad, s->stream);
+      return;
+    }
+    const double* send[3] = {s->pack, s->pack + pr, s->pack + 2 * pr};
+    double* recv[3] = {s->x_full, s->g_full, s->scal_all};
+    const size_t cnt[3] = {pr, pr, (size_t)SHARD_SCAL};
+    comm_allgather_group(s->comm->impl, 3, send, recv, cnt, s->stream);
     return;
   }
   const auto m = members(s);
+  auto cp = [&](double* dst, const double* src, size_t n) {
+    L1G_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+  };
   for (l1g_solver* dst : m)
-    for (size_t r = 0; r < m.size(); ++r)
-      L1G_CUDA(cudaMemcpyAsync((which == 0 ? dst->kd_recv : dst->g_recv) + r * cnt,
-                               which == 0 ? m[r]->kd_send : m[r]->g_send, cnt * sizeof(double),
-                               cudaMemcpyDeviceToDevice, s->stream));
+    for (size_t r = 0; r < m.size(); ++r) {
+      if (which == 0) {
+        cp(dst->kd_recv + r * pl.n_pad, m[r]->kd_send, (size_t)pl.n_pad);
+      } else {
+        cp(dst->x_full + r * pr, m[r]->pack, pr);
+        cp(dst->g_full + r * pr, m[r]->pack + pr, pr);
+        cp(dst->scal_all + r * SHARD_SCAL, m[r]->pack + 2 * pr, SHARD_SCAL);
+      }
+    }
 }
 
 // kernels (and exchanges) one iteration or gp_init enqueues, for launch accounting
 int64_t kernels_per_iteration(l1g_solver* s) {
-  return s->split() ? 7 * (int64_t)members(s).size() + (s->comm ? 2 : 0) : 5;
+  return s->split() ? 6 * (int64_t)members(s).size() + (s->comm ? 2 : 0) : 5;
 }
 
 // gpss.cpp:117-134
@@ -369,13 +463,20 @@ void solver_init(l1g_solver* s, const double* x0_host) {
   set_device(s->op->c);
   s->t0 = std::chrono::steady_clock::now();
   const auto m = members(s);
+  const bool sp = s->split();
   for (l1g_solver* q : m) {
-    L1G_CUDA(cudaMemsetAsync(q->vb.x[0], 0, q->p_pad * sizeof(double), s->stream));
+    const int64_t pq = q->op->plan.p, pq_pad = q->op->plan.p_pad;
+    L1G_CUDA(cudaMemsetAsync(q->vb.x[0], 0, pq_pad * sizeof(double), s->stream));
     if (x0_host) {
-      L1G_CUDA(cudaMemcpyAsync(q->vb.x[0], x0_host, q->p * sizeof(double), cudaMemcpyHostToDevice,
+      // L1Ball::contains(x0, 1e-12), prox.cpp:15-17, on the whole x0 (zero start is feasible)
+      double* full = sp ? q->x_full : q->vb.x[0];
+      L1G_CUDA(cudaMemsetAsync(full, 0, q->p_pad * sizeof(double), s->stream));
+      L1G_CUDA(cudaMemcpyAsync(full, x0_host, q->p * sizeof(double), cudaMemcpyHostToDevice,
                                s->stream));
-      // L1Ball::contains(x0, 1e-12), prox.cpp:15-17 (zero start is always feasible)
-      reduce(q->vb.x[0], nullptr, q->p_pad, RED_ABS, q->scal, 0, s->stream);
+      reduce(full, nullptr, q->p_pad, RED_ABS, q->scal, 0, s->stream);
+      if (sp)
+        L1G_CUDA(cudaMemcpyAsync(q->vb.x[0], full + q->col0, pq * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, s->stream));
       double l1 = 0.0;
       L1G_CUDA(cudaMemcpyAsync(&l1, q->scal, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
       L1G_CUDA(cudaStreamSynchronize(s->stream));
@@ -386,31 +487,27 @@ void solver_init(l1g_solver* s, const double* x0_host) {
     L1G_CUDA(cudaMemcpyAsync(q->st, &h, sizeof(h), cudaMemcpyHostToDevice, s->stream));
     state_start(q->st, s->stream);
   }
-  if (!s->split()) {
-    if (x0_host)
-      launch_fwd(*s->op, s->ws, FWD_INIT, s->vb.x[0], nullptr, &s->vb, s->st, s->stream);
-    else
-      launch_fwd_init_zero(*s->op, s->ws, &s->vb, s->st, s->stream);
-    launch_adj(*s->op, s->ws, ADJ_INIT, nullptr, nullptr, &s->vb, s->st, s->stream);
+  // r = K x0 - y, f (x0 = 0: the forward pass over K is skipped, launch_fwd_init_zero)
+  if (!x0_host) {
+    for (l1g_solver* q : m) launch_fwd_init_zero(*q->op, q->ws, &q->vb, q->st, s->stream);
+  } else if (!sp) {
+    launch_fwd(*s->op, s->ws, FWD_INIT, s->vb.x[0], nullptr, &s->vb, s->st, s->stream);
   } else {
     for (l1g_solver* q : m)
-      launch_fwd_part(*q->op, q->ws, q->vb.x[0] + q->col0, nullptr, false, q->kd_send, q->st,
-                      s->stream);
+      launch_fwd_part(*q->op, q->ws, q->vb.x[0], nullptr, false, q->kd_send, q->st, s->stream);
     exchange(s, 0);
     for (l1g_solver* q : m)
       launch_fwd_combine(*q->op, q->ws, FWD_INIT, q->kd_recv, q->nranks, &q->vb, q->st, s->stream);
-    for (l1g_solver* q : m)
-      launch_adj_part(*q->op, q->ws, ADJ_INIT, &q->vb, q->g_send, q->st, s->stream);
-    exchange(s, 1);
-    for (l1g_solver* q : m)
-      launch_adj_combine(*q->op, q->ws, ADJ_INIT, q->g_recv, q->p_pad, &q->vb, q->st, s->stream);
   }
+  // g = 2 K^T r over each shard's columns; shards then gather the full x0, g for alpha0
   for (l1g_solver* q : m)
-    launch_proj(q->pp, PROJ_ALPHA0, q->p, q->p_pad, q->vb.x[0], q->vb.g[0], nullptr, q->pscr,
-                q->st, &q->vb, s->stream);
-  // (x0 = 0 unsharded: the forward pass over K is skipped, launch_fwd_init_zero)
-  s->launches += (x0_host ? 7 : (s->split() ? 6 : 5)) * (int64_t)m.size() +
-                 (s->split() ? 2 * (int64_t)m.size() : 0);
+    launch_adj(*q->op, q->ws, ADJ_INIT, nullptr, nullptr, &q->vb, q->st, s->stream, q->pack);
+  if (sp) exchange(s, 1);
+  for (l1g_solver* q : m)
+    launch_proj(q->pp, PROJ_ALPHA0, q->p, q->p_pad, sp ? q->x_full : q->vb.x[0],
+                sp ? q->g_full : q->vb.g[0], nullptr, q->pscr, q->st, &q->vb, s->stream);
+  const int64_t fwd = x0_host ? (sp ? 3 : 2) : 1;
+  s->launches += (fwd + 3) * (int64_t)m.size() + (sp && s->comm ? (x0_host ? 2 : 1) : 0);
   s->inited = true;
 }
 
@@ -422,7 +519,8 @@ void enqueue_iteration(l1g_solver* s, Mark mark) {
   mark(0);
   for (l1g_solver* q : m)
     launch_proj(q->pp, PROJ_ITER, q->p, q->p_pad, nullptr, nullptr, nullptr, q->pscr, q->st,
-                &q->vb, s->stream);
+                q->d_full ? &q->vbp : &q->vb, s->stream, 1, 0,
+                q->d_full ? q->scal_all : nullptr, q->nranks);
   mark(1);
   if (!s->split()) {
     launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream, s->fwd_sparse);
@@ -432,17 +530,15 @@ void enqueue_iteration(l1g_solver* s, Mark mark) {
     return;
   }
   for (l1g_solver* q : m)
-    launch_fwd_part(*q->op, q->ws, q->vb.d + q->col0, q->vb.dmask + q->col0 / 32, q->fwd_sparse,
-                    q->kd_send, q->st, s->stream);
+    launch_fwd_part(*q->op, q->ws, q->vb.d, q->vb.dmask, q->fwd_sparse, q->kd_send, q->st,
+                    s->stream);
   exchange(s, 0);
   for (l1g_solver* q : m)
     launch_fwd_combine(*q->op, q->ws, FWD_ITER, q->kd_recv, q->nranks, &q->vb, q->st, s->stream);
   mark(2);
-  for (l1g_solver* q : m)
-    launch_adj_part(*q->op, q->ws, ADJ_ITER, &q->vb, q->g_send, q->st, s->stream);
+  for (l1g_solver* q : m)  // the shard's own x, g update and dots, written into its packet
+    launch_adj(*q->op, q->ws, ADJ_ITER, nullptr, nullptr, &q->vb, q->st, s->stream, q->pack);
   exchange(s, 1);
-  for (l1g_solver* q : m)
-    launch_adj_combine(*q->op, q->ws, ADJ_ITER, q->g_recv, q->p_pad, &q->vb, q->st, s->stream);
   mark(3);
 }
 void enqueue_iteration(l1g_solver* s) {
@@ -683,6 +779,7 @@ void solver_run(l1g_solver* s, const l1g_stop_rule& stop, l1g_result* res,
 void finalize(l1g_solver* s, l1g_result* res, l1g_iter_record* trace_host, int64_t cap) {
   DevState h;
   read_state(s, &h);
+  if (s->hx[0].rc || s->hx[1].rc) throw RuntimeFailure("sharded solver: host allgather failed");
   if (h.status == RUNNING) throw RuntimeFailure("gpss_solve: run did not reach a stop rule");
   std::memset(res, 0, sizeof(*res));
   res->iterations = h.k;
@@ -1832,6 +1929,21 @@ void l1g_comm_destroy(l1g_comm* c) {
   delete c;
 }
 
+int l1g_comm_create_host(l1g_ctx* ctx, int rank, int nranks, l1g_allgather_fn fn, void* user,
+                         l1g_comm** out) {
+  return guarded([&] {
+    *out = nullptr;
+    auto* c = new l1g_comm();
+    try {
+      c->impl = comm_create_host(ctx->device, rank, nranks, fn, user);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
 int l1g_solver_create_sharded(l1g_op* op, l1g_comm* comm, const double* y, double rho,
                               const l1g_gp_config* cfg, l1g_solver** out) {
   return guarded([&] {
@@ -1892,9 +2004,10 @@ int l1g_solver_get(l1g_solver* s, double* x, double* r, double* g, double* f, in
     DevState h;
     read_state(s, &h);
     const GemvPlan& pl = s->op->plan;
-    download(x, s->vb.x[h.cur], s->p, s->stream);
+    // sharded: the full x, g every rank gathered at the end of the last step (or gp_init)
+    download(x, s->x_full ? s->x_full : s->vb.x[h.cur], s->p, s->stream);
     download(r, s->vb.r[h.cur], pl.n, s->stream);
-    download(g, s->vb.g[h.cur], s->p, s->stream);
+    download(g, s->g_full ? s->g_full : s->vb.g[h.cur], s->p, s->stream);
     L1G_CUDA(cudaStreamSynchronize(s->stream));
     if (f) *f = h.f;
     if (k) *k = h.k;
@@ -2016,7 +2129,7 @@ int l1g_solver_x_dev(l1g_solver* s, const double** x_dev) {
   return guarded([&] {
     DevState h;
     read_state(s, &h);
-    *x_dev = s->vb.x[h.cur];
+    *x_dev = s->x_full ? s->x_full : s->vb.x[h.cur];
   });
 }
 

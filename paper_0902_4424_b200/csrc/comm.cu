@@ -27,6 +27,8 @@ struct NcclApi {
   ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                              cudaStream_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
 };
 
 NcclApi& api() {
@@ -47,7 +49,10 @@ NcclApi& api() {
     a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
     a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
     a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
-    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.all_gather;
+    a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.all_gather &&
+           a.group_start && a.group_end;
     if (!a.ok) a.err = "NCCL runtime lacks the expected entry points";
   });
   if (!a.ok) throw RuntimeFailure(a.err);
@@ -89,6 +94,18 @@ Comm* comm_create(int device, int rank, int nranks, const void* id_bytes) {
   return c;
 }
 
+Comm* comm_create_host(int device, int rank, int nranks, HostAllgatherFn fn, void* user) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidArgument("comm: bad rank / size");
+  if (!fn) throw InvalidArgument("comm: host transport needs an allgather function");
+  auto* c = new Comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->device = device;
+  c->host_fn = fn;
+  c->host_user = user;
+  return c;
+}
+
 void comm_destroy(Comm* c) {
   if (!c) return;
   if (c->handle) api().comm_destroy(static_cast<ncclComm_t>(c->handle));
@@ -98,6 +115,22 @@ void comm_destroy(Comm* c) {
 void comm_allgather(Comm* c, const double* send, double* recv, size_t count, cudaStream_t s) {
   check(api().all_gather(send, recv, count, ncclFloat64, static_cast<ncclComm_t>(c->handle), s),
         "ncclAllGather");
+}
+
+// several allgathers as one NCCL group (one launch; the pieces of a shard's packet)
+void comm_allgather_group(Comm* c, int n, const double* const* send, double* const* recv,
+                          const size_t* count, cudaStream_t s) {
+  NcclApi& a = api();
+  check(a.group_start(), "ncclGroupStart");
+  for (int i = 0; i < n; ++i) {
+    const ncclResult_t r = a.all_gather(send[i], recv[i], count[i], ncclFloat64,
+                                        static_cast<ncclComm_t>(c->handle), s);
+    if (r != ncclSuccess) {
+      a.group_end();
+      check(r, "ncclAllGather");
+    }
+  }
+  check(a.group_end(), "ncclGroupEnd");
 }
 
 }  // namespace l1g

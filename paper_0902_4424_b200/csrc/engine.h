@@ -173,21 +173,22 @@ void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, 
 void launch_fwd_init_zero(const Op& op, const Workspace& ws, const VecBufs* vb, DevState* st,
                           cudaStream_t s);
 void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
-                DevState* st, cudaStream_t s);
-// column-sharded runs: the shard's tree values (n_pad / p_pad of the shard) and the
-// combination of the gathered rank values with the fused epilogue of `mode`
+                DevState* st, cudaStream_t s, double* pack = nullptr);
+// scalars per rank in a shard's allgather packet: s'z, s's, z'z subtree values, clock
+constexpr int SHARD_SCAL = 8;
+// column-sharded runs: the shard's tree values of K d (n_pad) and the combination of the
+// gathered rank values with the fused epilogue of `mode`
 void launch_fwd_part(const Op& op, const Workspace& ws, const double* vin, const uint32_t* dmask,
                      bool sparse, double* out, DevState* st, cudaStream_t s);
 void launch_fwd_combine(const Op& op, const Workspace& ws, int mode, const double* recv, int nr,
                         const VecBufs* vb, DevState* st, cudaStream_t s);
-void launch_adj_part(const Op& op, const Workspace& ws, int mode, const VecBufs* vb, double* out,
-                     DevState* st, cudaStream_t s);
-void launch_adj_combine(const Op& op, const Workspace& ws, int mode, const double* recv,
-                        int64_t p_pad_total, const VecBufs* vb, DevState* st, cudaStream_t s);
 ProjPlan make_proj_plan(int64_t p_pad);
+// rank_scal (sharded runs): the ranks' packet scalars [nranks][SHARD_SCAL]; the projection
+// joins the secant dots over the ranks and takes the budget clock from them
 void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const double* xin,
                  const double* gin, double* out, double* scratch, DevState* st,
-                 const VecBufs* vb, cudaStream_t s, int nprob = 1, int64_t scr_stride = 0);
+                 const VecBufs* vb, cudaStream_t s, int nprob = 1, int64_t scr_stride = 0,
+                 const double* rank_scal = nullptr, int nranks = 1);
 ProjPlan make_proj_plan_single(int64_t p_pad, int cs = 1);
 size_t proj_scratch_doubles(int64_t p_pad);
 

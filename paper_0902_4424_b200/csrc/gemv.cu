@@ -74,6 +74,10 @@ struct AdjArgs {
   VecBufs vb;
   BatchStrides bs;
   int wpg;  // finish kernel: warps per output group (fin_wpg)
+  // column shard of a sharded solver (abi.cu): the finish also writes the
+  // shard's new x and g and its subtree values of s'z, s's, z'z plus its clock into the
+  // allgather packet [x (p_pad) | g (p_pad) | SHARD_SCAL scalars]
+  double* pack;
 };
 
 template <int N, class F>
@@ -405,6 +409,8 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
           gb[b] = __ldcg(reinterpret_cast<const double2*>(a0.vb.g[b] + ofp + col));
         }
         dd = __ldcg(reinterpret_cast<const double2*>(a0.vb.d + ofp + col));
+      } else if (a.pack) {  // ADJ_INIT of a shard: x0 travels with g
+        xb[0] = __ldcg(reinterpret_cast<const double2*>(a0.vb.x[cur] + col));
       }
     }
   }
@@ -428,6 +434,15 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
       const double g0 = mul(2.0, s0), g1 = mul(2.0, s1);  // 2 K^T r (gpss.cpp:130, :211)
       if (a.mode == ADJ_INIT) {
         *reinterpret_cast<double2*>(a0.vb.g[cur] + ofp + col) = make_double2(g0, g1);
+        if (a.pack) {
+          *reinterpret_cast<double2*>(a.pack + col) = xb[0];
+          *reinterpret_cast<double2*>(a.pack + a.p_pad + col) = make_double2(g0, g1);
+          if (blockIdx.x == 0 && wi == 0 && gl == 0 && lane == 0) {
+            double* sc = a.pack + 2 * a.p_pad;
+            sc[0] = sc[1] = sc[2] = 0.0;
+            sc[3] = elapsed_s(st);
+          }
+        }
       } else {
         // x' = x + lambda d (gpss.cpp:208), s = x' - x, z = g' - g (gpss.cpp:150-151)
         const double2 xo = cur ? xb[1] : xb[0];
@@ -435,6 +450,10 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
         const double x0n = add(xo.x, mul(lam, dd.x)), x1n = add(xo.y, mul(lam, dd.y));
         *reinterpret_cast<double2*>(a0.vb.x[cur ^ 1] + ofp + col) = make_double2(x0n, x1n);
         *reinterpret_cast<double2*>(a0.vb.g[cur ^ 1] + ofp + col) = make_double2(g0, g1);
+        if (a.pack) {
+          *reinterpret_cast<double2*>(a.pack + col) = make_double2(x0n, x1n);
+          *reinterpret_cast<double2*>(a.pack + a.p_pad + col) = make_double2(g0, g1);
+        }
         const double sa = sub(x0n, xo.x), sb = sub(x1n, xo.y);
         const double za = sub(g0, go.x), zb = sub(g1, go.y);
         const double dsz = warp_tree(add(mul(sa, za), mul(sb, zb)));
@@ -470,6 +489,13 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
   state_store(&s, lane, sw);
   if (lane != 0) return;
   *a.cnt_all = 0;
+  if (a.pack) {  // the shard's subtree values; the projection joins them over the ranks
+    double* sc = a.pack + 2 * a.p_pad;
+    sc[0] = SZ;
+    sc[1] = SS;
+    sc[2] = ZZ;
+    sc[3] = elapsed_s(&s);
+  }
   adj_tail(st, s, SZ, SS, ZZ);
   L1G_TL_STAMP(blockIdx.y == 0, g_tl_gemv, 11, s.k)
 }
@@ -1131,8 +1157,9 @@ void launch_fwd_init_zero(const Op& op, const Workspace& ws, const VecBufs* vb, 
 }
 
 void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
-                const VecBufs* vb, DevState* st, cudaStream_t s) {
-  const AdjArgs a = adj_args(op, ws, mode, vin, vout, vb, st);
+                const VecBufs* vb, DevState* st, cudaStream_t s, double* pack) {
+  AdjArgs a = adj_args(op, ws, mode, vin, vout, vb, st);
+  a.pack = pack;
   adj_main(op, a, s);
   fin_launch(a, s);
 }
@@ -1152,24 +1179,6 @@ void launch_fwd_combine(const Op& op, const Workspace& ws, int mode, const doubl
   a.part = const_cast<double*>(recv);
   a.ncr = nr;
   a.task_ctr = ws.counters + op.plan.nrg + op.plan.ncg + 2;
-  fin_launch(a, s);
-}
-
-void launch_adj_part(const Op& op, const Workspace& ws, int mode, const VecBufs* vb, double* out,
-                     DevState* st, cudaStream_t s) {
-  AdjArgs a = adj_args(op, ws, mode, nullptr, out, vb, st);
-  adj_main(op, a, s);
-  a.mode = ADJ_APPLY;
-  fin_launch(a, s);
-}
-
-void launch_adj_combine(const Op& op, const Workspace& ws, int mode, const double* recv,
-                        int64_t p_pad_total, const VecBufs* vb, DevState* st, cudaStream_t s) {
-  AdjArgs a = adj_args(op, ws, mode, nullptr, nullptr, vb, st);
-  a.part = const_cast<double*>(recv);
-  a.nrr = 1;
-  a.p_pad = p_pad_total;
-  a.bs.pstride = p_pad_total;
   fin_launch(a, s);
 }
 

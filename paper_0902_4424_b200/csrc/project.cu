@@ -62,6 +62,10 @@ struct ProjArgs {
   VecBufs vb;
   // batched runs: cluster k projects problem k (vectors bstride apart, states consecutive)
   int64_t bstride, scr_stride;
+  // sharded runs: per-rank packet scalars [nranks][SHARD_SCAL] (s'z, s's, z'z subtree values
+  // of the rank's columns, its clock)
+  const double* rank_scal;
+  int nranks;
 };
 
 struct ProjShared {
@@ -270,10 +274,33 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   if (a.mode == PROJ_ITER) {
     if (rank == 0 && tid == 0) {
       int dec = 0;
+      double el = 0.0;
+      if (a.nranks > 1) {
+        // column shards: the secant dots are the canonical tree over the ranks' subtree
+        // values (shard widths are equal powers of two, so the ranks' subtrees are the
+        // canonical column tree's), and every rank takes the budget decision on the same
+        // clock -- the latest any rank reported -- so all ranks stop on the same iteration
+        double t3[3][16];
+        for (int r = 0; r < a.nranks; ++r) {
+          for (int c = 0; c < 3; ++c) t3[c][r] = a.rank_scal[r * SHARD_SCAL + c];
+          el = fmax(el, a.rank_scal[r * SHARD_SCAL + 3]);
+        }
+        for (int h = 1; h < a.nranks; h <<= 1)
+          for (int i = 0; i + h < a.nranks; i += 2 * h)
+            for (int c = 0; c < 3; ++c) t3[c][i] = add(t3[c][i], t3[c][i + h]);
+        sst.sz = t3[0][0];
+        sst.ss = t3[1][0];
+        sst.zz = t3[2][0];
+        st->sz = sst.sz;
+        st->ss = sst.ss;
+        st->zz = sst.zz;
+      } else {
+        el = sst.max_seconds > 0.0 ? elapsed_s(&sst) : 0.0;
+      }
       if (!sst.single_step) {
         if (sst.max_iterations > 0 && sst.k >= sst.max_iterations) dec = 1 + L1G_MAX_ITERATIONS;
         else if (sst.max_matvecs > 0 && sst.matvecs >= sst.max_matvecs) dec = 1 + L1G_MAX_MATVECS;
-        else if (sst.max_seconds > 0.0 && elapsed_s(&sst) >= sst.max_seconds) dec = 1 + L1G_MAX_SECONDS;
+        else if (sst.max_seconds > 0.0 && el >= sst.max_seconds) dec = 1 + L1G_MAX_SECONDS;
       } else if (sst.stationary) {
         dec = 1 + L1G_STATIONARY;
       }
@@ -922,8 +949,12 @@ static void proj_dispatch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s,
 
 void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const double* xin,
                  const double* gin, double* out, double* scratch, DevState* st,
-                 const VecBufs* vb, cudaStream_t s, int nprob, int64_t scr_stride) {
+                 const VecBufs* vb, cudaStream_t s, int nprob, int64_t scr_stride,
+                 const double* rank_scal, int nranks) {
+  if (nranks > 16) throw InvalidArgument("sharded solver: at most 16 ranks");
   ProjArgs a{};
+  a.rank_scal = rank_scal;
+  a.nranks = rank_scal ? nranks : 1;
   a.mode = mode;
   a.p = p;
   a.p_pad = p_pad;

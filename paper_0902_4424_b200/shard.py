@@ -1,11 +1,14 @@
 """Column sharding of the GPSS iteration.
 
-Rank r of R owns columns [r*p/R, (r+1)*p/R) of K; x, g, d and every scalar are replicated.
-Per iteration the ranks exchange two vectors (allgather, NCCL inside the iteration graph):
+Rank r of R owns columns [r*p/R, (r+1)*p/R) of K and that slice of x and g.  Per iteration
+the ranks exchange two packets (allgather, NCCL inside the iteration graph):
 
   * the shard's tree values of K d (n per rank), joined by a pairwise tree over the ranks
     (fwd_finish_kernel with the rank values as its partials);
-  * the shard's tree values of K^T r (p/R per rank), which concatenate to the full gradient.
+  * after the adjoint: the shard's new x and g slices plus its subtree values of s'z, s's,
+    z'z and its clock (2 p/R + 8 per rank).  Every rank projects the gathered x - alpha g
+    (the threshold, the escalation loop and the feasibility bumps need all of v), joining
+    the secant dots over the ranks in the canonical tree order.
 
 With p/R a power of two the shard trees are subtrees of the canonical column tree, so the
 sharded run is bit-identical to the single-GPU run (tests/test_gpu_shard.py on one GPU with
@@ -112,6 +115,51 @@ class Comm:
             self.h = C.c_void_p()
 
 
+class HostComm:
+    """Sharded-solver communicator over the caller's own host allgather (no NCCL): the
+    engine stages every exchange through pinned host memory and calls `allgather` from a host
+    node of its iteration graphs.  With a torch.distributed group (e.g. gloo) this runs the
+    product's multi-rank path in processes that share one GPU (tests/test_gpu_shard_mp.py)."""
+
+    def __init__(self, ctx, rank: int, nranks: int, pg=None, allgather=None):
+        self.rank, self.nranks = rank, nranks
+        self.errors = []
+        if allgather is None:
+            allgather = torch_allgather(pg, nranks)
+
+        def _fn(send_p, recv_p, count, user):
+            try:
+                send = np.ctypeslib.as_array(send_p, shape=(count,))
+                recv = np.ctypeslib.as_array(recv_p, shape=(nranks * count,))
+                allgather(send, recv)
+                return 0
+            except BaseException as e:  # reported by the solver as a runtime failure
+                self.errors.append(e)
+                return 1
+
+        self._fn = L.ALLGATHER_FN(_fn)  # kept alive as long as the communicator
+        self.h = C.c_void_p()
+        check(L.load().l1g_comm_create_host(ctx.h, rank, nranks, self._fn, None,
+                                            C.byref(self.h)), "comm_create_host")
+
+    def close(self):
+        if self.h:
+            L.load().l1g_comm_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+def torch_allgather(pg, nranks: int):
+    """recv[r * count:(r + 1) * count] = rank r's send, over a torch.distributed group."""
+    import torch
+
+    def ag(send, recv):
+        src = torch.from_numpy(send.copy())
+        out = [torch.empty_like(src) for _ in range(nranks)]
+        pg.all_gather(out, src)
+        recv[:] = torch.cat(out).numpy()
+    return ag
+
+
 def create_group_solver(ops, y, rho, cfg):
     """In-process shards on one device (ops[r] = columns of shard r), run in lockstep."""
     arr = (C.c_void_p * len(ops))(*[o.h for o in ops])
@@ -122,8 +170,8 @@ def create_group_solver(ops, y, rho, cfg):
     return h
 
 
-def create_sharded_solver(op, comm: Comm, y, rho, cfg):
-    """This process's shard of an NCCL-sharded solve."""
+def create_sharded_solver(op, comm, y, rho, cfg):
+    """This process's shard of a sharded solve (comm: Comm over NCCL, or HostComm)."""
     h = C.c_void_p()
     yy = np.ascontiguousarray(y, dtype=np.float64)
     check(L.load().l1g_solver_create_sharded(op.h, comm.h, ptr(yy), rho, C.byref(cfg._c()),

@@ -1,9 +1,11 @@
 """Host side of the column-sharded path with world_size 2 and 4 on CPU.
 
-Each rank owns a column block, computes its shard values with the oracle's canonical trees,
-and the ranks exchange them over torch.distributed (gloo) exactly as the NCCL allgather does
-on the GPU: the K d values are joined with shard.rank_tree, the K^T r values concatenate.
-The NCCL unique-id broadcast is the same code the GPU path uses (with a stand-in id).
+Each rank owns a column block and its slices of x and g, computes its shard values with the
+oracle's canonical trees, and the ranks exchange them over torch.distributed (gloo) as the
+engine's allgathers do: the K d values are joined with shard.rank_tree; the packets [x | g |
+subtree values of s'z, s's, z'z] give the full x, g and, joined with the same rank tree, the
+full canonical dots.  The NCCL unique-id broadcast is the same code the GPU path uses (with
+a stand-in id).  (The product itself runs multi-process in tests/test_gpu_shard_mp.py.)
 """
 import os
 import socket
@@ -42,16 +44,25 @@ def _worker(rank, world, port, cases, out):
             Ks = np.ascontiguousarray(K[:, sh.cols])
             kd_part = torch.from_numpy(O.apply(Ks, np.ascontiguousarray(x[sh.cols])))
             g_part = torch.from_numpy(O.apply_adjoint(Ks, r))
+            # secant dots of this rank's slices (s = x' - x, z = g' - g), subtree values
+            sv, zv = x[sh.cols] * 0.5 - x[sh.cols], g_part.numpy() * 1.5 - g_part.numpy()
+            dots = torch.tensor([O.dot(sv, zv), O.dot(sv, sv), O.dot(zv, zv)], dtype=torch.float64)
+            dots_all = [torch.empty_like(dots) for _ in range(world)]
+            dist.all_gather(dots_all, dots)
             kd_all = [torch.empty_like(kd_part) for _ in range(world)]
             g_all = [torch.empty_like(g_part) for _ in range(world)]
             dist.all_gather(kd_all, kd_part)
             dist.all_gather(g_all, g_part)
             kd = S.rank_tree(np.stack([t.numpy() for t in kd_all]))
             g = np.concatenate([t.numpy() for t in g_all])
+            sd = S.rank_tree(np.stack([t.numpy() for t in dots_all]))
+            s_full, z_full = x * 0.5 - x, g * 1.5 - g
+            full_dots = [O.dot(s_full, z_full), O.dot(s_full, s_full), O.dot(z_full, z_full)]
             res[(n, p)] = dict(
                 kd_exact=bool(np.array_equal(kd, O.apply(K, x))),
                 kd_close=bool(np.allclose(kd, O.apply(K, x), rtol=1e-12, atol=1e-12)),
                 g_exact=bool(np.array_equal(g, O.apply_adjoint(K, r))),
+                dots_exact=bool(list(sd) == full_dots),
                 bit_exact_expected=S.bit_exact(p, world))
         uid = S.exchange_id(dist, rank, make_id=lambda: bytes(range(128)))
         res["uid"] = uid == bytes(range(128))
@@ -90,6 +101,7 @@ def test_sharded_exchange_matches_unsharded(world):
             assert r["kd_close"], (rank, n, p)
             if r["bit_exact_expected"]:
                 assert r["kd_exact"], (rank, n, p)
+                assert r["dots_exact"], (rank, n, p)
 
 
 def test_shard_plan_rules():
