@@ -11,7 +11,7 @@ if [ ! -d "$REF/src" ]; then
   exit 0
 fi
 mkdir -p "$OUT"
-SRCS="$REF/src/gpss.cpp $REF/src/prox.cpp $REF/src/linear_operator.cpp $REF/src/objective.cpp $REF/src/psd.cpp $REF/src/shrinkage.cpp $REF/src/problem_io.cpp $HERE/ref_capi.cpp"
+SRCS="$REF/src/gpss.cpp $REF/src/prox.cpp $REF/src/linear_operator.cpp $REF/src/objective.cpp $REF/src/psd.cpp $REF/src/shrinkage.cpp $REF/src/problem_io.cpp $REF/src/reference.cpp $HERE/ref_capi.cpp"
 CXX="${L1_REF_CXX:-/usr/bin/g++}"
 COMMON="-std=c++20 -fPIC -shared -ffp-contract=off -fno-fast-math -I$HERE/eigen_shim -I$REF/include"
 # OpenMP splits GEMV outputs over threads only: the canonical values do not depend on it

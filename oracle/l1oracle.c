@@ -1032,6 +1032,73 @@ int orc_shrinkage_solve(const double* K, int64_t n, int64_t p, const double* y, 
   return ORC_OK;
 }
 
+/* reference.cpp:9-13: ||x - S_lambda(x + K^T (y - K x))||_inf (2 matvecs) */
+double orc_penalized_fpr(const double* K, int64_t n, int64_t p, const double* y,
+                         const double* x, double lambda) {
+  double *kx = dalloc(n), *mis = dalloc(n), *r = dalloc(p), *v = dalloc(p), *u = dalloc(p);
+  double *tmp = dalloc(p);
+  orc_apply(K, n, p, x, kx);
+  for (int64_t i = 0; i < n; ++i) mis[i] = y[i] - kx[i];
+  orc_apply_adjoint(K, n, p, mis, r);
+  for (int64_t j = 0; j < p; ++j) v[j] = x[j] + r[j];
+  orc_soft_threshold(v, p, lambda, u);
+  const double c = linf_diff(x, u, p, tmp);
+  free(kx); free(mis); free(r); free(v); free(u); free(tmp);
+  return c;
+}
+
+/* reference.cpp:38-82: accelerated thresholding from x = 0 until the fixed-point certificate
+ * holds (checked every check_interval iterations, or when the step is already below the
+ * tolerance); lambda >= lambda_max gives the zero vector.  iters_out = iterations run. */
+int orc_reference_minimizer(const double* K, int64_t n, int64_t p, const double* y,
+                            double lambda, double oracle_tol, int64_t max_iterations,
+                            int64_t check_interval, double* x_out, double* certificate,
+                            int64_t* iters_out) {
+  if (!(lambda > 0.0)) return ORC_EINVAL;
+  double* g = dalloc(p);
+  orc_apply_adjoint(K, n, p, y, g); /* lambda_max = ||K^T y||_inf (prox.cpp lambda_max) */
+  const double lmax = orc_linf(g, p);
+  free(g);
+  memset(x_out, 0, sizeof(double) * (size_t)p);
+  *iters_out = 0;
+  if (lambda >= lmax) {
+    *certificate = orc_penalized_fpr(K, n, p, y, x_out, lambda);
+    return ORC_OK;
+  }
+  const double c = 0.999, c2 = c * c, lam_eff = lambda * c2; /* solver.hpp:128 */
+  double *x = dalloc(p), *xprev = dalloc(p), *pt = dalloc(p), *r = dalloc(p), *v = dalloc(p);
+  double *xn = dalloc(p), *tmp = dalloc(p), *kp = dalloc(n), *mis = dalloc(n);
+  double t = 1.0;
+  int rc = ORC_ERUNTIME;
+  for (int64_t k = 0; k < max_iterations; ++k) {
+    const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t)); /* fista_t_next */
+    const double coef = (t - 1.0) / t_next;
+    for (int64_t j = 0; j < p; ++j) pt[j] = x[j] + coef * (x[j] - xprev[j]);
+    orc_apply(K, n, p, pt, kp);
+    for (int64_t i = 0; i < n; ++i) mis[i] = kp[i] - y[i];
+    orc_apply_adjoint(K, n, p, mis, r);
+    for (int64_t j = 0; j < p; ++j) v[j] = pt[j] - c2 * r[j];
+    orc_soft_threshold(v, p, lam_eff, xn);
+    memcpy(xprev, x, sizeof(double) * (size_t)p);
+    memcpy(x, xn, sizeof(double) * (size_t)p);
+    t = t_next;
+    *iters_out = k + 1;
+    const double surrogate = linf_diff(x, pt, p, tmp);
+    if ((k + 1) % check_interval == 0 || surrogate <= oracle_tol) {
+      const double cert = orc_penalized_fpr(K, n, p, y, x, lambda);
+      if (cert <= oracle_tol) {
+        *certificate = cert;
+        rc = ORC_OK;
+        break;
+      }
+    }
+  }
+  if (rc != ORC_OK) *certificate = orc_penalized_fpr(K, n, p, y, x, lambda);
+  memcpy(x_out, x, sizeof(double) * (size_t)p);
+  free(x); free(xprev); free(pt); free(r); free(v); free(xn); free(tmp); free(kp); free(mis);
+  return rc;
+}
+
 /* ======================================================================== L1PROBv1 hash */
 /* problem_io.cpp:115-125: FNV-1a 64 (offset basis 1469598103934665603, prime 1099511628211) */
 uint64_t orc_fnv1a(const void* data, int64_t bytes, uint64_t h) {

@@ -153,6 +153,14 @@ int orc_gp_set(orc_gp* st, const double* x, const double* kx_minus_y, const doub
                double f, int64_t k, const double* f_history, int f_history_len,
                const orc_gp_config* cfg, double rho);
 
+/* ---- reference.cpp:9-82: penalized fixed-point residual and the reference minimizer ---- */
+double orc_penalized_fpr(const double* K, int64_t n, int64_t p, const double* y,
+                         const double* x, double lambda);
+int orc_reference_minimizer(const double* K, int64_t n, int64_t p, const double* y,
+                            double lambda, double oracle_tol, int64_t max_iterations,
+                            int64_t check_interval, double* x_out, double* certificate,
+                            int64_t* iters_out);
+
 /* ---- L1PROBv1 (problem_io.cpp): FNV-1a 64 over serialized bytes, chained from h */
 uint64_t orc_fnv1a(const void* data, int64_t bytes, uint64_t h);
 

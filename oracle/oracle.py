@@ -125,6 +125,9 @@ def lib():
             "orc_shrinkage_solve": (i32, [_dp, i64, i64, _dp, dbl, i32, C.POINTER(StopRule), _dp,
                                           C.POINTER(Result), C.c_void_p, i64]),
             "orc_fnv1a": (C.c_uint64, [C.c_void_p, i64, C.c_uint64]),
+            "orc_penalized_fpr": (dbl, [_dp, i64, i64, _dp, _dp, dbl]),
+            "orc_reference_minimizer": (i32, [_dp, i64, i64, _dp, dbl, dbl, i64, i64, _dp,
+                                              C.POINTER(dbl), C.POINTER(i64)]),
             "orc_gp_init": (i32, [_dp, i64, i64, _dp, dbl, C.POINTER(GpConfig), C.c_void_p,
                                   C.POINTER(C.c_void_p)]),
             "orc_gp_iterate": (i32, [C.c_void_p, dbl, C.POINTER(IterRecord),
@@ -323,6 +326,29 @@ def _result_dict(res):
     out["f_history"] = [res.f_history[i] for i in range(res.f_history_len)]
     out["reason_name"] = REASONS[res.reason]
     return out
+
+
+def penalized_fixed_point_residual(K, y, x, lam):
+    """reference.cpp:9-13."""
+    K = _a(K)
+    return lib().orc_penalized_fpr(K, K.shape[0], K.shape[1], _a(y), _a(x), lam)
+
+
+def reference_minimizer(K, y, lam, oracle_tol=1e-12, max_iterations=500000, check_interval=50,
+                        nnz_threshold=1e-10):
+    """reference.cpp:38-82.  Returns dict(x, lambda, rho, nnz, certificate, iterations)."""
+    K, y = _a(K), _a(y)
+    n, p = K.shape
+    x = np.zeros(p)
+    cert, its = C.c_double(), C.c_int64()
+    rc = lib().orc_reference_minimizer(K, n, p, y, lam, oracle_tol, max_iterations,
+                                       check_interval, x, C.byref(cert), C.byref(its))
+    if rc == 2:
+        raise RuntimeError(f"reference_minimizer: certificate {cert.value} did not reach "
+                           f"tolerance {oracle_tol} within {max_iterations} iterations")
+    _check(rc, "reference_minimizer")
+    return dict(x=x, **{"lambda": lam}, rho=l1norm(x), nnz=int(np.sum(np.abs(x) > nnz_threshold)),
+                certificate=cert.value, iterations=its.value, oracle_tol=oracle_tol)
 
 
 def psd_solve(K, y, rho, stop=None, trace=True):

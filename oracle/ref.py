@@ -55,6 +55,10 @@ def lib(kind="canon"):
         L.ref_problem_load.restype = C.c_int
         L.ref_problem_load.argtypes = [C.c_char_p, C.c_long, C.c_long, _dp, _dp, _dp,
                                        C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
+        L.ref_reference_minimizer.restype = C.c_int
+        L.ref_reference_minimizer.argtypes = [C.c_void_p, _dp, C.c_double, C.c_double, C.c_long,
+                                              C.c_long, _dp, C.POINTER(C.c_double),
+                                              C.POINTER(C.c_double), C.POINTER(C.c_long)]
         L.ref_problem_hash.restype = C.c_int
         L.ref_problem_hash.argtypes = [_dp, C.c_long, C.c_long, _dp, _dp, C.c_uint64,
                                        C.c_double, C.POINTER(C.c_uint64)]
@@ -79,6 +83,17 @@ class RefOperator:
         out = np.empty(self.p if adjoint else self.n)
         O._check(self.L.ref_apply(self.h, x, out, int(adjoint)), "apply")
         return out
+
+    def reference_minimizer(self, y, lam, oracle_tol=1e-12, max_iterations=500000,
+                            check_interval=50):
+        """reference.cpp:38-82 (the reference's own source). Returns (x, certificate, rho, nnz)."""
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        x = np.zeros(self.p)
+        cert, rho, nnz = C.c_double(), C.c_double(), C.c_long()
+        O._check(self.L.ref_reference_minimizer(self.h, y, lam, oracle_tol, max_iterations,
+                                                check_interval, x, C.byref(cert), C.byref(rho),
+                                                C.byref(nnz)), "reference_minimizer")
+        return x, cert.value, rho.value, nnz.value
 
     def spectral_norm(self, max_iters=1000, tol=1e-8):
         s = C.c_double()

@@ -17,6 +17,7 @@
 #include "l1solve/gpss.hpp"
 #include "l1solve/prox.hpp"
 #include "l1solve/problem_io.hpp"
+#include "l1solve/reference.hpp"
 #include "l1solve/solver.hpp"
 
 using namespace l1solve;
@@ -276,4 +277,25 @@ int ref_problem_hash(const double* K, long n, long p, const double* y, const dou
   }
 }
 
+
+int ref_reference_minimizer(ref_op* o, const double* y, double lambda, double oracle_tol,
+                            long max_iterations, long check_interval, double* x_out,
+                            double* certificate, double* rho, long* nnz) {
+  try {
+    const long n = o->op.rows(), p = o->op.cols();
+    const Objective obj(o->op, vec(y, n));
+    ReferenceOptions opt;
+    opt.oracle_tol = oracle_tol;
+    opt.max_iterations = max_iterations;
+    opt.check_interval = check_interval;
+    const ReferenceSolution r = reference_minimizer(obj, lambda, opt);
+    std::memcpy(x_out, r.x.data(), sizeof(double) * static_cast<size_t>(p));
+    *certificate = r.certificate;
+    *rho = r.rho;
+    *nnz = r.nnz;
+    return 0;
+  } catch (const std::exception& e) {
+    return code(e);
+  }
+}
 }  // extern "C"

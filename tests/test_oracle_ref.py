@@ -130,3 +130,20 @@ def test_l1prob_format_matches_reference(tmp_path):
     O.save_problem(tmp_path / "c.l1prob", K, np.zeros(3), np.zeros(4), 123, 0.0)
     raw = (tmp_path / "c.l1prob").read_bytes()
     assert raw[:8] == b"L1PROBv1" and np.frombuffer(raw, "<f8", 1, 48)[0] == K[0, 1]
+
+
+def test_reference_minimizer_bit_identical():
+    """reference.cpp:38-82 restated (oracle) == the reference's own source (oracle/_ref)."""
+    P = O.build_problem(PB.C1)
+    K, y = P["K"], P["y"]
+    lmax = float(np.abs(O.apply_adjoint(K, y)).max())
+    op = R.RefOperator(K)
+    for frac in (1.0 / 4.0, 1.0 / 64.0, 2.0):  # the last: lambda >= lambda_max -> zero
+        lam = lmax * frac
+        ro = O.reference_minimizer(K, y, lam)
+        xr, cert, rho, nnz = op.reference_minimizer(y, lam)
+        assert np.array_equal(ro["x"], xr) and ro["certificate"] == cert
+        assert ro["rho"] == rho and ro["nnz"] == nnz
+        assert ro["certificate"] <= 1e-12
+    with pytest.raises(ValueError):
+        O.reference_minimizer(K, y, 0.0)
