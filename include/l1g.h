@@ -221,6 +221,26 @@ int l1g_shrinkage_solve(l1g_op* op, const double* y, double lambda, int accelera
                         const l1g_stop_rule* stop, double* x_out, l1g_result* res,
                         l1g_iter_record* trace, int64_t cap, l1g_iter_cb cb, void* user);
 
+/* ---- the reference minimizer of the penalized problem (reference.cpp:38-82), on the
+ * device FISTA kernels: accelerated thresholding from x = 0 until the fixed-point certificate
+ * ||x - S_lambda(x + K^T (y - K x))||_inf <= oracle_tol (checked every check_interval
+ * iterations, or once a step is below the tolerance).  opt NULL = ReferenceOptions defaults
+ * (1e-12, 500000, 50, 1e-10).  Not converged: L1G_ERUNTIME (as the reference throws).
+ *   l1g_penalized_fixed_point_residual -> penalized_fixed_point_residual reference.cpp:9-13 */
+typedef struct {
+  double oracle_tol;
+  int64_t max_iterations, check_interval;
+  double nnz_threshold;
+} l1g_ref_options;
+typedef struct {
+  double lambda, rho, oracle_tol, certificate;
+  int64_t nnz, iterations, matvecs;
+} l1g_ref_solution;
+int l1g_reference_minimizer(l1g_op* op, const double* y, double lambda,
+                            const l1g_ref_options* opt, double* x_out, l1g_ref_solution* out);
+int l1g_penalized_fixed_point_residual(l1g_op* op, const double* y, const double* x,
+                                       double lambda, double* out);
+
 /* ---- column-sharded runs (no reference counterpart: the reference is
  * single-threaded).  Shard r of R holds columns [r*p/R, (r+1)*p/R) of K as its own l1g_op
  * (p/R a multiple of 256) and owns that slice of x and g.  Each iteration exchanges the shard
@@ -259,6 +279,10 @@ int l1g_batch_create(l1g_op* op, int B, const double* Y, const double* rho,
                      const l1g_gp_config* cfg, l1g_batch** out);
 int l1g_batch_init(l1g_batch* b, const double* X0);
 int l1g_batch_run(l1g_batch* b, const l1g_stop_rule* stop, l1g_result* results);
+/* continue after l1g_batch_run with a larger budget: problems a budget stopped resume
+ * exactly where they stopped; stationary / objective-tol stops stay stopped (one trajectory
+ * sampled at a budget ladder, isochrone.cpp:75-100) */
+int l1g_batch_resume(l1g_batch* b, const l1g_stop_rule* stop, l1g_result* results);
 int l1g_batch_get_x(l1g_batch* b, double* X);
 int l1g_batch_stream(l1g_batch* b, void** stream);
 int l1g_batch_launches(l1g_batch* b, int64_t* launches, int reset);

@@ -9,6 +9,8 @@ from .api import (  # noqa: F401
     gp_init, gp_iterate, gpss_solve, ista_solve, load_problem, problem_hash, psd_solve,
     save_problem, l1_norm, lambda_from_rho, lambda_max, linf_norm,
     project_l1_ball, project_l1_ball_with_threshold, rho_from_lambda, soft_threshold,
-    spectral_norm_estimate, squared_norm, steplength_init, steplength_select, to_string)
+    spectral_norm_estimate, squared_norm, steplength_init, steplength_select, to_string,
+    ReferenceOptions, ReferenceSolution, reference_minimizer, penalized_fixed_point_residual)
+from . import isochrone  # noqa: F401
 
 __version__ = "0.1.0"

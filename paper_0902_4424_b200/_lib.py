@@ -61,6 +61,17 @@ class GpStateC(C.Structure):  # l1g_gp_state
                 ("alpha2_history", C.c_double * 66), ("choice", SlChoiceC)]
 
 
+class RefOptionsC(C.Structure):  # l1g_ref_options
+    _fields_ = [("oracle_tol", C.c_double), ("max_iterations", C.c_int64),
+                ("check_interval", C.c_int64), ("nnz_threshold", C.c_double)]
+
+
+class RefSolutionC(C.Structure):  # l1g_ref_solution
+    _fields_ = [("lambda_", C.c_double), ("rho", C.c_double), ("oracle_tol", C.c_double),
+                ("certificate", C.c_double), ("nnz", C.c_int64), ("iterations", C.c_int64),
+                ("matvecs", C.c_int64)]
+
+
 RECORD_FIELDS = [f for f, _ in IterRecordC._fields_]
 ITER_CB = C.CFUNCTYPE(C.c_int, C.POINTER(IterRecordC), C.POINTER(C.c_double), C.c_int64,
                       C.c_void_p)
@@ -119,6 +130,7 @@ _SIGS = {
     "l1g_batch_init": (C.c_int, [_vp, _vp]),
     "l1g_batch_run": (C.c_int, [_vp, C.POINTER(StopRuleC), _vp]),
     "l1g_batch_get_x": (C.c_int, [_vp, _vp]),
+    "l1g_batch_resume": (C.c_int, [_vp, C.POINTER(StopRuleC), _vp]),
     "l1g_batch_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "l1g_batch_launches": (C.c_int, [_vp, C.POINTER(_i64), C.c_int]),
     "l1g_batch_destroy": (None, [_vp]),
@@ -161,6 +173,9 @@ _SIGS = {
     "l1g_problem_save": (C.c_int, [C.c_char_p, _vp, _vp, _vp, C.c_uint64, C.c_double]),
     "l1g_problem_hash": (C.c_int, [_vp, _vp, _vp, C.c_uint64, C.c_double,
                                    C.POINTER(C.c_uint64)]),
+    "l1g_reference_minimizer": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(RefOptionsC), _vp,
+                                          C.POINTER(RefSolutionC)]),
+    "l1g_penalized_fixed_point_residual": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp]),
     "l1g_host_alloc": (C.c_int, [_i64, C.POINTER(_vp)]),
     "l1g_host_free": (None, [_vp]),
 }

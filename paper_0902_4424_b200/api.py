@@ -788,6 +788,53 @@ def fista_solve(prob: Objective, lam: PenaltyWeight, stop: StopRule,
     return _other_solve(prob, lam.value(), 2, stop, cb, trace)
 
 
+# ------------------------------------------------------------------ reference minimizer
+@dataclass
+class ReferenceOptions:  # reference.hpp:19-24
+    oracle_tol: float = 1e-12
+    max_iterations: int = 500000
+    check_interval: int = 50
+    nnz_threshold: float = 1e-10
+
+
+@dataclass
+class ReferenceSolution:  # reference.hpp:9-17
+    lambda_: float = 0.0
+    rho: float = 0.0
+    x: Optional[np.ndarray] = None
+    nnz: int = 0
+    oracle_tol: float = 0.0
+    certificate: float = 0.0
+    iterations: int = 0
+    matvecs: int = 0
+
+
+def reference_minimizer(prob: Objective, lam: float,
+                        opt: Optional[ReferenceOptions] = None) -> ReferenceSolution:
+    """reference.cpp:38-82 on the device FISTA kernels: the penalized minimizer x(lambda),
+    driven until ||x - S_lambda(x + K^T(y - Kx))||_inf <= oracle_tol.  RuntimeError if the
+    certificate is not reached within max_iterations (as the reference throws)."""
+    opt = opt or ReferenceOptions()
+    op = _require_dense(prob)
+    o = L.RefOptionsC(opt.oracle_tol, opt.max_iterations, opt.check_interval, opt.nnz_threshold)
+    out = L.RefSolutionC()
+    x = np.empty(op.cols())
+    check(L.load().l1g_reference_minimizer(op.h, ptr(prob.y()), float(lam), C.byref(o), ptr(x),
+                                           C.byref(out)), "reference_minimizer")
+    return ReferenceSolution(out.lambda_, out.rho, x, out.nnz, out.oracle_tol, out.certificate,
+                             out.iterations, out.matvecs)
+
+
+def penalized_fixed_point_residual(prob: Objective, x, lam: float) -> float:
+    """reference.cpp:9-13 (2 matvecs on the device)."""
+    op = _require_dense(prob)
+    out = C.c_double()
+    check(L.load().l1g_penalized_fixed_point_residual(op.h, ptr(prob.y()), ptr(_f64(x)),
+                                                      float(lam), C.byref(out)),
+          "penalized_fixed_point_residual")
+    return out.value
+
+
 # ------------------------------------------------------------------ L1PROBv1 problem files
 @dataclass
 class GeneratedProblem:  # generators.hpp:14-20

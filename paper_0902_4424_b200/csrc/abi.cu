@@ -116,6 +116,29 @@ void loop_cond(const DevState* st, const int* nrun, cudaGraphConditionalHandle h
   L1G_CUDA(cudaGetLastError());
 }
 
+// resume (batched budget ladders): only runs a budget stopped are continued; a run that
+// stopped stationary, on its objective tolerance or failed stays stopped, and `nrun` counts
+// the resumed runs
+__global__ void resume_kernel(DevState* st, int B, l1g_stop_rule stop, int* nrun) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  DevState* s = st + i;
+  s->max_iterations = stop.max_iterations;
+  s->max_matvecs = stop.max_matvecs;
+  s->max_seconds = stop.max_seconds;
+  s->stationarity_tol = stop.stationarity_tol;
+  s->objective_tol = stop.objective_tol;
+  s->single_step = 0;
+  s->trace = nullptr;
+  s->trace_cap = 0;
+  const bool budget = s->reason == L1G_MAX_ITERATIONS || s->reason == L1G_MAX_MATVECS ||
+                      s->reason == L1G_MAX_SECONDS;
+  if (s->status == STOPPED && budget) {
+    s->status = RUNNING;
+    atomicAdd(nrun, 1);
+  }
+}
+
 __global__ void configure_kernel(DevState* st, l1g_stop_rule stop, int single_step,
                                  l1g_iter_record* trace, int64_t cap) {
   st->max_iterations = stop.max_iterations;
@@ -1063,18 +1086,25 @@ void batch_enqueue_iteration(l1g_batch* b) {
   batch_products(b, FWD_ITER, b->vb.d, ADJ_ITER, b->rn, true, true);
 }
 
-// gpss.cpp:221-292 for every problem, in lockstep
-void batch_run(l1g_batch* b, const l1g_stop_rule& stop, l1g_result* res) {
+// gpss.cpp:221-292 for every problem, in lockstep.  resume: continue the runs a budget stopped
+// (a budget ladder: one trajectory sampled at increasing budgets, isochrone.cpp:75-100)
+void batch_run(l1g_batch* b, const l1g_stop_rule& stop, l1g_result* res, bool resume = false) {
   check_stop(stop);
   if (!b->inited) throw InvalidArgument("batched solve: gp_init has not been run");
   set_device(b->op->c);
   cudaStream_t s = b->stream;
-  for (int i = 0; i < b->B; ++i) {
-    configure_kernel<<<1, 1, 0, s>>>(b->st + i, stop, 0, nullptr, 0);
-    L1G_CUDA(cudaGetLastError());
-  }
   const int B = b->B;
-  L1G_CUDA(cudaMemcpyAsync(b->nrun, &B, sizeof(int), cudaMemcpyHostToDevice, s));
+  if (resume) {
+    L1G_CUDA(cudaMemsetAsync(b->nrun, 0, sizeof(int), s));
+    resume_kernel<<<(B + 127) / 128, 128, 0, s>>>(b->st, B, stop, b->nrun);
+    L1G_CUDA(cudaGetLastError());
+  } else {
+    for (int i = 0; i < B; ++i) {
+      configure_kernel<<<1, 1, 0, s>>>(b->st + i, stop, 0, nullptr, 0);
+      L1G_CUDA(cudaGetLastError());
+    }
+    L1G_CUDA(cudaMemcpyAsync(b->nrun, &B, sizeof(int), cudaMemcpyHostToDevice, s));
+  }
   L1G_CUDA(cudaStreamSynchronize(s));
   if (!b->gexec) {
     const GemvPlan& pl = b->op->plan;
@@ -1095,7 +1125,11 @@ void batch_run(l1g_batch* b, const l1g_stop_rule& stop, l1g_result* res) {
   }
   const int64_t cap = stop.max_iterations > 0 ? stop.max_iterations / b->gsize + 3 : INT64_MAX;
   volatile int* flag = b->nrun_host;
-  if (b->gloop) {
+  int live = B;
+  if (resume) {
+    L1G_CUDA(cudaMemcpy(&live, b->nrun, sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  if (live > 0 && b->gloop) {
     int64_t k0 = 0, k1 = 0;
     L1G_CUDA(cudaMemcpyAsync(&k0, &b->st->k, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     L1G_CUDA(cudaGraphLaunch(b->gloop, s));
@@ -1103,7 +1137,7 @@ void batch_run(l1g_batch* b, const l1g_stop_rule& stop, l1g_result* res) {
     L1G_CUDA(cudaStreamSynchronize(s));
     b->launches += ((k1 - k0) / b->gsize + 1) * (6LL * b->gsize + 1);
   }
-  for (int64_t launched = 0; !b->gloop;) {
+  for (int64_t launched = 0; live > 0 && !b->gloop;) {
     L1G_CUDA(cudaGraphLaunch(b->gexec, s));
     b->launches += 6LL * b->gsize;
     L1G_CUDA(cudaMemcpyAsync((void*)flag, b->nrun, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1354,6 +1388,104 @@ void other_solve(l1g_op* op, const double* y_host, double param, int kind,
   res->elapsed_seconds = elapsed();
   download(x_out, x, pl.p, s);
   L1G_CUDA(cudaStreamSynchronize(s));
+}
+
+// ||x - S_lambda(x + K^T (y - K x))||_inf (reference.cpp:9-13), 2 matvecs; scratch buffers
+// kx, mis (n_pad), r, v, u (p_pad)
+double fixed_point_residual(l1g_op* op, LoopBufs& lb, const double* y, const double* x,
+                            double lambda, double* kx, double* mis, double* r, double* v,
+                            double* u) {
+  const GemvPlan& pl = op->plan;
+  cudaStream_t s = lb.s;
+  launch_fwd(*op, lb.ws, FWD_APPLY, x, kx, nullptr, nullptr, s);
+  vsub(y, kx, mis, pl.n_pad, s);
+  launch_adj(*op, lb.ws, ADJ_APPLY, mis, r, nullptr, nullptr, s);
+  lincomb(x, 1.0, r, v, pl.p_pad, s);  // x + r (1.0 * r is exact)
+  soft_threshold(v, u, pl.p_pad, lambda, s);
+  vsub(x, u, v, pl.p_pad, s);
+  reduce(v, nullptr, pl.p_pad, RED_MAX, lb.scal + 6, 0, s);
+  return fetch(lb, 6);
+}
+
+// reference.cpp:38-82: accelerated thresholding on the device until the unscaled fixed-point
+// certificate holds; the same element-wise kernels, GEMVs and reductions as fista_solve
+void reference_minimizer(l1g_op* op, const double* y_host, double lambda,
+                         const l1g_ref_options& o, double* x_out, l1g_ref_solution* out) {
+  if (!(lambda > 0.0)) throw InvalidArgument("reference_minimizer: lambda must be > 0");
+  if (o.check_interval < 1) throw InvalidArgument("reference_minimizer: check_interval must be >= 1");
+  set_device(op->c);
+  const GemvPlan& pl = op->plan;
+  LoopBufs lb;
+  L1G_CUDA(cudaStreamCreateWithFlags(&lb.s, cudaStreamNonBlocking));
+  alloc_ws(lb.ws, pl);
+  lb.scal = dalloc<double>(8);
+  double *x = lb.get(pl.p_pad), *xp = lb.get(pl.p_pad), *pt = lb.get(pl.p_pad),
+         *r = lb.get(pl.p_pad), *v = lb.get(pl.p_pad), *xn = lb.get(pl.p_pad),
+         *u = lb.get(pl.p_pad);
+  double *y = lb.get(pl.n_pad), *kx = lb.get(pl.n_pad), *mis = lb.get(pl.n_pad);
+  cudaStream_t s = lb.s;
+  L1G_CUDA(cudaMemcpyAsync(y, y_host, pl.n * 8, cudaMemcpyHostToDevice, s));
+  std::memset(out, 0, sizeof(*out));
+  out->lambda = lambda;
+  out->oracle_tol = o.oracle_tol;
+  // lambda_max = ||K^T y||_inf (prox.cpp lambda_max)
+  launch_adj(*op, lb.ws, ADJ_APPLY, y, r, nullptr, nullptr, s);
+  reduce(r, nullptr, pl.p_pad, RED_MAX, lb.scal + 0, 0, s);
+  const double lmax = fetch(lb, 0);
+  int64_t mv = 1;
+  bool done = false;
+  double cert = 0.0;
+  if (lambda >= lmax) {  // the penalized minimizer is zero; its certificate is exact
+    cert = fixed_point_residual(op, lb, y, x, lambda, kx, mis, r, v, u);
+    mv += 2;
+    done = true;
+  } else {
+    const double c = 0.999, c2 = c * c, lam_eff = lambda * c2;  // solver.hpp:128
+    double t = 1.0;
+    for (int64_t k = 0; k < o.max_iterations; ++k) {
+      const double t_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t * t));  // fista_t_next
+      extrap(x, xp, (t - 1.0) / t_next, pt, pl.p_pad, s);
+      launch_fwd(*op, lb.ws, FWD_APPLY, pt, kx, nullptr, nullptr, s);
+      vsub(kx, y, mis, pl.n_pad, s);
+      launch_adj(*op, lb.ws, ADJ_APPLY, mis, r, nullptr, nullptr, s);
+      mv += 2;
+      lincomb(pt, -c2, r, v, pl.p_pad, s);
+      soft_threshold(v, xn, pl.p_pad, lam_eff, s);
+      std::swap(xp, x);  // x_prev = x
+      std::swap(x, xn);  // x = x_new
+      t = t_next;
+      out->iterations = k + 1;
+      vsub(x, pt, v, pl.p_pad, s);
+      reduce(v, nullptr, pl.p_pad, RED_MAX, lb.scal + 1, 0, s);
+      const double surrogate = fetch(lb, 1);
+      if ((k + 1) % o.check_interval == 0 || surrogate <= o.oracle_tol) {
+        cert = fixed_point_residual(op, lb, y, x, lambda, kx, mis, r, v, u);
+        mv += 2;
+        if (cert <= o.oracle_tol) {
+          done = true;
+          break;
+        }
+      }
+    }
+  }
+  out->matvecs = mv;
+  if (!done) {
+    cert = fixed_point_residual(op, lb, y, x, lambda, kx, mis, r, v, u);
+    char msg[256];
+    std::snprintf(msg, sizeof(msg),
+                  "reference_minimizer: certificate %g did not reach tolerance %g within %lld "
+                  "iterations (lambda = %g)",
+                  cert, o.oracle_tol, (long long)o.max_iterations, lambda);
+    throw RuntimeFailure(msg);
+  }
+  out->certificate = cert;
+  reduce(x, nullptr, pl.p_pad, RED_ABS, lb.scal + 2, 0, s);  // rho = ||x||_1
+  out->rho = fetch(lb, 2);
+  std::vector<double> xh((size_t)pl.p);
+  download(xh.data(), x, pl.p, s);
+  L1G_CUDA(cudaStreamSynchronize(s));
+  for (double xv : xh) out->nnz += std::fabs(xv) > o.nnz_threshold;
+  if (x_out) std::memcpy(x_out, xh.data(), sizeof(double) * (size_t)pl.p);
 }
 
 }  // namespace
@@ -2273,6 +2405,10 @@ int l1g_batch_run(l1g_batch* b, const l1g_stop_rule* stop, l1g_result* results) 
   return guarded([&] { batch_run(b, *stop, results); });
 }
 
+int l1g_batch_resume(l1g_batch* b, const l1g_stop_rule* stop, l1g_result* results) {
+  return guarded([&] { batch_run(b, *stop, results, true); });
+}
+
 int l1g_batch_get_x(l1g_batch* b, double* X) {
   return guarded([&] { batch_get_x(b, X); });
 }
@@ -2369,6 +2505,33 @@ int l1g_shrinkage_solve(l1g_op* op, const double* y, double lambda, int accelera
                         l1g_iter_record* trace, int64_t cap, l1g_iter_cb cb, void* user) {
   return guarded([&] {
     other_solve(op, y, lambda, accelerated ? 2 : 1, *stop, x_out, res, trace, cap, cb, user);
+  });
+}
+
+int l1g_reference_minimizer(l1g_op* op, const double* y, double lambda,
+                            const l1g_ref_options* opt, double* x_out, l1g_ref_solution* out) {
+  return guarded([&] {
+    l1g_ref_options o{1e-12, 500000, 50, 1e-10};  // ReferenceOptions defaults, reference.hpp
+    if (opt) o = *opt;
+    reference_minimizer(op, y, lambda, o, x_out, out);
+  });
+}
+
+int l1g_penalized_fixed_point_residual(l1g_op* op, const double* y_host, const double* x_host,
+                                       double lambda, double* out) {
+  return guarded([&] {
+    set_device(op->c);
+    const GemvPlan& pl = op->plan;
+    LoopBufs lb;
+    L1G_CUDA(cudaStreamCreateWithFlags(&lb.s, cudaStreamNonBlocking));
+    alloc_ws(lb.ws, pl);
+    lb.scal = dalloc<double>(8);
+    double *x = lb.get(pl.p_pad), *r = lb.get(pl.p_pad), *v = lb.get(pl.p_pad),
+           *u = lb.get(pl.p_pad), *y = lb.get(pl.n_pad), *kx = lb.get(pl.n_pad),
+           *mis = lb.get(pl.n_pad);
+    L1G_CUDA(cudaMemcpyAsync(y, y_host, pl.n * 8, cudaMemcpyHostToDevice, lb.s));
+    L1G_CUDA(cudaMemcpyAsync(x, x_host, pl.p * 8, cudaMemcpyHostToDevice, lb.s));
+    *out = fixed_point_residual(op, lb, y, x, lambda, kx, mis, r, v, u);
   });
 }
 
