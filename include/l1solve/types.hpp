@@ -46,6 +46,35 @@ class Vector {
   Vector& operator*=(double c);
   Vector& operator/=(double c);
 
+  /// Eigen's comma initializer: v << a, b, c;
+  struct CommaInit {
+    Vector* v;
+    Index i;
+    CommaInit& operator,(double x) {
+      (*v)[i++] = x;
+      return *this;
+    }
+  };
+  CommaInit operator<<(double x) {
+    (*this)[0] = x;
+    return CommaInit{this, 1};
+  }
+  /// coefficient-wise view for (a.array() == b.array()).all()
+  struct Array {
+    const std::vector<double>* v;
+    struct Mask {
+      bool ok;
+      bool all() const { return ok; }
+    };
+    Mask operator==(const Array& o) const {
+      if (v->size() != o.v->size()) return {false};
+      for (std::size_t i = 0; i < v->size(); ++i)
+        if (!((*v)[i] == (*o.v)[i])) return {false};
+      return {true};
+    }
+  };
+  Array array() const { return Array{&v_}; }
+
  private:
   std::vector<double> v_;
 };
@@ -81,10 +110,62 @@ class Matrix {
   double& operator()(Index i, Index j) { return d_[static_cast<std::size_t>(j * r_ + i)]; }
   double operator()(Index i, Index j) const { return d_[static_cast<std::size_t>(j * r_ + i)]; }
 
+  // host-side helpers for callers written against Eigen (tests, generators); the solver's
+  // products run on the GPU through DenseOperator
+  Matrix transpose() const {
+    Matrix t(c_, r_);
+    for (Index j = 0; j < c_; ++j)
+      for (Index i = 0; i < r_; ++i) t(j, i) = (*this)(i, j);
+    return t;
+  }
+  Matrix& operator+=(const Matrix& o) {
+    for (std::size_t k = 0; k < d_.size(); ++k) d_[k] = d_[k] + o.d_[k];
+    return *this;
+  }
+  Matrix& operator/=(double c) {
+    for (auto& x : d_) x = x / c;
+    return *this;
+  }
+  Matrix& operator*=(double c) {
+    for (auto& x : d_) x = x * c;
+    return *this;
+  }
+  /// Eigen's comma initializer, row by row: m << a, b, c, d;
+  struct CommaInit {
+    Matrix* m;
+    Index k;
+    CommaInit& operator,(double x) {
+      (*m)(k / m->c_, k % m->c_) = x;
+      ++k;
+      return *this;
+    }
+  };
+  CommaInit operator<<(double x) {
+    (*this)(0, 0) = x;
+    return CommaInit{this, 1};
+  }
+  struct Array {
+    const Matrix* m;
+    Vector::Array::Mask operator==(const Array& o) const {
+      return {m->r_ == o.m->r_ && m->c_ == o.m->c_ && m->d_ == o.m->d_};
+    }
+  };
+  Array array() const { return Array{this}; }
+
  private:
   Index r_ = 0, c_ = 0;
   std::vector<double> d_;
 };
+
+inline Matrix operator*(double c, Matrix m) { return m *= c; }
+inline Matrix operator+(Matrix a, const Matrix& b) { return a += b; }
+/// host product (column-major accumulation, Eigen's plain GEMV order)
+inline Vector operator*(const Matrix& m, const Vector& x) {
+  Vector out(m.rows());
+  for (Index j = 0; j < m.cols(); ++j)
+    for (Index i = 0; i < m.rows(); ++i) out[i] = out[i] + m(i, j) * x[j];
+  return out;
+}
 
 /// Counts applications of K and K^T (types.hpp:15-17).
 struct MatvecCounter {

@@ -16,7 +16,10 @@
 
 #include "l1g.h"
 #include "l1solve/gpss.hpp"
+#include "l1solve/generators.hpp"
 #include "l1solve/problem_io.hpp"
+#include "l1solve/reference.hpp"
+#include "l1solve/rng.hpp"
 
 namespace l1solve {
 
@@ -836,6 +839,241 @@ SolverState ista_solve(const Objective& prob, const PenaltyWeight& lambda, const
 SolverState fista_solve(const Objective& prob, const PenaltyWeight& lambda, const StopRule& stop,
                         const IterationCallback& cb) {
   return other_solve(prob, lambda.value(), 2, stop, cb, "fista_solve");
+}
+
+}  // namespace l1solve
+
+// ------------------------------------------------------------------------- rng, generators
+// The reference's small seeded problems (generators.cpp:13-147) for callers and tests:
+// std::mt19937_64 uniforms, Box-Muller normals with libm, host arithmetic.
+namespace l1solve {
+
+double Rng::normal() {
+  if (has_spare_) {
+    has_spare_ = false;
+    return spare_;
+  }
+  double u1 = uniform();
+  while (u1 == 0.0) u1 = uniform();
+  const double u2 = uniform();
+  const double radius = std::sqrt(-2.0 * std::log(u1));
+  const double angle = 2.0 * M_PI * u2;
+  spare_ = radius * std::sin(angle);
+  has_spare_ = true;
+  return radius * std::cos(angle);
+}
+
+std::uint64_t Rng::below(std::uint64_t bound) {
+  if (bound == 0) throw std::invalid_argument("Rng::below: bound must be positive");
+  const std::uint64_t threshold = (0 - bound) % bound;  // 2^64 mod bound
+  for (;;) {
+    const std::uint64_t r = engine_();
+    if (r >= threshold) return r % bound;
+  }
+}
+
+Vector Rng::normal_vector(Index n) {
+  Vector v(n);
+  for (Index i = 0; i < n; ++i) v[i] = normal();
+  return v;
+}
+
+Matrix Rng::normal_matrix(Index rows, Index cols) {
+  Matrix m(rows, cols);
+  for (Index i = 0; i < rows; ++i)
+    for (Index j = 0; j < cols; ++j) m(i, j) = normal();
+  return m;
+}
+
+std::vector<Index> Rng::sample_indices(Index population, Index k) {
+  if (k > population) throw std::invalid_argument("Rng::sample_indices: k > population");
+  std::vector<Index> pool(static_cast<std::size_t>(population));
+  for (Index i = 0; i < population; ++i) pool[static_cast<std::size_t>(i)] = i;
+  for (Index i = 0; i < k; ++i) {
+    const Index j = i + static_cast<Index>(below(static_cast<std::uint64_t>(population - i)));
+    std::swap(pool[static_cast<std::size_t>(i)], pool[static_cast<std::size_t>(j)]);
+  }
+  pool.resize(static_cast<std::size_t>(k));
+  return pool;
+}
+
+namespace {
+
+void check_gen(Index n, Index p, Index nnz, double noise_level) {
+  if (n < 1 || p < 1) throw std::invalid_argument("problem generator: n and p must be positive");
+  if (nnz < 0 || nnz > p)
+    throw std::invalid_argument("problem generator: nnz must lie in [0, p], got " +
+                                std::to_string(nnz) + " with p = " + std::to_string(p));
+  if (noise_level < 0.0) throw std::invalid_argument("problem generator: noise_level must be >= 0");
+}
+
+// spikes of +-1 on a random support, y = K x + e with ||e|| = noise * ||K x||
+GeneratedProblem finish_problem(Rng& rng, Matrix k, Index nnz, double noise_level,
+                                std::uint64_t seed) {
+  GeneratedProblem prob;
+  prob.op = std::make_shared<DenseOperator>(k);
+  const Index p = k.cols();
+  prob.x_true = Vector::Zero(p);
+  for (const Index i : rng.sample_indices(p, nnz)) prob.x_true[i] = rng.sign();
+  MatvecCounter scratch;
+  prob.y = prob.op->apply(prob.x_true, scratch);
+  if (noise_level != 0.0) {
+    const Vector e = rng.normal_vector(k.rows());
+    const double e_norm = e.norm();
+    if (e_norm != 0.0) {
+      const double signal = prob.y.norm();
+      const double scale = (signal > 0.0 ? noise_level * signal : noise_level) / e_norm;
+      prob.y += scale * e;
+    }
+  }
+  prob.noise_level = noise_level;
+  prob.seed = seed;
+  return prob;
+}
+
+// thin Q (rows x cols, cols <= rows) of a Householder QR, column by column
+Matrix householder_q(Matrix a) {
+  const Index m = a.rows(), n = a.cols();
+  std::vector<Vector> vs;
+  for (Index j = 0; j < n; ++j) {
+    double norm = 0.0;
+    for (Index i = j; i < m; ++i) norm += a(i, j) * a(i, j);
+    norm = std::sqrt(norm);
+    Vector v(m);
+    const double alpha = a(j, j) > 0.0 ? -norm : norm;
+    for (Index i = j; i < m; ++i) v[i] = a(i, j);
+    v[j] = v[j] - alpha;
+    double vn = 0.0;
+    for (Index i = j; i < m; ++i) vn += v[i] * v[i];
+    if (vn > 0.0)
+      for (Index c = j; c < n; ++c) {
+        double dotv = 0.0;
+        for (Index i = j; i < m; ++i) dotv += v[i] * a(i, c);
+        const double f = 2.0 * dotv / vn;
+        for (Index i = j; i < m; ++i) a(i, c) = a(i, c) - f * v[i];
+      }
+    vs.push_back(std::move(v));
+  }
+  Matrix q = Matrix::Identity(m, n);
+  for (Index j = n - 1; j >= 0; --j) {
+    const Vector& v = vs[static_cast<std::size_t>(j)];
+    double vn = 0.0;
+    for (Index i = j; i < m; ++i) vn += v[i] * v[i];
+    if (vn == 0.0) continue;
+    for (Index c = 0; c < n; ++c) {
+      double dotv = 0.0;
+      for (Index i = j; i < m; ++i) dotv += v[i] * q(i, c);
+      const double f = 2.0 * dotv / vn;
+      for (Index i = j; i < m; ++i) q(i, c) = q(i, c) - f * v[i];
+    }
+  }
+  return q;
+}
+
+}  // namespace
+
+// generators.cpp:99-117
+GeneratedProblem gen_gaussian_problem(Index n, Index p, Index nnz, double noise_level,
+                                      std::uint64_t seed) {
+  check_gen(n, p, nnz, noise_level);
+  Rng rng(seed);
+  Matrix k = rng.normal_matrix(n, p);
+  {
+    const DenseOperator raw(k);
+    const double sigma = spectral_norm_estimate(raw, 1000, 1e-8);
+    if (sigma == 0.0) throw std::runtime_error("gen_gaussian_problem: degenerate matrix");
+    k /= sigma;
+  }
+  return finish_problem(rng, std::move(k), nnz, noise_level, seed);
+}
+
+// generators.cpp:119-147: singular values decay^(i-1) between Gaussian orthonormal factors
+GeneratedProblem gen_illconditioned_problem(Index n, Index p, Index nnz, double decay,
+                                            double noise_level, std::uint64_t seed) {
+  check_gen(n, p, nnz, noise_level);
+  if (!(decay > 0.0 && decay < 1.0))
+    throw std::invalid_argument("gen_illconditioned_problem: decay must lie strictly in (0,1)");
+  Rng rng(seed);
+  const Index r = std::min(n, p);
+  const Matrix u = householder_q(rng.normal_matrix(n, r));
+  const Matrix v = householder_q(rng.normal_matrix(p, r));
+  Matrix k(n, p);
+  double s = 1.0;
+  for (Index l = 0; l < r; ++l, s *= decay)
+    for (Index j = 0; j < p; ++j)
+      for (Index i = 0; i < n; ++i) k(i, j) = k(i, j) + u(i, l) * (s * v(j, l));
+  return finish_problem(rng, std::move(k), nnz, noise_level, seed);
+}
+
+// ------------------------------------------------------------------------- reference minimizer
+// reference.cpp:9-13
+double penalized_fixed_point_residual(const Objective& prob, const Vector& x, double lambda,
+                                      MatvecCounter& mv) {
+  const Vector r = prob.residual(x, mv);
+  return (x - soft_threshold(x + r, lambda)).lpNorm<Infinity>();
+}
+
+// reference.cpp:38-82 (DenseOperator: the device driver l1g_reference_minimizer)
+ReferenceSolution reference_minimizer(const Objective& prob, double lambda,
+                                      const ReferenceOptions& opt) {
+  if (!(lambda > 0.0)) throw std::invalid_argument("reference_minimizer: lambda must be > 0");
+  auto* dense = dynamic_cast<const DenseOperator*>(&prob.op());
+  ReferenceSolution ref;
+  ref.lambda = lambda;
+  ref.oracle_tol = opt.oracle_tol;
+  if (dense) {
+    l1g_ref_options o{opt.oracle_tol, opt.max_iterations, opt.check_interval, opt.nnz_threshold};
+    l1g_ref_solution out;
+    ref.x = Vector(prob.dim());
+    check(l1g_reference_minimizer(dense->handle(), prob.y().data(), lambda, &o, ref.x.data(),
+                                  &out));
+    ref.rho = out.rho;
+    ref.nnz = static_cast<long>(out.nnz);
+    ref.certificate = out.certificate;
+    return ref;
+  }
+  // matrix-free operator: the reference's loop over the device primitives
+  MatvecCounter mv;
+  const double lmax = lambda_max(prob.op(), prob.y(), mv);
+  Vector x = Vector::Zero(prob.dim());
+  double cert = 0.0;
+  bool ok = lambda >= lmax;
+  if (ok) {
+    cert = penalized_fixed_point_residual(prob, x, lambda, mv);
+  } else {
+    const double c2 = kShrinkageOperatorScale * kShrinkageOperatorScale;
+    const double lam_eff = lambda * c2;
+    Vector x_prev = x;
+    double t = 1.0;
+    for (long k = 0; k < opt.max_iterations && !ok; ++k) {
+      const double t_next = fista_t_next(t);
+      const Vector point = x + ((t - 1.0) / t_next) * (x - x_prev);
+      const Vector misfit = prob.op().apply(point, mv) - prob.y();
+      const Vector grad_half = prob.op().apply_adjoint(misfit, mv);
+      Vector x_new = soft_threshold(point - c2 * grad_half, lam_eff);
+      x_prev = std::move(x);
+      x = std::move(x_new);
+      t = t_next;
+      const double surrogate = (x - point).lpNorm<Infinity>();
+      if ((k + 1) % opt.check_interval == 0 || surrogate <= opt.oracle_tol) {
+        cert = penalized_fixed_point_residual(prob, x, lambda, mv);
+        ok = cert <= opt.oracle_tol;
+      }
+    }
+    if (!ok) {
+      MatvecCounter scratch;
+      cert = penalized_fixed_point_residual(prob, x, lambda, scratch);
+      throw std::runtime_error("reference_minimizer: certificate " + std::to_string(cert) +
+                               " did not reach tolerance " + std::to_string(opt.oracle_tol) +
+                               " within " + std::to_string(opt.max_iterations) +
+                               " iterations (lambda = " + std::to_string(lambda) + ")");
+    }
+  }
+  ref.rho = x.lpNorm<1>();
+  for (Index i = 0; i < x.size(); ++i) ref.nnz += std::abs(x[i]) > opt.nnz_threshold;
+  ref.certificate = cert;
+  ref.x = std::move(x);
+  return ref;
 }
 
 }  // namespace l1solve

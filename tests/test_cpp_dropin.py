@@ -29,3 +29,25 @@ def test_dropin_runs(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+REF_TESTS = os.path.join(ROOT, "tests", "cpp", "_ref", "ref_unit_tests")
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/tests"),
+                    reason="reference checkout absent (GPU box)")
+def test_reference_unit_tests_compile_unchanged():
+    """/root/reference/proj/tests/test_{gpss,prox,solvers}.cpp, unchanged, compile and link
+    against include/l1solve + libl1solve_b200.so (tests/cpp/build_ref_tests.sh)."""
+    subprocess.run([os.path.join(ROOT, "tests", "cpp", "build_ref_tests.sh")], check=True)
+    assert os.path.exists(REF_TESTS)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(REF_TESTS), reason="reference unit tests not built")
+def test_reference_unit_tests_pass():
+    """The reference's own unit tests (53 test cases of test_gpss / test_prox / test_solvers)
+    run on the GPU through the drop-in and pass."""
+    r = subprocess.run([REF_TESTS], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
