@@ -11,6 +11,9 @@
 // partials are joined by the finish kernels (gemv.cu), which also run every problem's
 // epilogue.  DMMA accumulates with fused multiply-adds in its own order, so the batched
 // path matches the per-problem canonical solve to rounding, not bit for bit.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "engine.h"
 #include "steps.cuh"
@@ -201,6 +204,156 @@ __global__ void __launch_bounds__(BT, 1) badj_kernel(const BGemmArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- 16-warp products
+// CTA tile 128 (rows | columns) x 128 problems, 16 warps of 32 x 32, k-chunks of 32 and a
+// 3-stage cp.async ring (73.7 KB per stage): twice the warps per SM of the 8-warp kernels
+// above, each staged K element reused by 128 problems and each staged vector by 128 outputs.
+constexpr int WT = 512;             // threads
+constexpr int W_KS = 4 * TR * KP;   // restaged K per stage: 4 x (32 columns x KP)
+constexpr int W_VP = 32 + VPAD;     // pitch of a staged 32-long vector chunk
+constexpr int W_VS = BW * W_VP;
+constexpr int W_STAGE = W_KS + W_VS;
+constexpr int W_STAGES = 3;
+size_t bwide_smem() { return (size_t)W_STAGES * W_STAGE * 8; }
+
+// forward: part[split][b][row] over this split's 32-column chunks (per_split chunks each)
+__global__ void __launch_bounds__(WT, 1) bfwd_wide_kernel(const BGemmArgs a) {
+  pdl_wait_and_trigger();
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wr = warp & 3, wc = warp >> 2;
+  const int64_t rb0 = 4LL * blockIdx.x;
+  const int b0 = blockIdx.z * BW;
+  const int nchunk = 2 * a.nblocks;  // 32-column chunks
+  const int c_begin = blockIdx.y * a.per_split;
+  const int c_end = c_begin + a.per_split < nchunk ? c_begin + a.per_split : nchunk;
+  const int nch = c_end > c_begin ? c_end - c_begin : 0;
+  auto load = [&](int c, int st) {
+    double* ks = sm + st * W_STAGE;
+    double* vs = ks + W_KS;
+    const int64_t ch = c_begin + c, cb = ch >> 1, half = ch & 1;
+    for (int q = tid; q < 4 * 512; q += WT) {  // 4 row blocks x 512 chunks of 16 bytes
+      const int r = q >> 9, cq = q & 511;
+      cp16(ks + r * (TR * KP) + kchunk_dst(cq),
+           a.K + tile_offset(rb0 + r, cb, a.ncb) + half * (TILE / 2) + 2 * cq);
+    }
+    for (int q = tid; q < BW * 16; q += WT) {
+      const int b = q >> 4, kq = (q & 15) * 2;
+      cp16(vs + b * W_VP + kq, a.V + (int64_t)(b0 + b) * a.vstride + ch * 32 + kq);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < W_STAGES - 1; ++st) {
+    if (st < nch) load(st, st);
+    cp_commit();
+  }
+  for (int c = 0; c < nch; ++c) {
+    cp_wait<W_STAGES - 2>();
+    __syncthreads();  // chunk c landed; the stage of chunk c - 1 is free
+    if (c + W_STAGES - 1 < nch) load(c + W_STAGES - 1, (c + W_STAGES - 1) % W_STAGES);
+    cp_commit();
+    const double* ks = sm + (c % W_STAGES) * W_STAGE + wr * (TR * KP);
+    const double* vs = sm + (c % W_STAGES) * W_STAGE + W_KS + (wc * 32) * W_VP;
+#pragma unroll
+    for (int kk = 0; kk < 32; kk += 4) {
+      const int col = kk + t;
+      double av[4], bv[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) av[mt] = ks[kpos(mt * 8 + g, col)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bv[nt] = vs[(nt * 8 + g) * W_VP + col];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av[mt], bv[nt]);
+    }
+  }
+  double* out = a.part + blockIdx.y * a.pslab;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int64_t row = (rb0 + wr) * TR + mt * 8 + g;
+      const int64_t b = b0 + wc * 32 + nt * 8 + 2 * t;
+      out[b * a.ostride + row] = acc[mt][nt][0];
+      out[(b + 1) * a.ostride + row] = acc[mt][nt][1];
+    }
+}
+
+// adjoint: part[split][b][col] over this split's row blocks (per_split each); a CTA covers
+// two column blocks (128 columns)
+__global__ void __launch_bounds__(WT, 1) badj_wide_kernel(const BGemmArgs a) {
+  pdl_wait_and_trigger();
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wm = warp & 3, wc = warp >> 2;
+  const int64_t cb0 = 2LL * blockIdx.x;
+  const int b0 = blockIdx.z * BW;
+  const int r_begin = blockIdx.y * a.per_split;
+  const int r_end = r_begin + a.per_split < a.nblocks ? r_begin + a.per_split : a.nblocks;
+  const int nch = r_end > r_begin ? r_end - r_begin : 0;
+  auto load = [&](int c, int st) {
+    double* ks = sm + st * W_STAGE;
+    double* vs = ks + W_KS;
+    const int64_t rb = r_begin + c;
+    for (int q = tid; q < 2 * 1024; q += WT) {  // two tiles of 1024 chunks
+      const int tl = q >> 10, cq = q & 1023;
+      cp16(ks + tl * KT_S + kchunk_dst(cq), a.K + tile_offset(rb, cb0 + tl, a.ncb) + 2 * cq);
+    }
+    for (int q = tid; q < BW * 16; q += WT) {
+      const int b = q >> 4, kq = (q & 15) * 2;
+      cp16(vs + b * W_VP + kq, a.V + (int64_t)(b0 + b) * a.vstride + rb * TR + kq);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < W_STAGES - 1; ++st) {
+    if (st < nch) load(st, st);
+    cp_commit();
+  }
+  const int tl = wm >> 1, cofs = (wm & 1) * 32;
+  for (int c = 0; c < nch; ++c) {
+    cp_wait<W_STAGES - 2>();
+    __syncthreads();
+    if (c + W_STAGES - 1 < nch) load(c + W_STAGES - 1, (c + W_STAGES - 1) % W_STAGES);
+    cp_commit();
+    const double* kt = sm + (c % W_STAGES) * W_STAGE + tl * KT_S;
+    const double* vs = sm + (c % W_STAGES) * W_STAGE + W_KS + (wc * 32) * W_VP;
+#pragma unroll
+    for (int kk = 0; kk < TR; kk += 4) {
+      const int row = kk + t;
+      double av[4], bv[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) av[mt] = kt[kpos(row, cofs + mt * 8 + g)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bv[nt] = vs[(nt * 8 + g) * W_VP + row];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av[mt], bv[nt]);
+    }
+  }
+  double* out = a.part + blockIdx.y * a.pslab;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int64_t col = (cb0 + tl) * TC + cofs + mt * 8 + g;
+      const int64_t b = b0 + wc * 32 + nt * 8 + 2 * t;
+      out[b * a.ostride + col] = acc[mt][nt][0];
+      out[(b + 1) * a.ostride + col] = acc[mt][nt][1];
+    }
+}
+
 template <int NA>
 __device__ __forceinline__ void warp_tree_arrays_b(const double* v, int count, int stride,
                                                    int lane, double* out) {
@@ -385,11 +538,46 @@ static int splits_for(int64_t tiles_out, int64_t nblocks, int sm_count) {
   return s;
 }
 
+// 16-warp kernels (one CTA per SM): the split count that best fills whole waves, a small
+// penalty per split for the partials it adds
+static int splits_wide(int64_t tiles_out, int64_t nchunks, int sm_count) {
+  int best = 1;
+  double best_score = -1.0;
+  for (int s = 1; s <= 64 && s <= nchunks; ++s) {
+    const int64_t ctas = tiles_out * s;
+    const int64_t waves = (ctas + sm_count - 1) / sm_count;
+    const double score = (double)ctas / (double)(waves * sm_count) - 0.002 * s;
+    if (score > best_score + 1e-12) {
+      best_score = score;
+      best = s;
+    }
+  }
+  return best;
+}
+
+static bool wide_products() {
+  static const bool w = [] {
+    const char* e = getenv("L1G_DMMA");
+    return !(e && std::strcmp(e, "8") == 0);
+  }();
+  return w;
+}
+
 BatchPlan make_batch_plan(const GemvPlan& pl, int B, int sm_count) {
   BatchPlan bp{};
   bp.B = B;
   bp.Bp = (B + BW - 1) / BW * BW;
   const int64_t bz = bp.Bp / BW;
+  bp.wide = wide_products();
+  if (bp.wide) {  // forward: 32-column chunks; adjoint: row blocks; 128-wide CTA tiles
+    bp.fwd_splits = splits_wide((pl.n_pad / 128) * bz, 2 * pl.ncb, sm_count);
+    bp.fwd_per = (int)((2 * pl.ncb + bp.fwd_splits - 1) / bp.fwd_splits);
+    bp.fwd_splits = (int)((2 * pl.ncb + bp.fwd_per - 1) / bp.fwd_per);
+    bp.adj_splits = splits_wide((pl.p_pad / 128) * bz, pl.nrb, sm_count);
+    bp.adj_per = (int)((pl.nrb + bp.adj_splits - 1) / bp.adj_splits);
+    bp.adj_splits = (int)((pl.nrb + bp.adj_per - 1) / bp.adj_per);
+    return bp;
+  }
   bp.fwd_splits = splits_for((pl.n_pad / 64) * bz, pl.ncb, sm_count);
   bp.fwd_per = (int)((pl.ncb + bp.fwd_splits - 1) / bp.fwd_splits);
   bp.adj_splits = splits_for(pl.ncb * bz, pl.nrb, sm_count);
@@ -417,6 +605,16 @@ void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* par
   a.ostride = pl.n_pad;
   a.per_split = bp.fwd_per;
   a.nblocks = (int)pl.ncb;
+  if (bp.wide) {
+    static std::atomic<unsigned long long> wattr{0};
+    once_per_device(wattr, [] {
+      L1G_CUDA(cudaFuncSetAttribute(bfwd_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)bwide_smem()));
+    });
+    const dim3 grid((unsigned)(pl.n_pad / 128), (unsigned)bp.fwd_splits, (unsigned)(bp.Bp / BW));
+    L1G_CUDA(launch_pdl(bfwd_wide_kernel, grid, WT, bwide_smem(), s, a));
+    return;
+  }
   const dim3 grid((unsigned)(pl.n_pad / 64), (unsigned)bp.fwd_splits, (unsigned)(bp.Bp / BW));
   L1G_CUDA(launch_pdl(bfwd_kernel, grid, BT, bfwd_smem(), s, a));
 }
@@ -440,6 +638,16 @@ void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* par
   a.ostride = pl.p_pad;
   a.per_split = bp.adj_per;
   a.nblocks = (int)pl.nrb;
+  if (bp.wide) {
+    static std::atomic<unsigned long long> wattr{0};
+    once_per_device(wattr, [] {
+      L1G_CUDA(cudaFuncSetAttribute(badj_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)bwide_smem()));
+    });
+    const dim3 grid((unsigned)(pl.ncb / 2), (unsigned)bp.adj_splits, (unsigned)(bp.Bp / BW));
+    L1G_CUDA(launch_pdl(badj_wide_kernel, grid, WT, bwide_smem(), s, a));
+    return;
+  }
   const dim3 grid((unsigned)pl.ncb, (unsigned)bp.adj_splits, (unsigned)(bp.Bp / BW));
   L1G_CUDA(launch_pdl(badj_kernel, grid, BT, badj_smem(), s, a));
 }

@@ -139,6 +139,7 @@ struct BatchPlan {
   int B, Bp;                 // problems, padded to the CTA width (128)
   int fwd_splits, fwd_per;   // column blocks per split of the forward reduction
   int adj_splits, adj_per;   // row blocks per split of the adjoint reduction
+  int wide;                  // 1: the 16-warp 128x128 product kernels (dmma.cu), 0: 8-warp
 };
 struct BGemmArgs {
   const double* K;

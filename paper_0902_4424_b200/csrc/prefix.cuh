@@ -124,6 +124,8 @@ struct ScanShared {
   int epos[2][PREFIX_MAXW];       // per warp: first event (position, kind, count before)
   int ekind[2][PREFIX_MAXW];
   long long en[2][PREFIX_MAXW];
+  long long fq[2][PREFIX_MAXW];   // fast path: warp sums of grid counts, any tie in the warp
+  int ftie[2][PREFIX_MAXW];
   int hbad[PREFIX_MAXW];
   int epochs;  // telemetry: windows scanned by the last call
 };
@@ -242,39 +244,77 @@ __device__ long long prefix_break(const double* c, long long Ll, double rho, Sca
     const long long sbits = __double_as_longlong(S_prev);
     const int be = (int)(sbits >> 52);
     const long long base_q = (sbits & ((1LL << 52) - 1)) | (1LL << 52);  // S_prev / u
-    // pass 1: this thread's run as a parity segment; warp scan; warp totals to shared
-    ParSeg me = seg_id();
+    // pass 1: grid counts of this thread's run.  Rounding ties are rare; without any in the
+    // window the running counts are a plain integer prefix sum (one int64 warp scan and the
+    // 16 warp totals), with one the parity segments below decide them
+    long long qs = 0;
+    bool anytie = false;
 #pragma unroll 4
     for (int i = p0; i < p1; ++i) {
       bool t;
-      const long long q = grid_count(c[i], be, &t);
-      me = seg_then(me, seg_elem(q, t));
+      qs += grid_count(c[i], be, &t);
+      anytie |= t;
+    }
+    const unsigned tball = __ballot_sync(FULL, anytie);
+    long long qinc = qs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(FULL, qinc, o);
+      if (lane >= o) qinc += y;
+    }
+    if (lane == 31) {
+      ss.fq[par][warp] = qinc;
+      ss.ftie[par][warp] = tball != 0;
     }
     L1G_PSTAMP(0)
-    const ParSeg incl = seg_warp_scan(me, lane);
-    if (lane == 31) {
-      ss.wd0[par][warp] = incl.d0;
-      ss.wpk[par][warp] = seg_pack(incl);
-    }
     __syncthreads();
     L1G_PSTAMP(1)
-    // concrete counts: the warps' starts by applying the warp segments in order (the
-    // parity chain is a 1-bit select per warp; increments add up independently)
-    long long Nw = base_q, accd = base_q;
-    int accl = 0, pb = (int)(base_q & 1);
+    long long N, Nend;
+    {
+      long long wex = 0, tot = 0;
+      int ties = 0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const long long d0 = ss.wd0[par][w];
-      const int pk = ss.wpk[par][w];
-      Nw = w == warp ? accd + accl : Nw;
-      accl += pb ? (pk & 3) - 1 : 0;
-      accd += d0;
-      pb = pb ? (pk >> 3) & 1 : (pk >> 2) & 1;
+      for (int w = 0; w < NW; ++w) {
+        const long long d = ss.fq[par][w];
+        wex += w < warp ? d : 0;
+        tot += d;
+        ties |= ss.ftie[par][w];
+      }
+      N = base_q + wex + (qinc - qs);
+      Nend = base_q + tot;
+      if (ties) {  // uniform over the block: the parity-segment scan
+        ParSeg me = seg_id();
+#pragma unroll 4
+        for (int i = p0; i < p1; ++i) {
+          bool t;
+          const long long q = grid_count(c[i], be, &t);
+          me = seg_then(me, seg_elem(q, t));
+        }
+        const ParSeg incl = seg_warp_scan(me, lane);
+        if (lane == 31) {
+          ss.wd0[par][warp] = incl.d0;
+          ss.wpk[par][warp] = seg_pack(incl);
+        }
+        __syncthreads();
+        // concrete counts: the warps' starts by applying the warp segments in order (the
+        // parity chain is a 1-bit select per warp; increments add up independently)
+        long long Nw = base_q, accd = base_q;
+        int accl = 0, pb = (int)(base_q & 1);
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const long long d0 = ss.wd0[par][w];
+          const int pk = ss.wpk[par][w];
+          Nw = w == warp ? accd + accl : Nw;
+          accl += pb ? (pk & 3) - 1 : 0;
+          accd += d0;
+          pb = pb ? (pk >> 3) & 1 : (pk >> 2) & 1;
+        }
+        Nend = accd + accl;
+        ParSeg ex = seg_shfl_up(incl, 1);
+        if (lane == 0) ex = seg_id();
+        N = seg_apply(ex, Nw);
+      }
     }
-    const long long Nend = accd + accl;
-    ParSeg ex = seg_shfl_up(incl, 1);
-    if (lane == 0) ex = seg_id();
-    long long N = seg_apply(ex, Nw);
     L1G_PSTAMP(2)
     // pass 2: exact sums and tests; my first event (1 failure, 2 binade exit,
     // 3 test too close to call), branch-free so positions overlap

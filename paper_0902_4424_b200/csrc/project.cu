@@ -78,16 +78,18 @@ struct ProjShared {
 };
 
 // ---------------------------------------------------------------- distributed sort state
-constexpr int NB = 256;  // key-bit bins of the cluster bucket sort
+constexpr int NB = 256;  // key-bit bins of the cluster bucket sort (small M)
+constexpr int NB_LARGE = 1024;  // M >= 16 (C4-class vectors: tens of thousands of candidates)
 constexpr int RANK_MAXBIN = 256;  // largest bin the rank sort takes (else bitonic sorts)
 constexpr int SMALL_RANK = 256;   // single-CTA path: rank sort up to this many candidates
+template <int NBv>
 struct SortShared {
-  int hist[NB];    // this CTA's candidates per bin
-  int gcnt[NB];    // cluster-wide candidates per bin
-  int myoff[NB];   // this CTA's offset inside each bin
-  int start[NB];   // global position of each bin (bins in descending value order)
-  int cursor[NB];
-  int dest[NB];
+  int hist[NBv];    // this CTA's candidates per bin
+  int gcnt[NBv];    // cluster-wide candidates per bin
+  int myoff[NBv];   // this CTA's offset inside each bin
+  int start[NBv];   // global position of each bin (bins in descending value order)
+  int cursor[NBv];
+  int dest[NBv];
   int base[MAX_CS + 1];
   double next;
   int total, shift, ok, maxbin;
@@ -230,7 +232,9 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   __shared__ ProjShared sh;
   __shared__ ScanShared scan_sh;
   __shared__ DevState sst;
-  __shared__ SortShared srt;
+  // key-bit bins: enough that the bins stay narrow for the rank sort on large vectors
+  constexpr int NBK = M >= 16 ? NB_LARGE : NB;
+  __shared__ SortShared<NBK> srt;
   const int prob = (int)(blockIdx.x / (unsigned)a.cs);
   const int64_t pofs = prob * a.bstride;
   DevState* st = a.st + prob;
@@ -499,10 +503,10 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           const long long kspan = __double_as_longlong(vinf) - kmin;  // candidates: key > kmin
           if (tid == 0) {
             int sh_ = 0;
-            while ((kspan >> sh_) >= NB) ++sh_;
+            while ((kspan >> sh_) >= NBK) ++sh_;
             srt.shift = sh_;
           }
-          for (int t = tid; t < NB; t += PT) {
+          for (int t = tid; t < NBK; t += PT) {
             srt.hist[t] = 0;
             srt.cursor[t] = 0;
           }
@@ -514,7 +518,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
             if (m > lo) atomicAdd(&srt.hist[(int)((__double_as_longlong(m) - kmin) >> shft)], 1);
           }
           cl.sync();
-          for (int t = tid; t < NB; t += PT) {
+          for (int t = tid; t < NBK; t += PT) {
             int h[MAX_CS];
 #pragma unroll
             for (int r = 0; r < MAX_CS; ++r)
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           if (tid < 32) {  // descending exclusive scan over bins, destination CTAs
             const int lane = tid;
             int carry = 0, mx = 0;
-            for (int c0 = NB - 32; c0 >= 0; c0 -= 32) {
+            for (int c0 = NBK - 32; c0 >= 0; c0 -= 32) {
               const int b = c0 + 31 - lane;  // lane 0 takes the highest bin of the chunk
               int x = srt.gcnt[b], inc = x;
               mx = max(mx, x);
@@ -545,7 +549,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
               carry += __shfl_sync(0xffffffffu, inc, 31);
             }
             const int share = (carry + cs - 1) / cs;
-            for (int b = lane; b < NB; b += 32) {
+            for (int b = lane; b < NBK; b += 32) {
               const int d = share > 0 ? srt.start[b] / share : 0;
               srt.dest[b] = d < cs ? d : cs - 1;
             }
@@ -561,7 +565,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
             const int w = tid >> 5, lane = tid & 31;
             if (w < cs) {
               int bmin = srt.total;
-              for (int b = lane; b < NB; b += 32)
+              for (int b = lane; b < NBK; b += 32)
                 if (srt.dest[b] >= w && srt.gcnt[b] > 0) bmin = min(bmin, srt.start[b]);
 #pragma unroll
               for (int o = 16; o > 0; o >>= 1) bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
