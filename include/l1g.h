@@ -295,10 +295,12 @@ int l1g_gpss_solve_batched(l1g_op* op, int B, const double* Y, const double* rho
  * linear_operator.hpp:45-46): 1 = over the columns where d != 0 only (default; same bits),
  * 0 = dense streaming pass over all of K.  Environment L1G_FWD=dense sets 0 at creation. */
 int l1g_solver_set_forward(l1g_solver* s, int sparse);
-/* projection phase profile accumulated since gp_init (24 doubles): [0..7] SM cycles per
+/* projection phase profile accumulated since gp_init (32 doubles): [0..7] SM cycles per
  * phase, [8] calls, [9] attempts, [10] pivot rounds, [11] candidates, [12] bumps,
- * [13] retries, [14..17] sub-phases of the cluster sort */
-int l1g_solver_proj_profile(l1g_solver* s, double* out24);
+ * [13] retries, [14..17], [21], [22] sub-phases of the cluster sort, [18..19] sparse
+ * forward support columns / calls, [20] prefix epochs, [24..30] sub-phases of the
+ * cluster-wide exact prefix (CTA 0's SM cycles) */
+int l1g_solver_proj_profile(l1g_solver* s, double* out32);
 int l1g_solver_timing(l1g_solver* s, double* proj_ms, double* fwd_ms, double* adj_ms,
                       int64_t* iterations, int64_t* launches, int reset);
 void l1g_solver_destroy(l1g_solver* s);

@@ -2324,11 +2324,11 @@ int l1g_solver_timing(l1g_solver* s, double* proj_ms, double* fwd_ms, double* ad
   return L1G_OK;
 }
 
-int l1g_solver_proj_profile(l1g_solver* s, double* out16) {
+int l1g_solver_proj_profile(l1g_solver* s, double* out32) {
   return guarded([&] {
     DevState h;
     read_state(s, &h);
-    std::memcpy(out16, h.prof, sizeof(h.prof));  // 24 doubles
+    std::memcpy(out32, h.prof, sizeof(h.prof));  // 32 doubles
   });
 }
 

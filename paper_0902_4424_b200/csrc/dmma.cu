@@ -30,6 +30,9 @@ __device__ __forceinline__ void cp16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void cp16s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -228,19 +231,24 @@ __global__ void __launch_bounds__(WT, 1) bfwd_wide_kernel(const BGemmArgs a) {
   const int c_begin = blockIdx.y * a.per_split;
   const int c_end = c_begin + a.per_split < nchunk ? c_begin + a.per_split : nchunk;
   const int nch = c_end > c_begin ? c_end - c_begin : 0;
+  // per-thread copy offsets, fixed across chunks: K chunk tid of 4 row blocks (the 16-byte
+  // chunks of half a tile), V rows tid/16 + 32 i at column pair tid%16
+  const uint32_t s_base = smem_u32(sm);
+  const uint32_t s_k = (uint32_t)kchunk_dst(tid) * 8u;
+  const uint32_t s_v = (uint32_t)(W_KS + (tid >> 4) * W_VP + (tid & 15) * 2) * 8u;
+  const double* g_k = a.K + rb0 * a.ncb * TILE + 2 * tid;
+  const int64_t k_rs = a.ncb * TILE;  // one row block further
+  const double* g_v = a.V + (int64_t)(b0 + (tid >> 4)) * a.vstride + (tid & 15) * 2;
+  const int64_t v_rs = 32 * a.vstride;
   auto load = [&](int c, int st) {
-    double* ks = sm + st * W_STAGE;
-    double* vs = ks + W_KS;
     const int64_t ch = c_begin + c, cb = ch >> 1, half = ch & 1;
-    for (int q = tid; q < 4 * 512; q += WT) {  // 4 row blocks x 512 chunks of 16 bytes
-      const int r = q >> 9, cq = q & 511;
-      cp16(ks + r * (TR * KP) + kchunk_dst(cq),
-           a.K + tile_offset(rb0 + r, cb, a.ncb) + half * (TILE / 2) + 2 * cq);
-    }
-    for (int q = tid; q < BW * 16; q += WT) {
-      const int b = q >> 4, kq = (q & 15) * 2;
-      cp16(vs + b * W_VP + kq, a.V + (int64_t)(b0 + b) * a.vstride + ch * 32 + kq);
-    }
+    const uint32_t so = s_base + (uint32_t)(st * W_STAGE) * 8u;
+    const double* gk = g_k + cb * TILE + half * (TILE / 2);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) cp16s(so + s_k + (uint32_t)(r * TR * KP * 8), gk + r * k_rs);
+    const double* gv = g_v + ch * 32;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cp16s(so + s_v + (uint32_t)(i * 32 * W_VP * 8), gv + i * v_rs);
   };
   double acc[4][4][2];
 #pragma unroll
@@ -297,18 +305,25 @@ __global__ void __launch_bounds__(WT, 1) badj_wide_kernel(const BGemmArgs a) {
   const int r_begin = blockIdx.y * a.per_split;
   const int r_end = r_begin + a.per_split < a.nblocks ? r_begin + a.per_split : a.nblocks;
   const int nch = r_end > r_begin ? r_end - r_begin : 0;
+  // per-thread copy offsets, fixed across chunks: 16-byte chunks tid and tid + 512 of the two
+  // tiles (chunk j + 32 columns has the same swizzle: offset + 32 KP), V rows tid/16 + 32 i
+  const uint32_t s_base = smem_u32(sm);
+  const uint32_t s_k = (uint32_t)kchunk_dst(tid) * 8u;
+  const uint32_t s_v = (uint32_t)(W_KS + (tid >> 4) * W_VP + (tid & 15) * 2) * 8u;
+  const double* g_k = a.K + cb0 * TILE + 2 * tid;
+  const double* g_v = a.V + (int64_t)(b0 + (tid >> 4)) * a.vstride + (tid & 15) * 2;
+  const int64_t v_rs = 32 * a.vstride;
   auto load = [&](int c, int st) {
-    double* ks = sm + st * W_STAGE;
-    double* vs = ks + W_KS;
     const int64_t rb = r_begin + c;
-    for (int q = tid; q < 2 * 1024; q += WT) {  // two tiles of 1024 chunks
-      const int tl = q >> 10, cq = q & 1023;
-      cp16(ks + tl * KT_S + kchunk_dst(cq), a.K + tile_offset(rb, cb0 + tl, a.ncb) + 2 * cq);
-    }
-    for (int q = tid; q < BW * 16; q += WT) {
-      const int b = q >> 4, kq = (q & 15) * 2;
-      cp16(vs + b * W_VP + kq, a.V + (int64_t)(b0 + b) * a.vstride + rb * TR + kq);
-    }
+    const uint32_t so = s_base + (uint32_t)(st * W_STAGE) * 8u;
+    const double* gk = g_k + rb * a.ncb * TILE;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      cp16s(so + s_k + (uint32_t)(((i >> 1) * KT_S + (i & 1) * 32 * KP) * 8),
+            gk + (i >> 1) * TILE + (i & 1) * 1024);
+    const double* gv = g_v + rb * TR;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) cp16s(so + s_v + (uint32_t)(i * 32 * W_VP * 8), gv + i * v_rs);
   };
   double acc[4][4][2];
 #pragma unroll

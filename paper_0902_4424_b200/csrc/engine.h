@@ -69,7 +69,7 @@ struct DevState {
   double x0_l1;
   double h_inf;  // alpha0 projection inf-norm
   // projection phase profile (SM cycles of CTA 0 / event counts), see project.cu
-  double prof[24];
+  double prof[32];
   // batched runs: live-problem counter, decremented when this problem stops (steps.cuh)
   int* nrun;
 };

@@ -130,6 +130,34 @@ struct ScanShared {
   int epochs;  // telemetry: windows scanned by the last call
 };
 
+// The reference's sequential cumulative sum over head[0..H) in place (head is PREFIX_HEAD
+// long, zero past H): one thread, vector loads one batch ahead, each sum in its own register.
+__device__ __forceinline__ void head_sums(double* head, int H) {
+  double2* hp = reinterpret_cast<double2*>(head);
+  double run = 0.0;
+  double2 v[4], w[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) v[u] = hp[u];
+  for (int i0 = 0; i0 < H; i0 += 8) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      w[u] = i0 + 8 < PREFIX_HEAD ? hp[(i0 + 8) / 2 + u] : make_double2(0.0, 0.0);
+    double hs[8];
+    hs[0] = add(run, v[0].x);
+    hs[1] = add(hs[0], v[0].y);
+#pragma unroll
+    for (int u = 1; u < 4; ++u) {
+      hs[2 * u] = add(hs[2 * u - 1], v[u].x);
+      hs[2 * u + 1] = add(hs[2 * u], v[u].y);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) hp[i0 / 2 + u] = make_double2(hs[2 * u], hs[2 * u + 1]);
+    run = hs[7];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = w[u];
+  }
+}
+
 // Exact emulation of the reference's sequential cumulative sum (prox.cpp:44-51) over the
 // sorted candidates c[0..L) (descending, >= 0), fused with its break test.  While the
 // running sum S stays inside one binade [2^e, 2^(e+1)), every fl(S + m) is S plus m rounded
@@ -163,31 +191,7 @@ __device__ long long prefix_break(const double* c, long long Ll, double rho, Sca
   if (warp == 0) {
     for (int i = lane; i < PREFIX_HEAD; i += 32) ss.head[i] = i < H ? c[i] : 0.0;
     __syncwarp();
-    if (lane == 0) {
-      double2* hp = reinterpret_cast<double2*>(ss.head);
-      double run = 0.0;
-      double2 v[4], w[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = hp[u];
-      for (int i0 = 0; i0 < H; i0 += 8) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          w[u] = i0 + 8 < PREFIX_HEAD ? hp[(i0 + 8) / 2 + u] : make_double2(0.0, 0.0);
-        double hs[8];
-        hs[0] = add(run, v[0].x);
-        hs[1] = add(hs[0], v[0].y);
-#pragma unroll
-        for (int u = 1; u < 4; ++u) {
-          hs[2 * u] = add(hs[2 * u - 1], v[u].x);
-          hs[2 * u + 1] = add(hs[2 * u], v[u].y);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) hp[i0 / 2 + u] = make_double2(hs[2 * u], hs[2 * u + 1]);
-        run = hs[7];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = w[u];
-      }
-    }
+    if (lane == 0) head_sums(ss.head, H);
   }
   L1G_HSTAMP(1)
   __syncthreads();

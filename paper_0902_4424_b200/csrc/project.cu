@@ -38,6 +38,9 @@ namespace l1g {
 #ifndef L1G_PROJ_KEEP  // keep x, g in registers between the first and the last pass up to this M
 #define L1G_PROJ_KEEP 2
 #endif
+#ifndef L1G_PROJ_VS_MIN  // v lives in shared memory from this M up (see proj_kernel)
+#define L1G_PROJ_VS_MIN 4
+#endif
 #ifndef L1G_PROJ_WARM
 #define L1G_PROJ_WARM 0
 #endif
@@ -69,8 +72,8 @@ struct ProjArgs {
 };
 
 struct ProjShared {
-  double slot[2][MAX_CS][4];  // cluster reduction slots (double-buffered)
-  long long slotl[2][MAX_CS];
+  double slot[2][MAX_CS][4];  // cluster exchange slots (double-buffered), filled by st.async
+  uint64_t xbar[2];           // their mbarriers (complete_tx of every CTA's values)
   double wv[2][PW][4];         // warp partials (double-buffered)
   long long wl[PW][2];
   double bc[8];
@@ -82,6 +85,10 @@ constexpr int NB = 256;  // key-bit bins of the cluster bucket sort (small M)
 constexpr int NB_LARGE = 1024;  // M >= 16 (C4-class vectors: tens of thousands of candidates)
 constexpr int RANK_MAXBIN = 256;  // largest bin the rank sort takes (else bitonic sorts)
 constexpr int SMALL_RANK = 256;   // single-CTA path: rank sort up to this many candidates
+#ifndef L1G_PREFIX_CLUSTER_MIN  // more candidates than this: the exact prefix runs cluster-wide
+#define L1G_PREFIX_CLUSTER_MIN 8192
+#endif
+constexpr long long PREFIX_CLUSTER_MIN = L1G_PREFIX_CLUSTER_MIN;
 template <int NBv>
 struct SortShared {
   int hist[NBv];    // this CTA's candidates per bin
@@ -107,8 +114,32 @@ __device__ __forceinline__ int swz(int e) {  // bank-conflict-free thread-run la
 // threads run the same sequence of reductions), so no barrier is spent on flipping them, and
 // a buffer is rewritten only after the barrier of the reduction in between.
 struct RedPar {
-  int b, c;  // block (warp partials), cluster (rank slots)
+  int b, c;     // block (warp partials), cluster (rank slots)
+  unsigned ph;  // bit c: phase parity of the exchange mbarrier of slot buffer c
 };
+
+// Cluster exchange: every CTA sends nv doubles into slot[buf][its rank][0..nv) of every CTA
+// with st.async, completing on that CTA's mbarrier xbar[buf]; a CTA proceeds once all cs * nv
+// values have arrived.  One remote-store round trip instead of DSMEM stores + a full
+// cluster barrier (954 vs 1669 cycles at cs = 16, tools/bench_cluster_sync.cu).  A buffer is
+// rewritten two exchanges later, and any CTA's sends for exchange k + 2 follow its receipt of
+// exchange k + 1, which every CTA sends only after reading exchange k: double-buffering is
+// enough.  Returns the buffer holding the values; every CTA must call it in the same order.
+__device__ __forceinline__ int cluster_exchange(const double* vals, int nv, ProjShared& sh,
+                                                cg::cluster_group& cl, int cs, RedPar& rp) {
+  const unsigned rank = cl.block_rank();
+  const int buf = rp.c;
+  if (threadIdx.x == 0) mbar_arrive_expect_tx(&sh.xbar[buf], (uint32_t)(cs * nv * 8));
+  if ((int)threadIdx.x < cs) {
+    const uint32_t ra = mapa_u32(smem_u32(&sh.slot[buf][rank][0]), (int)threadIdx.x);
+    const uint32_t rb = mapa_u32(smem_u32(&sh.xbar[buf]), (int)threadIdx.x);
+    for (int c = 0; c < nv; ++c) st_async_f64(ra + 8u * c, vals[c], rb);
+  }
+  mbar_wait_cluster(&sh.xbar[buf], (rp.ph >> buf) & 1u);
+  rp.ph ^= 1u << buf;
+  rp.c ^= 1;
+  return buf;
+}
 
 // Several block reductions with one barrier.  kinds[c]: 0 = canonical tree over the threads'
 // aligned runs (warp butterfly, then butterfly over the warp index), 1 = max, 2 = plain sum.
@@ -160,29 +191,23 @@ __device__ __forceinline__ long long block_excl_scan(long long v, ProjShared& sh
 }
 
 // Cluster-wide combine of per-CTA values (identical in every thread of a CTA).  kinds[c]:
-// 0 = canonical tree over ranks, 1 = max, 2 = plain sum.  Each CTA pushes its values into
-// every CTA's slots (DSMEM stores ahead of the cluster barrier), then every warp combines the
-// local slots by a butterfly over the rank.  Every CTA must call it in the same order.
+// 0 = canonical tree over ranks, 1 = max, 2 = plain sum.  The values are exchanged into
+// every CTA's slots (cluster_exchange), then every warp combines the local slots by a
+// butterfly over the rank.  Every CTA must call it in the same order.
 __device__ __forceinline__ void cluster_combine(double* vals, const int* kinds, int nv,
                                                 ProjShared& sh, cg::cluster_group& cl, int cs,
                                                 RedPar& rp) {
   if (cs == 1) return;
-  const unsigned rank = cl.block_rank();
-  if ((int)threadIdx.x < cs) {
-    ProjShared* dst = cl.map_shared_rank(&sh, (int)threadIdx.x);
-    for (int c = 0; c < nv; ++c) dst->slot[rp.c][rank][c] = vals[c];
-  }
-  cl.sync();
+  const int buf = cluster_exchange(vals, nv, sh, cl, cs, rp);
   const int lane = threadIdx.x & 31;
   for (int c = 0; c < nv; ++c) {
-    double x = lane < cs ? sh.slot[rp.c][lane][c] : (kinds[c] == 1 ? -1.0 : 0.0);
+    double x = lane < cs ? sh.slot[buf][lane][c] : (kinds[c] == 1 ? -1.0 : 0.0);
     for (int o = 1; o < cs; o <<= 1) {
       const double y = __shfl_xor_sync(0xffffffffu, x, o);
       x = kinds[c] == 1 ? fmax(x, y) : add(x, y);
     }
     vals[c] = __shfl_sync(0xffffffffu, x, 0);
   }
-  rp.c ^= 1;
 }
 
 // descending bitonic sort of n2 (power of two) values by the first min(PT, n2/2) threads
@@ -207,6 +232,311 @@ __device__ void bitonic_desc(P c, int n2) {
       if (nthr == 32) __syncwarp();
       else named_bar_sync(2, nthr);
     }
+  }
+}
+
+// Pairwise tree over a thread's run of M leaves.  With v in shared memory (VS) the run is
+// summed as 8-leaf subtrees pushed into a binary counter, so at most a few partial sums are
+// live (a full unroll would hold all M leaves in registers); the value is the same tree.
+template <int M, bool VS, class F>
+__device__ __forceinline__ double run_tree(const F& leaf) {
+  if constexpr (!VS || M <= 8) {
+    return tree<M>(leaf);
+  } else {
+    Counter<6> c;
+#pragma unroll 1
+    for (int grp = 0; grp < M / 8; ++grp) c.template push_node<3>(tree<8>(leaf, grp * 8), (uint32_t)grp);
+    return c.final_value((uint32_t)(M / 8) << 3);
+  }
+}
+
+// LB coalesced elements j = tid + PT*(i0 + b) of x (and g when `wg`), every load issued before
+// any is used: explicit global loads at a clamped (always valid) index, so the compiler keeps
+// them in flight instead of interleaving them with the shared-memory staging stores.  Kept
+// registers (KEEP) are used instead when the caller holds x and g already.
+template <int LB, bool KEEP, int KM>
+__device__ __forceinline__ void load_batch(double (&xb)[LB], double (&gb)[LB], const double (&xr)[KM],
+                                           const double (&gr)[KM], const double* x, const double* g,
+                                           int i0, int tid, int64_t base, int64_t lim, bool wg) {
+#pragma unroll
+  for (int b = 0; b < LB; ++b) {
+    if (KEEP) {
+      xb[b] = xr[KEEP ? i0 + b : 0];
+      gb[b] = gr[KEEP ? i0 + b : 0];
+    } else {
+      const int64_t j = tid + (int64_t)PT * (i0 + b);
+      const int64_t gj = j < lim ? base + j : 0;
+      xb[b] = __ldcg(x + gj);
+      gb[b] = wg ? __ldcg(g + gj) : 0.0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- cluster-wide exact prefix
+// The sorted-prefix threshold search of prox.cpp:43-52 (see prefix_break in prefix.cuh for
+// the arithmetic) over a candidate list distributed across the cluster: CTA r holds the
+// descending run of global positions [B[r], E_r) in its own shared memory (E_r = B[r + 1],
+// the last CTA's run extends to L), so the sorted candidates are never gathered into one
+// CTA and every epoch's window is scanned by all CTAs that hold part of it.  Per epoch two
+// cluster exchanges replace the block barriers of the one-CTA version: the CTAs' grid-count
+// totals (or, with rounding ties, their parity segments) fix each CTA's exact running count,
+// and the CTAs' first events (failure, binade exit, close call) give the window's first
+// event.  Every CTA returns the same ff and S_{ff-1}.
+__device__ __forceinline__ double cand_at(long long i, const int* B, int cs, double* cand,
+                                          cg::cluster_group& cl) {
+  int r = 0;
+  while (r + 1 < cs && B[r + 1] <= i) ++r;
+  return cl.map_shared_rank(cand, r)[i - B[r]];
+}
+
+__device__ long long prefix_break_cluster(double* cand, const int* B, int cs, long long L,
+                                          double rho, ScanShared& ss, ProjShared& sh,
+                                          cg::cluster_group& cl, RedPar& rp, double* s_before,
+                                          double* pf) {
+  long long t_pf = clock64();
+  auto pmark = [&](int idx) {  // sub-phase cycles into pf[idx] (CTA 0, thread 0 only)
+    if (pf) {
+      const long long t = clock64();
+      pf[idx] += (double)(t - t_pf);
+      t_pf = t;
+    }
+  };
+  constexpr int NW = PT / 32;
+  constexpr long long TWO53 = 1LL << 53;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rank = (int)cl.block_rank();
+  if (L <= 0) {
+    *s_before = 0.0;
+    return 0;
+  }
+  // ---- head (CTA 0): the reference's own sequential adds over the first H positions
+  const int H = L < PREFIX_HEAD ? (int)L : PREFIX_HEAD;
+  {
+    double hv[3] = {-1.0, 0.0, 0.0};  // first failure (or -1), S_{H-1}, S before the failure
+    if (rank == 0) {
+      const double m = tid < H ? cand_at(tid, B, cs, cand, cl) : 0.0;
+      if (tid < PREFIX_HEAD) ss.head[tid] = m;
+      __syncthreads();
+      if (tid == 0) head_sums(ss.head, H);
+      __syncthreads();
+      const bool bad = tid < H && !passes(m, ss.head[tid], rho, tid + 1);
+      const unsigned bb = __ballot_sync(FULL, bad);
+      if (lane == 0) ss.hbad[warp] = bb ? warp * 32 + __ffs(bb) - 1 : INT_MAX;
+      __syncthreads();
+      int ff = INT_MAX;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) ff = min(ff, ss.hbad[w]);
+      hv[0] = ff == INT_MAX ? -1.0 : (double)ff;
+      hv[1] = ss.head[H - 1];
+      hv[2] = ff == INT_MAX ? 0.0 : (ff > 0 ? ss.head[ff - 1] : 0.0);
+    }
+    pmark(24);
+    const int xb = cluster_exchange(hv, 3, sh, cl, cs, rp);
+    const double hf = sh.slot[xb][0][0];
+    pmark(27);
+    if (hf >= 0.0 || H == L) {
+      if (tid == 0) ss.epochs = 0;
+      *s_before = hf >= 0.0 ? sh.slot[xb][0][2] : sh.slot[xb][0][1];
+      return hf >= 0.0 ? (long long)hf : L;
+    }
+    hv[1] = sh.slot[xb][0][1];
+    __syncthreads();  // every thread read the slots before the next exchange
+    double S_prev = hv[1];
+    // ---- epochs
+    const long long Br = B[rank], Er = rank == cs - 1 ? L : B[rank + 1];
+    const double* c = cand - Br;  // c[i] for global positions i in [Br, Er)
+    long long i0 = H, window = 2 * H;
+    int par = 0, nep = 0;
+    while (i0 < L) {
+      ++nep;
+      if (!(S_prev >= 0x1.0p-960)) {  // (sub)tiny running sum: one scalar step, uniform
+        const double ci = cand_at(i0, B, cs, cand, cl);
+        const double S = add(S_prev, ci);
+        if (!passes(ci, S, rho, i0 + 1)) {
+          *s_before = S_prev;
+          if (tid == 0) ss.epochs = nep;
+          return i0;
+        }
+        S_prev = S;
+        ++i0;
+        continue;
+      }
+      const long long n = (L - i0) < window ? (L - i0) : window;
+      const long long wend = i0 + n;
+      const long long lo = i0 > Br ? i0 : Br, hi = wend < Er ? wend : Er;
+      const long long len = hi > lo ? hi - lo : 0;
+      const long long E = (len + PT - 1) / PT;
+      const long long p0 = lo + tid * E < hi ? lo + tid * E : hi;
+      const long long p1 = p0 + E < hi ? p0 + E : hi;
+      const long long sbits = __double_as_longlong(S_prev);
+      const int be = (int)(sbits >> 52);
+      const long long base_q = (sbits & ((1LL << 52) - 1)) | (1LL << 52);
+      // pass 1: this thread's grid counts; CTA totals (or parity segments with ties)
+      long long qs = 0;
+      bool anytie = false;
+      for (long long i = p0; i < p1; ++i) {
+        bool t;
+        qs += grid_count(c[i], be, &t);
+        anytie |= t;
+      }
+      const unsigned tball = __ballot_sync(FULL, anytie);
+      long long qinc = qs;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(FULL, qinc, o);
+        if (lane >= o) qinc += y;
+      }
+      if (lane == 31) {
+        ss.fq[par][warp] = qinc;
+        ss.ftie[par][warp] = tball != 0;
+      }
+      __syncthreads();
+      pmark(25);
+      long long wex = 0, tot = 0;
+      int ties = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const long long d = ss.fq[par][w];
+        wex += w < warp ? d : 0;
+        tot += d;
+        ties |= ss.ftie[par][w];
+      }
+      ParSeg cta = seg_elem(tot, false), incl = seg_id();  // the CTA's run; this thread's (ties)
+      if (ties) {  // uniform over the CTA
+        ParSeg me = seg_id();
+        for (long long i = p0; i < p1; ++i) {
+          bool t;
+          const long long q = grid_count(c[i], be, &t);
+          me = seg_then(me, seg_elem(q, t));
+        }
+        incl = seg_warp_scan(me, lane);
+        if (lane == 31) {
+          ss.wd0[par][warp] = incl.d0;
+          ss.wpk[par][warp] = seg_pack(incl);
+        }
+        __syncthreads();
+        cta = seg_id();
+#pragma unroll
+        for (int w = 0; w < NW; ++w) cta = seg_then(cta, seg_unpack(ss.wd0[par][w], ss.wpk[par][w]));
+      }
+      pmark(26);
+      // exchange 1: the CTAs' segments -> this CTA's exact starting count and the window's end
+      double xs[2] = {__longlong_as_double(cta.d0), (double)seg_pack(cta)};
+      const int x1 = cluster_exchange(xs, 2, sh, cl, cs, rp);
+      pmark(27);
+      long long Nr = base_q, Nend = base_q;
+      for (int r = 0; r < cs; ++r) {
+        const ParSeg sr = seg_unpack(__double_as_longlong(sh.slot[x1][r][0]), (int)sh.slot[x1][r][1]);
+        Nr = r == rank ? Nend : Nr;
+        Nend = seg_apply(sr, Nend);
+      }
+      long long N;
+      if (ties) {  // the warps' starts, then the lanes' within the warp
+        long long Nw = Nr;
+        long long acc = Nr;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const ParSeg sw = seg_unpack(ss.wd0[par][w], ss.wpk[par][w]);
+          Nw = w == warp ? acc : Nw;
+          acc = seg_apply(sw, acc);
+        }
+        ParSeg ex = seg_shfl_up(incl, 1);
+        if (lane == 0) ex = seg_id();
+        N = seg_apply(ex, Nw);
+      } else {
+        N = Nr + wex + (qinc - qs);
+      }
+      // pass 2: exact sums and tests; this thread's first event
+      int my_ev = INT_MAX, kind = 0;
+      long long my_n = 0;
+      double kd = (double)(p0 + 1);
+      for (long long i = p0; i < p1; ++i) {
+        const double m = c[i];
+        bool tie;
+        const long long q = grid_count(m, be, &tie);
+        const long long Nn = N + q + (tie ? ((N + q) & 1) : 0);
+        const int stt = Nn >= TWO53 ? 2 : quick_test(m, from_grid(Nn, be), rho, kd);
+        const bool take = stt != 0 && my_ev == INT_MAX;
+        my_ev = take ? (int)i : my_ev;
+        kind = take ? stt : kind;
+        my_n = take ? N : my_n;
+        N = Nn;
+        kd = add(kd, 1.0);
+      }
+      const unsigned have = __ballot_sync(FULL, my_ev != INT_MAX);
+      if (have) {
+        if (lane == __ffs(have) - 1) {
+          ss.epos[par][warp] = my_ev;
+          ss.ekind[par][warp] = kind;
+          ss.en[par][warp] = my_n;
+        }
+      } else if (lane == 0) {
+        ss.epos[par][warp] = INT_MAX;
+      }
+      __syncthreads();
+      int ew = -1;
+#pragma unroll
+      for (int w = NW - 1; w >= 0; --w) ew = ss.epos[par][w] != INT_MAX ? w : ew;
+      pmark(28);
+      // exchange 2: the CTAs' first events -> the window's first event
+      double xe[4] = {-1.0, 0.0, 0.0, 0.0};
+      if (ew >= 0) {
+        const int ev = ss.epos[par][ew];
+        xe[0] = (double)ev;
+        xe[1] = (double)ss.ekind[par][ew];
+        xe[2] = __longlong_as_double(ss.en[par][ew]);
+        xe[3] = c[ev];
+      }
+      const int x2 = cluster_exchange(xe, 4, sh, cl, cs, rp);
+      pmark(29);
+      int er = -1;
+      for (int r = cs - 1; r >= 0; --r) er = sh.slot[x2][r][0] >= 0.0 ? r : er;  // lowest rank
+      par ^= 1;
+      if (er < 0) {  // the whole window is exact and passes: the epoch continues
+        S_prev = from_grid(Nend, be);
+        i0 = wend;
+        window *= 2;
+        __syncthreads();  // slots read before the next exchange
+        continue;
+      }
+      const long long ev = (long long)sh.slot[x2][er][0];
+      const int evk = (int)sh.slot[x2][er][1];
+      const long long nb = __double_as_longlong(sh.slot[x2][er][2]);
+      const double cev = sh.slot[x2][er][3];
+      __syncthreads();  // slots read before the next exchange
+      const double sb = from_grid(nb, be);  // S_{ev-1}
+      if (evk == 1) {
+        *s_before = sb;
+        if (tid == 0) ss.epochs = nep;
+        return ev;
+      }
+      if (evk == 3) {  // exact test with the division; on success the epoch goes on
+        bool t;
+        const long long qe = grid_count(cev, be, &t);
+        const double Se = from_grid(nb + qe + (t ? ((nb + qe) & 1) : 0), be);
+        if (!passes(cev, Se, rho, ev + 1)) {
+          *s_before = sb;
+          if (tid == 0) ss.epochs = nep;
+          return ev;
+        }
+        S_prev = Se;
+        i0 = ev + 1;
+        continue;
+      }
+      const double S = add(sb, cev);  // the binade exit: one IEEE addition
+      if (!passes(cev, S, rho, ev + 1)) {
+        *s_before = sb;
+        if (tid == 0) ss.epochs = nep;
+        return ev;
+      }
+      window = ((2 * (ev + 1) + 31) >> 5) << 5;
+      S_prev = S;
+      i0 = ev + 1;
+    }
+    *s_before = S_prev;
+    if (tid == 0) ss.epochs = nep;
+    return L;
   }
 }
 
@@ -239,7 +569,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   const int64_t pofs = prob * a.bstride;
   DevState* st = a.st + prob;
   const int tid = threadIdx.x;
-  RedPar rp{0, 0};
+  RedPar rp{0, 0, 0u};
   const bool prof = (a.mode == PROJ_ITER) && rank == 0 && tid == 0;
   long long t_last = clock64();
   auto mark = [&](int idx) {
@@ -257,6 +587,11 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sst);
     for (int i = tid; i < (int)(sizeof(DevState) / 8); i += PT) dst[i] = src[i];
+  }
+  if (tid == 0) {
+    mbar_init(&sh.xbar[0], 1);
+    mbar_init(&sh.xbar[1], 1);
+    fence_barrier_init();  // visible cluster-wide before the first cluster barrier
   }
   __syncthreads();
   if (a.mode == PROJ_ITER && sst.status != RUNNING) return;  // uniform over the cluster
@@ -351,9 +686,21 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   double first_stat = 0.0;
   count(8, 1.0);
   mark(0);
-  double v[M];
+  // v = x - alpha g: in registers (thread-run order) for small M; in shared memory for
+  // M >= 16, where 2M registers for v would leave too few for the rest and spill
+  constexpr bool VS = M >= L1G_PROJ_VS_MIN;
+  constexpr int UK = VS ? 4 : M;  // unroll of the passes over v (register arrays need all M)
+  double vr[VS ? 1 : M] = {};
+  double* const cand = dyn + (VS ? LS : 0);  // candidate buffer (sort, gather, prefix)
+  auto VG = [&](int k) -> double { return VS ? dyn[swz<M>(tid * M + k)] : vr[VS ? 0 : k]; };
+  auto VSET = [&](int k, double val) {
+    if (VS) dyn[swz<M>(tid * M + k)] = val;
+    else vr[VS ? 0 : k] = val;
+  };
   // x and g in the coalesced order (j = tid + PT*i), kept for the final pass when small
   constexpr bool KEEP = M <= L1G_PROJ_KEEP;
+  constexpr int LB = M < 8 ? M : 8;  // loads in flight per vector and thread
+  constexpr int UB = VS ? 1 : M / LB;  // batches of coalesced loads (VS: one batch's addresses live)
   double xr[KEEP ? M : 1], gr[KEEP ? M : 1];
   if (KEEP) {
 #pragma unroll
@@ -367,31 +714,36 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   for (int attempt = 0;; ++attempt) {
     count(9, 1.0);
     // ---- v = x - alpha g  (gpss.cpp:167; alpha0: x0 - grad, gpss.cpp:95): coalesced
-    //      loads, staged through shared memory into per-thread registers
+    //      loads (issued in batches of LB per vector, all in flight before the first use),
+    //      staged through shared memory into per-thread registers
+#pragma unroll UB
+    for (int i0 = 0; i0 < M; i0 += LB) {
+      double xb[LB], gb[LB];
+      load_batch<LB, KEEP>(xb, gb, xr, gr, x, g, i0, tid, base, lim, a.mode != PROJ_PLAIN);
 #pragma unroll
-    for (int i = 0; i < M; ++i) {
-      const int64_t j = tid + (int64_t)PT * i;
-      double val = 0.0;
-      if (j < lim) {
-        const int64_t gj = base + j;
-        const double xv = KEEP ? xr[KEEP ? i : 0] : x[gj];
-        const double gv = KEEP ? gr[KEEP ? i : 0] : (a.mode != PROJ_PLAIN ? g[gj] : 0.0);
-        if (a.mode == PROJ_PLAIN) val = xv;
-        else if (a.mode == PROJ_ALPHA0) val = sub(xv, gv);
-        else val = sub(xv, mul(alpha, gv));
+      for (int b = 0; b < LB; ++b) {
+        const int64_t j = tid + (int64_t)PT * (i0 + b);
+        double val = 0.0;
+        if (j < lim) {
+          if (a.mode == PROJ_PLAIN) val = xb[b];
+          else if (a.mode == PROJ_ALPHA0) val = sub(xb[b], gb[b]);
+          else val = sub(xb[b], mul(alpha, gb[b]));
+        }
+        dyn[swz<M>((int)j)] = val;
       }
-      dyn[swz<M>((int)j)] = val;
     }
     __syncthreads();
+    if (!VS) {
 #pragma unroll
-    for (int k = 0; k < M; ++k) v[k] = dyn[swz<M>(tid * M + k)];
+      for (int k = 0; k < M; ++k) VSET(k, dyn[swz<M>(tid * M + k)]);
+    }
     __syncthreads();
     double red[2];
     {
-      const double t = tree<M>([&](int k) { return fabs(v[k]); });
+      const double t = run_tree<M, VS>([&](int k) { return fabs(VG(k)); });
       double m = 0.0;
-#pragma unroll
-      for (int k = 0; k < M; ++k) m = fmax(m, fabs(v[k]));
+#pragma unroll UK
+      for (int k = 0; k < M; ++k) m = fmax(m, fabs(VG(k)));
       red[0] = t;
       red[1] = m;
       const int kinds[2] = {0, 1};
@@ -424,9 +776,9 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       const int kinds_cs[2] = {2, 2};
       for (int it = 0; it < 64; ++it) {
         double v2[2] = {0.0, 0.0};
-#pragma unroll
+#pragma unroll UK
         for (int k = 0; k < M; ++k) {
-          const double m = fabs(v[k]);
+          const double m = fabs(VG(k));
           if (m > th) {
             v2[0] += 1.0;
             v2[1] += m;
@@ -459,9 +811,9 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       for (int tries = 0;; ++tries) {
         long long myc = 0;
         double mynext = -1.0;
-#pragma unroll
+#pragma unroll UK
         for (int k = 0; k < M; ++k) {
-          const double m = fabs(v[k]);
+          const double m = fabs(VG(k));
           if (m > lo) ++myc;
           else mynext = fmax(mynext, m);
         }
@@ -474,24 +826,19 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         long long before = 0, total = ctot;
         double next = bnext;
         if (cs > 1) {  // counts and the next value below the bracket, pushed to every CTA
-          if (tid < cs) {
-            ProjShared* dst = cl.map_shared_rank(&sh, tid);
-            dst->slotl[rp.c][rank] = ctot;
-            dst->slot[rp.c][rank][0] = bnext;
-          }
-          cl.sync();
+          const double xv[2] = {(double)ctot, bnext};  // counts < 2^53: exact
+          const int xb = cluster_exchange(xv, 2, sh, cl, cs, rp);
           long long b = 0, tt = 0;
           double nx = -1.0;
           for (int r = 0; r < cs; ++r) {
-            const long long cr = sh.slotl[rp.c][r];
+            const long long cr = (long long)sh.slot[xb][r][0];
             b += r < (int)rank ? cr : 0;
             tt += cr;
-            nx = fmax(nx, sh.slot[rp.c][r][0]);
+            nx = fmax(nx, sh.slot[xb][r][1]);
           }
           before = b;
           total = tt;
           next = nx;
-          rp.c ^= 1;
         }
         const long long L = total + (next >= 0.0 ? 1 : 0);
         mark(14);
@@ -512,12 +859,13 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           }
           __syncthreads();
           const int shft = srt.shift;
-#pragma unroll
+#pragma unroll UK
           for (int k = 0; k < M; ++k) {
-            const double m = fabs(v[k]);
+            const double m = fabs(VG(k));
             if (m > lo) atomicAdd(&srt.hist[(int)((__double_as_longlong(m) - kmin) >> shft)], 1);
           }
           cl.sync();
+          mark(21);
           for (int t = tid; t < NBK; t += PT) {
             int h[MAX_CS];
 #pragma unroll
@@ -533,6 +881,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
             srt.myoff[t] = mine;
           }
           __syncthreads();
+          mark(22);
           if (tid < 32) {  // descending exclusive scan over bins, destination CTAs
             const int lane = tid;
             int carry = 0, mx = 0;
@@ -585,29 +934,29 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           __syncthreads();
           mark(15);
           if (srt.ok) {
-#pragma unroll
+#pragma unroll UK
             for (int k = 0; k < M; ++k) {
-              const double m = fabs(v[k]);
+              const double m = fabs(VG(k));
               if (m > lo) {
                 const int b = (int)((__double_as_longlong(m) - kmin) >> shft);
                 const int d = srt.dest[b];
                 const int pos = srt.start[b] + srt.myoff[b] + atomicAdd(&srt.cursor[b], 1) - srt.base[d];
-                cl.map_shared_rank(dyn, d)[pos] = m;
+                cl.map_shared_rank(cand, d)[pos] = m;
               }
             }
           }
           cl.sync();
           mark(16);
           if (srt.ok) {
+            // each CTA sorts its own range of global positions [base[r], base[r + 1]) in place;
+            // the exact prefix then runs over the distributed ranges (prefix_break_cluster)
             const int cnt = srt.base[rank + 1] - srt.base[rank];
-            const bool gather_smem = total + 1 <= a.cand_cap;
             constexpr int RK = M >= 16 ? 8 : 2;  // candidates per thread on the rank path
             int maxcnt = 0;  // the path must be the same in every CTA (cluster barriers)
             for (int d = 0; d < cs; ++d) maxcnt = max(maxcnt, srt.base[d + 1] - srt.base[d]);
             if (maxcnt <= RK * PT && srt.maxbin <= RANK_MAXBIN) {
               // rank sort: bins are narrow, so an element's place is its bin's start plus the
-              // number of larger bin mates (equal ones ordered by position); each element is
-              // written straight to its final place in CTA 0 (or the global scratch)
+              // number of larger bin mates (equal ones ordered by position)
               const int b0 = srt.base[rank];
               double mv[RK];
               int pos[RK];
@@ -617,72 +966,68 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
                 pos[k] = -1;
                 mv[k] = 0.0;
                 if (i < cnt) {
-                  const double m = dyn[i];
+                  const double m = cand[i];
                   const int b = (int)((__double_as_longlong(m) - kmin) >> shft);
                   const int s0 = srt.start[b] - b0, s1 = s0 + srt.gcnt[b];
                   int r = 0;
                   for (int j = s0; j < s1; ++j) {
-                    const double y = dyn[j];
+                    const double y = cand[j];
                     r += (y > m) | ((y == m) & (j < i));
                   }
                   mv[k] = m;
-                  pos[k] = srt.start[b] + r;
+                  pos[k] = srt.start[b] + r - b0;
                 }
               }
-              __syncthreads();  // CTA 0 overwrites its own unsorted range
+              __syncthreads();  // the range is rewritten in place
               mark(17);
-              double* dst = gather_smem ? cl.map_shared_rank(dyn, 0) : gcand;
 #pragma unroll
               for (int k = 0; k < RK; ++k)
-                if (pos[k] >= 0) dst[pos[k]] = mv[k];
-              if (!gather_smem) __threadfence();
+                if (pos[k] >= 0) cand[pos[k]] = mv[k];
             } else {
               int m2 = 1;
               while (m2 < cnt) m2 <<= 1;
-              for (int i = cnt + tid; i < m2; i += PT) dyn[i] = 0.0;
+              for (int i = cnt + tid; i < m2; i += PT) cand[i] = 0.0;
               __syncthreads();
-              if (cnt > 1) bitonic_desc(dyn, m2);
-              __syncthreads();
-              cl.sync();  // every range sorted before CTA 0's buffer receives the others
+              if (cnt > 1) bitonic_desc(cand, m2);
               mark(17);
-              if (gather_smem) {
-                if (rank != 0) {
-                  double* dst = cl.map_shared_rank(dyn, 0) + srt.base[rank];
-                  for (int i = tid; i < cnt; i += PT) dst[i] = dyn[i];
-                }
-              } else {
-                double* dst = gcand + srt.base[rank];
-                for (int i = tid; i < cnt; i += PT) dst[i] = dyn[i];
-                __threadfence();
-              }
             }
-            cl.sync();
-            mark(3);
+            __syncthreads();
+            long long ff;
+            double s_before = 0.0;
             count(11, (double)total);
-            if (rank == 0) {
-              double* const c = gather_smem ? dyn : gcand;
-              if (tid == 0 && next >= 0.0) c[total] = next;
-              if (!gather_smem) __threadfence_block();
-              __syncthreads();
-              mark(4);
-              double s_before = 0.0;
-              const long long ff = prefix_break(c, L, rho, scan_sh, &s_before);
-              count(20, (double)scan_sh.epochs);
-              if (tid == 0) {
-                sh.bc[4] = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
-                sh.dec = (ff == L && next >= 0.0) ? 1 : 0;
+            if (total > PREFIX_CLUSTER_MIN) {
+              // the largest element below the bracket closes the list (position `total`)
+              if (rank == (unsigned)(cs - 1) && tid == 0 && next >= 0.0) cand[cnt] = next;
+              cl.sync();  // every range final before other CTAs read it
+              mark(3);
+              ff = prefix_break_cluster(cand, srt.base, cs, L, rho, scan_sh, sh, cl, rp,
+                                        &s_before, prof ? sst.prof : nullptr);
+            } else {
+              // few candidates: the per-epoch cluster exchanges would cost more than they
+              // save; the ranges are gathered into CTA 0, which scans them alone
+              cl.sync();  // every range sorted
+              if (rank != 0) {
+                double* dst = cl.map_shared_rank(cand, 0) + srt.base[rank];
+                for (int i = tid; i < cnt; i += PT) dst[i] = cand[i];
               }
-              mark(5);
-              __syncthreads();
-              if (tid > 0 && tid < cs) {  // push theta and the decision to the other CTAs
-                ProjShared* dst = cl.map_shared_rank(&sh, tid);
-                dst->bc[4] = sh.bc[4];
-                dst->dec = sh.dec;
+              if (rank == (unsigned)(cs - 1) && tid == 0 && next >= 0.0)
+                cl.map_shared_rank(cand, 0)[total] = next;
+              cl.sync();
+              mark(3);
+              double res[2] = {0.0, 0.0};
+              if (rank == 0) {
+                res[0] = (double)prefix_break(cand, L, rho, scan_sh, &res[1]);
               }
+              const int xb = cluster_exchange(res, 2, sh, cl, cs, rp);
+              ff = (long long)sh.slot[xb][0][0];
+              s_before = sh.slot[xb][0][1];
             }
-            cl.sync();
-            if (!sh.dec) {
-              theta = sh.bc[4];
+            count(20, (double)scan_sh.epochs);
+            mark(5);
+            // theta = candidate of the last passing index (prox.cpp:47-50); 0 if none passed.
+            // All passed although smaller elements exist: the bracket was too high.
+            if (!(ff == L && next >= 0.0)) {
+              theta = ff > 0 ? dvd(sub(s_before, rho), (double)ff) : 0.0;
               break;
             }
             count(13, 1.0);
@@ -694,11 +1039,11 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         int64_t n2 = 1;
         while (n2 < total) n2 <<= 1;
         const bool in_smem = (n2 + 1 <= a.cand_cap);
-        double* cbuf = in_smem ? cl.map_shared_rank(dyn, 0) : gcand;
+        double* cbuf = in_smem ? cl.map_shared_rank(cand, 0) : gcand;
         long long pos = before + off;
-#pragma unroll
+#pragma unroll UK
         for (int k = 0; k < M; ++k) {
-          const double m = fabs(v[k]);
+          const double m = fabs(VG(k));
           if (m > lo) cbuf[pos++] = m;
         }
         if (!in_smem) __threadfence();
@@ -706,7 +1051,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         mark(3);
         count(11, (double)total);
         if (rank == 0) {
-          double* c = in_smem ? dyn : gcand;
+          double* c = in_smem ? cand : gcand;
           if (total <= SMALL_RANK) {
             // few candidates: each one's place is the number of larger ones (equal ones by
             // position), one thread per candidate, every read a shared-memory broadcast
@@ -763,7 +1108,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       int guard = 0;
       for (;;) {
         const double thc = theta;
-        double l1u[1] = {tree<M>([&](int k) { return fabs(soft(v[k], thc)); })};
+        double l1u[1] = {run_tree<M, VS>([&](int k) { return fabs(soft(VG(k), thc)); })};
         block_reduce<1>(l1u, k_sum, sh, rp);
         cluster_combine(l1u, k_sum, 1, sh, cl, cs, rp);
         if (!(l1u[0] > rho && guard++ < 64)) break;
@@ -778,46 +1123,54 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     const double th = theta;
     double hmax = 0.0;
     long long sup = 0;
-#pragma unroll
+#pragma unroll UK
     for (int k = 0; k < M; ++k) {
-      const double h = branch == 0 ? 0.0 : (branch == 1 ? v[k] : soft(v[k], th));
-      v[k] = h;  // v holds h from here on (an escalation recomputes v)
+      const double h = branch == 0 ? 0.0 : (branch == 1 ? VG(k) : soft(VG(k), th));
+      VSET(k, h);  // v holds h from here on (an escalation recomputes v)
       sup += (h != 0.0);
       hmax = fmax(hmax, fabs(h));
     }
     double gdl = 0.0, lmax = 0.0;
     if (a.mode != PROJ_ALPHA0) {
       // stage h, then coalesced d = h - x (written out) and leaf g_j d_j
+      if (!VS) {
 #pragma unroll
-      for (int k = 0; k < M; ++k) dyn[swz<M>(tid * M + k)] = v[k];
+        for (int k = 0; k < M; ++k) dyn[swz<M>(tid * M + k)] = VG(k);
+      }
       __syncthreads();
+#pragma unroll UB
+      for (int i0 = 0; i0 < M; i0 += LB) {
+        double xb[LB], gb[LB];
+        load_batch<LB, KEEP>(xb, gb, xr, gr, x, g, i0, tid, base, lim, a.mode == PROJ_ITER);
 #pragma unroll
-      for (int i = 0; i < M; ++i) {
-        const int64_t j = tid + (int64_t)PT * i;
-        const int p = swz<M>((int)j);
-        const double h = dyn[p];
-        double leaf = 0.0;
-        bool nz = false;
-        if (j < lim) {
-          const int64_t gj = base + j;
-          const double xv = KEEP ? xr[KEEP ? i : 0] : x[gj];
-          const double dj = a.mode == PROJ_PLAIN ? h : sub(h, xv);
-          lmax = fmax(lmax, fabs(dj));
-          dout[gj] = dj;
-          if (a.mode == PROJ_ITER) leaf = mul(KEEP ? gr[KEEP ? i : 0] : g[gj], dj);
-          nz = dj != 0.0;
+        for (int b = 0; b < LB; ++b) {
+          const int64_t j = tid + (int64_t)PT * (i0 + b);
+          const int p = swz<M>((int)j);
+          const double h = dyn[p];
+          double leaf = 0.0;
+          bool nz = false;
+          if (j < lim) {
+            const int64_t gj = base + j;
+            const double dj = a.mode == PROJ_PLAIN ? h : sub(h, xb[b]);
+            lmax = fmax(lmax, fabs(dj));
+            dout[gj] = dj;
+            if (a.mode == PROJ_ITER) leaf = mul(gb[b], dj);
+            nz = dj != 0.0;
+          }
+          dyn[p] = leaf;
+          // support bitmap of d for the sparse forward product (whole warps are in or out)
+          const unsigned bits = __ballot_sync(0xffffffffu, nz);
+          if (a.mode == PROJ_ITER && (tid & 31) == 0 && j < lim)
+            a.vb.dmask[(pofs + base + j) >> 5] = bits;
         }
-        dyn[p] = leaf;
-        // support bitmap of d for the sparse forward product (whole warps are in or out)
-        const unsigned bits = __ballot_sync(0xffffffffu, nz);
-        if (a.mode == PROJ_ITER && (tid & 31) == 0 && j < lim)
-          a.vb.dmask[(pofs + base + j) >> 5] = bits;
       }
       __syncthreads();
       if (a.mode == PROJ_ITER) {
+        if (!VS) {
 #pragma unroll
-        for (int k = 0; k < M; ++k) v[k] = dyn[swz<M>(tid * M + k)];
-        gdl = tree<M>([&](int k) { return v[k]; });
+          for (int k = 0; k < M; ++k) VSET(k, dyn[swz<M>(tid * M + k)]);
+        }
+        gdl = run_tree<M, VS>([&](int k) { return VG(k); });
       }
     }
     double red2[4] = {gdl, lmax, hmax, (double)sup};
@@ -876,7 +1229,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     break;
   }
   if (prof)
-    for (int i = 0; i < 24; ++i) st->prof[i] = sst.prof[i];
+    for (int i = 0; i < 32; ++i) st->prof[i] = sst.prof[i];
   L1G_TL_STAMP(a.mode == PROJ_ITER && blockIdx.x == 0 && tid == 0, g_tl_proj, 14, sst.k)
   cl.sync();
 }
@@ -886,6 +1239,23 @@ static int64_t pow2_at_least(int64_t v) {
   int64_t n = 1;
   while (n < v) n <<= 1;
   return n;
+}
+
+// Dynamic shared memory: [candidates] when v is in registers; [v (LS) | candidates] when v
+// lives in shared memory (M >= L1G_PROJ_VS_MIN, see proj_kernel), with at most vs_cand(M)
+// candidates beside v (the 1024 key bins of M >= 16 take 24 KB more static memory).
+static constexpr int64_t vs_cand(int M) { return M >= 16 ? 8192 : SMEM_CAND; }
+static constexpr size_t proj_dyn_bytes(int M) {
+  return M >= L1G_PROJ_VS_MIN ? (size_t)(PT * M + vs_cand(M) + 1) * 8 : (size_t)(SMEM_CAND + 1) * 8;
+}
+static void set_proj_smem(ProjPlan& pp) {
+  const int M = (int)(pp.ls / PT);
+  if (M >= L1G_PROJ_VS_MIN) {
+    if (pp.cand_cap > vs_cand(M) + 1) pp.cand_cap = vs_cand(M) + 1;
+    pp.smem = (size_t)(pp.ls + pp.cand_cap) * 8;
+  } else {
+    pp.smem = (size_t)pp.cand_cap * 8;
+  }
 }
 
 ProjPlan make_proj_plan(int64_t p_pad) {
@@ -906,7 +1276,7 @@ ProjPlan make_proj_plan(int64_t p_pad) {
   pp.cs = cs;
   pp.ls = PT * m;
   pp.cand_cap = (pp.ls > SMEM_CAND ? pp.ls : SMEM_CAND) + 1;
-  pp.smem = (size_t)pp.cand_cap * 8;
+  set_proj_smem(pp);
   return pp;
 }
 
@@ -919,7 +1289,7 @@ static void proj_launch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s, i
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, [] {
     L1G_CUDA(cudaFuncSetAttribute(proj_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)((SMEM_CAND + 1) * 8)));
+                                  (int)proj_dyn_bytes(M)));
     L1G_CUDA(cudaFuncSetAttribute(proj_kernel<M>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   });
   cudaLaunchConfig_t cfg = {};
@@ -987,7 +1357,7 @@ ProjPlan make_proj_plan_single(int64_t p_pad, int cs) {
   pp.ls = PT * m;
   pp.cand_cap = (pp.ls > SMEM_CAND ? pp.ls : SMEM_CAND) + 1;
   if (cs == 1) pp.cand_cap = pp.ls + 1;
-  pp.smem = (size_t)pp.cand_cap * 8;
+  set_proj_smem(pp);
   return pp;
 }
 

@@ -77,6 +77,7 @@ def main():
     ap.add_argument("--profile", action="store_true", help="print projection phase profile")
     ap.add_argument("--timing", action="store_true", help="per-kernel CUDA-event timing")
     ap.add_argument("--trace", action="store_true", help="print per-iteration support sizes")
+    ap.add_argument("--clock-ghz", type=float, default=1.965)
     ap.add_argument("--timeline", action="store_true",
                     help="in-graph kernel start times per iteration (libl1g_tl.so)")
     a = ap.parse_args()
@@ -124,9 +125,24 @@ def main():
               f"adj {ta.value/it:.4f}  GB/s fwd {kb/(tf.value/it)/1e6:.0f} "
               f"adj {kb/(ta.value/it)/1e6:.0f}  ({it} iterations, {tl.value} launches)")
     if a.profile and hasattr(lib, "l1g_solver_proj_profile"):
-        out = (C.c_double * 24)()
+        out = (C.c_double * 32)()
         lib.l1g_solver_proj_profile(h, out)
         print("proj profile:", [round(v, 3) for v in out])
+        calls = max(out[8], 1.0)
+        names = {0: "steplength", 1: "v + |v|_1", 2: "michelot", 14: "count", 21: "hist atomics",
+                 22: "hist gather", 15: "bins/bases", 16: "scatter", 17: "rank sort",
+                 3: "gather", 4: "next", 5: "exact prefix", 6: "feasibility", 7: "h/d/g'd"}
+        ghz = a.clock_ghz
+        print("proj phases (us per call, CTA 0 clock at %.3f GHz): " % ghz + "  ".join(
+            f"{nm} {out[i] / calls / ghz / 1e3:.2f}" for i, nm in names.items()) +
+            f"  | total {sum(out[i] for i in names) / calls / ghz / 1e3:.2f}; michelot rounds "
+            f"{out[10] / calls:.2f}, candidates {out[11] / calls:.0f}, bumps {out[12] / calls:.2f},"
+            f" retries {out[13] / calls:.2f}, prefix epochs {out[20] / calls:.2f}")
+        pn = {24: "head", 25: "pass1", 26: "tie segs", 27: "exchanges 1", 28: "pass2+events",
+              29: "exchanges 2"}
+        if any(out[i] for i in pn):
+            print("cluster prefix (us per call): " + "  ".join(
+                f"{nm} {out[i] / calls / ghz / 1e3:.2f}" for i, nm in pn.items()))
         if out[19] > 0:
             cols = out[18] / out[19]
             print(f"sparse forward: {cols:.1f} support columns per call "
