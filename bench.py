@@ -586,7 +586,7 @@ def run_b200(args, world, rank, local, pg):
                 "allgather_xg_packet_ms": round(max_over_ranks(pg, xg.value), 5),
                 "share_of_iteration": round((xk.value + xg.value) /
                                             (dev_ms / max(done_iters, 1)), 4)}
-    prof = (C.c_double * 24)()
+    prof = (C.c_double * 32)()
     lib.l1g_solver_proj_profile(h, prof)
     sp_cols = prof[18] / prof[19] if prof[19] > 0 else None
 

@@ -292,13 +292,18 @@ int l1g_gpss_solve_batched(l1g_op* op, int B, const double* Y, const double* rho
                            const l1g_gp_config* cfg, const l1g_stop_rule* stop, double* X_out,
                            l1g_result* results);
 /* forward product of the iteration (gpss.cpp:194, DenseOperator::do_apply,
- * linear_operator.hpp:45-46): 1 = over the columns where d != 0 only (default; same bits),
- * 0 = dense streaming pass over all of K.  Environment L1G_FWD=dense sets 0 at creation. */
+ * linear_operator.hpp:45-46), all modes giving the same bits:
+ *   1 = over the columns where d != 0 only, switching on the device to the dense stream
+ *       when d has at least L1G_FWD_DENSE_FRAC (default 0.8) * p nonzeros (default);
+ *   2 = over the columns where d != 0 only, never switching;
+ *   0 = dense streaming pass over all of K.
+ * Environment L1G_FWD=dense / L1G_FWD=sparse set 0 / 2 at creation. */
 int l1g_solver_set_forward(l1g_solver* s, int sparse);
 /* projection phase profile accumulated since gp_init (32 doubles): [0..7] SM cycles per
  * phase, [8] calls, [9] attempts, [10] pivot rounds, [11] candidates, [12] bumps,
  * [13] retries, [14..17], [21], [22] sub-phases of the cluster sort, [18..19] sparse
- * forward support columns / calls, [20] prefix epochs, [24..30] sub-phases of the
+ * forward support columns / calls, [20] prefix epochs, [23] forward products the density
+ * switch ran as the dense stream, [24..30] sub-phases of the
  * cluster-wide exact prefix (CTA 0's SM cycles) */
 int l1g_solver_proj_profile(l1g_solver* s, double* out32);
 int l1g_solver_timing(l1g_solver* s, double* proj_ms, double* fwd_ms, double* adj_ms,

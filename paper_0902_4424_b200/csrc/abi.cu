@@ -248,6 +248,7 @@ struct l1g_solver {
   // optional per-kernel timing: events [graph][iteration][4] around proj / fwd / adj
   bool timing = false;
   bool fwd_sparse = true;  // forward product over the support of d only (gemv.cu)
+  bool fwd_switch = true;  // ... switching to the dense stream on the device when d is dense
   std::vector<cudaEvent_t> tev;
   double t_proj = 0.0, t_fwd = 0.0, t_adj = 0.0;
   int64_t t_iters = 0, launches = 0;
@@ -375,6 +376,7 @@ l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho, int nra
     {
       const char* e = getenv("L1G_FWD");
       s->fwd_sparse = !(e && std::strcmp(e, "dense") == 0);
+      s->fwd_switch = !(e && std::strcmp(e, "sparse") == 0);
     }
     s->y = dalloc<double>(pl.n_pad);
     s->vb.y = s->y;
@@ -546,7 +548,8 @@ void enqueue_iteration(l1g_solver* s, Mark mark) {
                 q->d_full ? q->scal_all : nullptr, q->nranks);
   mark(1);
   if (!s->split()) {
-    launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream, s->fwd_sparse);
+    launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream, s->fwd_sparse,
+               s->fwd_switch);
     mark(2);
     launch_adj(*s->op, s->ws, ADJ_ITER, nullptr, nullptr, &s->vb, s->st, s->stream);
     mark(3);
@@ -2278,8 +2281,12 @@ int l1g_solver_set_forward(l1g_solver* s, int sparse) {
   return guarded([&] {
     set_device(s->op->c);
     L1G_CUDA(cudaStreamSynchronize(s->stream));
-    if (s->fwd_sparse != (sparse != 0)) drop_graphs(s);
-    for (l1g_solver* q : members(s)) q->fwd_sparse = sparse != 0;
+    if (sparse < 0 || sparse > 2) throw InvalidArgument("set_forward: mode must be 0, 1 or 2");
+    if (s->fwd_sparse != (sparse != 0) || s->fwd_switch != (sparse == 1)) drop_graphs(s);
+    for (l1g_solver* q : members(s)) {
+      q->fwd_sparse = sparse != 0;
+      q->fwd_switch = sparse == 1;
+    }
   });
 }
 

@@ -61,6 +61,7 @@ struct DevState {
   double alpha_used, stat, gd, theta, f_max, step, f_new, a, b;
   int32_t halvings;
   int64_t support;
+  int64_t dsup;  // nonzeros of the last direction d (the forward product's support columns)
   l1g_iter_record last;  // record of the last completed (or stationary) iteration
   // telemetry
   l1g_iter_record* trace;
@@ -84,6 +85,9 @@ struct GemvPlan {
   int adj_blocks, ncg, nrr;
   // sparse forward (support columns only): column ranges of sp_tiles * 64 columns
   int sp_tiles, sp_ncr;
+  // the sparse forward switches to the dense TMA stream (fwd_kernel) on the device when d
+  // has at least this many nonzeros (measured crossover)
+  int64_t dense_min;
   int grid;
 };
 
@@ -170,7 +174,7 @@ void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* par
 // host launchers (gemv.cu, project.cu)
 GemvPlan make_plan(int64_t n, int64_t p, int sm_count);
 void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,
-                DevState* st, cudaStream_t s, bool sparse = false);
+                DevState* st, cudaStream_t s, bool sparse = false, bool dense_switch = false);
 void launch_fwd_init_zero(const Op& op, const Workspace& ws, const VecBufs* vb, DevState* st,
                           cudaStream_t s);
 void launch_adj(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,

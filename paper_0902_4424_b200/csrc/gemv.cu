@@ -13,6 +13,8 @@
 //   forward/INIT : r = Kx0 - y, f = ||r||^2;
 //   adjoint/ITER : r += lambda Kd (prologue), g' = 2 K^T r, x' = x + lambda d,
 //                  s'z, s's, z'z for the next BB step, telemetry, stop tests.
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -54,6 +56,9 @@ struct FwdArgs {
   unsigned* cnt_grp;
   unsigned* cnt_all;
   unsigned* task_ctr;  // sparse forward: dynamic task counter (reset by fwd_finish)
+  // sparse forward with the density switch: the support size from which the dense stream
+  // runs instead (0: never); it keeps the sparse column ranges, so the finish is the same
+  int64_t dense_min;
   DevState* st;
   VecBufs vb;
   BatchStrides bs;     // finish kernels: partial stride, per-problem offsets (blockIdx.y)
@@ -79,6 +84,7 @@ struct AdjArgs {
   // allgather packet [x (p_pad) | g (p_pad) | SHARD_SCAL scalars]
   double* pack;
 };
+
 
 template <int N, class F>
 __device__ __forceinline__ double2 tree2(const F& leaf, int base = 0) {
@@ -321,9 +327,10 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a0) {
       }
     }
   }
-  const int B = fin_block_w(a.ncr, wpg);
+  const int ncr = a.ncr;
+  const int B = fin_block_w(ncr, wpg);
   {
-    const int lo = wi * B, hi = lo + B < a.ncr ? lo + B : a.ncr;
+    const int lo = wi * B, hi = lo + B < ncr ? lo + B : ncr;
     double bv[1] = {0.0};
     if (live && hi > lo) chunk_trees<1>(a.part + row, a.bs.pstride, lo, hi, bv);
     sv[warp][lane] = bv[0];
@@ -331,7 +338,7 @@ __global__ void __launch_bounds__(FIN_T) fwd_finish_kernel(const FwdArgs a0) {
   }
   if (status != RUNNING) return;
   if (wi == 0 && live) {
-    const double kd = fin_join_w(sv + gl * wpg, wpg, (a.ncr + B - 1) / B, lane);
+    const double kd = fin_join_w(sv + gl * wpg, wpg, (ncr + B - 1) / B, lane);
     if (a.mode == FWD_APPLY) {
       a.vout[row] = kd;
     } else {
@@ -501,20 +508,19 @@ __global__ void __launch_bounds__(FIN_T) adj_finish_kernel(const AdjArgs a0) {
 }
 
 // ============================================================================ forward
-template <int SPLIT>
-__global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdArgs a) {
-  pdl_wait_and_trigger();
+// The dense forward stream as a device function: fwd_kernel, and fwd_sparse_kernel when d
+// is dense enough (its first 32 * (4 * SPLIT + 1) threads run this, the others return).
+template <int SPLIT, int NST = STAGES>
+__device__ __forceinline__ void fwd_dense_body(const FwdArgs& a, unsigned char* smem) {
   constexpr int NCONS = 4 * SPLIT;
   constexpr int NQ = 32 / SPLIT;  // column pairs per lane group
   constexpr int RPW = 32 / SPLIT; // rows per warp
-  if (a.mode != FWD_APPLY && a.st->status != RUNNING) return;
-  extern __shared__ __align__(128) unsigned char smem[];
   double* sbase = reinterpret_cast<double*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * FWD_STAGE_DBL * 8);
-  uint64_t* empty = full + STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NST * FWD_STAGE_DBL * 8);
+  uint64_t* empty = full + NST;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCONS);
     }
@@ -543,7 +549,7 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdA
 #pragma unroll
           for (int g = 0; g < SPLIT; ++g)
             bulk_g2s(ddst + 2 * d_pos<SPLIT>(g * NQ), dsrc + 2 * g * NQ, 512 / SPLIT, &full[stage]);
-          if (++stage == STAGES) {
+          if (++stage == NST) {
             stage = 0;
             phase ^= 1u;
           }
@@ -582,7 +588,7 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdA
 #pragma unroll
       for (int o = RPW; o < 32; o <<= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
       acc.push(v, (uint32_t)s);
-      if (++stage == STAGES) {
+      if (++stage == NST) {
         stage = 0;
         phase ^= 1u;
       }
@@ -593,6 +599,15 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdA
     }
   }
 }
+
+template <int SPLIT>
+__global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) fwd_kernel(const FwdArgs a) {
+  pdl_wait_and_trigger();
+  if (a.mode != FWD_APPLY && a.st->status != RUNNING) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  fwd_dense_body<SPLIT>(a, smem);
+}
+
 
 // ============================================================================ adjoint
 template <int SPLIT>
@@ -763,14 +778,23 @@ __global__ void __launch_bounds__(32 * (4 * SPLIT + 1), 1) adj_kernel(const AdjA
 // control is shared) and streams their 256-byte column runs straight from HBM with a
 // SP_PF-deep register prefetch; slots live in shared memory.
 // Range partials go to the dense kernel's buffer, so fwd_finish_kernel is shared.
-constexpr int SP_NCW = 16;     // consumer warps
+#ifndef L1G_SP_NCW
+#define L1G_SP_NCW 16
+#endif
+#ifndef L1G_SP_PF
+#define L1G_SP_PF 16
+#endif
+#ifndef L1G_FWD_DENSE_FRAC_DEFAULT
+#define L1G_FWD_DENSE_FRAC_DEFAULT 0.8
+#endif
+constexpr int SP_NCW = L1G_SP_NCW;  // consumer warps
 constexpr int SP_RPW = 2;      // row blocks per consumer warp (lane = one row in each)
 constexpr int SP_RB = SP_NCW * SP_RPW;  // row blocks per task
 constexpr int SP_NT = SP_NCW * 32 * SP_RPW;  // slot columns (one per row)
 constexpr int SP_MAXT = 16;    // tiles per range (<= 1024 columns, levels 1..10)
 constexpr int SP_W = SP_MAXT * TC;
 constexpr int SP_LVLS = 11;
-constexpr int SP_PF = 16;      // loads in flight per consumer thread
+constexpr int SP_PF = L1G_SP_PF;  // loads in flight per consumer thread and row
 struct SpEnt {
   int coff;  // (tile column block) * TILE + j * 32
   int meta;  // [0,5) level (31 = last leaf), [5,9) column swizzle, [9,20) open slots absorbed
@@ -779,17 +803,33 @@ struct SpEnt {
 struct SpInfo {
   int task, count;
 };
-static size_t sp_smem() {
+static size_t sp_smem_own() {
   return (size_t)2 * SP_W * sizeof(SpEnt) + (size_t)SP_LVLS * SP_NT * 8 + 2 * sizeof(SpInfo) +
          4 * 8 + 16;
+}
+// the sparse kernel also hosts the dense stream (density switch), with a 2-stage ring so
+// the kernel's shared memory stays near its own 122 KB
+constexpr int SP_DENSE_STAGES = 2;
+static size_t sp_smem() {
+  return std::max(sp_smem_own(),
+                  (size_t)SP_DENSE_STAGES * FWD_STAGE_DBL * 8 + 2 * SP_DENSE_STAGES * 8);
 }
 
 __global__ void __launch_bounds__(32 * (SP_NCW + 1), 1) fwd_sparse_kernel(const FwdArgs a) {
   L1G_TL_ENTRY
   pdl_wait_and_trigger();
   L1G_TL_WAITED(true, g_tl_gemv, 1, a.st->k)
-  if (a.st->status != RUNNING) return;
+  const int status = __ldcg(&a.st->status);
+  const int64_t dsup = a.dense_min > 0 ? __ldcg(&a.st->dsup) : 0;  // both loads in flight
+  if (status != RUNNING) return;
   extern __shared__ __align__(128) unsigned char smem[];
+  if (a.dense_min > 0 && dsup >= a.dense_min) {
+    // dense d: the TMA stream over all of K beats the gather; same column ranges (and tree)
+    if (threadIdx.x >= 32 * 5) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&a.st->prof[23], 1.0);  // telemetry
+    fwd_dense_body<1, SP_DENSE_STAGES>(a, smem);
+    return;
+  }
   SpEnt* ent = reinterpret_cast<SpEnt*>(smem);  // [2][SP_W]
   double* slots = reinterpret_cast<double*>(ent + 2 * SP_W);
   SpInfo* info = reinterpret_cast<SpInfo*>(slots + (size_t)SP_LVLS * SP_NT);
@@ -1001,6 +1041,13 @@ GemvPlan make_plan(int64_t n, int64_t p, int sm_count) {
   while (t > 1 && nrq * cdiv(pl.ncb, t) < (int64_t)sp_waves * sm_count) t >>= 1;
   pl.sp_tiles = t;
   pl.sp_ncr = (int)cdiv(pl.ncb, t);
+  // density switch: from this fraction of nonzero columns in d the dense stream (6.5 TB/s over
+  // all of K) beats the gather over the support columns (L1G_FWD_DENSE_FRAC; <= 0 disables)
+  static const double dense_frac = [] {
+    const char* e = getenv("L1G_FWD_DENSE_FRAC");
+    return e ? atof(e) : L1G_FWD_DENSE_FRAC_DEFAULT;
+  }();
+  pl.dense_min = dense_frac > 0.0 ? std::max<int64_t>(1, (int64_t)std::ceil(dense_frac * (double)p)) : 0;
   pl.grid = sm_count;
   return pl;
 }
@@ -1090,9 +1137,10 @@ static AdjArgs adj_args(const Op& op, const Workspace& ws, int mode, const doubl
 // main forward kernel over the operator's columns -> range partials in ws.fwd_part;
 // returns the args the finish kernel needs (range count / widths)
 static FwdArgs fwd_main(const Op& op, const Workspace& ws, FwdArgs a, const uint32_t* dmask,
-                        bool sparse, cudaStream_t s) {
+                        bool sparse, cudaStream_t s, bool dense_switch = false) {
   const GemvPlan& pl = op.plan;
   if (sparse && dmask) {
+    a.dense_min = (dense_switch && a.mode == FWD_ITER) ? pl.dense_min : 0;
     static std::atomic<unsigned long long> attr{0};
     once_per_device(attr, [] {
       L1G_CUDA(cudaFuncSetAttribute(fwd_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1138,9 +1186,9 @@ static void fin_launch(AdjArgs a, cudaStream_t s) {
 }
 
 void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout,
-                const VecBufs* vb, DevState* st, cudaStream_t s, bool sparse) {
+                const VecBufs* vb, DevState* st, cudaStream_t s, bool sparse, bool dense_switch) {
   FwdArgs a = fwd_args(op, ws, mode, (mode == FWD_ITER) ? vb->d : vin, vout, vb, st);
-  a = fwd_main(op, ws, a, a.vb.dmask, sparse && mode == FWD_ITER, s);
+  a = fwd_main(op, ws, a, a.vb.dmask, sparse && mode == FWD_ITER, s, dense_switch);
   fin_launch(a, s);
 }
 

@@ -72,9 +72,9 @@ struct ProjArgs {
 };
 
 struct ProjShared {
-  double slot[2][MAX_CS][4];  // cluster exchange slots (double-buffered), filled by st.async
+  double slot[2][MAX_CS][6];  // cluster exchange slots (double-buffered), filled by st.async
   uint64_t xbar[2];           // their mbarriers (complete_tx of every CTA's values)
-  double wv[2][PW][4];         // warp partials (double-buffered)
+  double wv[2][PW][6];         // warp partials (double-buffered)
   long long wl[PW][2];
   double bc[8];
   int dec;
@@ -1130,7 +1130,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       sup += (h != 0.0);
       hmax = fmax(hmax, fabs(h));
     }
-    double gdl = 0.0, lmax = 0.0;
+    double gdl = 0.0, lmax = 0.0, dnz = 0.0;
     if (a.mode != PROJ_ALPHA0) {
       // stage h, then coalesced d = h - x (written out) and leaf g_j d_j
       if (!VS) {
@@ -1160,8 +1160,10 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           dyn[p] = leaf;
           // support bitmap of d for the sparse forward product (whole warps are in or out)
           const unsigned bits = __ballot_sync(0xffffffffu, nz);
-          if (a.mode == PROJ_ITER && (tid & 31) == 0 && j < lim)
+          if (a.mode == PROJ_ITER && (tid & 31) == 0 && j < lim) {
             a.vb.dmask[(pofs + base + j) >> 5] = bits;
+            dnz += (double)__popc(bits);
+          }
         }
       }
       __syncthreads();
@@ -1173,10 +1175,10 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         gdl = run_tree<M, VS>([&](int k) { return VG(k); });
       }
     }
-    double red2[4] = {gdl, lmax, hmax, (double)sup};
-    const int kinds2[4] = {0, 1, 1, 2};
-    block_reduce<4>(red2, kinds2, sh, rp);
-    cluster_combine(red2, kinds2, 4, sh, cl, cs, rp);
+    double red2[5] = {gdl, lmax, hmax, (double)sup, dnz};
+    const int kinds2[5] = {0, 1, 1, 2, 2};
+    block_reduce<5>(red2, kinds2, sh, rp);
+    cluster_combine(red2, kinds2, 5, sh, cl, cs, rp);
     const double gd = red2[0], stat = red2[1], hinf = red2[2];
     const long long support = (long long)red2[3];
     mark(7);
@@ -1206,6 +1208,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     if (rank == 0 && tid == 0) {
       st->out_stationarity = outcome == 2 ? first_stat : stat;
       if (outcome == 1) {
+        st->dsup = (int64_t)red2[4];  // nonzeros of d: the forward product's density switch
         st->alpha_used = alpha;
         st->stat = stat;
         st->gd = gd;
