@@ -369,6 +369,191 @@ __global__ void __launch_bounds__(WT, 1) badj_wide_kernel(const BGemmArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- producer-warp products
+// The 16-warp products with the copies taken off the consumers: a 17th warp issues every
+// cp.async of a stage (the 512 consumer threads' share, 128 copies per lane) and its lanes'
+// cp.async arrivals complete the stage's `full` mbarrier; each consumer warp waits only for
+// the stage it reads and marks it `empty` when done, so consumers never wait for each other
+// and the DMMA pipe is not drained at every chunk boundary.
+constexpr int WP = WT + 32;  // 16 consumer warps + 1 producer warp
+__device__ __forceinline__ void cp_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
+  pdl_wait_and_trigger();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ uint64_t full[W_STAGES], empty[W_STAGES];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int64_t rb0 = 4LL * blockIdx.x;
+  const int b0 = blockIdx.z * BW;
+  const int nchunk = 2 * a.nblocks;  // 32-column chunks
+  const int c_begin = blockIdx.y * a.per_split;
+  const int c_end = c_begin + a.per_split < nchunk ? c_begin + a.per_split : nchunk;
+  const int nch = c_end > c_begin ? c_end - c_begin : 0;
+  if (tid == 0) {
+    for (int st = 0; st < W_STAGES; ++st) {
+      mbar_init(&full[st], 32);
+      mbar_init(&empty[st], WT / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == WT / 32) {  // ---- producer: the copies of all 512 consumer threads
+    const uint32_t s_base = smem_u32(sm);
+    const int64_t k_rs = a.ncb * TILE;
+    const int64_t v_rs = 32 * a.vstride;
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % W_STAGES;
+      if (c >= W_STAGES) mbar_wait(&empty[st], (uint32_t)((c / W_STAGES - 1) & 1));
+      const int64_t ch = c_begin + c, cb = ch >> 1, half = ch & 1;
+      const uint32_t so = s_base + (uint32_t)(st * W_STAGE) * 8u;
+      const double* gk = a.K + rb0 * k_rs + cb * TILE + half * (TILE / 2);
+      const double* gv = a.V + (int64_t)b0 * a.vstride + ch * 32;
+#pragma unroll 4
+      for (int vt = lane; vt < WT; vt += 32) {
+        const uint32_t s_k = so + (uint32_t)kchunk_dst(vt) * 8u;
+        const double* k0 = gk + 2 * vt;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) cp16s(s_k + (uint32_t)(r * TR * KP * 8), k0 + r * k_rs);
+        const uint32_t s_v = so + (uint32_t)(W_KS + (vt >> 4) * W_VP + (vt & 15) * 2) * 8u;
+        const double* v0 = gv + (int64_t)(vt >> 4) * a.vstride + (vt & 15) * 2;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + i * v_rs);
+      }
+      cp_arrive_noinc(&full[st]);
+    }
+    cp_wait<0>();
+    return;
+  }
+  // ---- consumers
+  const int wr = warp & 3, wc = warp >> 2;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int c = 0; c < nch; ++c) {
+    const int st = c % W_STAGES;
+    mbar_wait(&full[st], (uint32_t)((c / W_STAGES) & 1));
+    const double* ks = sm + st * W_STAGE + wr * (TR * KP);
+    const double* vs = sm + st * W_STAGE + W_KS + (wc * 32) * W_VP;
+#pragma unroll
+    for (int kk = 0; kk < 32; kk += 4) {
+      const int col = kk + t;
+      double av[4], bv[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) av[mt] = ks[kpos(mt * 8 + g, col)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bv[nt] = vs[(nt * 8 + g) * W_VP + col];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av[mt], bv[nt]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  double* out = a.part + blockIdx.y * a.pslab;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int64_t row = (rb0 + wr) * TR + mt * 8 + g;
+      const int64_t b = b0 + wc * 32 + nt * 8 + 2 * t;
+      out[b * a.ostride + row] = acc[mt][nt][0];
+      out[(b + 1) * a.ostride + row] = acc[mt][nt][1];
+    }
+}
+
+__global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
+  pdl_wait_and_trigger();
+  extern __shared__ __align__(16) double sm[];
+  __shared__ uint64_t full[W_STAGES], empty[W_STAGES];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int64_t cb0 = 2LL * blockIdx.x;
+  const int b0 = blockIdx.z * BW;
+  const int r_begin = blockIdx.y * a.per_split;
+  const int r_end = r_begin + a.per_split < a.nblocks ? r_begin + a.per_split : a.nblocks;
+  const int nch = r_end > r_begin ? r_end - r_begin : 0;
+  if (tid == 0) {
+    for (int st = 0; st < W_STAGES; ++st) {
+      mbar_init(&full[st], 32);
+      mbar_init(&empty[st], WT / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == WT / 32) {  // ---- producer
+    const uint32_t s_base = smem_u32(sm);
+    const int64_t v_rs = 32 * a.vstride;
+    for (int c = 0; c < nch; ++c) {
+      const int st = c % W_STAGES;
+      if (c >= W_STAGES) mbar_wait(&empty[st], (uint32_t)((c / W_STAGES - 1) & 1));
+      const int64_t rb = r_begin + c;
+      const uint32_t so = s_base + (uint32_t)(st * W_STAGE) * 8u;
+      const double* gk = a.K + (rb * a.ncb + cb0) * TILE;
+      const double* gv = a.V + (int64_t)b0 * a.vstride + rb * TR;
+#pragma unroll 4
+      for (int vt = lane; vt < WT; vt += 32) {
+        const uint32_t s_k = so + (uint32_t)kchunk_dst(vt) * 8u;
+        const double* k0 = gk + 2 * vt;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          cp16s(s_k + (uint32_t)(((i >> 1) * KT_S + (i & 1) * 32 * KP) * 8),
+                k0 + (i >> 1) * TILE + (i & 1) * 1024);
+        const uint32_t s_v = so + (uint32_t)(W_KS + (vt >> 4) * W_VP + (vt & 15) * 2) * 8u;
+        const double* v0 = gv + (int64_t)(vt >> 4) * a.vstride + (vt & 15) * 2;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + i * v_rs);
+      }
+      cp_arrive_noinc(&full[st]);
+    }
+    cp_wait<0>();
+    return;
+  }
+  // ---- consumers
+  const int wm = warp & 3, wc = warp >> 2;
+  const int tl = wm >> 1, cofs = (wm & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int c = 0; c < nch; ++c) {
+    const int st = c % W_STAGES;
+    mbar_wait(&full[st], (uint32_t)((c / W_STAGES) & 1));
+    const double* kt = sm + st * W_STAGE + tl * KT_S;
+    const double* vs = sm + st * W_STAGE + W_KS + (wc * 32) * W_VP;
+#pragma unroll
+    for (int kk = 0; kk < TR; kk += 4) {
+      const int row = kk + t;
+      double av[4], bv[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) av[mt] = kt[kpos(row, cofs + mt * 8 + g)];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bv[nt] = vs[(nt * 8 + g) * W_VP + row];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt], av[mt], bv[nt]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  double* out = a.part + blockIdx.y * a.pslab;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int64_t col = (cb0 + tl) * TC + cofs + mt * 8 + g;
+      const int64_t b = b0 + wc * 32 + nt * 8 + 2 * t;
+      out[b * a.ostride + col] = acc[mt][nt][0];
+      out[(b + 1) * a.ostride + col] = acc[mt][nt][1];
+    }
+}
+
 template <int NA>
 __device__ __forceinline__ void warp_tree_arrays_b(const double* v, int count, int stride,
                                                    int lane, double* out) {
@@ -577,6 +762,14 @@ static bool wide_products() {
   }();
   return w;
 }
+// L1G_DMMA=wide: the 16-warp kernels whose consumers issue the copies themselves
+static bool ws_products() {
+  static const bool w = [] {
+    const char* e = getenv("L1G_DMMA");
+    return !(e && std::strcmp(e, "wide") == 0);
+  }();
+  return w;
+}
 
 BatchPlan make_batch_plan(const GemvPlan& pl, int B, int sm_count) {
   BatchPlan bp{};
@@ -625,9 +818,12 @@ void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* par
     once_per_device(wattr, [] {
       L1G_CUDA(cudaFuncSetAttribute(bfwd_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)bwide_smem()));
+      L1G_CUDA(cudaFuncSetAttribute(bfwd_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)bwide_smem()));
     });
     const dim3 grid((unsigned)(pl.n_pad / 128), (unsigned)bp.fwd_splits, (unsigned)(bp.Bp / BW));
-    L1G_CUDA(launch_pdl(bfwd_wide_kernel, grid, WT, bwide_smem(), s, a));
+    if (ws_products()) L1G_CUDA(launch_pdl(bfwd_ws_kernel, grid, WP, bwide_smem(), s, a));
+    else L1G_CUDA(launch_pdl(bfwd_wide_kernel, grid, WT, bwide_smem(), s, a));
     return;
   }
   const dim3 grid((unsigned)(pl.n_pad / 64), (unsigned)bp.fwd_splits, (unsigned)(bp.Bp / BW));
@@ -658,9 +854,12 @@ void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* par
     once_per_device(wattr, [] {
       L1G_CUDA(cudaFuncSetAttribute(badj_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)bwide_smem()));
+      L1G_CUDA(cudaFuncSetAttribute(badj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)bwide_smem()));
     });
     const dim3 grid((unsigned)(pl.ncb / 2), (unsigned)bp.adj_splits, (unsigned)(bp.Bp / BW));
-    L1G_CUDA(launch_pdl(badj_wide_kernel, grid, WT, bwide_smem(), s, a));
+    if (ws_products()) L1G_CUDA(launch_pdl(badj_ws_kernel, grid, WP, bwide_smem(), s, a));
+    else L1G_CUDA(launch_pdl(badj_wide_kernel, grid, WT, bwide_smem(), s, a));
     return;
   }
   const dim3 grid((unsigned)pl.ncb, (unsigned)bp.adj_splits, (unsigned)(bp.Bp / BW));
