@@ -11,6 +11,7 @@
 // partials are joined by the finish kernels (gemv.cu), which also run every problem's
 // epilogue.  DMMA accumulates with fused multiply-adds in its own order, so the batched
 // path matches the per-problem canonical solve to rounding, not bit for bit.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -381,17 +382,32 @@ __device__ __forceinline__ void cp_arrive_noinc(uint64_t* bar) {
                : "memory");
 }
 
+// Persistent: CTA i takes work items i, i + grid, ... (item = (row tile, split, problem
+// block) in the order of the former grid), and the ring runs on across items, so the next
+// item's first stages load while the consumers finish the current one.
+struct WsItem {
+  int x, y, z;
+};
+__device__ __forceinline__ WsItem ws_item(int it, int nx, int ny) {
+  WsItem w;
+  w.x = it % nx;
+  w.y = (it / nx) % ny;
+  w.z = it / (nx * ny);
+  return w;
+}
+
 __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
   pdl_wait_and_trigger();
   extern __shared__ __align__(16) double sm[];
   __shared__ uint64_t full[W_STAGES], empty[W_STAGES];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int64_t rb0 = 4LL * blockIdx.x;
-  const int b0 = blockIdx.z * BW;
   const int nchunk = 2 * a.nblocks;  // 32-column chunks
-  const int c_begin = blockIdx.y * a.per_split;
-  const int c_end = c_begin + a.per_split < nchunk ? c_begin + a.per_split : nchunk;
-  const int nch = c_end > c_begin ? c_end - c_begin : 0;
+  const int nitems = a.nx * a.ny * a.nz;
+  auto nch_of = [&](const WsItem& w) {
+    const int c_begin = w.y * a.per_split;
+    const int c_end = c_begin + a.per_split < nchunk ? c_begin + a.per_split : nchunk;
+    return c_end > c_begin ? c_end - c_begin : 0;
+  };
   if (tid == 0) {
     for (int st = 0; st < W_STAGES; ++st) {
       mbar_init(&full[st], 32);
@@ -404,9 +420,15 @@ __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
     const uint32_t s_base = smem_u32(sm);
     const int64_t k_rs = a.ncb * TILE;
     const int64_t v_rs = 32 * a.vstride;
-    for (int c = 0; c < nch; ++c) {
-      const int st = c % W_STAGES;
-      if (c >= W_STAGES) mbar_wait(&empty[st], (uint32_t)((c / W_STAGES - 1) & 1));
+    int gc = 0;  // ring position across items
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+     const WsItem w = ws_item(it, a.nx, a.ny);
+     const int64_t rb0 = 4LL * w.x;
+     const int b0 = w.z * BW;
+     const int c_begin = w.y * a.per_split, nch = nch_of(w);
+     for (int c = 0; c < nch; ++c, ++gc) {
+      const int st = gc % W_STAGES;
+      if (gc >= W_STAGES) mbar_wait(&empty[st], (uint32_t)((gc / W_STAGES - 1) & 1));
       const int64_t ch = c_begin + c, cb = ch >> 1, half = ch & 1;
       const uint32_t so = s_base + (uint32_t)(st * W_STAGE) * 8u;
       const double* gk = a.K + rb0 * k_rs + cb * TILE + half * (TILE / 2);
@@ -423,20 +445,27 @@ __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
         for (int i = 0; i < 4; ++i) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + i * v_rs);
       }
       cp_arrive_noinc(&full[st]);
+     }
     }
     cp_wait<0>();
     return;
   }
   // ---- consumers
   const int wr = warp & 3, wc = warp >> 2;
+  int gc = 0;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+  const WsItem w = ws_item(it, a.nx, a.ny);
+  const int64_t rb0 = 4LL * w.x;
+  const int b0 = w.z * BW;
+  const int nch = nch_of(w);
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int c = 0; c < nch; ++c) {
-    const int st = c % W_STAGES;
-    mbar_wait(&full[st], (uint32_t)((c / W_STAGES) & 1));
+  for (int c = 0; c < nch; ++c, ++gc) {
+    const int st = gc % W_STAGES;
+    mbar_wait(&full[st], (uint32_t)((gc / W_STAGES) & 1));
     const double* ks = sm + st * W_STAGE + wr * (TR * KP);
     const double* vs = sm + st * W_STAGE + W_KS + (wc * 32) * W_VP;
 #pragma unroll
@@ -455,7 +484,7 @@ __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
-  double* out = a.part + blockIdx.y * a.pslab;
+  double* out = a.part + w.y * a.pslab;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -465,6 +494,7 @@ __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
       out[b * a.ostride + row] = acc[mt][nt][0];
       out[(b + 1) * a.ostride + row] = acc[mt][nt][1];
     }
+  }
 }
 
 __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
@@ -472,11 +502,12 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
   extern __shared__ __align__(16) double sm[];
   __shared__ uint64_t full[W_STAGES], empty[W_STAGES];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int64_t cb0 = 2LL * blockIdx.x;
-  const int b0 = blockIdx.z * BW;
-  const int r_begin = blockIdx.y * a.per_split;
-  const int r_end = r_begin + a.per_split < a.nblocks ? r_begin + a.per_split : a.nblocks;
-  const int nch = r_end > r_begin ? r_end - r_begin : 0;
+  const int nitems = a.nx * a.ny * a.nz;
+  auto nch_of = [&](const WsItem& w) {
+    const int r_begin = w.y * a.per_split;
+    const int r_end = r_begin + a.per_split < a.nblocks ? r_begin + a.per_split : a.nblocks;
+    return r_end > r_begin ? r_end - r_begin : 0;
+  };
   if (tid == 0) {
     for (int st = 0; st < W_STAGES; ++st) {
       mbar_init(&full[st], 32);
@@ -488,9 +519,15 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
   if (warp == WT / 32) {  // ---- producer
     const uint32_t s_base = smem_u32(sm);
     const int64_t v_rs = 32 * a.vstride;
-    for (int c = 0; c < nch; ++c) {
-      const int st = c % W_STAGES;
-      if (c >= W_STAGES) mbar_wait(&empty[st], (uint32_t)((c / W_STAGES - 1) & 1));
+    int gc = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+     const WsItem w = ws_item(it, a.nx, a.ny);
+     const int64_t cb0 = 2LL * w.x;
+     const int b0 = w.z * BW;
+     const int r_begin = w.y * a.per_split, nch = nch_of(w);
+     for (int c = 0; c < nch; ++c, ++gc) {
+      const int st = gc % W_STAGES;
+      if (gc >= W_STAGES) mbar_wait(&empty[st], (uint32_t)((gc / W_STAGES - 1) & 1));
       const int64_t rb = r_begin + c;
       const uint32_t so = s_base + (uint32_t)(st * W_STAGE) * 8u;
       const double* gk = a.K + (rb * a.ncb + cb0) * TILE;
@@ -509,6 +546,7 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
         for (int i = 0; i < 4; ++i) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + i * v_rs);
       }
       cp_arrive_noinc(&full[st]);
+     }
     }
     cp_wait<0>();
     return;
@@ -516,14 +554,20 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
   // ---- consumers
   const int wm = warp & 3, wc = warp >> 2;
   const int tl = wm >> 1, cofs = (wm & 1) * 32;
+  int gc = 0;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+  const WsItem w = ws_item(it, a.nx, a.ny);
+  const int64_t cb0 = 2LL * w.x;
+  const int b0 = w.z * BW;
+  const int nch = nch_of(w);
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int c = 0; c < nch; ++c) {
-    const int st = c % W_STAGES;
-    mbar_wait(&full[st], (uint32_t)((c / W_STAGES) & 1));
+  for (int c = 0; c < nch; ++c, ++gc) {
+    const int st = gc % W_STAGES;
+    mbar_wait(&full[st], (uint32_t)((gc / W_STAGES) & 1));
     const double* kt = sm + st * W_STAGE + tl * KT_S;
     const double* vs = sm + st * W_STAGE + W_KS + (wc * 32) * W_VP;
 #pragma unroll
@@ -542,7 +586,7 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
-  double* out = a.part + blockIdx.y * a.pslab;
+  double* out = a.part + w.y * a.pslab;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -552,6 +596,7 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
       out[b * a.ostride + col] = acc[mt][nt][0];
       out[(b + 1) * a.ostride + col] = acc[mt][nt][1];
     }
+  }
 }
 
 template <int NA>
@@ -762,6 +807,8 @@ static bool wide_products() {
   }();
   return w;
 }
+// persistent producer-warp products: one CTA per SM
+static int ws_grid(const Op& op) { return op.plan.grid; }
 // L1G_DMMA=wide: the 16-warp kernels whose consumers issue the copies themselves
 static bool ws_products() {
   static const bool w = [] {
@@ -822,7 +869,11 @@ void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* par
                                     (int)bwide_smem()));
     });
     const dim3 grid((unsigned)(pl.n_pad / 128), (unsigned)bp.fwd_splits, (unsigned)(bp.Bp / BW));
-    if (ws_products()) L1G_CUDA(launch_pdl(bfwd_ws_kernel, grid, WP, bwide_smem(), s, a));
+    if (ws_products()) {
+      a.nx = (int)grid.x, a.ny = (int)grid.y, a.nz = (int)grid.z;
+      const int items = a.nx * a.ny * a.nz;
+      L1G_CUDA(launch_pdl(bfwd_ws_kernel, std::min(items, ws_grid(op)), WP, bwide_smem(), s, a));
+    }
     else L1G_CUDA(launch_pdl(bfwd_wide_kernel, grid, WT, bwide_smem(), s, a));
     return;
   }
@@ -858,7 +909,11 @@ void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* par
                                     (int)bwide_smem()));
     });
     const dim3 grid((unsigned)(pl.ncb / 2), (unsigned)bp.adj_splits, (unsigned)(bp.Bp / BW));
-    if (ws_products()) L1G_CUDA(launch_pdl(badj_ws_kernel, grid, WP, bwide_smem(), s, a));
+    if (ws_products()) {
+      a.nx = (int)grid.x, a.ny = (int)grid.y, a.nz = (int)grid.z;
+      const int items = a.nx * a.ny * a.nz;
+      L1G_CUDA(launch_pdl(badj_ws_kernel, std::min(items, ws_grid(op)), WP, bwide_smem(), s, a));
+    }
     else L1G_CUDA(launch_pdl(badj_wide_kernel, grid, WT, bwide_smem(), s, a));
     return;
   }

@@ -153,6 +153,7 @@ struct BGemmArgs {
   double* part;      // [splits][Bp][ostride]
   int64_t pslab, ostride;
   int per_split, nblocks;
+  int nx, ny, nz;  // persistent products: work items (tiles x splits x problem blocks)
 };
 struct BFinArgs {  // batched finishes (dmma.cu): problem b's vectors at b * ostride
   int mode, B, splits;
