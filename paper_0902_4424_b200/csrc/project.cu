@@ -141,8 +141,24 @@ __device__ __forceinline__ int cluster_exchange(const double* vals, int nv, Proj
   return buf;
 }
 
+// Max over a warp of doubles that are >= 0 or exactly -1 (-1: none), as two 32-bit REDUX
+// ops on the bit patterns (signed order of the high words, then the low words of the lanes
+// holding the maximal high word) instead of five dependent shuffle + compare steps.
+__device__ __forceinline__ double warp_max_nn(double v) {
+  const long long b = __double_as_longlong(v);
+  const int hi = (int)(b >> 32);
+  const int mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? (unsigned)b : 0u);
+  return __longlong_as_double((long long)(((unsigned long long)(unsigned)mhi << 32) | mlo));
+}
+// Sum over a warp of small non-negative integer counts held as doubles (REDUX)
+__device__ __forceinline__ double warp_count(double v) {
+  return (double)__reduce_add_sync(0xffffffffu, (unsigned)v);
+}
+
 // Several block reductions with one barrier.  kinds[c]: 0 = canonical tree over the threads'
-// aligned runs (warp butterfly, then butterfly over the warp index), 1 = max, 2 = plain sum.
+// aligned runs (warp butterfly, then butterfly over the warp index), 1 = max (values >= 0 or
+// -1), 2 = plain sum, 3 = count (integer-valued, < 2^32).
 // Every thread receives the results.
 template <int N>
 __device__ __forceinline__ void block_reduce(double (&v)[N], const int (&kinds)[N],
@@ -150,19 +166,23 @@ __device__ __forceinline__ void block_reduce(double (&v)[N], const int (&kinds)[
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int c = 0; c < N; ++c) {
-    const double x = kinds[c] == 1 ? warp_max(v[c]) : warp_tree(v[c]);
+    const double x = kinds[c] == 1 ? warp_max_nn(v[c])
+                                   : (kinds[c] == 3 ? warp_count(v[c]) : warp_tree(v[c]));
     if (lane == 0) sh.wv[rp.b][warp][c] = x;
   }
   __syncthreads();
 #pragma unroll
   for (int c = 0; c < N; ++c) {
     double x = lane < PW ? sh.wv[rp.b][lane][c] : (kinds[c] == 1 ? -1.0 : 0.0);
+    if (kinds[c] == 1) {
+      v[c] = warp_max_nn(x);
+    } else if (kinds[c] == 3) {
+      v[c] = warp_count(x);
+    } else {
 #pragma unroll
-    for (int o = 1; o < PW; o <<= 1) {
-      const double y = __shfl_xor_sync(0xffffffffu, x, o);
-      x = kinds[c] == 1 ? fmax(x, y) : add(x, y);
+      for (int o = 1; o < PW; o <<= 1) x = add(x, __shfl_xor_sync(0xffffffffu, x, o));
+      v[c] = __shfl_sync(0xffffffffu, x, 0);
     }
-    v[c] = __shfl_sync(0xffffffffu, x, 0);
   }
   rp.b ^= 1;
 }
@@ -191,7 +211,7 @@ __device__ __forceinline__ long long block_excl_scan(long long v, ProjShared& sh
 }
 
 // Cluster-wide combine of per-CTA values (identical in every thread of a CTA).  kinds[c]:
-// 0 = canonical tree over ranks, 1 = max, 2 = plain sum.  The values are exchanged into
+// 0 = canonical tree over ranks, 1 = max (>= 0 or -1), 2 = plain sum, 3 = count.  The values are exchanged into
 // every CTA's slots (cluster_exchange), then every warp combines the local slots by a
 // butterfly over the rank.  Every CTA must call it in the same order.
 __device__ __forceinline__ void cluster_combine(double* vals, const int* kinds, int nv,
@@ -202,11 +222,14 @@ __device__ __forceinline__ void cluster_combine(double* vals, const int* kinds, 
   const int lane = threadIdx.x & 31;
   for (int c = 0; c < nv; ++c) {
     double x = lane < cs ? sh.slot[buf][lane][c] : (kinds[c] == 1 ? -1.0 : 0.0);
-    for (int o = 1; o < cs; o <<= 1) {
-      const double y = __shfl_xor_sync(0xffffffffu, x, o);
-      x = kinds[c] == 1 ? fmax(x, y) : add(x, y);
+    if (kinds[c] == 1) {
+      vals[c] = warp_max_nn(x);
+    } else if (kinds[c] == 3) {
+      vals[c] = warp_count(x);
+    } else {
+      for (int o = 1; o < cs; o <<= 1) x = add(x, __shfl_xor_sync(0xffffffffu, x, o));
+      vals[c] = __shfl_sync(0xffffffffu, x, 0);
     }
-    vals[c] = __shfl_sync(0xffffffffu, x, 0);
   }
 }
 
@@ -773,7 +796,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
                   sst.theta < vinf;
       double th = warm ? sst.theta : th_cold;
       double cnt_prev = (double)a.p_pad + 1.0;
-      const int kinds_cs[2] = {2, 2};
+      const int kinds_cs[2] = {3, 2};
       for (int it = 0; it < 64; ++it) {
         double v2[2] = {0.0, 0.0};
 #pragma unroll UK
@@ -1138,6 +1161,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         for (int k = 0; k < M; ++k) dyn[swz<M>(tid * M + k)] = VG(k);
       }
       __syncthreads();
+      mark(30);
 #pragma unroll UB
       for (int i0 = 0; i0 < M; i0 += LB) {
         double xb[LB], gb[LB];
@@ -1167,6 +1191,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         }
       }
       __syncthreads();
+      mark(31);
       if (a.mode == PROJ_ITER) {
         if (!VS) {
 #pragma unroll
@@ -1176,8 +1201,9 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       }
     }
     double red2[5] = {gdl, lmax, hmax, (double)sup, dnz};
-    const int kinds2[5] = {0, 1, 1, 2, 2};
+    const int kinds2[5] = {0, 1, 1, 3, 3};
     block_reduce<5>(red2, kinds2, sh, rp);
+    mark(4);
     cluster_combine(red2, kinds2, 5, sh, cl, cs, rp);
     const double gd = red2[0], stat = red2[1], hinf = red2[2];
     const long long support = (long long)red2[3];

@@ -32,6 +32,17 @@ __device__ __forceinline__ void wait_par(uint64_t* bar, uint32_t parity) {
       "DONE_%=:\n\t}" ::"r"(su32(bar)), "r"(parity) : "memory");
 }
 
+__device__ __forceinline__ double wtree(double v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double wmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 __global__ void k_sync(long long* out, int mode) {
   cg::cluster_group cl = cg::this_cluster();
   __shared__ double slot[2][16][4];
@@ -79,6 +90,32 @@ __global__ void k_sync(long long* out, int mode) {
       double x = lane < cs ? slot[b][lane][0] : 0.0;
       for (int o = 1; o < cs; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
       acc += x * 1e-30;
+    } else if (mode == 5 || mode == 6) {  // block reduce of 5 doubles (project.cu block_reduce)
+      __shared__ double wv[2][16][6];
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      double v[5] = {acc, acc + 1, acc + 2, acc + 3, acc + 4};
+      const int kinds[5] = {0, 1, 1, 2, 2};
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        const double x = kinds[c] == 1 ? wmax(v[c]) : wtree(v[c]);
+        if (lane == 0) wv[r & 1][warp][c] = x;
+      }
+      __syncthreads();
+      if (mode == 5) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          double x = lane < 16 ? wv[r & 1][lane][c] : 0.0;
+#pragma unroll
+          for (int o = 1; o < 16; o <<= 1) {
+            const double y = __shfl_xor_sync(0xffffffffu, x, o);
+            x = kinds[c] == 1 ? fmax(x, y) : __dadd_rn(x, y);
+          }
+          v[c] = __shfl_sync(0xffffffffu, x, 0);
+        }
+      }
+      acc += (v[0] + v[1] + v[2] + v[3] + v[4]) * 1e-30;
+    } else if (mode == 7) {  // one warp tree of one double
+      acc += wtree(acc) * 1e-30;
     } else if (mode == 3) {  // barrier.cluster arrive.relaxed + wait (no fence)
       asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
     }
@@ -92,11 +129,11 @@ __global__ void k_sync(long long* out, int mode) {
 int main() {
   long long* d;
   cudaMalloc(&d, 16);
-  const char* names[5] = {"__syncthreads", "cluster.sync", "cluster_combine(2)", "barrier.cluster relaxed",
-                          "st.async combine(2)"};
-  for (int mode = 0; mode < 5; ++mode) {
+  const char* names[8] = {"__syncthreads", "cluster.sync", "cluster_combine(2)", "barrier.cluster relaxed",
+                          "st.async combine(2)", "block_reduce<5>", "block_reduce<5> 1st half", "warp_tree(1)"};
+  for (int mode = 0; mode < 8; ++mode) {
     for (int cs : {1, 2, 4, 8, 16}) {
-      if (mode == 0 && cs > 1) continue;
+      if ((mode == 0 || mode >= 5) && cs > 1) continue;
       cudaFuncSetAttribute(k_sync, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cs, 1, 1);

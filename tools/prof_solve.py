@@ -131,7 +131,8 @@ def main():
         calls = max(out[8], 1.0)
         names = {0: "steplength", 1: "v + |v|_1", 2: "michelot", 14: "count", 21: "hist atomics",
                  22: "hist gather", 15: "bins/bases", 16: "scatter", 17: "rank sort",
-                 3: "gather", 4: "next", 5: "exact prefix", 6: "feasibility", 7: "h/d/g'd"}
+                 3: "gather", 5: "exact prefix", 6: "feasibility", 30: "h + stage",
+                 31: "x,g loads, d, bitmap", 4: "g'd tree + block", 7: "exchange"}
         ghz = a.clock_ghz
         print("proj phases (us per call, CTA 0 clock at %.3f GHz): " % ghz + "  ".join(
             f"{nm} {out[i] / calls / ghz / 1e3:.2f}" for i, nm in names.items()) +
