@@ -173,7 +173,14 @@ __device__ __forceinline__ void head_sums(double* head, int H) {
 template <int NT = 512>
 __device__ long long prefix_break(const double* c, long long Ll, double rho, ScanShared& ss,
                                   double* s_before) {
-  static_assert(NT % 32 == 0 && NT <= 32 * PREFIX_MAXW && PREFIX_HEAD <= NT && PREFIX_HEAD % 32 == 0, "prefix_break block shape");
+  static_assert(NT % 32 == 0 && NT <= 32 * PREFIX_MAXW &&
+                    (PREFIX_HEAD % NT == 0 || NT % PREFIX_HEAD == 0),
+                "prefix_break block shape");
+  // the first NT threads of the block run it: a block barrier, or a named one for fewer
+  auto bsync = [] {
+    if constexpr (NT == 512) __syncthreads();
+    else named_bar_sync(3, NT);
+  };
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr long long TWO53 = 1LL << 53;
@@ -194,14 +201,20 @@ __device__ long long prefix_break(const double* c, long long Ll, double rho, Sca
     if (lane == 0) head_sums(ss.head, H);
   }
   L1G_HSTAMP(1)
-  __syncthreads();
+  bsync();
   {
-    const bool bad = tid < H && !passes(c[tid], ss.head[tid], rho, tid + 1);
-    const unsigned bb = __ballot_sync(FULL, bad);
-    if (lane == 0) ss.hbad[warp] = bb ? warp * 32 + __ffs(bb) - 1 : INT_MAX;
+    int first = INT_MAX;
+#pragma unroll
+    for (int i0 = 0; i0 < PREFIX_HEAD; i0 += NT) {  // every thread tests positions tid, tid + NT, ..
+      const int i = i0 + tid;
+      const bool bad = i < H && !passes(c[i], ss.head[i], rho, i + 1);
+      const unsigned bb = __ballot_sync(FULL, bad);
+      if (first == INT_MAX && bb) first = i0 + warp * 32 + __ffs(bb) - 1;
+    }
+    if (lane == 0) ss.hbad[warp] = first;
   }
   L1G_HSTAMP(2)
-  __syncthreads();
+  bsync();
   L1G_HSTAMP(3)
   {
     int ff = INT_MAX;
@@ -271,7 +284,7 @@ __device__ long long prefix_break(const double* c, long long Ll, double rho, Sca
       ss.ftie[par][warp] = tball != 0;
     }
     L1G_PSTAMP(0)
-    __syncthreads();
+    bsync();
     L1G_PSTAMP(1)
     long long N, Nend;
     {
@@ -299,7 +312,7 @@ __device__ long long prefix_break(const double* c, long long Ll, double rho, Sca
           ss.wd0[par][warp] = incl.d0;
           ss.wpk[par][warp] = seg_pack(incl);
         }
-        __syncthreads();
+        bsync();
         // concrete counts: the warps' starts by applying the warp segments in order (the
         // parity chain is a 1-bit select per warp; increments add up independently)
         long long Nw = base_q, accd = base_q;
@@ -352,7 +365,7 @@ __device__ long long prefix_break(const double* c, long long Ll, double rho, Sca
     } else if (lane == 0) {
       ss.epos[par][warp] = INT_MAX;
     }
-    __syncthreads();
+    bsync();
     int ew = -1;
 #pragma unroll
     for (int w = NW - 1; w >= 0; --w) ew = ss.epos[par][w] != INT_MAX ? w : ew;

@@ -89,6 +89,10 @@ constexpr int SMALL_RANK = 256;   // single-CTA path: rank sort up to this many 
 #define L1G_PREFIX_CLUSTER_MIN 8192
 #endif
 constexpr long long PREFIX_CLUSTER_MIN = L1G_PREFIX_CLUSTER_MIN;
+#ifndef L1G_PREFIX_NT  // threads of the one-CTA exact prefix (fewer warps: cheaper barriers)
+#define L1G_PREFIX_NT 512
+#endif
+constexpr int PREFIX_NT = L1G_PREFIX_NT;
 template <int NBv>
 struct SortShared {
   int hist[NBv];    // this CTA's candidates per bin
@@ -1038,9 +1042,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
               cl.sync();
               mark(3);
               double res[2] = {0.0, 0.0};
-              if (rank == 0) {
-                res[0] = (double)prefix_break(cand, L, rho, scan_sh, &res[1]);
-              }
+              if (rank == 0 && tid < PREFIX_NT)  // (the senders, tid < cs, are among them)
+                res[0] = (double)prefix_break<PREFIX_NT>(cand, L, rho, scan_sh, &res[1]);
               const int xb = cluster_exchange(res, 2, sh, cl, cs, rp);
               ff = (long long)sh.slot[xb][0][0];
               s_before = sh.slot[xb][0][1];
@@ -1099,7 +1102,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           __syncthreads();
           mark(4);
           double s_before = 0.0;
-          const long long ff = prefix_break(c, L, rho, scan_sh, &s_before);
+          const long long ff =
+              tid < PREFIX_NT ? prefix_break<PREFIX_NT>(c, L, rho, scan_sh, &s_before) : 0;
           count(20, (double)scan_sh.epochs);
           if (tid == 0) {
             // theta = candidate of the last passing index (prox.cpp:47-50); 0 if none passed
