@@ -91,6 +91,23 @@ def test_projection_large(p):
             assert np.array_equal(pr.point, u)
 
 
+@pytest.mark.parametrize("p", [65536, 262144])
+def test_projection_cluster_prefix_ties(p):
+    """The cluster-wide exact prefix (> 8192 candidates, project.cu prefix_break_cluster) on
+    values from a coarse grid: many equal magnitudes (rank-sort ties) and running sums whose
+    next addend is an odd multiple of half a grid step (rounding ties resolved by parity
+    segments composed across CTAs)."""
+    rng = np.random.default_rng(p + 3)
+    for grid_bits, frac in ((12, 0.95), (20, 0.6), (8, 0.8)):
+        x = rng.integers(1, 1 << grid_bits, size=p) * 2.0 ** -grid_bits
+        x *= rng.choice([-1.0, 1.0], size=p)
+        rho = frac * float(np.abs(x).sum())
+        u, th, sup = O.project_l1(x, rho)
+        pr = l1.project_l1_ball_with_threshold(x, l1.L1Ball(rho))
+        assert pr.threshold == th and pr.support == sup, (grid_bits, frac)
+        assert np.array_equal(pr.point, u)
+
+
 def test_generators_bit_identical():
     K = O.gaussian_matrix(11, 130, 333)
     op = l1.DenseOperator.generate_gaussian(130, 333, 11)
