@@ -128,7 +128,9 @@ struct RedPar {
 // cluster barrier (954 vs 1669 cycles at cs = 16, tools/bench_cluster_sync.cu).  A buffer is
 // rewritten two exchanges later, and any CTA's sends for exchange k + 2 follow its receipt of
 // exchange k + 1, which every CTA sends only after reading exchange k: double-buffering is
-// enough.  Returns the buffer holding the values; every CTA must call it in the same order.
+// enough, provided every caller separates its reads of the slots from its next exchange by
+// a block barrier (so no sender thread, tid < cs, runs ahead of a slow reader); all callers
+// do.  Returns the buffer holding the values; every CTA must call it in the same order.
 __device__ __forceinline__ int cluster_exchange(const double* vals, int nv, ProjShared& sh,
                                                 cg::cluster_group& cl, int cs, RedPar& rp) {
   const unsigned rank = cl.block_rank();
