@@ -978,8 +978,13 @@ l1g_batch* batch_new(l1g_op* op, int B, const double* Y, const double* rho,
     b->rho.assign(rho, rho + B);
     b->bp = make_batch_plan(pl, B, op->c->sm_count);
     {  // a small cluster per problem (>= 4096 elements per CTA): C5 measured best at 4
+      static const int cs_max = [] {
+        const char* e = getenv("L1G_BATCH_PROJ_CS");
+        const int v = e ? atoi(e) : 4;
+        return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 4;
+      }();
       int cs = 1;
-      while (cs < 4 && pl.p_pad / (cs * 2) >= 4096) cs *= 2;
+      while (cs < cs_max && pl.p_pad / (cs * 2) >= 4096) cs *= 2;
       b->pp = make_proj_plan_single(pl.p_pad, cs);
     }
     const size_t Bp = (size_t)b->bp.Bp;
