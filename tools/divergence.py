@@ -120,7 +120,7 @@ def run(name):
     out["window"] = window
     out["final_rel_dx"] = float(np.linalg.norm(xc - xl) / max(np.linalg.norm(xc), 1e-300))
     out["final_abs_df"] = abs(rc["objective"] - rl["objective"])
-    if R.available("fast"):
+    if R.available("fast") and K.nbytes <= 32 << 30:  # C4: no room for the column-major copy
         xf, rf, recf = R.RefOperator(K, "fast").gpss_solve(y, rho, O.GpConfig(), stop)
         same_recs = len(recf) == len(recl) and all(
             all((a[f] == b[f]) or (np.isnan(a[f]) and np.isnan(b[f]))
