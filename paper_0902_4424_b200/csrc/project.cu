@@ -729,7 +729,8 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   // x and g in the coalesced order (j = tid + PT*i), kept for the final pass when small
   constexpr bool KEEP = M <= L1G_PROJ_KEEP;
   constexpr int LB = M < 8 ? M : 8;  // loads in flight per vector and thread
-  constexpr int UB = VS ? 1 : M / LB;  // batches of coalesced loads (VS: one batch's addresses live)
+  constexpr int UB = VS ? 1 : M / LB;  // batches unrolled (VS: one batch's addresses live)
+  constexpr int UBV = VS ? (M >= 32 ? 2 : 1) : M / LB;  // the first pass: two for M = 32
   double xr[KEEP ? M : 1], gr[KEEP ? M : 1];
   if (KEEP) {
 #pragma unroll
@@ -745,7 +746,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
     // ---- v = x - alpha g  (gpss.cpp:167; alpha0: x0 - grad, gpss.cpp:95): coalesced
     //      loads (issued in batches of LB per vector, all in flight before the first use),
     //      staged through shared memory into per-thread registers
-#pragma unroll UB
+#pragma unroll UBV
     for (int i0 = 0; i0 < M; i0 += LB) {
       double xb[LB], gb[LB];
       load_batch<LB, KEEP>(xb, gb, xr, gr, x, g, i0, tid, base, lim, a.mode != PROJ_PLAIN);
