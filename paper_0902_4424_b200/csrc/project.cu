@@ -47,7 +47,7 @@ namespace l1g {
 
 constexpr int PT = 512;
 constexpr int PW = PT / 32;
-constexpr int MAX_M = 32;
+constexpr int MAX_M = 128;  // M > 32: v in global scratch (p up to 1 048 576)
 constexpr int MAX_CS = 16;
 constexpr int64_t SMEM_CAND = 16384;             // candidates sortable in shared memory
 
@@ -60,7 +60,7 @@ struct ProjArgs {
   const double* gin;
   double* out;
   double* gcand;  // global scratch: candidates (next_pow2(p_pad) + 1)
-  double* gpre;   // global scratch: sequential prefix sums (p_pad + 2)
+  double* gpre;   // global scratch: v of M > 32 plans (2 next_pow2(p_pad) + 2)
   DevState* st;
   VecBufs vb;
   // batched runs: cluster k projects problem k (vectors bstride apart, states consecutive)
@@ -269,10 +269,11 @@ __device__ void bitonic_desc(P c, int n2) {
 // live (a full unroll would hold all M leaves in registers); the value is the same tree.
 template <int M, bool VS, class F>
 __device__ __forceinline__ double run_tree(const F& leaf) {
+  static_assert(M < 256, "run_tree: the counter holds fewer than 2^8 leaves");
   if constexpr (!VS || M <= 8) {
     return tree<M>(leaf);
   } else {
-    Counter<6> c;
+    Counter<8> c;  // M <= 128 leaves (< 2^8)
 #pragma unroll 1
     for (int grp = 0; grp < M / 8; ++grp) c.template push_node<3>(tree<8>(leaf, grp * 8), (uint32_t)grp);
     return c.final_value((uint32_t)(M / 8) << 3);
@@ -720,10 +721,14 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   constexpr bool VS = M >= L1G_PROJ_VS_MIN;
   constexpr int UK = VS ? 4 : M;  // unroll of the passes over v (register arrays need all M)
   double vr[VS ? 1 : M] = {};
-  double* const cand = dyn + (VS ? LS : 0);  // candidate buffer (sort, gather, prefix)
-  auto VG = [&](int k) -> double { return VS ? dyn[swz<M>(tid * M + k)] : vr[VS ? 0 : k]; };
+  // beyond M = 32 (p > 262 144) v does not fit in shared memory beside the candidates: it
+  // lives in the L2-resident global scratch, the CTA's slice at its cluster offset
+  constexpr bool VGLOB = M > 32;
+  double* const vbuf = VGLOB ? a.gpre + prob * a.scr_stride + base : dyn;
+  double* const cand = dyn + ((VS && !VGLOB) ? LS : 0);  // candidate buffer (sort, gather, prefix)
+  auto VG = [&](int k) -> double { return VS ? vbuf[swz<M>(tid * M + k)] : vr[VS ? 0 : k]; };
   auto VSET = [&](int k, double val) {
-    if (VS) dyn[swz<M>(tid * M + k)] = val;
+    if (VS) vbuf[swz<M>(tid * M + k)] = val;
     else vr[VS ? 0 : k] = val;
   };
   // x and g in the coalesced order (j = tid + PT*i), kept for the final pass when small
@@ -759,13 +764,13 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
           else if (a.mode == PROJ_ALPHA0) val = sub(xb[b], gb[b]);
           else val = sub(xb[b], mul(alpha, gb[b]));
         }
-        dyn[swz<M>((int)j)] = val;
+        vbuf[swz<M>((int)j)] = val;
       }
     }
     __syncthreads();
     if (!VS) {
 #pragma unroll
-      for (int k = 0; k < M; ++k) VSET(k, dyn[swz<M>(tid * M + k)]);
+      for (int k = 0; k < M; ++k) VSET(k, vbuf[swz<M>(tid * M + k)]);
     }
     __syncthreads();
     double red[2];
@@ -1165,7 +1170,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       // stage h, then coalesced d = h - x (written out) and leaf g_j d_j
       if (!VS) {
 #pragma unroll
-        for (int k = 0; k < M; ++k) dyn[swz<M>(tid * M + k)] = VG(k);
+        for (int k = 0; k < M; ++k) vbuf[swz<M>(tid * M + k)] = VG(k);
       }
       __syncthreads();
       mark(30);
@@ -1177,7 +1182,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
         for (int b = 0; b < LB; ++b) {
           const int64_t j = tid + (int64_t)PT * (i0 + b);
           const int p = swz<M>((int)j);
-          const double h = dyn[p];
+          const double h = vbuf[p];
           double leaf = 0.0;
           bool nz = false;
           if (j < lim) {
@@ -1188,7 +1193,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
             if (a.mode == PROJ_ITER) leaf = mul(gb[b], dj);
             nz = dj != 0.0;
           }
-          dyn[p] = leaf;
+          vbuf[p] = leaf;
           // support bitmap of d for the sparse forward product (whole warps are in or out)
           const unsigned bits = __ballot_sync(0xffffffffu, nz);
           if (a.mode == PROJ_ITER && (tid & 31) == 0 && j < lim) {
@@ -1202,7 +1207,7 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
       if (a.mode == PROJ_ITER) {
         if (!VS) {
 #pragma unroll
-          for (int k = 0; k < M; ++k) VSET(k, dyn[swz<M>(tid * M + k)]);
+          for (int k = 0; k < M; ++k) VSET(k, vbuf[swz<M>(tid * M + k)]);
         }
         gdl = run_tree<M, VS>([&](int k) { return VG(k); });
       }
@@ -1282,14 +1287,16 @@ static int64_t pow2_at_least(int64_t v) {
 // candidates beside v (the 1024 key bins of M >= 16 take 24 KB more static memory).
 static constexpr int64_t vs_cand(int M) { return M >= 16 ? 8192 : SMEM_CAND; }
 static constexpr size_t proj_dyn_bytes(int M) {
-  return M >= L1G_PROJ_VS_MIN ? (size_t)(PT * M + vs_cand(M) + 1) * 8 : (size_t)(SMEM_CAND + 1) * 8;
+  return (M >= L1G_PROJ_VS_MIN && M <= 32) ? (size_t)(PT * M + vs_cand(M) + 1) * 8
+                                           : (size_t)(SMEM_CAND + 1) * 8;
 }
 static void set_proj_smem(ProjPlan& pp) {
   const int M = (int)(pp.ls / PT);
-  if (M >= L1G_PROJ_VS_MIN) {
+  if (M >= L1G_PROJ_VS_MIN && M <= 32) {
     if (pp.cand_cap > vs_cand(M) + 1) pp.cand_cap = vs_cand(M) + 1;
     pp.smem = (size_t)(pp.ls + pp.cand_cap) * 8;
   } else {
+    if (M > 32 && pp.cand_cap > SMEM_CAND + 1) pp.cand_cap = SMEM_CAND + 1;  // v is global
     pp.smem = (size_t)pp.cand_cap * 8;
   }
 }
@@ -1316,8 +1323,9 @@ ProjPlan make_proj_plan(int64_t p_pad) {
   return pp;
 }
 
+// [candidates: next_pow2(p_pad) + 1 | v of M > 32 plans: 2 next_pow2(p_pad) (>= cs * ls)]
 size_t proj_scratch_doubles(int64_t p_pad) {
-  return (size_t)(pow2_at_least(p_pad) + 1) + (size_t)(p_pad + 2) + 64;
+  return (size_t)(pow2_at_least(p_pad) + 1) + (size_t)(2 * pow2_at_least(p_pad) + 2) + 64;
 }
 
 template <int M>
@@ -1353,6 +1361,8 @@ static void proj_dispatch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s,
     case 8: proj_launch<8>(pp, a, s, nprob); break;
     case 16: proj_launch<16>(pp, a, s, nprob); break;
     case 32: proj_launch<32>(pp, a, s, nprob); break;
+    case 64: proj_launch<64>(pp, a, s, nprob); break;
+    case 128: proj_launch<128>(pp, a, s, nprob); break;
     default: throw InvalidArgument("projection: unsupported slice length");
   }
 }

@@ -91,6 +91,37 @@ def test_projection_large(p):
             assert np.array_equal(pr.point, u)
 
 
+@pytest.mark.parametrize("p", [400000, 1048576])
+def test_projection_beyond_shared_memory(p):
+    """p > 262 144: the cluster keeps v in the L2-resident global scratch (M = 64, 128)."""
+    rng = np.random.default_rng(p)
+    x = rng.normal(size=p)
+    for frac in (0.5, 0.02):
+        rho = frac * float(np.abs(x).sum())
+        u, th, sup = O.project_l1(x, rho)
+        pr = l1.project_l1_ball_with_threshold(x, l1.L1Ball(rho))
+        assert pr.threshold == th and pr.support == sup
+        assert np.array_equal(pr.point, u)
+
+
+def test_trajectory_beyond_shared_memory():
+    """A whole solve with p = 600 000 (projection with v in global scratch) equals the oracle."""
+    spec = O.ProblemSpec("gaussian", 64, 600000, 40, 31, "normal", 1e-2, "rel",
+                         sigma_hat=800.0, name="wide")
+    P = O.build_problem(spec)
+    iters = 25
+    xo, ro, reco, _ = O.gpss_solve(P["K"], P["y"], P["rho"], O.GpConfig(),
+                                   O.StopRule(iters, 0, 0, 0.0))
+    trace = []
+    sol = l1.gpss_solve(l1.Objective(l1.DenseOperator(P["K"]), P["y"]), l1.L1Ball(P["rho"]),
+                        l1.GpConfig(), l1.StopRule(max_iterations=iters, stationarity_tol=0.0),
+                        trace=trace)
+    assert sol.iterations == ro["iterations"]
+    assert np.array_equal(sol.x, xo), float(np.abs(sol.x - xo).max())
+    assert [r.f for r in trace] == [r["f"] for r in reco]
+    assert [r.support for r in trace] == [r["support"] for r in reco]
+
+
 @pytest.mark.parametrize("p", [65536, 262144])
 def test_projection_cluster_prefix_ties(p):
     """The cluster-wide exact prefix (> 8192 candidates, project.cu prefix_break_cluster) on
