@@ -47,7 +47,7 @@ namespace l1g {
 
 constexpr int PT = 512;
 constexpr int PW = PT / 32;
-constexpr int MAX_M = 128;  // M > 32: v in global scratch (p up to 1 048 576)
+constexpr int MAX_M = 512;  // M > 32: v in global scratch (p up to 4 194 304)
 constexpr int MAX_CS = 16;
 constexpr int64_t SMEM_CAND = 16384;             // candidates sortable in shared memory
 
@@ -269,11 +269,11 @@ __device__ void bitonic_desc(P c, int n2) {
 // live (a full unroll would hold all M leaves in registers); the value is the same tree.
 template <int M, bool VS, class F>
 __device__ __forceinline__ double run_tree(const F& leaf) {
-  static_assert(M < 256, "run_tree: the counter holds fewer than 2^8 leaves");
+  constexpr int L = M <= 128 ? 8 : (M <= 256 ? 9 : 10);  // the counter holds < 2^L leaves
   if constexpr (!VS || M <= 8) {
     return tree<M>(leaf);
   } else {
-    Counter<8> c;  // M <= 128 leaves (< 2^8)
+    Counter<L> c;
 #pragma unroll 1
     for (int grp = 0; grp < M / 8; ++grp) c.template push_node<3>(tree<8>(leaf, grp * 8), (uint32_t)grp);
     return c.final_value((uint32_t)(M / 8) << 3);
@@ -1363,6 +1363,8 @@ static void proj_dispatch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s,
     case 32: proj_launch<32>(pp, a, s, nprob); break;
     case 64: proj_launch<64>(pp, a, s, nprob); break;
     case 128: proj_launch<128>(pp, a, s, nprob); break;
+    case 256: proj_launch<256>(pp, a, s, nprob); break;
+    case 512: proj_launch<512>(pp, a, s, nprob); break;
     default: throw InvalidArgument("projection: unsupported slice length");
   }
 }

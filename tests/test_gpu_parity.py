@@ -91,9 +91,9 @@ def test_projection_large(p):
             assert np.array_equal(pr.point, u)
 
 
-@pytest.mark.parametrize("p", [400000, 1048576])
+@pytest.mark.parametrize("p", [400000, 1048576, 3000000])
 def test_projection_beyond_shared_memory(p):
-    """p > 262 144: the cluster keeps v in the L2-resident global scratch (M = 64, 128)."""
+    """p > 262 144: the cluster keeps v in the L2-resident global scratch (M = 64 .. 512)."""
     rng = np.random.default_rng(p)
     x = rng.normal(size=p)
     for frac in (0.5, 0.02):
