@@ -879,7 +879,9 @@ void solver_iterate(l1g_solver* s, double tol, l1g_iter_record* info, int32_t* s
 }
 
 l1g_op* op_alloc(l1g_ctx* ctx, int64_t n, int64_t p) {
-  if (n < 1 || p < 1) throw InvalidArgument("DenseOperator: dimensions must be positive");
+  // empty operators are valid, as in the reference (an Eigen matrix with no rows or no
+  // columns): the padded tiles are zeros and every product is exactly zero
+  if (n < 0 || p < 0) throw InvalidArgument("DenseOperator: dimensions must be non-negative");
   set_device(ctx);
   auto* op = new l1g_op();
   op->c = ctx;
@@ -1637,6 +1639,10 @@ int l1g_op_create_dense(l1g_ctx* c, const double* K, int64_t n, int64_t p, int r
     l1g_op* op = op_alloc(c, n, p);
     try {
       const GemvPlan& pl = op->plan;
+      if (n == 0 || p == 0) {  // nothing to upload: the zero-filled padding is the operator
+        *out = op;
+        return;
+      }
       // stream row blocks through a bounded device buffer (<= 256 MB)
       int64_t chunk = std::max<int64_t>(TR, ((int64_t)(256 << 20) / (p * 8)) / TR * TR);
       chunk = std::min<int64_t>(chunk, pad_to(n, TR));

@@ -332,3 +332,21 @@ def test_operator_extreme_magnitudes():
             op = l1.DenseOperator(K)
             assert np.array_equal(op.apply(x), O.apply(K, x)), (n, p, kscale)
             assert np.array_equal(op.apply_adjoint(r), O.apply_adjoint(K, r)), (n, p, kscale)
+
+
+@pytest.mark.parametrize("n,p", [(3, 0), (0, 4), (1, 1)])
+def test_empty_and_degenerate_shapes(n, p):
+    """Empty operators and vectors (prox.cpp:38-73 on an empty x; gp_init / gp_iterate with no
+    columns or no rows): the reference stops stationary at k = 0 (oracle and reference sources
+    agree); the drop-in does the same with the same x and objective."""
+    rng = np.random.default_rng(n * 10 + p)
+    K = rng.normal(size=(n, p))
+    y = rng.normal(size=n)
+    xo, ro, _, _ = O.gpss_solve(K, y, 1.0, O.GpConfig(), O.StopRule(10, 0, 0, 0.0))
+    sol = l1.gpss_solve(l1.Objective(l1.DenseOperator(K), y), l1.L1Ball(1.0), l1.GpConfig(),
+                        l1.StopRule(max_iterations=10, stationarity_tol=0.0))
+    assert sol.iterations == ro["iterations"] and int(sol.reason) == ro["reason"]
+    assert np.array_equal(sol.x, xo) and sol.objective == ro["objective"]
+    u, th, sup = O.project_l1(np.zeros(p), 1.0)
+    pr = l1.project_l1_ball_with_threshold(np.zeros(p), l1.L1Ball(1.0))
+    assert np.array_equal(pr.point, u) and pr.threshold == th and pr.support == sup
