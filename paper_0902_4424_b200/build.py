@@ -6,7 +6,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["gemv.cu", "dmma.cu", "project.cu", "vec.cu", "comm.cu", "abi.cu"]
+SOURCES = ["gemv.cu", "dmma.cu", "project.cu", "small.cu", "vec.cu", "comm.cu", "abi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-fmad=false", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-ldl"]

@@ -249,6 +249,7 @@ struct l1g_solver {
   bool timing = false;
   bool fwd_sparse = true;  // forward product over the support of d only (gemv.cu)
   bool fwd_switch = true;  // ... switching to the dense stream on the device when d is dense
+  bool small_iter = false; // K within one cluster's shared memory: small.cu runs the step
   std::vector<cudaEvent_t> tev;
   double t_proj = 0.0, t_fwd = 0.0, t_adj = 0.0;
   int64_t t_iters = 0, launches = 0;
@@ -377,6 +378,9 @@ l1g_solver* solver_new(l1g_op* op, const l1g_gp_config& cfg, double rho, int nra
       const char* e = getenv("L1G_FWD");
       s->fwd_sparse = !(e && std::strcmp(e, "dense") == 0);
       s->fwd_switch = !(e && std::strcmp(e, "sparse") == 0);
+      const char* es = getenv("L1G_SMALL");
+      s->small_iter = !(nranks > 1 || sharded) && small_iter_fits(pl) &&
+                      !(es && std::strcmp(es, "0") == 0);
     }
     s->y = dalloc<double>(pl.n_pad);
     s->vb.y = s->y;
@@ -480,7 +484,7 @@ void exchange(l1g_solver* s, int which) {
 
 // kernels (and exchanges) one iteration or gp_init enqueues, for launch accounting
 int64_t kernels_per_iteration(l1g_solver* s) {
-  return s->split() ? 6 * (int64_t)members(s).size() + (s->comm ? 2 : 0) : 5;
+  return s->split() ? 6 * (int64_t)members(s).size() + (s->comm ? 2 : 0) : (s->small_iter ? 2 : 5);
 }
 
 // gpss.cpp:117-134
@@ -547,6 +551,12 @@ void enqueue_iteration(l1g_solver* s, Mark mark) {
                 q->d_full ? &q->vbp : &q->vb, s->stream, 1, 0,
                 q->d_full ? q->scal_all : nullptr, q->nranks);
   mark(1);
+  if (!s->split() && s->small_iter) {  // forward, line search, adjoint and step: one kernel
+    launch_small_iter(*s->op, &s->vb, s->st, s->stream);
+    mark(2);
+    mark(3);
+    return;
+  }
   if (!s->split()) {
     launch_fwd(*s->op, s->ws, FWD_ITER, nullptr, nullptr, &s->vb, s->st, s->stream, s->fwd_sparse,
                s->fwd_switch);

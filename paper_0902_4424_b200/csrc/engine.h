@@ -172,6 +172,10 @@ BatchPlan make_batch_plan(const GemvPlan& pl, int B, int sm_count);
 void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* part, cudaStream_t s);
 void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* part, cudaStream_t s);
 
+// small problems (small.cu): the whole step after the projection as one cluster kernel
+bool small_iter_fits(const GemvPlan& pl);
+void launch_small_iter(const Op& op, const VecBufs* vb, DevState* st, cudaStream_t s);
+
 // host launchers (gemv.cu, project.cu)
 GemvPlan make_plan(int64_t n, int64_t p, int sm_count);
 void launch_fwd(const Op& op, const Workspace& ws, int mode, const double* vin, double* vout, const VecBufs* vb,

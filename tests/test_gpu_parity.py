@@ -350,3 +350,24 @@ def test_empty_and_degenerate_shapes(n, p):
     u, th, sup = O.project_l1(np.zeros(p), 1.0)
     pr = l1.project_l1_ball_with_threshold(np.zeros(p), l1.L1Ball(1.0))
     assert np.array_equal(pr.point, u) and pr.threshold == th and pr.support == sup
+
+
+def test_small_step_kernel_and_large_path_identical(monkeypatch):
+    """C1-sized problems run the step after the projection as one cluster kernel (small.cu);
+    the five-kernel large path (L1G_SMALL=0) must give the same bits, both equal to the oracle."""
+    P = O.build_problem(PB.C1)
+    iters = 60
+    xo, ro, reco, _ = O.gpss_solve(P["K"], P["y"], P["rho"], O.GpConfig(),
+                                   O.StopRule(iters, 0, 0, 0.0))
+    out = []
+    for small in ("1", "0"):
+        monkeypatch.setenv("L1G_SMALL", small)
+        trace = []
+        sol = l1.gpss_solve(l1.Objective(l1.DenseOperator(P["K"]), P["y"]), l1.L1Ball(P["rho"]),
+                            l1.GpConfig(), l1.StopRule(max_iterations=iters, stationarity_tol=0.0),
+                            trace=trace)
+        assert sol.iterations == ro["iterations"]
+        assert np.array_equal(sol.x, xo)
+        assert [r.f for r in trace] == [r["f"] for r in reco]
+        out.append(sol)
+    assert np.array_equal(out[0].x, out[1].x)
