@@ -299,6 +299,10 @@ int l1g_gpss_solve_batched(l1g_op* op, int B, const double* Y, const double* rho
  *   0 = dense streaming pass over all of K.
  * Environment L1G_FWD=dense / L1G_FWD=sparse set 0 / 2 at creation. */
 int l1g_solver_set_forward(l1g_solver* s, int sparse);
+/* 1 if the solver runs the step after the projection as the one-cluster small-problem kernel
+ * (K within one cluster's shared memory: n_pad <= 384, p_pad <= 1024; L1G_SMALL=0 disables),
+ * 0 if it runs the large path's four kernels */
+int l1g_solver_small_path(l1g_solver* s, int* small);
 /* projection phase profile accumulated since gp_init (32 doubles): [0..7] SM cycles per
  * phase, [8] calls, [9] attempts, [10] pivot rounds, [11] candidates, [12] bumps,
  * [13] retries, [14..17], [21], [22] sub-phases of the cluster sort, [18..19] sparse

@@ -156,6 +156,7 @@ _SIGS = {
     "l1g_solver_destroy": (None, [_vp]),
     "l1g_solver_set_timing": (C.c_int, [_vp, C.c_int]),
     "l1g_solver_set_forward": (C.c_int, [_vp, C.c_int]),
+    "l1g_solver_small_path": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "l1g_solver_proj_profile": (C.c_int, [_vp, _dp]),
     "l1g_solver_timing": (C.c_int, [_vp, _dp, _dp, _dp, C.POINTER(_i64), C.POINTER(_i64),
                                     C.c_int]),

@@ -2298,6 +2298,11 @@ int l1g_solver_set_timing(l1g_solver* s, int on) {
   });
 }
 
+int l1g_solver_small_path(l1g_solver* s, int* small) {
+  *small = s->small_iter ? 1 : 0;
+  return L1G_OK;
+}
+
 int l1g_solver_set_forward(l1g_solver* s, int sparse) {
   return guarded([&] {
     set_device(s->op->c);

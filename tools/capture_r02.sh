@@ -6,7 +6,7 @@
 set -x
 mkdir -p gpurun_out
 O=gpurun_out
-what="${*:-c4launch c4full c2full c5full}"
+what="${*:-c4launch c4full c2full c2launch c5full c5launch}"
 for w in $what; do
 case $w in
 c4launch)  # the bench default (C4): every launch of one timed solve, cold-cache, serialised
@@ -25,6 +25,8 @@ c2full)
   ncu --set full --import-source on --clock-control none \
       -k regex:"adj_kernel|fwd_sparse|proj_kernel|fwd_finish|adj_finish" -s 200 -c 5 \
       -o $O/full_c2 -f python tools/prof_solve.py --config C2 --iters 60 > $O/ncu_full_c2.log 2>&1
+  ;;
+c2launch)
   python tools/prof_solve.py --config C2 --iters 80 > $O/plain_c2l.log 2>&1 &&
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launch_c2.csv \
       python tools/prof_solve.py --config C2 --iters 80 > $O/ncu_launch_c2.log 2>&1
@@ -33,6 +35,8 @@ c5full)
   python tools/prof_batch.py --iters 5 --solves 1 > $O/plain_c5f.log 2>&1 &&
   ncu --set full --import-source on --clock-control none -k regex:"bfwd|badj|proj_kernel|bfin" \
       -s 12 -c 6 -o $O/full_c5 -f python tools/prof_batch.py --iters 5 --solves 1 > $O/ncu_full_c5.log 2>&1
+  ;;
+c5launch)
   python tools/prof_batch.py --iters 20 --solves 1 > $O/plain_c5l.log 2>&1 &&
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launch_c5.csv \
       python tools/prof_batch.py --iters 20 --solves 1 > $O/ncu_launch_c5.log 2>&1

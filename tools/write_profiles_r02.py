@@ -69,7 +69,7 @@ def main():
             kn = o["kernel"].split("<")[0]
             key = {"adj_kernel": "adj", "fwd_sparse_kernel": "fwd_sparse", "fwd_kernel": "fwd",
                    "bfwd_wide_kernel": "bfwd", "badj_wide_kernel": "badj", "bfwd_kernel": "bfwd",
-                   "badj_kernel": "badj"}.get(kn)
+                   "badj_kernel": "badj", "bfwd_ws_kernel": "bfwd", "badj_ws_kernel": "badj"}.get(kn)
             if key:
                 tr[f"{k.upper()}_{key}"] = dram_bytes(o)
                 if key == "fwd_sparse":  # the bench's dominant-kernel key for the forward
