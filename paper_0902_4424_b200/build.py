@@ -45,13 +45,33 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def _compile_link(out: str, defines: list[str], verbose: bool):
+    """One nvcc per source file, run side by side, then one link."""
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+    cflags = [f for f in FLAGS if f not in ("-shared", "-cudart", "static", "-ldl")]
+    with tempfile.TemporaryDirectory(prefix="l1g_build_") as tmp:
+        objs = [os.path.join(tmp, s.replace(".cu", ".o")) for s in SOURCES]
+        cmds = [[NVCC, *cflags, *defines, "-c", os.path.join(CSRC, s), "-o", o]
+                for s, o in zip(SOURCES, objs)]
+        if verbose:
+            for c in cmds:
+                print(" ".join(c))
+        with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+            for r in ex.map(lambda c: subprocess.run(c), cmds):
+                if r.returncode != 0:
+                    raise subprocess.CalledProcessError(r.returncode, r.args)
+        link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC", "-shared",
+                "-cudart", "static", "-ldl", "-o", out, *objs]
+        if verbose:
+            print(" ".join(link))
+        subprocess.run(link, check=True)
+
+
 def build(force: bool = False, verbose: bool = False):
     if not force and not needs_build():
         return lib_path()
-    cmd = [NVCC, *FLAGS, "-o", lib_path(), *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+    _compile_link(lib_path(), [], verbose)
     build_dropin(verbose)
     return lib_path()
 
@@ -60,10 +80,7 @@ def build_variant(name: str, defines: list[str], verbose: bool = False) -> str:
     """Debug variants (e.g. -DL1G_TIMELINE) as lib<name>.so next to libl1g.so; loaded through
     L1G_LIB_PATH by the profiling tools only."""
     out = os.path.join(HERE, f"lib{name}.so")
-    cmd = [NVCC, *FLAGS, *defines, "-o", out, *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+    _compile_link(out, defines, verbose)
     return out
 
 
