@@ -143,17 +143,127 @@ def one_projection(rng, case):
     return desc, bad
 
 
+def one_shard(rng, case):
+    """Column-sharded in-process group (R shards in lockstep on one GPU, power-of-two shard
+    widths) against the one-GPU solve: bit-identical trajectories."""
+    from paper_0902_4424_b200 import _lib as L
+    from paper_0902_4424_b200 import shard as S
+    R = int(rng.choice([2, 4, 8]))
+    w = int(rng.choice([256, 512, 1024]))
+    p = R * w
+    n = draw_dim(rng, EDGES_N, 400)
+    K = rng.normal(size=(n, p)) / np.sqrt(max(n, p))
+    nnz = int(rng.integers(1, 40))
+    xt = np.zeros(p)
+    xt[rng.choice(p, size=nnz, replace=False)] = rng.normal(size=nnz)
+    y = K @ xt + rng.normal(size=n) * 1e-2
+    rho = float(np.abs(xt).sum()) * float(rng.choice([0.0, 0.3, 1.0, 1.0, 3.0]))
+    cfg = l1.GpConfig(memory=int(rng.choice([1, 3, 10])))
+    iters = int(rng.choice([1, 2, 30, 90]))
+    tol = float(rng.choice([0.0, 0.0, 1e-6]))
+    fwd_mode = int(rng.choice([0, 1, 2]))
+    x0 = None
+    if rng.random() < 0.3 and rho > 0:
+        x0 = rng.normal(size=p)
+        x0 *= 0.5 * rho / float(np.abs(x0).sum())
+    desc = dict(case=case, kind="shard", n=n, p=p, R=R, rho=rho, iters=iters, tol=tol,
+                memory=cfg.memory, fwd=fwd_mode, x0=x0 is not None)
+    stop = l1.StopRule(max_iterations=iters, stationarity_tol=tol)
+    trace = []
+    sol = l1.gpss_solve(l1.Objective(l1.DenseOperator(K), y), l1.L1Ball(rho), cfg, stop, x0=x0,
+                        trace=trace)
+    ops = [l1.DenseOperator(np.ascontiguousarray(K[:, sh.cols])) for sh in S.shard_plan(p, R)]
+    h = S.create_group_solver(ops, y, rho, cfg)
+    try:
+        L.check(L.load().l1g_solver_set_forward(h, fwd_mode))
+        res, recs = S.solve(h, stop, x0=x0, trace_cap=iters + 1)
+        x = S.solver_x(h, p)
+    finally:
+        L.load().l1g_solver_destroy(h)
+    bad = []
+    if res.iterations != sol.iterations:
+        bad.append(("iterations", res.iterations, sol.iterations))
+    if res.reason != int(sol.reason):
+        bad.append(("reason", res.reason, int(sol.reason)))
+    if not np.array_equal(x, sol.x):
+        bad.append(("x", float(np.abs(x - sol.x).max())))
+    if not same(res.objective, sol.objective):
+        bad.append(("objective", res.objective, sol.objective))
+    for a, b in zip(recs, trace):
+        for f in ["k", "f", "stationarity", "alpha", "step", "matvecs", "bb_active", "halvings",
+                  "theta", "support", "f_max", "dir_derivative"]:
+            if not same(getattr(a, f), getattr(b, f)):
+                bad.append((f"rec[{b.k}].{f}", getattr(a, f), getattr(b, f)))
+                break
+        if bad:
+            break
+    return desc, bad
+
+
+def one_other(rng, case):
+    """psd / ista / fista device drivers against the oracle, bit for bit."""
+    n = draw_dim(rng, EDGES_N, 400)
+    p = draw_dim(rng, EDGES_P, 3000)
+    K = rng.normal(size=(n, p)) / np.sqrt(max(n, p))
+    nnz = int(rng.integers(0, min(p, 30) + 1))
+    xt = np.zeros(p)
+    if nnz:
+        xt[rng.choice(p, size=nnz, replace=False)] = rng.normal(size=nnz)
+    y = K @ xt + rng.normal(size=n) * 1e-2
+    solver = str(rng.choice(["psd", "ista", "fista"]))
+    iters = int(rng.choice([1, 5, 60]))
+    tol = float(rng.choice([0.0, 1e-7]))
+    ostop = O.StopRule(iters, 0, 0, tol, 1e-12 if tol else 0.0)
+    stop = l1.StopRule(max_iterations=iters, stationarity_tol=tol,
+                       objective_tol=1e-12 if tol else 0.0)
+    obj = l1.Objective(l1.DenseOperator(K), y)
+    trace = []
+    desc = dict(case=case, kind="other", solver=solver, n=n, p=p, iters=iters, tol=tol)
+    if solver == "psd":
+        rho = (float(np.abs(xt).sum()) or 1.0) * float(rng.choice([0.0, 0.5, 1.0, 2.0]))
+        desc["rho"] = rho
+        xo, ro, reco = O.psd_solve(K, y, rho, ostop)
+        sol = l1.psd_solve(obj, l1.L1Ball(rho), stop, trace=trace)
+    else:
+        lam = float(rng.choice([0.01, 0.05, 0.5, 1.5])) * float(np.abs(O.apply_adjoint(K, y)).max())
+        desc["lam"] = lam
+        xo, ro, reco = O.shrinkage_solve(K, y, lam, solver == "fista", ostop)
+        fn = l1.fista_solve if solver == "fista" else l1.ista_solve
+        sol = fn(obj, l1.PenaltyWeight(lam), stop, trace=trace)
+    bad = []
+    if sol.iterations != ro["iterations"] or int(sol.reason) != ro["reason"]:
+        bad.append(("stop", sol.iterations, ro["iterations"], int(sol.reason), ro["reason"]))
+    if not np.array_equal(sol.x, xo):
+        bad.append(("x", float(np.abs(sol.x - xo).max())))
+    if not same(sol.objective, ro["objective"]):
+        bad.append(("objective", sol.objective, ro["objective"]))
+    for a, b in zip(trace, reco):
+        for f in ["k", "f", "stationarity", "alpha", "step", "matvecs"]:
+            if not same(getattr(a, f), b[f]):
+                bad.append((f"rec[{b['k']}].{f}", getattr(a, f), b[f]))
+                break
+        if bad:
+            break
+    return desc, bad
+
+
+KINDS = {"solve": one_solve, "projection": one_projection, "shard": one_shard, "other": one_other}
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--kinds", default="solve,projection",
+                    help="comma list of solve, projection, shard, other")
     ap.add_argument("--seconds", type=float, default=60.0)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     rng = np.random.default_rng(args.seed)
     t0 = time.time()
-    cases, failures, counts = 0, [], {"solve": 0, "projection": 0}
+    kinds = args.kinds.split(",")
+    cases, failures, counts = 0, [], {k: 0 for k in kinds}
     while time.time() - t0 < args.seconds:
-        fn = one_solve if rng.random() < 0.6 else one_projection
+        fn = KINDS[kinds[int(rng.integers(0, len(kinds)))]]
         desc, bad = fn(rng, cases)
         counts[desc["kind"]] += 1
         cases += 1
