@@ -938,6 +938,7 @@ struct l1g_batch {
   unsigned* counters = nullptr;
   int* nrun = nullptr;
   int* nrun_host = nullptr;
+  int* active = nullptr;  // [Bp] live problems in index order, then their count (bcompact_kernel)
   cudaGraphExec_t gexec = nullptr;
   cudaGraphExec_t gloop = nullptr;  // WHILE (live problems) { gsize lockstep iterations }
   bool gloop_tried = false;
@@ -970,6 +971,7 @@ void batch_free(l1g_batch* b) {
   dfree(b->st);
   dfree(b->counters);
   dfree(b->nrun);
+  dfree(b->active);
   if (b->nrun_host) cudaFreeHost(b->nrun_host);
   if (b->stream) cudaStreamDestroy(b->stream);
   delete b;
@@ -1021,6 +1023,7 @@ l1g_batch* batch_new(l1g_op* op, int B, const double* Y, const double* rho,
     b->st = dalloc<DevState>(B);
     b->counters = dalloc<unsigned>(B);
     b->nrun = dalloc<int>(1);
+    b->active = dalloc<int>(Bp + 1);
     L1G_CUDA(cudaHostAlloc(&b->nrun_host, 64, cudaHostAllocDefault));
     L1G_CUDA(cudaMemcpy2DAsync(b->y, pl.n_pad * 8, Y, pl.n * 8, pl.n * 8, B,
                                cudaMemcpyHostToDevice, b->stream));
@@ -1049,15 +1052,32 @@ BFinArgs bfin_args(l1g_batch* b, int mode, bool adjoint) {
   return a;
 }
 
+bool batch_compaction() {
+  static const bool on = [] {
+    const char* e = getenv("L1G_BATCH_COMPACT");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
+// kernels of one lockstep iteration: proj, (compaction), bfwd, bfin_fwd, brupdate, badj, bfin_adj
+int batch_iteration_kernels() { return batch_compaction() ? 7 : 6; }
+
 void batch_products(l1g_batch* b, int fmode, const double* D, int amode, const double* R,
                     bool rupdate, bool proj_first) {
   const GemvPlan& pl = b->op->plan;
   cudaStream_t s = b->stream;
+  // an iteration's products run on the live problems only, compacted into the leading columns
+  // (stopped problems keep their slabs; whole problem blocks, warp groups and tiles without a
+  // live problem are skipped); L1G_BATCH_COMPACT=0 keeps every problem in place
+  const bool compact = proj_first && batch_compaction();
+  const int* act = compact ? b->active : nullptr;
+  const int* nact = compact ? b->active + b->bp.Bp : nullptr;
   if (proj_first)
     launch_proj(b->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, b->pscr, b->st,
                 &b->vb, s, b->B, b->scr_stride);
+  if (compact) launch_bcompact(b->st, b->B, b->active, b->active + b->bp.Bp, s);
   if (D) {
-    launch_bfwd(*b->op, b->bp, D, b->part, s);
+    launch_bfwd(*b->op, b->bp, D, b->part, s, act, nact);
     launch_bfin(bfin_args(b, fmode, false), false, pl.n_pad, s);
   } else {  // gp_init from X0 = 0: K X0 is exactly zero (see launch_fwd_init_zero)
     BFinArgs fa = bfin_args(b, fmode, false);
@@ -1066,7 +1086,7 @@ void batch_products(l1g_batch* b, int fmode, const double* D, int amode, const d
     launch_bfin(fa, false, pl.n_pad, s);
   }
   if (rupdate) launch_brupdate(bfin_args(b, fmode, false), b->rn, s);
-  launch_badj(*b->op, b->bp, R, b->part, s);
+  launch_badj(*b->op, b->bp, R, b->part, s, act, nact);
   launch_bfin(bfin_args(b, amode, true), true, pl.p_pad, s);
 }
 
@@ -1155,11 +1175,11 @@ void batch_run(l1g_batch* b, const l1g_stop_rule& stop, l1g_result* res, bool re
     L1G_CUDA(cudaGraphLaunch(b->gloop, s));
     L1G_CUDA(cudaMemcpyAsync(&k1, &b->st->k, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     L1G_CUDA(cudaStreamSynchronize(s));
-    b->launches += ((k1 - k0) / b->gsize + 1) * (6LL * b->gsize + 1);
+    b->launches += ((k1 - k0) / b->gsize + 1) * ((int64_t)batch_iteration_kernels() * b->gsize + 1);
   }
   for (int64_t launched = 0; live > 0 && !b->gloop;) {
     L1G_CUDA(cudaGraphLaunch(b->gexec, s));
-    b->launches += 6LL * b->gsize;
+    b->launches += (int64_t)batch_iteration_kernels() * b->gsize;
     L1G_CUDA(cudaMemcpyAsync((void*)flag, b->nrun, sizeof(int), cudaMemcpyDeviceToHost, s));
     L1G_CUDA(cudaStreamSynchronize(s));
     ++launched;

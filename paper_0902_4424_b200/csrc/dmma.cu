@@ -388,6 +388,35 @@ __device__ __forceinline__ void cp_arrive_noinc(uint64_t* bar) {
 struct WsItem {
   int x, y, z;
 };
+// Live-problem compaction (BGemmArgs::active / nact): the product's column j of problem
+// block b0 is problem active[b0 + j]; columns past the live count are not computed.
+__device__ __forceinline__ int ws_live(int na, int b0) {
+  const int nl = na - b0;
+  return nl < 0 ? 0 : (nl > BW ? BW : nl);
+}
+__device__ __forceinline__ int ws_tiles(int nl, int wc) {  // live 8-problem tiles of group wc
+  const int wl = nl - wc * 32;
+  return wl <= 0 ? 0 : (wl >= 32 ? 4 : (wl + 7) >> 3);
+}
+__device__ __forceinline__ int64_t ws_problem(const int* active, int b0, int j) {
+  return active ? (int64_t)__ldg(active + b0 + j) : (int64_t)(b0 + j);
+}
+// the producer warp's table of source rows (columns past the live count repeat the last one,
+// so a partly live tile reads valid memory)
+// Returns true when the block is whole and in place (column j is problem b0 + j): the copies
+// then use plain strides instead of the table.
+__device__ __forceinline__ bool ws_fill_rows(int* s_act, const int* active, int b0, int nl, int lane) {
+  __syncwarp();
+  bool same = nl == BW;
+  for (int j = lane; j < BW; j += 32) {
+    const int jj = j < nl ? j : nl - 1;
+    const int b = active ? __ldg(active + b0 + jj) : b0 + jj;
+    s_act[j] = b;
+    same &= b == b0 + j;
+  }
+  __syncwarp();
+  return __all_sync(0xffffffffu, same);
+}
 __device__ __forceinline__ WsItem ws_item(int it, int nx, int ny) {
   WsItem w;
   w.x = it % nx;
@@ -396,10 +425,13 @@ __device__ __forceinline__ WsItem ws_item(int it, int nx, int ny) {
   return w;
 }
 
-__global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
-  pdl_wait_and_trigger();
+// CP = false: every problem live and in place (the code without any of the compaction);
+// CP = true: columns gathered through active[], dead blocks / groups / tiles skipped.
+template <bool CP>
+__device__ __forceinline__ void bfwd_ws_impl(const BGemmArgs& a, const int na) {
   extern __shared__ __align__(16) double sm[];
   __shared__ uint64_t full[W_STAGES], empty[W_STAGES];
+  __shared__ int s_act[CP ? BW : 1];  // producer warp only
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int nchunk = 2 * a.nblocks;  // 32-column chunks
   const int nitems = a.nx * a.ny * a.nz;
@@ -425,6 +457,10 @@ __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
      const WsItem w = ws_item(it, a.nx, a.ny);
      const int64_t rb0 = 4LL * w.x;
      const int b0 = w.z * BW;
+     const int nl = CP ? ws_live(na, b0) : BW;
+     if (CP && nl == 0) continue;  // no live problem in this block (the consumers skip it too)
+     const bool inplace = CP ? ws_fill_rows(s_act, a.active, b0, nl, lane) : true;
+     const int nl8 = (nl + 7) & ~7;
      const int c_begin = w.y * a.per_split, nch = nch_of(w);
      for (int c = 0; c < nch; ++c, ++gc) {
       const int st = gc % W_STAGES;
@@ -432,17 +468,35 @@ __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
       const int64_t ch = c_begin + c, cb = ch >> 1, half = ch & 1;
       const uint32_t so = s_base + (uint32_t)(st * W_STAGE) * 8u;
       const double* gk = a.K + rb0 * k_rs + cb * TILE + half * (TILE / 2);
-      const double* gv = a.V + (int64_t)b0 * a.vstride + ch * 32;
+      const double* gv = a.V + ch * 32;
+      if (!CP || inplace) {
+        const double* gvb = gv + (int64_t)b0 * a.vstride;
 #pragma unroll 4
-      for (int vt = lane; vt < WT; vt += 32) {
-        const uint32_t s_k = so + (uint32_t)kchunk_dst(vt) * 8u;
-        const double* k0 = gk + 2 * vt;
+        for (int vt = lane; vt < WT; vt += 32) {
+          const uint32_t s_k = so + (uint32_t)kchunk_dst(vt) * 8u;
+          const double* k0 = gk + 2 * vt;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) cp16s(s_k + (uint32_t)(r * TR * KP * 8), k0 + r * k_rs);
-        const uint32_t s_v = so + (uint32_t)(W_KS + (vt >> 4) * W_VP + (vt & 15) * 2) * 8u;
-        const double* v0 = gv + (int64_t)(vt >> 4) * a.vstride + (vt & 15) * 2;
+          for (int r = 0; r < 4; ++r) cp16s(s_k + (uint32_t)(r * TR * KP * 8), k0 + r * k_rs);
+          const uint32_t s_v = so + (uint32_t)(W_KS + (vt >> 4) * W_VP + (vt & 15) * 2) * 8u;
+          const double* v0 = gvb + (int64_t)(vt >> 4) * a.vstride + (vt & 15) * 2;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + i * v_rs);
+          for (int i = 0; i < 4; ++i) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + i * v_rs);
+        }
+      } else {
+#pragma unroll 4
+        for (int vt = lane; vt < WT; vt += 32) {
+          const uint32_t s_k = so + (uint32_t)kchunk_dst(vt) * 8u;
+          const double* k0 = gk + 2 * vt;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) cp16s(s_k + (uint32_t)(r * TR * KP * 8), k0 + r * k_rs);
+          const uint32_t s_v = so + (uint32_t)(W_KS + (vt >> 4) * W_VP + (vt & 15) * 2) * 8u;
+          const double* v0 = gv + (vt & 15) * 2;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int j = (vt >> 4) + 32 * i;  // column of the product; tiles past nl8 are not read
+            if (j < nl8) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + (int64_t)s_act[j] * a.vstride);
+          }
+        }
       }
       cp_arrive_noinc(&full[st]);
      }
@@ -457,12 +511,16 @@ __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
   const WsItem w = ws_item(it, a.nx, a.ny);
   const int64_t rb0 = 4LL * w.x;
   const int b0 = w.z * BW;
+  const int nl = CP ? ws_live(na, b0) : BW;
+  if (CP && nl == 0) continue;
+  const int ntl = CP ? ws_tiles(nl, wc) : 4;  // live 8-problem tiles of this warp's 32-problem group
   const int nch = nch_of(w);
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (!CP || ntl == 4) {  // a whole group: the full 32 x 32 warp tile
   for (int c = 0; c < nch; ++c, ++gc) {
     const int st = gc % W_STAGES;
     mbar_wait(&full[st], (uint32_t)((gc / W_STAGES) & 1));
@@ -484,23 +542,66 @@ __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
+  } else {  // a partly live group: only its live tiles (same sums per problem); a dead one
+            // just keeps the ring's barriers in step
+  for (int c = 0; c < nch; ++c, ++gc) {
+    const int st = gc % W_STAGES;
+    mbar_wait(&full[st], (uint32_t)((gc / W_STAGES) & 1));
+    const double* ks = sm + st * W_STAGE + wr * (TR * KP);
+    const double* vs = sm + st * W_STAGE + W_KS + (wc * 32) * W_VP;
+    if (ntl > 0) {
+#pragma unroll 2
+      for (int kk = 0; kk < 32; kk += 4) {
+        const int col = kk + t;
+        double av[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) av[mt] = ks[kpos(mt * 8 + g, col)];
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt)
+          if (nt < ntl) {
+            const double bv = vs[(nt * 8 + g) * W_VP + col];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) dmma884(acc[mt][nt], av[mt], bv);
+          }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  }
   double* out = a.part + w.y * a.pslab;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int64_t row = (rb0 + wr) * TR + mt * 8 + g;
-      const int64_t b = b0 + wc * 32 + nt * 8 + 2 * t;
-      out[b * a.ostride + row] = acc[mt][nt][0];
-      out[(b + 1) * a.ostride + row] = acc[mt][nt][1];
+      const int j = wc * 32 + nt * 8 + 2 * t;  // column of the product
+      if (!CP) {
+        out[(int64_t)(b0 + j) * a.ostride + row] = acc[mt][nt][0];
+        out[(int64_t)(b0 + j + 1) * a.ostride + row] = acc[mt][nt][1];
+      } else {
+        if (j < nl) out[ws_problem(a.active, b0, j) * a.ostride + row] = acc[mt][nt][0];
+        if (j + 1 < nl) out[ws_problem(a.active, b0, j + 1) * a.ostride + row] = acc[mt][nt][1];
+      }
     }
   }
 }
 
-__global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
+// (its own function: the all-live path above keeps its registers and schedule)
+__device__ __noinline__ void bfwd_ws_compact(const BGemmArgs& a, const int na) { bfwd_ws_impl<true>(a, na); }
+
+__global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
   pdl_wait_and_trigger();
+  const int na = a.nact ? __ldcg(a.nact) : a.nz * BW;  // live problems (compacted columns)
+  if (na >= a.nb) bfwd_ws_impl<false>(a, na);        // all live: active[] is the identity
+  else bfwd_ws_compact(a, na);
+}
+
+template <bool CP>
+__device__ __forceinline__ void badj_ws_impl(const BGemmArgs& a, const int na) {
   extern __shared__ __align__(16) double sm[];
   __shared__ uint64_t full[W_STAGES], empty[W_STAGES];
+  __shared__ int s_act[CP ? BW : 1];  // producer warp only
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int nitems = a.nx * a.ny * a.nz;
   auto nch_of = [&](const WsItem& w) {
@@ -524,6 +625,10 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
      const WsItem w = ws_item(it, a.nx, a.ny);
      const int64_t cb0 = 2LL * w.x;
      const int b0 = w.z * BW;
+     const int nl = CP ? ws_live(na, b0) : BW;
+     if (CP && nl == 0) continue;
+     const bool inplace = CP ? ws_fill_rows(s_act, a.active, b0, nl, lane) : true;
+     const int nl8 = (nl + 7) & ~7;
      const int r_begin = w.y * a.per_split, nch = nch_of(w);
      for (int c = 0; c < nch; ++c, ++gc) {
       const int st = gc % W_STAGES;
@@ -531,19 +636,39 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
       const int64_t rb = r_begin + c;
       const uint32_t so = s_base + (uint32_t)(st * W_STAGE) * 8u;
       const double* gk = a.K + (rb * a.ncb + cb0) * TILE;
-      const double* gv = a.V + (int64_t)b0 * a.vstride + rb * TR;
+      const double* gv = a.V + rb * TR;
+      if (!CP || inplace) {
+        const double* gvb = gv + (int64_t)b0 * a.vstride;
 #pragma unroll 4
-      for (int vt = lane; vt < WT; vt += 32) {
-        const uint32_t s_k = so + (uint32_t)kchunk_dst(vt) * 8u;
-        const double* k0 = gk + 2 * vt;
+        for (int vt = lane; vt < WT; vt += 32) {
+          const uint32_t s_k = so + (uint32_t)kchunk_dst(vt) * 8u;
+          const double* k0 = gk + 2 * vt;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          cp16s(s_k + (uint32_t)(((i >> 1) * KT_S + (i & 1) * 32 * KP) * 8),
-                k0 + (i >> 1) * TILE + (i & 1) * 1024);
-        const uint32_t s_v = so + (uint32_t)(W_KS + (vt >> 4) * W_VP + (vt & 15) * 2) * 8u;
-        const double* v0 = gv + (int64_t)(vt >> 4) * a.vstride + (vt & 15) * 2;
+          for (int i = 0; i < 4; ++i)
+            cp16s(s_k + (uint32_t)(((i >> 1) * KT_S + (i & 1) * 32 * KP) * 8),
+                  k0 + (i >> 1) * TILE + (i & 1) * 1024);
+          const uint32_t s_v = so + (uint32_t)(W_KS + (vt >> 4) * W_VP + (vt & 15) * 2) * 8u;
+          const double* v0 = gvb + (int64_t)(vt >> 4) * a.vstride + (vt & 15) * 2;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + i * v_rs);
+          for (int i = 0; i < 4; ++i) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + i * v_rs);
+        }
+      } else {
+#pragma unroll 4
+        for (int vt = lane; vt < WT; vt += 32) {
+          const uint32_t s_k = so + (uint32_t)kchunk_dst(vt) * 8u;
+          const double* k0 = gk + 2 * vt;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            cp16s(s_k + (uint32_t)(((i >> 1) * KT_S + (i & 1) * 32 * KP) * 8),
+                  k0 + (i >> 1) * TILE + (i & 1) * 1024);
+          const uint32_t s_v = so + (uint32_t)(W_KS + (vt >> 4) * W_VP + (vt & 15) * 2) * 8u;
+          const double* v0 = gv + (vt & 15) * 2;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int j = (vt >> 4) + 32 * i;
+            if (j < nl8) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + (int64_t)s_act[j] * a.vstride);
+          }
+        }
       }
       cp_arrive_noinc(&full[st]);
      }
@@ -559,12 +684,16 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
   const WsItem w = ws_item(it, a.nx, a.ny);
   const int64_t cb0 = 2LL * w.x;
   const int b0 = w.z * BW;
+  const int nl = CP ? ws_live(na, b0) : BW;
+  if (CP && nl == 0) continue;
+  const int ntl = CP ? ws_tiles(nl, wc) : 4;
   const int nch = nch_of(w);
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if (!CP || ntl == 4) {
   for (int c = 0; c < nch; ++c, ++gc) {
     const int st = gc % W_STAGES;
     mbar_wait(&full[st], (uint32_t)((gc / W_STAGES) & 1));
@@ -586,17 +715,58 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
+  } else {
+  for (int c = 0; c < nch; ++c, ++gc) {
+    const int st = gc % W_STAGES;
+    mbar_wait(&full[st], (uint32_t)((gc / W_STAGES) & 1));
+    const double* kt = sm + st * W_STAGE + tl * KT_S;
+    const double* vs = sm + st * W_STAGE + W_KS + (wc * 32) * W_VP;
+    if (ntl > 0) {
+#pragma unroll 2
+      for (int kk = 0; kk < TR; kk += 4) {
+        const int row = kk + t;
+        double av[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) av[mt] = kt[kpos(row, cofs + mt * 8 + g)];
+#pragma unroll
+        for (int nt = 0; nt < 3; ++nt)
+          if (nt < ntl) {
+            const double bv = vs[(nt * 8 + g) * W_VP + row];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) dmma884(acc[mt][nt], av[mt], bv);
+          }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  }
   double* out = a.part + w.y * a.pslab;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int64_t col = (cb0 + tl) * TC + cofs + mt * 8 + g;
-      const int64_t b = b0 + wc * 32 + nt * 8 + 2 * t;
-      out[b * a.ostride + col] = acc[mt][nt][0];
-      out[(b + 1) * a.ostride + col] = acc[mt][nt][1];
+      const int j = wc * 32 + nt * 8 + 2 * t;
+      if (!CP) {
+        out[(int64_t)(b0 + j) * a.ostride + col] = acc[mt][nt][0];
+        out[(int64_t)(b0 + j + 1) * a.ostride + col] = acc[mt][nt][1];
+      } else {
+        if (j < nl) out[ws_problem(a.active, b0, j) * a.ostride + col] = acc[mt][nt][0];
+        if (j + 1 < nl) out[ws_problem(a.active, b0, j + 1) * a.ostride + col] = acc[mt][nt][1];
+      }
     }
   }
+}
+
+// (its own function: the all-live path above keeps its registers and schedule)
+__device__ __noinline__ void badj_ws_compact(const BGemmArgs& a, const int na) { badj_ws_impl<true>(a, na); }
+
+__global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
+  pdl_wait_and_trigger();
+  const int na = a.nact ? __ldcg(a.nact) : a.nz * BW;
+  if (na >= a.nb) badj_ws_impl<false>(a, na);
+  else badj_ws_compact(a, na);
 }
 
 template <int NA>
@@ -842,7 +1012,7 @@ BatchPlan make_batch_plan(const GemvPlan& pl, int B, int sm_count) {
 }
 
 void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* part,
-                 cudaStream_t s) {
+                 cudaStream_t s, const int* active, const int* nact) {
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, [] {
     L1G_CUDA(cudaFuncSetAttribute(bfwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -871,6 +1041,7 @@ void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* par
     const dim3 grid((unsigned)(pl.n_pad / 128), (unsigned)bp.fwd_splits, (unsigned)(bp.Bp / BW));
     if (ws_products()) {
       a.nx = (int)grid.x, a.ny = (int)grid.y, a.nz = (int)grid.z;
+      a.active = active, a.nact = nact, a.nb = bp.B;
       const int items = a.nx * a.ny * a.nz;
       L1G_CUDA(launch_pdl(bfwd_ws_kernel, std::min(items, ws_grid(op)), WP, bwide_smem(), s, a));
     }
@@ -882,7 +1053,7 @@ void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* par
 }
 
 void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* part,
-                 cudaStream_t s) {
+                 cudaStream_t s, const int* active, const int* nact) {
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, [] {
     L1G_CUDA(cudaFuncSetAttribute(badj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -911,6 +1082,7 @@ void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* par
     const dim3 grid((unsigned)(pl.ncb / 2), (unsigned)bp.adj_splits, (unsigned)(bp.Bp / BW));
     if (ws_products()) {
       a.nx = (int)grid.x, a.ny = (int)grid.y, a.nz = (int)grid.z;
+      a.active = active, a.nact = nact, a.nb = bp.B;
       const int items = a.nx * a.ny * a.nz;
       L1G_CUDA(launch_pdl(badj_ws_kernel, std::min(items, ws_grid(op)), WP, bwide_smem(), s, a));
     }
@@ -919,6 +1091,38 @@ void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* par
   }
   const dim3 grid((unsigned)pl.ncb, (unsigned)bp.adj_splits, (unsigned)(bp.Bp / BW));
   L1G_CUDA(launch_pdl(badj_kernel, grid, BT, badj_smem(), s, a));
+}
+
+// The live problems of a batch in index order: active[0 .. *nact).  One CTA; the producer-warp
+// products read the list right after (same stream, programmatic dependency).
+constexpr int BC_T = 256;
+__global__ void __launch_bounds__(BC_T) bcompact_kernel(const DevState* st, int B, int* active,
+                                                        int* nact) {
+  pdl_wait_and_trigger();
+  __shared__ int wcnt[BC_T / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int base = 0;
+  for (int b0 = 0; b0 < B; b0 += BC_T) {
+    const int b = b0 + threadIdx.x;
+    const bool live = b < B && __ldcg(&st[b].status) == RUNNING;
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    if (lane == 0) wcnt[warp] = __popc(m);
+    __syncthreads();
+    int before = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < BC_T / 32; ++w) {
+      before += w < warp ? wcnt[w] : 0;
+      tot += wcnt[w];
+    }
+    if (live) active[base + before + __popc(m & ((1u << lane) - 1u))] = b;
+    base += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *nact = base;
+}
+
+void launch_bcompact(const DevState* st, int B, int* active, int* nact, cudaStream_t s) {
+  L1G_CUDA(launch_pdl(bcompact_kernel, 1, BC_T, 0, s, st, B, active, nact));
 }
 
 void launch_bfin(const BFinArgs& a, bool adjoint, int64_t len_pad, cudaStream_t s) {

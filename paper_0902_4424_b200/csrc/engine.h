@@ -154,6 +154,12 @@ struct BGemmArgs {
   int64_t pslab, ostride;
   int per_split, nblocks;
   int nx, ny, nz;  // persistent products: work items (tiles x splits x problem blocks)
+  // live-problem compaction (producer-warp products): column j of the product is problem
+  // active[j], j < *nact; problem blocks, 32-problem warp groups and 8-problem tiles past
+  // *nact are skipped.  nullptr: every problem, in place.
+  const int* active;
+  const int* nact;
+  int nb;  // problems in the batch: *nact == nb means all live (active[] is the identity)
 };
 struct BFinArgs {  // batched finishes (dmma.cu): problem b's vectors at b * ostride
   int mode, B, splits;
@@ -169,8 +175,11 @@ struct BFinArgs {  // batched finishes (dmma.cu): problem b's vectors at b * ost
 void launch_bfin(const BFinArgs& a, bool adjoint, int64_t len_pad, cudaStream_t s);
 void launch_brupdate(const BFinArgs& a, double* rn, cudaStream_t s);
 BatchPlan make_batch_plan(const GemvPlan& pl, int B, int sm_count);
-void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* part, cudaStream_t s);
-void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* part, cudaStream_t s);
+void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* part, cudaStream_t s,
+                 const int* active = nullptr, const int* nact = nullptr);
+void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* part, cudaStream_t s,
+                 const int* active = nullptr, const int* nact = nullptr);
+void launch_bcompact(const DevState* st, int B, int* active, int* nact, cudaStream_t s);
 
 // small problems (small.cu): the whole step after the projection as one cluster kernel
 bool small_iter_fits(const GemvPlan& pl);

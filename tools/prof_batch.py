@@ -40,4 +40,8 @@ for s in range(a.solves):
     print(f"solve {s}: {dt*1e3:.1f} ms, max iterations {max(its)}, min {min(its)}, "
           f"{max(its)/dt:.1f} lockstep it/s, {sum(its)/dt:.0f} problem-it/s, "
           f"{4.0*n*p*B*max(its)/dt/1e12:.1f} TFLOP/s (4npB per lockstep iteration)", flush=True)
+if os.environ.get("L1G_PRINT_LIVE"):
+    live = [sum(1 for v in its if v > k) for k in range(max(its))]
+    print("live problems per lockstep iteration:", live)
+    print("live 32-groups after compaction:", [(v + 31) // 32 for v in live])
 lib.l1g_batch_destroy(h)
