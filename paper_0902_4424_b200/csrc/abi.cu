@@ -927,7 +927,9 @@ struct l1g_batch {
   l1g_op* op = nullptr;
   int B = 0;
   BatchPlan bp{};
-  ProjPlan pp{};
+  ProjPlan pp{};     // a small cluster per problem (lowest latency: few live problems)
+  ProjPlan pp_one{};  // one CTA per problem (highest throughput: many live problems)
+  bool two_plans = false;
   cudaStream_t stream = nullptr;
   l1g_gp_config cfg{};
   std::vector<double> rho;
@@ -977,6 +979,8 @@ void batch_free(l1g_batch* b) {
   delete b;
 }
 
+constexpr int BATCH_PROJ_ONE_ABOVE = 37;  // live problems above which one CTA per problem wins
+
 l1g_batch* batch_new(l1g_op* op, int B, const double* Y, const double* rho,
                      const l1g_gp_config& cfg) {
   check_cfg(cfg);
@@ -1000,6 +1004,17 @@ l1g_batch* batch_new(l1g_op* op, int B, const double* Y, const double* rho,
       int cs = 1;
       while (cs < cs_max && pl.p_pad / (cs * 2) >= 4096) cs *= 2;
       b->pp = make_proj_plan_single(pl.p_pad, cs);
+      // with a cluster plan, iterations with many live problems use one CTA per problem instead
+      // (C5, all 128 live: 75 us against 145-180 us in 4 rounds of 4-CTA clusters; 37 clusters fit
+      // at once); both launches sit in the iteration and the live count picks one on the device
+      static const bool two = [] {
+        const char* e = getenv("L1G_BATCH_PROJ_TWO");
+        return !(e && std::strcmp(e, "0") == 0);
+      }();
+      if (two && cs > 1 && B > BATCH_PROJ_ONE_ABOVE) {
+        b->pp_one = make_proj_plan_single(pl.p_pad, 1);
+        b->two_plans = b->pp_one.cs == 1;
+      }
     }
     const size_t Bp = (size_t)b->bp.Bp;
     L1G_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
@@ -1059,8 +1074,11 @@ bool batch_compaction() {
   }();
   return on;
 }
-// kernels of one lockstep iteration: proj, (compaction), bfwd, bfin_fwd, brupdate, badj, bfin_adj
-int batch_iteration_kernels() { return batch_compaction() ? 7 : 6; }
+// kernels of one lockstep iteration: proj (one or both plans), (compaction), bfwd, bfin_fwd,
+// brupdate, badj, bfin_adj
+int batch_iteration_kernels(const l1g_batch* b) {
+  return 6 + (batch_compaction() ? 1 : 0) + (batch_compaction() && b->two_plans ? 1 : 0);
+}
 
 void batch_products(l1g_batch* b, int fmode, const double* D, int amode, const double* R,
                     bool rupdate, bool proj_first) {
@@ -1072,9 +1090,17 @@ void batch_products(l1g_batch* b, int fmode, const double* D, int amode, const d
   const bool compact = proj_first && batch_compaction();
   const int* act = compact ? b->active : nullptr;
   const int* nact = compact ? b->active + b->bp.Bp : nullptr;
-  if (proj_first)
+  if (proj_first) {
+    // (the live count is the previous iteration's: nothing stops between it and this launch)
+    const int* live = b->active + b->bp.Bp;
+    const bool two = b->two_plans && compact;
+    if (two)
+      launch_proj(b->pp_one, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, b->pscr, b->st,
+                  &b->vb, s, b->B, b->scr_stride, nullptr, 1, live, BATCH_PROJ_ONE_ABOVE, 1);
     launch_proj(b->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, b->pscr, b->st,
-                &b->vb, s, b->B, b->scr_stride);
+                &b->vb, s, b->B, b->scr_stride, nullptr, 1, two ? live : nullptr,
+                BATCH_PROJ_ONE_ABOVE, 2);
+  }
   if (compact) launch_bcompact(b->st, b->B, b->active, b->active + b->bp.Bp, s);
   if (D) {
     launch_bfwd(*b->op, b->bp, D, b->part, s, act, nact);
@@ -1145,6 +1171,8 @@ void batch_run(l1g_batch* b, const l1g_stop_rule& stop, l1g_result* res, bool re
     }
     L1G_CUDA(cudaMemcpyAsync(b->nrun, &B, sizeof(int), cudaMemcpyHostToDevice, s));
   }
+  // the live list the first iteration's projection plan and products read
+  if (batch_compaction()) launch_bcompact(b->st, B, b->active, b->active + b->bp.Bp, s);
   L1G_CUDA(cudaStreamSynchronize(s));
   if (!b->gexec) {
     const GemvPlan& pl = b->op->plan;
@@ -1175,11 +1203,11 @@ void batch_run(l1g_batch* b, const l1g_stop_rule& stop, l1g_result* res, bool re
     L1G_CUDA(cudaGraphLaunch(b->gloop, s));
     L1G_CUDA(cudaMemcpyAsync(&k1, &b->st->k, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     L1G_CUDA(cudaStreamSynchronize(s));
-    b->launches += ((k1 - k0) / b->gsize + 1) * ((int64_t)batch_iteration_kernels() * b->gsize + 1);
+    b->launches += ((k1 - k0) / b->gsize + 1) * ((int64_t)batch_iteration_kernels(b) * b->gsize + 1);
   }
   for (int64_t launched = 0; live > 0 && !b->gloop;) {
     L1G_CUDA(cudaGraphLaunch(b->gexec, s));
-    b->launches += (int64_t)batch_iteration_kernels() * b->gsize;
+    b->launches += (int64_t)batch_iteration_kernels(b) * b->gsize;
     L1G_CUDA(cudaMemcpyAsync((void*)flag, b->nrun, sizeof(int), cudaMemcpyDeviceToHost, s));
     L1G_CUDA(cudaStreamSynchronize(s));
     ++launched;

@@ -489,13 +489,13 @@ __device__ __forceinline__ void bfwd_ws_impl(const BGemmArgs& a, const int na) {
           const double* k0 = gk + 2 * vt;
 #pragma unroll
           for (int r = 0; r < 4; ++r) cp16s(s_k + (uint32_t)(r * TR * KP * 8), k0 + r * k_rs);
-          const uint32_t s_v = so + (uint32_t)(W_KS + (vt >> 4) * W_VP + (vt & 15) * 2) * 8u;
-          const double* v0 = gv + (vt & 15) * 2;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int j = (vt >> 4) + 32 * i;  // column of the product; tiles past nl8 are not read
-            if (j < nl8) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + (int64_t)s_act[j] * a.vstride);
-          }
+        }
+        // the live columns' vector chunks only (16 copies of 16 bytes per column; tiles past
+        // nl8 are never read)
+#pragma unroll 2
+        for (int idx = lane; idx < nl8 * 16; idx += 32) {
+          const int j = idx >> 4, cc = (idx & 15) * 2;
+          cp16s(so + (uint32_t)(W_KS + j * W_VP + cc) * 8u, gv + (int64_t)s_act[j] * a.vstride + cc);
         }
       }
       cp_arrive_noinc(&full[st]);
@@ -661,13 +661,11 @@ __device__ __forceinline__ void badj_ws_impl(const BGemmArgs& a, const int na) {
           for (int i = 0; i < 4; ++i)
             cp16s(s_k + (uint32_t)(((i >> 1) * KT_S + (i & 1) * 32 * KP) * 8),
                   k0 + (i >> 1) * TILE + (i & 1) * 1024);
-          const uint32_t s_v = so + (uint32_t)(W_KS + (vt >> 4) * W_VP + (vt & 15) * 2) * 8u;
-          const double* v0 = gv + (vt & 15) * 2;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int j = (vt >> 4) + 32 * i;
-            if (j < nl8) cp16s(s_v + (uint32_t)(i * 32 * W_VP * 8), v0 + (int64_t)s_act[j] * a.vstride);
-          }
+        }
+#pragma unroll 2
+        for (int idx = lane; idx < nl8 * 16; idx += 32) {
+          const int j = idx >> 4, cc = (idx & 15) * 2;
+          cp16s(so + (uint32_t)(W_KS + j * W_VP + cc) * 8u, gv + (int64_t)s_act[j] * a.vstride + cc);
         }
       }
       cp_arrive_noinc(&full[st]);

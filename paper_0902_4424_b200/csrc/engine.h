@@ -207,7 +207,8 @@ ProjPlan make_proj_plan(int64_t p_pad);
 void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const double* xin,
                  const double* gin, double* out, double* scratch, DevState* st,
                  const VecBufs* vb, cudaStream_t s, int nprob = 1, int64_t scr_stride = 0,
-                 const double* rank_scal = nullptr, int nranks = 1);
+                 const double* rank_scal = nullptr, int nranks = 1, const int* sel = nullptr,
+                 int sel_thr = 0, int sel_mode = 0);
 ProjPlan make_proj_plan_single(int64_t p_pad, int cs = 1);
 size_t proj_scratch_doubles(int64_t p_pad);
 

@@ -69,6 +69,11 @@ struct ProjArgs {
   // of the rank's columns, its clock)
   const double* rank_scal;
   int nranks;
+  // batched runs keep two plans in the iteration (one CTA per problem while many problems are
+  // live, a cluster per problem once few are): this launch runs only if the live count *sel
+  // is above (sel_mode 1) / at most (sel_mode 2) sel_thr
+  const int* sel;
+  int sel_thr, sel_mode;
 };
 
 struct ProjShared {
@@ -584,6 +589,10 @@ __global__ void __launch_bounds__(PT, 1) proj_kernel(const ProjArgs a) {
   L1G_TL_ENTRY
   pdl_wait_and_trigger();
   L1G_TL_WAITED(a.mode == PROJ_ITER && blockIdx.x == 0, g_tl_proj, 0, a.st->k)
+  if (a.sel_mode != 0) {  // the other plan's launch takes this iteration (uniform over the grid)
+    const int live = __ldcg(a.sel);
+    if ((a.sel_mode == 1) != (live > a.sel_thr)) return;
+  }
   cg::cluster_group cl = cg::this_cluster();
   const unsigned rank = cl.block_rank();
   const int cs = a.cs;
@@ -1372,11 +1381,14 @@ static void proj_dispatch(const ProjPlan& pp, const ProjArgs& a, cudaStream_t s,
 void launch_proj(const ProjPlan& pp, int mode, int64_t p, int64_t p_pad, const double* xin,
                  const double* gin, double* out, double* scratch, DevState* st,
                  const VecBufs* vb, cudaStream_t s, int nprob, int64_t scr_stride,
-                 const double* rank_scal, int nranks) {
+                 const double* rank_scal, int nranks, const int* sel, int sel_thr, int sel_mode) {
   if (nranks > 16) throw InvalidArgument("sharded solver: at most 16 ranks");
   ProjArgs a{};
   a.rank_scal = rank_scal;
   a.nranks = rank_scal ? nranks : 1;
+  a.sel = sel;
+  a.sel_thr = sel_thr;
+  a.sel_mode = sel ? sel_mode : 0;
   a.mode = mode;
   a.p = p;
   a.p_pad = p_pad;
