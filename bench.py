@@ -478,6 +478,12 @@ def run_batch(args, world, rank, local, pg):
                            "lockstep_iterations_per_step": lock_its / args.steps,
                            "problem_iterations_per_s": world * prob_its / (dev_ms / 1e3),
                            "l2": "inputs larger than L2 (K = 0.5 GiB, partials 67 MB)",
+                           "products": "on the live problems only: stopped problems are "
+                                       "compacted out of the DMMA products (problem blocks, "
+                                       "32-problem warp groups and 8-problem tiles without a live "
+                                       "problem are skipped; same bits per problem); the "
+                                       "roofline launches below are full-width (all problems)",
+                           "mean_live_problems": prob_its / max(lock_its, 1),
                            "parallelism": "replicas" if world > 1 else "single",
                            "setup_s": round(setup_s, 3)},
                 "e2e": {"value": world * e2e_its / e2e_s, "unit": UNIT,

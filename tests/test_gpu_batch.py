@@ -97,3 +97,52 @@ def test_batched_solve_matches_single(n, p, B, iters, strict):
             assert np.abs(X[b] - sol.x).max() <= 1e-7 * scale, (b, np.abs(X[b] - sol.x).max())
         assert abs(res[b].objective - sol.objective) <= 1e-9 * abs(sol.objective), b
         assert np.abs(X[b]).sum() <= rho[b] * (1 + 1e-12) + 1e-12
+
+
+_COMPACT_SNIPPET = r"""
+import ctypes as C, sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_0902_4424_b200 as l1
+from paper_0902_4424_b200 import _lib as L
+from tests.test_gpu_batch import batch_problems
+K, Y, rho = batch_problems(256, 2048, 140, 77)
+op = l1.DenseOperator(K)
+lib = L.load()
+cfg = l1.GpConfig()._c()
+stop = l1.StopRule(max_iterations=400, stationarity_tol=0.0)._c()
+B = Y.shape[0]
+X = np.empty((B, 2048))
+res = (L.ResultC * B)()
+L.check(lib.l1g_gpss_solve_batched(op.h, B, L.ptr(np.ascontiguousarray(Y)), L.ptr(rho),
+                                   C.byref(cfg), C.byref(stop), L.ptr(X), res), "batched")
+np.savez({out!r}, X=X, its=np.array([res[b].iterations for b in range(B)]),
+         f=np.array([res[b].objective for b in range(B)]),
+         reason=np.array([res[b].reason for b in range(B)]))
+"""
+
+
+def test_compaction_bit_identical(tmp_path):
+    """Products on the compacted live problems (dead blocks, warp groups and tiles skipped,
+    either projection plan) give every problem the bits of the in-place full-width products:
+    a 140-problem batch (two problem blocks) run to every problem's stop, with problems
+    stopping at different iterations, in three processes (the switches are read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for name, env in [("plain", {"L1G_BATCH_COMPACT": "0"}),
+                      ("compact", {"L1G_BATCH_COMPACT": "1", "L1G_BATCH_PROJ_TWO": "0"}),
+                      ("compact2", {"L1G_BATCH_COMPACT": "1", "L1G_BATCH_PROJ_TWO": "1"})]:
+        out = str(tmp_path / f"{name}.npz")
+        e = dict(os.environ, **env)
+        r = subprocess.run([sys.executable, "-c", _COMPACT_SNIPPET.format(root=root, out=out)],
+                           env=e, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    a = outs[0]
+    assert len(set(a["its"].tolist())) > 3  # the problems do stop at different iterations
+    for b in outs[1:]:
+        assert np.array_equal(a["its"], b["its"]) and np.array_equal(a["reason"], b["reason"])
+        assert np.array_equal(a["f"], b["f"])
+        assert np.array_equal(a["X"], b["X"])
