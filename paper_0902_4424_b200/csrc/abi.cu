@@ -1077,7 +1077,8 @@ bool batch_compaction() {
 // kernels of one lockstep iteration: proj (one or both plans), (compaction), bfwd, bfin_fwd,
 // brupdate, badj, bfin_adj
 int batch_iteration_kernels(const l1g_batch* b) {
-  return 6 + (batch_compaction() ? 1 : 0) + (batch_compaction() && b->two_plans ? 1 : 0);
+  return 6 + (batch_compaction() ? 1 : 0) + (batch_compaction() && b->two_plans ? 1 : 0) +
+         (batch_compaction() && batch_tail_kernels() && b->bp.wide ? 2 : 0);
 }
 
 void batch_products(l1g_batch* b, int fmode, const double* D, int amode, const double* R,

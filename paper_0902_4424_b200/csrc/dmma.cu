@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(WT, 1) badj_wide_kernel(const BGemmArgs a) {
 // the stage it reads and marks it `empty` when done, so consumers never wait for each other
 // and the DMMA pipe is not drained at every chunk boundary.
 constexpr int WP = WT + 32;  // 16 consumer warps + 1 producer warp
+constexpr int T_VROWS = 8;   // live problems the few-live-problems variant (bws_tail_kernel) takes
 __device__ __forceinline__ void cp_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -593,6 +594,7 @@ __device__ __noinline__ void bfwd_ws_compact(const BGemmArgs& a, const int na) {
 __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
   pdl_wait_and_trigger();
   const int na = a.nact ? __ldcg(a.nact) : a.nz * BW;  // live problems (compacted columns)
+  if (a.tail && na <= T_VROWS) return;               // bws_tail_kernel takes this launch
   if (na >= a.nb) bfwd_ws_impl<false>(a, na);        // all live: active[] is the identity
   else bfwd_ws_compact(a, na);
 }
@@ -763,8 +765,133 @@ __device__ __noinline__ void badj_ws_compact(const BGemmArgs& a, const int na) {
 __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
   pdl_wait_and_trigger();
   const int na = a.nact ? __ldcg(a.nact) : a.nz * BW;
+  if (a.tail && na <= T_VROWS) return;
   if (na >= a.nb) badj_ws_impl<false>(a, na);
   else badj_ws_compact(a, na);
+}
+
+// ---------------------------------------------------------------- few live problems
+// With at most 8 live problems (one 8-problem tile) a product is bound by one accumulator's
+// dependent DMMA chain along the reduction (an item takes 128 m8n8k4 steps in a row), not by
+// the tensor pipe or by HBM.  This variant runs two CTAs per SM -- four consumer warps (32 rows
+// or columns x the 8 problems each) and a producer warp, two stages of [K tiles | 8 vector
+// rows] -- so two items' chains run side by side on every SM.  Same chunks in the same order
+// per accumulator, so the bits are those of the full-size kernels.  Both launches sit in the
+// iteration; the live count picks one (the other returns at once).
+constexpr int T_CW = 4;
+constexpr int T_THREADS = 32 * (T_CW + 1);
+constexpr int T_STAGE = W_KS + T_VROWS * W_VP;    // doubles per stage
+constexpr int T_STAGES = 2;
+size_t btail_smem() { return (size_t)T_STAGES * T_STAGE * 8; }
+
+template <bool ADJ>
+__global__ void __launch_bounds__(T_THREADS, 2) bws_tail_kernel(const BGemmArgs a) {
+  pdl_wait_and_trigger();
+  const int na = __ldcg(a.nact);
+  if (na <= 0 || na > T_VROWS) return;  // the full-size kernel takes this launch
+  extern __shared__ __align__(16) double sm[];
+  __shared__ uint64_t full[T_STAGES], empty[T_STAGES];
+  __shared__ int s_act[T_VROWS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int nitems = a.nx * a.ny;  // the live problems are the leading columns of block 0
+  const int nred = ADJ ? a.nblocks : 2 * a.nblocks;  // reduction chunks (row blocks | 32 columns)
+  auto nch_of = [&](const WsItem& w) {
+    const int c_begin = w.y * a.per_split;
+    const int c_end = c_begin + a.per_split < nred ? c_begin + a.per_split : nred;
+    return c_end > c_begin ? c_end - c_begin : 0;
+  };
+  if (tid == 0) {
+    for (int st = 0; st < T_STAGES; ++st) {
+      mbar_init(&full[st], 32);
+      mbar_init(&empty[st], T_CW);
+    }
+    fence_barrier_init();
+  }
+  if (tid < T_VROWS) s_act[tid] = __ldg(a.active + (tid < na ? tid : na - 1));
+  __syncthreads();
+  if (warp == T_CW) {  // ---- producer
+    const uint32_t s_base = smem_u32(sm);
+    const int64_t k_rs = a.ncb * TILE;
+    int gc = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const WsItem w = ws_item(it, a.nx, a.ny);
+      const int c_begin = w.y * a.per_split, nch = nch_of(w);
+      for (int c = 0; c < nch; ++c, ++gc) {
+        const int st = gc % T_STAGES;
+        if (gc >= T_STAGES) mbar_wait(&empty[st], (uint32_t)((gc / T_STAGES - 1) & 1));
+        const uint32_t so = s_base + (uint32_t)(st * T_STAGE) * 8u;
+        const int64_t ch = c_begin + c;
+        const double* gk;
+        const double* gv;
+        if (ADJ) {
+          gk = a.K + (ch * a.ncb + 2LL * w.x) * TILE;
+          gv = a.V + ch * TR;
+        } else {
+          gk = a.K + 4LL * w.x * k_rs + (ch >> 1) * TILE + (ch & 1) * (TILE / 2);
+          gv = a.V + ch * 32;
+        }
+#pragma unroll 4
+        for (int vt = lane; vt < WT; vt += 32) {
+          const uint32_t s_k = so + (uint32_t)kchunk_dst(vt) * 8u;
+          const double* k0 = gk + 2 * vt;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (ADJ)
+              cp16s(s_k + (uint32_t)(((i >> 1) * KT_S + (i & 1) * 32 * KP) * 8),
+                    k0 + (i >> 1) * TILE + (i & 1) * 1024);
+            else
+              cp16s(s_k + (uint32_t)(i * TR * KP * 8), k0 + i * k_rs);
+          }
+        }
+#pragma unroll
+        for (int idx = lane; idx < T_VROWS * 16; idx += 32) {
+          const int j = idx >> 4, cc = (idx & 15) * 2;
+          cp16s(so + (uint32_t)(W_KS + j * W_VP + cc) * 8u, gv + (int64_t)s_act[j] * a.vstride + cc);
+        }
+        cp_arrive_noinc(&full[st]);
+      }
+    }
+    cp_wait<0>();
+    return;
+  }
+  // ---- consumers: warp = row block of the tile (forward) / 32-column group (adjoint)
+  const int tl = warp >> 1, cofs = (warp & 1) * 32;
+  int gc = 0;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const WsItem w = ws_item(it, a.nx, a.ny);
+    const int nch = nch_of(w);
+    double acc[4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int c = 0; c < nch; ++c, ++gc) {
+      const int st = gc % T_STAGES;
+      mbar_wait(&full[st], (uint32_t)((gc / T_STAGES) & 1));
+      const double* kb = sm + st * T_STAGE + (ADJ ? tl * KT_S : warp * (TR * KP));
+      const double* vs = sm + st * T_STAGE + W_KS;
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 4) {
+        const int q = kk + t;  // column of the chunk (forward) / row of the block (adjoint)
+        double av[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+          av[mt] = ADJ ? kb[kpos(q, cofs + mt * 8 + g)] : kb[kpos(mt * 8 + g, q)];
+        const double bv = vs[g * W_VP + q];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) dmma884(acc[mt], av[mt], bv);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    double* out = a.part + w.y * a.pslab;
+    const int j = 2 * t;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int64_t o = ADJ ? (2LL * w.x + tl) * TC + cofs + mt * 8 + g
+                            : (4LL * w.x + warp) * TR + mt * 8 + g;
+      if (j < na) out[(int64_t)s_act[j] * a.ostride + o] = acc[mt][0];
+      if (j + 1 < na) out[(int64_t)s_act[j + 1] * a.ostride + o] = acc[mt][1];
+    }
+  }
 }
 
 template <int NA>
@@ -977,6 +1104,14 @@ static bool wide_products() {
 }
 // persistent producer-warp products: one CTA per SM
 static int ws_grid(const Op& op) { return op.plan.grid; }
+// L1G_BATCH_TAIL=0: no few-live-problems variant beside the compacted products
+bool batch_tail_kernels() {
+  static const bool on = [] {
+    const char* e = getenv("L1G_BATCH_TAIL");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
 // L1G_DMMA=wide: the 16-warp kernels whose consumers issue the copies themselves
 static bool ws_products() {
   static const bool w = [] {
@@ -1040,8 +1175,18 @@ void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* par
     if (ws_products()) {
       a.nx = (int)grid.x, a.ny = (int)grid.y, a.nz = (int)grid.z;
       a.active = active, a.nact = nact, a.nb = bp.B;
+      a.tail = (nact && batch_tail_kernels()) ? 1 : 0;
       const int items = a.nx * a.ny * a.nz;
       L1G_CUDA(launch_pdl(bfwd_ws_kernel, std::min(items, ws_grid(op)), WP, bwide_smem(), s, a));
+      if (a.tail) {
+        static std::atomic<unsigned long long> tattr{0};
+        once_per_device(tattr, [] {
+          L1G_CUDA(cudaFuncSetAttribute(bws_tail_kernel<false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)btail_smem()));
+        });
+        L1G_CUDA(launch_pdl(bws_tail_kernel<false>, std::min(a.nx * a.ny, 2 * ws_grid(op)),
+                            T_THREADS, btail_smem(), s, a));
+      }
     }
     else L1G_CUDA(launch_pdl(bfwd_wide_kernel, grid, WT, bwide_smem(), s, a));
     return;
@@ -1081,8 +1226,18 @@ void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* par
     if (ws_products()) {
       a.nx = (int)grid.x, a.ny = (int)grid.y, a.nz = (int)grid.z;
       a.active = active, a.nact = nact, a.nb = bp.B;
+      a.tail = (nact && batch_tail_kernels()) ? 1 : 0;
       const int items = a.nx * a.ny * a.nz;
       L1G_CUDA(launch_pdl(badj_ws_kernel, std::min(items, ws_grid(op)), WP, bwide_smem(), s, a));
+      if (a.tail) {
+        static std::atomic<unsigned long long> tattr{0};
+        once_per_device(tattr, [] {
+          L1G_CUDA(cudaFuncSetAttribute(bws_tail_kernel<true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)btail_smem()));
+        });
+        L1G_CUDA(launch_pdl(bws_tail_kernel<true>, std::min(a.nx * a.ny, 2 * ws_grid(op)),
+                            T_THREADS, btail_smem(), s, a));
+      }
     }
     else L1G_CUDA(launch_pdl(badj_wide_kernel, grid, WT, bwide_smem(), s, a));
     return;

@@ -160,6 +160,7 @@ struct BGemmArgs {
   const int* active;
   const int* nact;
   int nb;  // problems in the batch: *nact == nb means all live (active[] is the identity)
+  int tail;  // a bws_tail_kernel launch follows: it takes the launch when *nact <= 8
 };
 struct BFinArgs {  // batched finishes (dmma.cu): problem b's vectors at b * ostride
   int mode, B, splits;
@@ -179,6 +180,7 @@ void launch_bfwd(const Op& op, const BatchPlan& bp, const double* D, double* par
                  const int* active = nullptr, const int* nact = nullptr);
 void launch_badj(const Op& op, const BatchPlan& bp, const double* R, double* part, cudaStream_t s,
                  const int* active = nullptr, const int* nact = nullptr);
+bool batch_tail_kernels();
 void launch_bcompact(const DevState* st, int B, int* active, int* nact, cudaStream_t s);
 
 // small problems (small.cu): the whole step after the projection as one cluster kernel
