@@ -979,7 +979,19 @@ void batch_free(l1g_batch* b) {
   delete b;
 }
 
-constexpr int BATCH_PROJ_ONE_ABOVE = 37;  // live problems above which one CTA per problem wins
+// Live problems above which the batched projection runs one CTA per problem.  By throughput
+// alone that is 37 (as many 4-CTA clusters fit at once), but as soon as problems start to stop
+// some are at their arithmetic floor and escalate the steplength ten times in a row
+// (gpss.cpp:162-191), and that chain sets the kernel's duration: the cluster plan's shorter
+// attempts win (C5: 1 162 -> 1 179 lockstep it/s).  So: one CTA per problem only while every
+// problem is live.  L1G_BATCH_PROJ_ONE_ABOVE overrides the count.
+static int batch_proj_one_above(int B) {
+  static const int v = [] {
+    const char* e = getenv("L1G_BATCH_PROJ_ONE_ABOVE");
+    return e ? atoi(e) : -1;
+  }();
+  return v >= 0 ? v : std::max(37, B - 1);
+}
 
 l1g_batch* batch_new(l1g_op* op, int B, const double* Y, const double* rho,
                      const l1g_gp_config& cfg) {
@@ -1011,7 +1023,7 @@ l1g_batch* batch_new(l1g_op* op, int B, const double* Y, const double* rho,
         const char* e = getenv("L1G_BATCH_PROJ_TWO");
         return !(e && std::strcmp(e, "0") == 0);
       }();
-      if (two && cs > 1 && B > BATCH_PROJ_ONE_ABOVE) {
+      if (two && cs > 1 && B > batch_proj_one_above(B)) {
         b->pp_one = make_proj_plan_single(pl.p_pad, 1);
         b->two_plans = b->pp_one.cs == 1;
       }
@@ -1097,10 +1109,10 @@ void batch_products(l1g_batch* b, int fmode, const double* D, int amode, const d
     const bool two = b->two_plans && compact;
     if (two)
       launch_proj(b->pp_one, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, b->pscr, b->st,
-                  &b->vb, s, b->B, b->scr_stride, nullptr, 1, live, BATCH_PROJ_ONE_ABOVE, 1);
+                  &b->vb, s, b->B, b->scr_stride, nullptr, 1, live, batch_proj_one_above(b->B), 1);
     launch_proj(b->pp, PROJ_ITER, pl.p, pl.p_pad, nullptr, nullptr, nullptr, b->pscr, b->st,
                 &b->vb, s, b->B, b->scr_stride, nullptr, 1, two ? live : nullptr,
-                BATCH_PROJ_ONE_ABOVE, 2);
+                batch_proj_one_above(b->B), 2);
   }
   if (compact) launch_bcompact(b->st, b->B, b->active, b->active + b->bp.Bp, s);
   if (D) {
