@@ -377,7 +377,11 @@ __global__ void __launch_bounds__(WT, 1) badj_wide_kernel(const BGemmArgs a) {
 // the stage it reads and marks it `empty` when done, so consumers never wait for each other
 // and the DMMA pipe is not drained at every chunk boundary.
 constexpr int WP = WT + 32;  // 16 consumer warps + 1 producer warp
-constexpr int T_VROWS = 8;   // live problems the few-live-problems variant (bws_tail_kernel) takes
+#ifndef L1G_TAIL_NT
+#define L1G_TAIL_NT 4
+#endif
+constexpr int T_MAXNT = L1G_TAIL_NT;      // 8-problem tiles the few-live-problems variant takes
+constexpr int T_VROWS = 8 * T_MAXNT;      // i.e. live problems (bws_tail_kernel)
 __device__ __forceinline__ void cp_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -771,27 +775,26 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
 }
 
 // ---------------------------------------------------------------- few live problems
-// With at most 8 live problems (one 8-problem tile) a product is bound by one accumulator's
-// dependent DMMA chain along the reduction (an item takes 128 m8n8k4 steps in a row), not by
-// the tensor pipe or by HBM.  This variant runs two CTAs per SM -- four consumer warps (32 rows
-// or columns x the 8 problems each) and a producer warp, two stages of [K tiles | 8 vector
-// rows] -- so two items' chains run side by side on every SM.  Same chunks in the same order
-// per accumulator, so the bits are those of the full-size kernels.  Both launches sit in the
-// iteration; the live count picks one (the other returns at once).
+// With few live problems a product is bound by one accumulator's dependent DMMA chain along the
+// reduction (an item takes 128 m8n8k4 steps in a row), not by the tensor pipe or by HBM.  This
+// variant runs two CTAs per SM -- four consumer warps (32 rows or columns x the live problems
+// each) and a producer warp, two stages of [K tiles | live vector rows] -- so two items' chains
+// run side by side on every SM.  NT = 1: at most 8 live problems (one 8-problem tile per warp);
+// NT = 4: at most 32.  Same chunks in the same order per accumulator, so the bits are those of
+// the full-size kernels.  Both launches sit in the iteration; the live count picks one (the other
+// returns at once).
 constexpr int T_CW = 4;
 constexpr int T_THREADS = 32 * (T_CW + 1);
-constexpr int T_STAGE = W_KS + T_VROWS * W_VP;    // doubles per stage
 constexpr int T_STAGES = 2;
-size_t btail_smem() { return (size_t)T_STAGES * T_STAGE * 8; }
+constexpr int T_MAXROWS = 8 * T_MAXNT;
+size_t btail_smem() { return (size_t)T_STAGES * (W_KS + 8 * T_MAXNT * W_VP) * 8; }  // [K | rows] x 2
 
-template <bool ADJ>
-__global__ void __launch_bounds__(T_THREADS, 2) bws_tail_kernel(const BGemmArgs a) {
-  pdl_wait_and_trigger();
-  const int na = __ldcg(a.nact);
-  if (na <= 0 || na > T_VROWS) return;  // the full-size kernel takes this launch
+template <bool ADJ, int NT>
+__device__ __forceinline__ void bws_tail_body(const BGemmArgs& a, const int na) {
+  constexpr int VROWS = 8 * NT, STAGE = W_KS + 8 * NT * W_VP;  // doubles per stage
   extern __shared__ __align__(16) double sm[];
   __shared__ uint64_t full[T_STAGES], empty[T_STAGES];
-  __shared__ int s_act[T_VROWS];
+  __shared__ int s_act[VROWS];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int nitems = a.nx * a.ny;  // the live problems are the leading columns of block 0
   const int nred = ADJ ? a.nblocks : 2 * a.nblocks;  // reduction chunks (row blocks | 32 columns)
@@ -807,8 +810,9 @@ __global__ void __launch_bounds__(T_THREADS, 2) bws_tail_kernel(const BGemmArgs 
     }
     fence_barrier_init();
   }
-  if (tid < T_VROWS) s_act[tid] = __ldg(a.active + (tid < na ? tid : na - 1));
+  if (tid < VROWS) s_act[tid] = __ldg(a.active + (tid < na ? tid : na - 1));
   __syncthreads();
+  const int nl8 = (na + 7) & ~7;  // vector rows staged (whole 8-problem tiles)
   if (warp == T_CW) {  // ---- producer
     const uint32_t s_base = smem_u32(sm);
     const int64_t k_rs = a.ncb * TILE;
@@ -819,7 +823,7 @@ __global__ void __launch_bounds__(T_THREADS, 2) bws_tail_kernel(const BGemmArgs 
       for (int c = 0; c < nch; ++c, ++gc) {
         const int st = gc % T_STAGES;
         if (gc >= T_STAGES) mbar_wait(&empty[st], (uint32_t)((gc / T_STAGES - 1) & 1));
-        const uint32_t so = s_base + (uint32_t)(st * T_STAGE) * 8u;
+        const uint32_t so = s_base + (uint32_t)(st * STAGE) * 8u;
         const int64_t ch = c_begin + c;
         const double* gk;
         const double* gv;
@@ -843,8 +847,8 @@ __global__ void __launch_bounds__(T_THREADS, 2) bws_tail_kernel(const BGemmArgs 
               cp16s(s_k + (uint32_t)(i * TR * KP * 8), k0 + i * k_rs);
           }
         }
-#pragma unroll
-        for (int idx = lane; idx < T_VROWS * 16; idx += 32) {
+#pragma unroll 2
+        for (int idx = lane; idx < nl8 * 16; idx += 32) {
           const int j = idx >> 4, cc = (idx & 15) * 2;
           cp16s(so + (uint32_t)(W_KS + j * W_VP + cc) * 8u, gv + (int64_t)s_act[j] * a.vstride + cc);
         }
@@ -856,18 +860,21 @@ __global__ void __launch_bounds__(T_THREADS, 2) bws_tail_kernel(const BGemmArgs 
   }
   // ---- consumers: warp = row block of the tile (forward) / 32-column group (adjoint)
   const int tl = warp >> 1, cofs = (warp & 1) * 32;
+  const int ntl = nl8 >> 3;  // live tiles (1 .. NT)
   int gc = 0;
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     const WsItem w = ws_item(it, a.nx, a.ny);
     const int nch = nch_of(w);
-    double acc[4][2];
+    double acc[4][NT][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) acc[i][n][0] = acc[i][n][1] = 0.0;
     for (int c = 0; c < nch; ++c, ++gc) {
       const int st = gc % T_STAGES;
       mbar_wait(&full[st], (uint32_t)((gc / T_STAGES) & 1));
-      const double* kb = sm + st * T_STAGE + (ADJ ? tl * KT_S : warp * (TR * KP));
-      const double* vs = sm + st * T_STAGE + W_KS;
+      const double* kb = sm + st * STAGE + (ADJ ? tl * KT_S : warp * (TR * KP));
+      const double* vs = sm + st * STAGE + W_KS;
 #pragma unroll
       for (int kk = 0; kk < 32; kk += 4) {
         const int q = kk + t;  // column of the chunk (forward) / row of the block (adjoint)
@@ -875,23 +882,38 @@ __global__ void __launch_bounds__(T_THREADS, 2) bws_tail_kernel(const BGemmArgs 
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt)
           av[mt] = ADJ ? kb[kpos(q, cofs + mt * 8 + g)] : kb[kpos(mt * 8 + g, q)];
-        const double bv = vs[g * W_VP + q];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) dmma884(acc[mt], av[mt], bv);
+        for (int nt = 0; nt < NT; ++nt)
+          if (NT == 1 || nt < ntl) {
+            const double bv = vs[(nt * 8 + g) * W_VP + q];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) dmma884(acc[mt][nt], av[mt], bv);
+          }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
     double* out = a.part + w.y * a.pslab;
-    const int j = 2 * t;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      const int64_t o = ADJ ? (2LL * w.x + tl) * TC + cofs + mt * 8 + g
-                            : (4LL * w.x + warp) * TR + mt * 8 + g;
-      if (j < na) out[(int64_t)s_act[j] * a.ostride + o] = acc[mt][0];
-      if (j + 1 < na) out[(int64_t)s_act[j + 1] * a.ostride + o] = acc[mt][1];
-    }
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int64_t o = ADJ ? (2LL * w.x + tl) * TC + cofs + mt * 8 + g
+                              : (4LL * w.x + warp) * TR + mt * 8 + g;
+        const int j = nt * 8 + 2 * t;
+        if (j < na) out[(int64_t)s_act[j] * a.ostride + o] = acc[mt][nt][0];
+        if (j + 1 < na) out[(int64_t)s_act[j + 1] * a.ostride + o] = acc[mt][nt][1];
+      }
   }
+}
+
+template <bool ADJ>
+__global__ void __launch_bounds__(T_THREADS, 2) bws_tail_kernel(const BGemmArgs a) {
+  pdl_wait_and_trigger();
+  const int na = __ldcg(a.nact);
+  if (na <= 0 || na > T_MAXROWS) return;  // the full-size kernel takes this launch
+  if (na <= 8) bws_tail_body<ADJ, 1>(a, na);
+  else bws_tail_body<ADJ, T_MAXNT>(a, na);
 }
 
 template <int NA>
