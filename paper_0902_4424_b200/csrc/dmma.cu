@@ -599,7 +599,9 @@ __global__ void __launch_bounds__(WP, 1) bfwd_ws_kernel(const BGemmArgs a) {
   pdl_wait_and_trigger();
   const int na = a.nact ? __ldcg(a.nact) : a.nz * BW;  // live problems (compacted columns)
   if (a.tail && na <= T_VROWS) return;               // bws_tail_kernel takes this launch
-  if (na >= a.nb) bfwd_ws_impl<false>(a, na);        // all live: active[] is the identity
+  // all live -- or so many that no 32-problem group could be skipped: every problem in place
+  // (the gather costs more than the few dead columns; stopped problems' columns are ignored)
+  if ((na + 31) / 32 >= (a.nb + 31) / 32) bfwd_ws_impl<false>(a, na);
   else bfwd_ws_compact(a, na);
 }
 
@@ -770,7 +772,7 @@ __global__ void __launch_bounds__(WP, 1) badj_ws_kernel(const BGemmArgs a) {
   pdl_wait_and_trigger();
   const int na = a.nact ? __ldcg(a.nact) : a.nz * BW;
   if (a.tail && na <= T_VROWS) return;
-  if (na >= a.nb) badj_ws_impl<false>(a, na);
+  if ((na + 31) / 32 >= (a.nb + 31) / 32) badj_ws_impl<false>(a, na);
   else badj_ws_compact(a, na);
 }
 
