@@ -11,6 +11,14 @@
 // partials are joined by the finish kernels (gemv.cu), which also run every problem's
 // epilogue.  DMMA accumulates with fused multiply-adds in its own order, so the batched
 // path matches the per-problem canonical solve to rounding, not bit for bit.
+//
+// Kernels, oldest first: bfwd/badj_kernel (8 warps), b*_wide_kernel (16 warps, consumer-issued
+// copies), b*_ws_kernel (16 consumer warps + a producer warp, persistent; the default).  The
+// default products run on the live problems only (bcompact_kernel lists them each iteration):
+// b*_ws_kernel is two instances behind one entry -- every problem in place, or the compacted
+// columns with dead problem blocks / warp groups / tiles skipped -- and bws_tail_kernel takes
+// the launches with at most 32 live problems (two CTAs per SM).  A column's sums do not depend
+// on its place in a tile, so all of these give a problem the same bits.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
